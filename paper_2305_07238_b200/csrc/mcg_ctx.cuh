@@ -1,0 +1,157 @@
+// Host-side device runtime state shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "host_internal.hpp"
+#include "mcg_device.cuh"
+
+namespace mcg {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        fail(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? MCG_ERR_NO_DEVICE
+                                                                        : MCG_ERR_CUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+// Growable device buffer (capacity only grows; contents undefined after grow).
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cuda_check(cudaMalloc(&p, need), "cudaMalloc");
+        bytes = need;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct KernelAcc {
+    uint64_t launches = 0;
+    double ms = 0.0;
+    double bytes = 0.0;
+};
+
+struct EventRec {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+};
+
+// Device copy of a prepared scene.
+struct DeviceScene {
+    std::vector<DevMem> bufs;
+    mcgd::SceneView view{};
+    uint32_t max_stack = 1;
+    uint32_t max_cache_points = 0;
+    mcg_flat_scene cam{};   // camera/env fields only (no pointers used)
+    bool loaded = false;
+    void clear() {
+        for (DevMem& m : bufs) m.release();
+        bufs.clear();
+        view = mcgd::SceneView{};
+        loaded = false;
+    }
+};
+
+}  // namespace mcg
+
+struct mcg_cache {
+    mcg_ctx* ctx = nullptr;
+    uint64_t n_cells = 0;
+    uint32_t n_entries = 0;
+    uint64_t magic = 0;
+    uint64_t* slots = nullptr;
+    unsigned long long* counters = nullptr;  // lookups, hits, won, lost_full, lost_race
+    mcgd::CacheView view() const { return {slots, n_cells, magic, n_entries}; }
+};
+
+struct mcg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool profile = false;
+    uint64_t launches = 0;
+    std::map<std::string, mcg::KernelAcc> times;
+    std::vector<mcg::EventRec> pending;
+    std::vector<cudaEvent_t> event_pool;
+    mcg::DeviceScene scene;
+    mcg_cache* own_cache = nullptr;
+    // scratch
+    mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
+    mcg::DevMem path_mem, queue_mem, stats_mem;
+};
+
+namespace mcg {
+
+cudaEvent_t take_event(mcg_ctx* ctx);
+void resolve_events(mcg_ctx* ctx);  // synchronizes on the pending events
+
+// Brackets one kernel launch: counts it and, when profiling, records CUDA
+// events on the context stream around it.
+class LaunchScope {
+public:
+    LaunchScope(mcg_ctx* ctx, const char* name, double bytes) : ctx_(ctx), name_(name), bytes_(bytes) {
+        if (ctx_->profile) {
+            a_ = take_event(ctx_);
+            cudaEventRecord(a_, ctx_->stream);
+        }
+    }
+    void done() {
+        cuda_check(cudaGetLastError(), name_);
+        ++ctx_->launches;
+        if (ctx_->profile) {
+            cudaEvent_t b = take_event(ctx_);
+            cudaEventRecord(b, ctx_->stream);
+            ctx_->pending.push_back({name_, a_, b, bytes_});
+        }
+    }
+
+private:
+    mcg_ctx* ctx_;
+    const char* name_;
+    double bytes_;
+    cudaEvent_t a_ = nullptr;
+};
+
+inline unsigned grid_for(size_t n, unsigned block) {
+    return static_cast<unsigned>((n + block - 1) / block);
+}
+
+inline uint64_t mod_magic(uint64_t n) { return ~0ull / n; }
+
+inline int bits_for(uint64_t v) {  // bits needed to hold values in [0, v]
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) ++b;
+    return b;
+}
+
+void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* keys_in, unsigned long long* keys_out,
+                    const unsigned long long* vals_in, unsigned long long* vals_out, size_t n,
+                    int end_bit);
+void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* keys_in, uint32_t* keys_out,
+                    const uint32_t* vals_in, uint32_t* vals_out, size_t n, int end_bit);
+
+// Applies sorted (cell << order_bits | order) -> (check << 32 | payload)
+// records cell by cell in order (the deterministic-insert rule). Outcomes are
+// optionally scattered back to index = order.
+void apply_ordered(mcg_ctx* ctx, mcg_cache* cache, const unsigned long long* keys,
+                   const unsigned long long* vals, size_t n, int order_bits, uint8_t* d_outcome,
+                   uint64_t* d_slot, uint64_t* d_packed, unsigned long long* d_stats);
+
+}  // namespace mcg

@@ -1,0 +1,439 @@
+// Device-side building blocks shared by the runtime and render translation
+// units: the HBM table probe/insert (cache.cpp:94-136) and the warp-uniform
+// stack-machine interpreter (stackvm.cpp:248-368).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_math.cuh"
+
+namespace mcgd {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Table view
+// ---------------------------------------------------------------------------
+struct CacheView {
+    uint64_t* slots;          // n_cells * n_entries words, cell-major (cache.cpp:159 dump order)
+    uint64_t n_cells;
+    uint64_t magic;           // floor((2^64-1) / n_cells) for fast_mod
+    uint32_t n_entries;
+};
+
+// Result of scanning one cell as lookup() does (cache.cpp:121-136): a match,
+// or the first empty slot (where update() would CAS, cache.cpp:108), or a
+// full cell (update() -> CellFull).
+struct Probe {
+    uint32_t payload;
+    int32_t where;   // hit: matching slot; miss: first empty slot; -1: cell full
+    bool hit;
+};
+
+// Scans a cell. The first 16 bytes are loaded first: in a sparse table the
+// scan ends there (one DRAM sector); otherwise the remaining words are
+// fetched together. Loads bypass L1 (ld.global.cg) so concurrent inserts
+// from other SMs are seen as early as L2 sees them.
+__device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, uint32_t check) {
+    Probe r{0u, -1, false};
+    const uint32_t ne = c.n_entries;
+    const uint64_t* cell = c.slots + base;
+    uint32_t i = 0;
+    const bool aligned = ((base & 1ull) == 0ull);
+    if (aligned && ne >= 2) {
+        const ulonglong2 w = __ldcg(reinterpret_cast<const ulonglong2*>(cell));
+        if (w.x == 0ull) { r.where = 0; return r; }
+        if (static_cast<uint32_t>(w.x >> 32) == check) { r.hit = true; r.where = 0; r.payload = static_cast<uint32_t>(w.x); return r; }
+        if (w.y == 0ull) { r.where = 1; return r; }
+        if (static_cast<uint32_t>(w.y >> 32) == check) { r.hit = true; r.where = 1; r.payload = static_cast<uint32_t>(w.y); return r; }
+        i = 2;
+        // Remaining pairs, issued back to back (up to Ne = 16 in registers).
+        if (ne <= 16) {
+            ulonglong2 rest[7];
+            const uint32_t npairs = (ne - 2) / 2;
+#pragma unroll
+            for (uint32_t k = 0; k < 7; ++k) {
+                if (k < npairs) rest[k] = __ldcg(reinterpret_cast<const ulonglong2*>(cell + 2 + 2 * k));
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < 7; ++k) {
+                if (k >= npairs) break;
+                const uint64_t a = rest[k].x, b = rest[k].y;
+                const int32_t sa = static_cast<int32_t>(2 + 2 * k);
+                if (a == 0ull) { r.where = sa; return r; }
+                if (static_cast<uint32_t>(a >> 32) == check) { r.hit = true; r.where = sa; r.payload = static_cast<uint32_t>(a); return r; }
+                if (b == 0ull) { r.where = sa + 1; return r; }
+                if (static_cast<uint32_t>(b >> 32) == check) { r.hit = true; r.where = sa + 1; r.payload = static_cast<uint32_t>(b); return r; }
+            }
+            i = 2 + 2 * npairs;
+        }
+    }
+    for (; i < ne; ++i) {
+        const uint64_t w = __ldcg(cell + i);
+        if (w == 0ull) { r.where = static_cast<int32_t>(i); return r; }
+        if (static_cast<uint32_t>(w >> 32) == check) { r.hit = true; r.where = static_cast<int32_t>(i); r.payload = static_cast<uint32_t>(w); return r; }
+    }
+    return r;  // full, no match
+}
+
+// One CAS from zero on the slot the scan found empty (cache.cpp:108-114).
+// Returns MCG_INSERT_WON / LOST_RACE / CELL_FULL.
+__device__ __forceinline__ int insert_at(const CacheView& c, uint64_t base, int32_t where,
+                                         uint32_t check, uint32_t payload) {
+    if (where < 0) return MCG_INSERT_CELL_FULL;
+    const unsigned long long packed = (static_cast<unsigned long long>(check) << 32) | payload;
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long*>(c.slots + base + where), 0ull, packed);
+    return prev == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
+}
+
+// ---------------------------------------------------------------------------
+// Scene view (device pointers; include/mcg.h layouts)
+// ---------------------------------------------------------------------------
+struct SceneView {
+    const float4* prim_geom;      // 3 float4 per prim
+    const float2* prim_uv;        // 3 float2 per prim
+    const uint32_t* prim_info;
+    const float4* nodes;          // 2 float4 per BVH node
+    uint32_t n_nodes;
+    const mcg_point_light* plights;
+    uint32_t n_plights;
+    const mcg_rect_light* rlights;
+    uint32_t n_rlights;
+    const mcg_program* programs;
+    uint32_t n_programs;
+    const mcg_insn* code;
+    const mcg_const* consts;
+    const mcg_noise* noise;
+    const mcg_ramp* ramps;
+    const mcg_ramp_stop* stops;
+    const mcg_texture* textures;
+    const float4* texels;
+    float env[3];
+};
+
+// Per-lane shading input (ShadingPoint, geom.hpp:49-56).
+struct ShadeIn {
+    float px, py, pz, nx, ny, nz, ix, iy, iz, u, v, g1x, g1y, g2x, g2y;
+};
+
+struct VmCounters {
+    uint32_t instrs = 0, lookups = 0, hits = 0, stores = 0, won = 0, full = 0;
+};
+
+// Sink for deterministic-mode stores: (cell, pixel-order key) -> (check, payload).
+struct StoreQueue {
+    unsigned long long* keys;
+    unsigned long long* vals;
+    unsigned int* count;
+    unsigned int capacity;
+};
+
+// Value stack in shared memory: three planes [slot][threads of the block];
+// slot numbers are compile-time (mcg_insn.sp), so a warp always touches one
+// row and the accesses are bank-conflict free.
+struct Stack {
+    float* x;
+    float* y;
+    float* z;
+    int stride;
+    int tid;
+    __device__ __forceinline__ void put(int s, float a, float b, float c, bool scalar) const {
+        x[s * stride + tid] = a;
+        if (!scalar) {
+            y[s * stride + tid] = b;
+            z[s * stride + tid] = c;
+        }
+    }
+    __device__ __forceinline__ float3 get(int s, bool scalar) const {
+        const float a = x[s * stride + tid];
+        if (scalar) return make_float3(a, a, a);
+        return make_float3(a, y[s * stride + tid], z[s * stride + tid]);
+    }
+    __device__ __forceinline__ float sx(int s) const { return x[s * stride + tid]; }
+};
+
+__device__ __forceinline__ float luminance(float3 c) {  // Value::as_scalar, value.hpp:36-38
+    return 0.2126f * c.x + 0.7152f * c.y + 0.0722f * c.z;
+}
+
+__device__ __forceinline__ float bin_op(uint8_t op, float x, float y, float t) {
+    switch (op) {
+        case MCG_OP_ADD: return x + y;
+        case MCG_OP_SUB: return x - y;
+        case MCG_OP_MUL: return x * y;
+        case MCG_OP_DIV: return y == 0.0f ? 0.0f : x / y;  // value.hpp:106-108
+        case MCG_OP_MIX: return x * (1.0f - t) + y * t;    // value.hpp:110-113
+        default: return power(x, y);                        // value.hpp:132-137
+    }
+}
+
+struct VmResult {
+    float3 value;
+    bool scalar;
+};
+
+// Interprets material `slot` for every lane of `grp` (a set of lanes of this
+// warp that all run the same program). The program counter is warp-uniform:
+// the instruction word is one broadcast 16-byte load and the opcode switch
+// never diverges. A lookup hit does not branch away: the lane parks until the
+// bracket's resume point while the lanes that missed evaluate the subtree;
+// when every lane of the group hits, the group jumps (skip_offset, Alg. 2).
+//
+// kDeferred: deterministic mode -- lookups read the epoch-start table and
+// stores are queued with an order key (applied later, lowest key first);
+// otherwise stores CAS immediately (concurrent mode).
+template <bool kDeferred>
+__device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheView& C,
+                                                bool cache_on, int mip_offset, uint32_t slot,
+                                                const ShadeIn& sp, unsigned grp, const Stack& st,
+                                                const uint8_t* perm, uint32_t order_key,
+                                                const StoreQueue& q, VmCounters& cnt) {
+    const mcg_program prog = S.programs[slot];
+    const uint4* code = reinterpret_cast<const uint4*>(S.code + prog.code_offset);
+    const unsigned lane = threadIdx.x & 31u;
+    bool parked = false;
+    int resume = -1;
+    uint64_t p_base = 0;
+    uint32_t p_check = 0;
+    int32_t p_where = -1;
+    unsigned long long p_cell = 0;
+    VmResult out{make_float3(0.0f, 0.0f, 0.0f), true};
+    for (int pc = 0;; ++pc) {
+        if (pc == resume) {
+            parked = false;
+            resume = -1;
+        }
+        const uint4 w = __ldg(code + pc);
+        const uint8_t op = static_cast<uint8_t>(w.x & 0xffu);
+        const uint8_t flags = static_cast<uint8_t>((w.x >> 8) & 0xffu);
+        const int d = static_cast<int>((w.x >> 16) & 0xffu);
+        const uint8_t tags = static_cast<uint8_t>(w.x >> 24);
+        const uint32_t arg = w.y;
+        const bool act = !parked;
+        cnt.instrs += act ? 1u : 0u;
+        const bool ta = tags & MCG_T_A, tb = tags & MCG_T_B, tc = tags & MCG_T_C,
+                   tr = tags & MCG_T_R;
+        switch (op) {
+            case MCG_OP_PUSH_CONST:
+                if (act) {
+                    const float4 c = __ldg(reinterpret_cast<const float4*>(S.consts + arg));
+                    st.put(d, c.x, c.y, c.z, tr);
+                }
+                break;
+            case MCG_OP_LOAD_UV:
+                if (act) {
+                    const unsigned ch = (flags >> MCG_F_UV_SHIFT) & 3u;
+                    if (ch == 0) st.put(d, sp.u, sp.v, 0.0f, false);
+                    else st.put(d, ch == 1 ? sp.u : sp.v, 0.0f, 0.0f, true);
+                }
+                break;
+            case MCG_OP_LOAD_POSITION:
+                if (act) st.put(d, sp.px, sp.py, sp.pz, false);
+                break;
+            case MCG_OP_LOAD_NORMAL:
+                if (act) st.put(d, sp.nx, sp.ny, sp.nz, false);
+                break;
+            case MCG_OP_LOAD_INCOMING:
+                if (act) st.put(d, sp.ix, sp.iy, sp.iz, false);
+                break;
+            case MCG_OP_TEX_SAMPLE:
+                if (act) {
+                    const float3 c = bilinear(S.textures[arg], S.texels, sp.u, sp.v,
+                                              (flags & MCG_F_WRAP_CLAMP) != 0);
+                    st.put(d, c.x, c.y, c.z, false);
+                }
+                break;
+            case MCG_OP_CHECKER:
+                if (act) st.put(d, checker(__uint_as_float(w.w), sp.u, sp.v), 0.0f, 0.0f, true);
+                break;
+            case MCG_OP_NOISE:
+                if (act) {
+                    const float4 nz = __ldg(reinterpret_cast<const float4*>(S.noise + arg));
+                    const mcg_noise p{__float_as_int(nz.x), nz.y, nz.z, nz.w};
+                    st.put(d, fbm2(p, sp.u, sp.v, perm), 0.0f, 0.0f, true);
+                }
+                break;
+            case MCG_OP_ADD: case MCG_OP_SUB: case MCG_OP_MUL: case MCG_OP_DIV: case MCG_OP_POWER:
+                if (act) {
+                    if (ta && tb) {
+                        st.put(d - 2, bin_op(op, st.sx(d - 2), st.sx(d - 1), 0.0f), 0.0f, 0.0f, true);
+                    } else {
+                        const float3 a = st.get(d - 2, ta), b = st.get(d - 1, tb);
+                        st.put(d - 2, bin_op(op, a.x, b.x, 0.0f), bin_op(op, a.y, b.y, 0.0f),
+                               bin_op(op, a.z, b.z, 0.0f), false);
+                    }
+                }
+                break;
+            case MCG_OP_MIX:
+                if (act) {
+                    const float t = tc ? st.sx(d - 1) : luminance(st.get(d - 1, false));
+                    if (ta && tb) {
+                        st.put(d - 3, bin_op(MCG_OP_MIX, st.sx(d - 3), st.sx(d - 2), t), 0.0f, 0.0f, true);
+                    } else {
+                        const float3 a = st.get(d - 3, ta), b = st.get(d - 2, tb);
+                        st.put(d - 3, bin_op(MCG_OP_MIX, a.x, b.x, t), bin_op(MCG_OP_MIX, a.y, b.y, t),
+                               bin_op(MCG_OP_MIX, a.z, b.z, t), false);
+                    }
+                }
+                break;
+            case MCG_OP_CLAMP:
+                if (act) {
+                    const float3 a = st.get(d - 1, ta);
+                    st.put(d - 1, fminf(fmaxf(a.x, 0.0f), 1.0f), fminf(fmaxf(a.y, 0.0f), 1.0f),
+                           fminf(fmaxf(a.z, 0.0f), 1.0f), ta);
+                }
+                break;
+            case MCG_OP_SIN_WAVE:
+                if (act) {
+                    if (ta) {
+                        st.put(d - 1, sin_wave(st.sx(d - 1)), 0.0f, 0.0f, true);
+                    } else {
+                        const float3 a = st.get(d - 1, false);
+                        st.put(d - 1, sin_wave(a.x), sin_wave(a.y), sin_wave(a.z), false);
+                    }
+                }
+                break;
+            case MCG_OP_DOT:  // value.hpp:119-123
+                if (act) {
+                    const float3 a = st.get(d - 2, ta), b = st.get(d - 1, tb);
+                    st.put(d - 2, a.x * b.x + a.y * b.y + a.z * b.z, 0.0f, 0.0f, true);
+                }
+                break;
+            case MCG_OP_RAMP:  // value.hpp:141-156
+                if (act) {
+                    const float t = ta ? st.sx(d - 1) : luminance(st.get(d - 1, false));
+                    const mcg_ramp rp = S.ramps[arg];
+                    const float4* s4 = reinterpret_cast<const float4*>(S.stops + rp.first);
+                    float3 c = make_float3(0.0f, 0.0f, 0.0f);
+                    if (rp.count > 0) {
+                        const float4 first = __ldg(s4), last = __ldg(s4 + rp.count - 1);
+                        if (t <= first.x) {
+                            c = make_float3(first.y, first.z, first.w);
+                        } else if (t >= last.x) {
+                            c = make_float3(last.y, last.z, last.w);
+                        } else {
+                            c = make_float3(last.y, last.z, last.w);
+                            float4 lo = first;
+                            for (uint32_t i = 1; i < rp.count; ++i) {
+                                const float4 hi = __ldg(s4 + i);
+                                if (t <= hi.x) {
+                                    const float span = hi.x - lo.x;
+                                    const float wt = span > 0.0f ? (t - lo.x) / span : 0.0f;
+                                    const float u = 1.0f - wt;
+                                    c = make_float3(lo.y * u + hi.y * wt, lo.z * u + hi.z * wt,
+                                                    lo.w * u + hi.w * wt);
+                                    break;
+                                }
+                                lo = hi;
+                            }
+                        }
+                    }
+                    st.put(d - 1, c.x, c.y, c.z, false);
+                }
+                break;
+            case MCG_OP_BSDF_DIFFUSE:
+                if (act) {
+                    const float3 a = st.get(d - 1, ta);
+                    st.put(d - 1, a.x, a.y, a.z, false);
+                }
+                break;
+            case MCG_OP_CACHE_LOOKUP: {  // stackvm.cpp:328-349
+                if (!cache_on) break;
+                // Brackets never nest, so every lane of the group is active here.
+                Desc desc{prog.material_id, arg, 0u, 0u, 0u};
+                if (flags & MCG_F_USES_UV) {
+                    desc.mip = mip_level(sp.g1x, sp.g1y, sp.g2x, sp.g2y, mip_offset);
+                    desc.tx = texel_index(sp.u, desc.mip);
+                    desc.ty = texel_index(sp.v, desc.mip);
+                }
+                uint64_t h;
+                hash_desc(desc, h, p_check);
+                const uint64_t cell = fast_mod(h, C.n_cells, C.magic);
+                p_base = cell * C.n_entries;
+                p_cell = cell;
+                // Lanes asking for the same (cell, check) share one probe.
+                const unsigned long long key = (cell << 32) ^ p_check;
+                const unsigned peers = __match_any_sync(grp, key);
+                const int leader = __ffs(peers) - 1;
+                Probe pr{0u, -1, false};
+                if (static_cast<int>(lane) == leader) pr = probe_cell(C, p_base, p_check);
+                pr.payload = __shfl_sync(grp, pr.payload, leader);
+                pr.where = __shfl_sync(grp, pr.where, leader);
+                pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;
+                ++cnt.lookups;
+                p_where = pr.where;
+                if (pr.hit) {
+                    const float3 v = decode_rgbe(pr.payload);
+                    if (flags & MCG_F_SCALAR_RESULT) st.put(d, v.x, 0.0f, 0.0f, true);
+                    else st.put(d, v.x, v.y, v.z, false);
+                    ++cnt.hits;
+                    parked = true;
+                }
+                const int skip = static_cast<int>(w.w);
+                if (__all_sync(grp, pr.hit)) {
+                    parked = false;
+                    pc += skip;  // the whole group skips the subtree
+                } else {
+                    resume = pc + 1 + skip;
+                }
+                break;
+            }
+            case MCG_OP_CACHE_STORE: {  // stackvm.cpp:350-357
+                if (!cache_on) break;
+                const unsigned m = __ballot_sync(grp, act);
+                if (act) {
+                    ++cnt.stores;
+                    const float3 v = st.get(d - 1, ta);
+                    const uint32_t payload = encode_rgbe(v.x, v.y, v.z);
+                    if (kDeferred) {
+                        const unsigned rank = __popc(m & ((1u << lane) - 1u));
+                        const int ldr = __ffs(m) - 1;
+                        unsigned base = 0;
+                        if (static_cast<int>(lane) == ldr) base = atomicAdd(q.count, __popc(m));
+                        base = __shfl_sync(m, base, ldr);
+                        const unsigned pos = base + rank;
+                        if (pos < q.capacity) {
+                            q.keys[pos] = (p_cell << 32) |
+                                          static_cast<unsigned long long>(order_key | ((w.z >> 16) & 0xffu));
+                            q.vals[pos] = (static_cast<unsigned long long>(p_check) << 32) | payload;
+                        }
+                    } else {
+                        // One CAS per distinct (cell, check) in the warp; the
+                        // others saw the same empty slot and now find it taken
+                        // by their own key (AlreadyPresent).
+                        const unsigned long long key = (p_cell << 32) ^ p_check;
+                        const unsigned peers = __match_any_sync(m, key);
+                        const int leader = __ffs(peers) - 1;
+                        int res = MCG_INSERT_ALREADY_PRESENT;
+                        if (static_cast<int>(lane) == leader) {
+                            res = insert_at(C, p_base, p_where, p_check, payload);
+                        } else if (p_where < 0) {
+                            res = MCG_INSERT_CELL_FULL;
+                        }
+                        cnt.won += res == MCG_INSERT_WON;
+                        cnt.full += res == MCG_INSERT_CELL_FULL;
+                    }
+                }
+                break;
+            }
+            case MCG_OP_END:
+            default: {
+                out.value = st.get(d - 1, ta);
+                out.scalar = tr;
+                return out;
+            }
+        }
+    }
+}
+
+// Warp-aggregated counter update: one atomic per warp.
+__device__ __forceinline__ void warp_add(unsigned long long* dst, uint32_t v) {
+    const unsigned m = __activemask();
+    const uint32_t s = __reduce_add_sync(m, v);
+    if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(m) - 1) && s) atomicAdd(dst, static_cast<unsigned long long>(s));
+}
+
+}  // namespace mcgd

@@ -1,0 +1,707 @@
+// Wavefront path tracer driving the material cache on the GPU: the body of
+// render() (tracer.hpp:69-70, absent in the reference; restated per
+// tracer.hpp:7-94 + SPEC.md:378-434 with the decisions pinned in DESIGN.md
+// §render). One pass = k samples of every pixel of this shard in flight;
+// per bounce:
+//
+//   k_bounce   NEE + cosine bounce for the previous vertex, then BVH closest
+//              hit, surface, ray-cone propagation and footprint gradients
+//              (scene.cpp:252-278, raycone.cpp:15-65) -> shading record
+//   sort       hit points by material slot (CUB radix sort, stable)
+//   k_shade    warp-uniform bytecode VM with inline cache lookup/store
+//              (stackvm.cpp:248-368, cache.cpp:94-136)
+//   [deterministic mode: sort queued stores by (cell, sample, pixel, ord)
+//    and apply them cell by cell -- the epoch rule, DESIGN.md §determinism]
+//
+// and k_accumulate adds each finished pass into the double framebuffers in
+// sample order (FrameBuffers, tracer.hpp:24-43).
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "host_scene.hpp"
+#include "mcg_ctx.cuh"
+
+using namespace mcg;
+using mcgd::V3;
+
+namespace {
+
+constexpr float kTMin = 1e-4f;
+constexpr float kEps = 1e-4f;
+constexpr float kInvPi = 0.318309886183790671538f;
+
+// Render counters (device, u64): see kStat*.
+enum {
+    kStatLookups = 0, kStatHits, kStatWon, kStatFull, kStatLost, kStatStores, kStatInstrs,
+    kStatShade, kStatShadow, kStatMaxStack, kStatQueue, kStatCount = 16
+};
+
+struct RenderView {
+    mcgd::SceneView S;
+    mcgd::CacheView C;
+    int cache_on;
+    int mip_offset;
+    float cam[12];
+    float cam_pos[3];
+    int W, H;
+    int max_bounces;
+    unsigned long long seed;
+    float diffuse_spread;
+    uint32_t n_pix;           // pixels of this shard
+    const uint32_t* pix;      // shard pixel indices, ascending
+    uint32_t n_paths;         // n_pix * samples in this pass
+    uint32_t sample0;         // sample index of pass slot 0
+    uint32_t hps_base;        // hits_per_sample index of pass slot 0
+    float4* ro;               // origin.xyz, cone width
+    float4* rd;               // direction.xyz, cone spread
+    float4* thr;              // throughput.rgb, nodes_found (uint bits)
+    float4* L;                // radiance.rgb, alive (uint bits)
+    float4* sh0;              // position.xyz, u
+    float4* sh1;              // normal.xyz, v
+    float4* sh2;              // g1.xy, g2.xy
+    float4* base;             // base colour from the VM
+    uint32_t* key;            // material slot, kInvalid if no hit this bounce
+    double* radiance;
+    double* nodes_found;
+    uint32_t* samples;
+    unsigned long long* hps;
+    unsigned long long* stats;
+    mcgd::StoreQueue q;
+};
+
+__device__ __forceinline__ uint32_t dim_rect(int b, int j, int k) { return 2u + 64u * b + 2u * j + k; }
+__device__ __forceinline__ uint32_t dim_bounce(int b, int k) { return 2u + 64u * b + 62u + k; }
+
+// ray_aabb (scene.cpp:42-56) with the per-ray reciprocals of the reference.
+__device__ __forceinline__ bool ray_box(V3 o, V3 inv, float4 lo, float4 hi, float tmin, float tmax) {
+    float t0 = (lo.x - o.x) * inv.x, t1 = (hi.x - o.x) * inv.x;
+    if (inv.x < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    tmin = fmaxf(tmin, t0);
+    tmax = fminf(tmax, t1);
+    if (tmax < tmin) return false;
+    t0 = (lo.y - o.y) * inv.y; t1 = (hi.y - o.y) * inv.y;
+    if (inv.y < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    tmin = fmaxf(tmin, t0);
+    tmax = fminf(tmax, t1);
+    if (tmax < tmin) return false;
+    t0 = (lo.z - o.z) * inv.z; t1 = (hi.z - o.z) * inv.z;
+    if (inv.z < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    tmin = fmaxf(tmin, t0);
+    tmax = fminf(tmax, t1);
+    return !(tmax < tmin);
+}
+
+// ray_triangle (scene.cpp:58-78) / ray_sphere (scene.cpp:80-94)
+__device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V3 o, V3 d,
+                                         float tmin, float tmax, float& t, float& b1, float& b2) {
+    const float4 g0 = __ldg(S.prim_geom + 3 * i);
+    if (__ldg(S.prim_info + i) & MCG_PRIM_SPHERE) {
+        const V3 oc = o - V3{g0.x, g0.y, g0.z};
+        const float b = mcgd::dot(oc, d);
+        const float c = mcgd::dot(oc, oc) - g0.w * g0.w;
+        const float disc = b * b - c;
+        if (disc < 0.0f) return false;
+        const float sq = sqrtf(disc);
+        float root = -b - sq;
+        if (root <= tmin || root >= tmax) {
+            root = -b + sq;
+            if (root <= tmin || root >= tmax) return false;
+        }
+        t = root;
+        b1 = b2 = 0.0f;
+        return true;
+    }
+    const float4 g1 = __ldg(S.prim_geom + 3 * i + 1), g2 = __ldg(S.prim_geom + 3 * i + 2);
+    const V3 p0{g0.x, g0.y, g0.z}, e1{g1.x, g1.y, g1.z}, e2{g2.x, g2.y, g2.z};
+    const V3 pvec = mcgd::cross(d, e2);
+    const float det = mcgd::dot(e1, pvec);
+    if (fabsf(det) < 1e-12f) return false;
+    const float inv_det = 1.0f / det;
+    const V3 tvec = o - p0;
+    const float u = mcgd::dot(tvec, pvec) * inv_det;
+    if (u < 0.0f || u > 1.0f) return false;
+    const V3 qvec = mcgd::cross(tvec, e1);
+    const float v = mcgd::dot(d, qvec) * inv_det;
+    if (v < 0.0f || u + v > 1.0f) return false;
+    const float ht = mcgd::dot(e2, qvec) * inv_det;
+    if (ht <= tmin || ht >= tmax) return false;
+    t = ht;
+    b1 = u;
+    b2 = v;
+    return true;
+}
+
+// Scene::intersect (scene.cpp:252-278) / Scene::occluded (:280-298): the
+// reference's unordered DFS (left pushed first, so the right child is
+// visited first) -- closest-hit ties at equal t resolve identically.
+template <bool kAnyHit>
+__device__ bool traverse(const mcgd::SceneView& S, V3 o, V3 d, float tmin, float tmax,
+                         uint32_t& prim, float& t_out, float& b1_out, float& b2_out) {
+    if (S.n_nodes == 0) return false;
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t stack[64];
+    int top = 0;
+    stack[top++] = 0;
+    bool found = false;
+    float closest = tmax;
+    while (top > 0) {
+        const int32_t ni = stack[--top];
+        const float4 lo = __ldg(S.nodes + 2 * ni), hi = __ldg(S.nodes + 2 * ni + 1);
+        if (!ray_box(o, inv, lo, hi, tmin, closest)) continue;
+        const int32_t a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+        if (a < 0) {
+            const uint32_t first = static_cast<uint32_t>(~a);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                    if (kAnyHit) return true;
+                    closest = t;
+                    prim = i;
+                    t_out = t;
+                    b1_out = b1;
+                    b2_out = b2;
+                    found = true;
+                }
+            }
+        } else {
+            stack[top++] = a;
+            stack[top++] = b;
+        }
+    }
+    return found;
+}
+
+struct Surface {
+    V3 p, n;
+    float u, v;
+    V3 e1, e2;
+    float2 d1, d2;
+    uint32_t slot;
+};
+
+// HitRecord construction (scene.cpp:211-247).
+__device__ Surface surface(const mcgd::SceneView& S, V3 o, V3 d, uint32_t prim, float t, float b1,
+                           float b2) {
+    Surface s;
+    const uint32_t info = __ldg(S.prim_info + prim);
+    s.slot = info & ~MCG_PRIM_SPHERE;
+    s.p = o + d * t;
+    const float4 g0 = __ldg(S.prim_geom + 3 * prim);
+    if (!(info & MCG_PRIM_SPHERE)) {
+        const float4 g1 = __ldg(S.prim_geom + 3 * prim + 1), g2 = __ldg(S.prim_geom + 3 * prim + 2);
+        s.e1 = V3{g1.x, g1.y, g1.z};
+        s.e2 = V3{g2.x, g2.y, g2.z};
+        V3 n = mcgd::normalize(mcgd::cross(s.e1, s.e2));
+        if (mcgd::dot(n, d) > 0.0f) n = V3{-n.x, -n.y, -n.z};
+        s.n = n;
+        const float2 uv0 = __ldg(S.prim_uv + 3 * prim), uv1 = __ldg(S.prim_uv + 3 * prim + 1),
+                     uv2 = __ldg(S.prim_uv + 3 * prim + 2);
+        const float w0 = 1.0f - b1 - b2;
+        s.u = uv0.x * w0 + uv1.x * b1 + uv2.x * b2;
+        s.v = uv0.y * w0 + uv1.y * b1 + uv2.y * b2;
+        s.d1 = make_float2(uv1.x - uv0.x, uv1.y - uv0.y);
+        s.d2 = make_float2(uv2.x - uv0.x, uv2.y - uv0.y);
+        return s;
+    }
+    // Sphere (scene.cpp:227-246). atan2f/acosf are CUDA's: sphere uv is the
+    // one quantity not bit-pinned to glibc.
+    const float kPi = 3.14159265358979323846f;
+    const V3 m = mcgd::normalize(s.p - V3{g0.x, g0.y, g0.z});
+    V3 n = m;
+    if (mcgd::dot(n, d) > 0.0f) n = V3{-n.x, -n.y, -n.z};
+    s.n = n;
+    s.u = 0.5f + atan2f(m.z, m.x) / (2.0f * kPi);
+    s.v = acosf(fminf(fmaxf(m.y, -1.0f), 1.0f)) / kPi;
+    const float sin_t = sqrtf(fmaxf(0.0f, 1.0f - m.y * m.y));
+    const float r = g0.w;
+    if (sin_t > 1e-6f) {
+        s.e1 = V3{-m.z, 0.0f, m.x} * (2.0f * kPi * r);
+        const float cphi = m.x / sin_t, sphi = m.z / sin_t;
+        s.e2 = V3{m.y * cphi, -sin_t, m.y * sphi} * (kPi * r);
+    } else {
+        s.e1 = V3{1.0f, 0.0f, 0.0f} * (2.0f * kPi * r);
+        s.e2 = V3{0.0f, 0.0f, 1.0f} * (kPi * r);
+    }
+    s.d1 = make_float2(1.0f, 0.0f);
+    s.d2 = make_float2(0.0f, 1.0f);
+    return s;
+}
+
+__device__ __forceinline__ void add_light(float4& L, V3 tf, const float* emit, float w) {
+    L.x = L.x + tf.x * (emit[0] * w);
+    L.y = L.y + tf.y * (emit[1] * w);
+    L.z = L.z + tf.z * (emit[2] * w);
+}
+
+// One wavefront step for path i: finish vertex b-1 (next-event estimation
+// over every light, then the cosine bounce) and trace vertex b.
+__global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t shadow = 0;
+    if (i < R.n_paths) {
+        const uint32_t slot_j = i / R.n_pix;
+        const uint32_t pixel = R.pix[i - slot_j * R.n_pix];
+        const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
+        float4 ro, rd, thr, L;
+        bool alive = true;
+        if (b == 0) {
+            // Primary ray (camera).
+            const int x = static_cast<int>(pixel % static_cast<uint32_t>(R.W));
+            const int y = static_cast<int>(pixel / static_cast<uint32_t>(R.W));
+            const float jx = mcgd::path_sample(rkey, 0), jy = mcgd::path_sample(rkey, 1);
+            const float sx = ((static_cast<float>(x) + jx) / static_cast<float>(R.W)) * 2.0f - 1.0f;
+            const float sy = 1.0f - ((static_cast<float>(y) + jy) / static_cast<float>(R.H)) * 2.0f;
+            const float a = (sx * R.cam[9]) * R.cam[10];
+            const float bq = sy * R.cam[9];
+            const V3 fwd{R.cam[0], R.cam[1], R.cam[2]}, right{R.cam[3], R.cam[4], R.cam[5]},
+                up{R.cam[6], R.cam[7], R.cam[8]};
+            const V3 dir = mcgd::normalize((fwd + right * a) + up * bq);
+            ro = make_float4(R.cam_pos[0], R.cam_pos[1], R.cam_pos[2], 0.0f);
+            rd = make_float4(dir.x, dir.y, dir.z, R.cam[11]);
+            thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
+            L = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(1u));
+        } else {
+            L = R.L[i];
+            if (__float_as_uint(L.w) == 0u) {
+                alive = false;
+            } else {
+                ro = R.ro[i];
+                rd = R.rd[i];
+                thr = R.thr[i];
+                const int pb = b - 1;
+                const float4 s0 = R.sh0[i], s1 = R.sh1[i], bc = R.base[i];
+                const V3 n{s1.x, s1.y, s1.z};
+                const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
+                             fminf(fmaxf(bc.z, 0.0f), 1.0f)};
+                const V3 f = alb * kInvPi;
+                const V3 tf{thr.x * f.x, thr.y * f.y, thr.z * f.z};
+                const V3 o = V3{s0.x, s0.y, s0.z} + n * kEps;
+                uint32_t pdummy;
+                float td, t1, t2;
+                for (uint32_t li = 0; li < R.S.n_plights; ++li) {
+                    const mcg_point_light& l = R.S.plights[li];
+                    const V3 toL = V3{l.position[0], l.position[1], l.position[2]} - o;
+                    const float d2 = mcgd::dot(toL, toL);
+                    const float dist = sqrtf(d2);
+                    const V3 wi = toL * (1.0f / dist);
+                    const float cs = mcgd::dot(n, wi);
+                    if (cs > 0.0f) {
+                        ++shadow;
+                        if (!traverse<true>(R.S, o, wi, kTMin, dist, pdummy, td, t1, t2)) {
+                            add_light(L, tf, l.intensity, cs / d2);
+                        }
+                    }
+                }
+                for (uint32_t j = 0; j < R.S.n_rlights; ++j) {
+                    const mcg_rect_light& l = R.S.rlights[j];
+                    const float u = mcgd::path_sample(rkey, dim_rect(pb, static_cast<int>(j), 0));
+                    const float vv = mcgd::path_sample(rkey, dim_rect(pb, static_cast<int>(j), 1));
+                    const V3 eu{l.edge_u[0], l.edge_u[1], l.edge_u[2]};
+                    const V3 ev{l.edge_v[0], l.edge_v[1], l.edge_v[2]};
+                    const V3 pl = (V3{l.corner[0], l.corner[1], l.corner[2]} + eu * u) + ev * vv;
+                    const V3 nl = mcgd::cross(eu, ev);
+                    const float area = mcgd::length(nl);
+                    const V3 toL = pl - o;
+                    const float d2 = mcgd::dot(toL, toL);
+                    const float dist = sqrtf(d2);
+                    const V3 wi = toL * (1.0f / dist);
+                    const float cs = mcgd::dot(n, wi);
+                    const float cl = fabsf(mcgd::dot(nl, wi)) / area;
+                    if (cs > 0.0f && cl > 0.0f) {
+                        ++shadow;
+                        if (!traverse<true>(R.S, o, wi, kTMin, dist, pdummy, td, t1, t2)) {
+                            add_light(L, tf, l.radiance, ((cs * cl) * area) / d2);
+                        }
+                    }
+                }
+                if (pb == R.max_bounces) {
+                    alive = false;
+                } else {
+                    // Cosine-weighted bounce in Duff et al.'s branchless frame.
+                    const float r1 = mcgd::path_sample(rkey, dim_bounce(pb, 0));
+                    const float r2 = mcgd::path_sample(rkey, dim_bounce(pb, 1));
+                    float sphi, cphi;
+                    mcgd::det_sincosf(r1 * mcgd::kTwoPi, sphi, cphi);
+                    const float r = sqrtf(r2);
+                    const float lx = r * cphi, ly = r * sphi;
+                    const float lz = sqrtf(fmaxf(0.0f, 1.0f - r2));
+                    const float sign = copysignf(1.0f, n.z);
+                    const float a = -1.0f / (sign + n.z);
+                    const float bb = (n.x * n.y) * a;
+                    const V3 t{1.0f + ((sign * n.x) * n.x) * a, sign * bb, -sign * n.x};
+                    const V3 bt{bb, sign + ((n.y * n.y) * a), -n.y};
+                    const V3 nd = mcgd::normalize((t * lx + bt * ly) + n * lz);
+                    thr.x = thr.x * alb.x;
+                    thr.y = thr.y * alb.y;
+                    thr.z = thr.z * alb.z;
+                    rd = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
+                    ro = make_float4(o.x, o.y, o.z, ro.w);
+                }
+            }
+        }
+        uint32_t key = R.S.n_programs;  // sorts after every material slot
+        if (alive) {
+            const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
+            uint32_t prim = 0;
+            float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+            if (!traverse<false>(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2)) {
+                L.x = L.x + thr.x * R.S.env[0];
+                L.y = L.y + thr.y * R.S.env[1];
+                L.z = L.z + thr.z * R.S.env[2];
+                alive = false;
+            } else {
+                const Surface s = surface(R.S, o, d, prim, t, b1, b2);
+                const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+                float2 g1, g2;
+                mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+                R.sh0[i] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+                R.sh1[i] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+                R.sh2[i] = make_float4(g1.x, g1.y, g2.x, g2.y);
+                ro.w = width;
+                key = s.slot;
+            }
+        }
+        if (b == 0 || alive || __float_as_uint(L.w) != 0u) {
+            L.w = __uint_as_float(alive ? 1u : 0u);
+            R.L[i] = L;
+            if (alive) {
+                R.ro[i] = ro;
+                R.rd[i] = rd;
+                R.thr[i] = thr;
+            } else if (b == 0) {
+                R.thr[i] = thr;  // nodes_found = 0
+            }
+        }
+        R.key[i] = key;
+    }
+    mcgd::warp_add(R.stats + kStatShadow, shadow);
+}
+
+// Material evaluation of every live hit, in material order.
+template <bool kDeferred>
+__global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __restrict__ skey,
+                                               const uint32_t* __restrict__ order, int max_stack,
+                                               uint32_t wh) {
+    extern __shared__ float smem[];
+    __shared__ uint8_t s_perm[256];
+    mcgd::stage_perm(s_perm);
+    __syncthreads();
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t slot = i < R.n_paths ? skey[i] : R.S.n_programs;
+    const bool valid = slot < R.S.n_programs;
+    const unsigned live = __ballot_sync(mcgd::kFull, valid);
+    if (!valid) return;
+    const uint32_t p = order[i];
+    const unsigned grp = __match_any_sync(live, slot);
+    const float4 s0 = R.sh0[p], s1 = R.sh1[p], s2 = R.sh2[p], rd = R.rd[p];
+    const mcgd::ShadeIn in{s0.x, s0.y, s0.z, s1.x, s1.y, s1.z, rd.x, rd.y, rd.z,
+                           s0.w, s1.w, s2.x, s2.y, s2.z, s2.w};
+    mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
+                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
+    const uint32_t slot_j = p / R.n_pix;
+    const uint32_t pixel = R.pix[p - slot_j * R.n_pix];
+    const uint32_t okey = (slot_j * wh + pixel) << 6;
+    mcgd::VmCounters cnt;
+    const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
+                                                          slot, in, grp, st, s_perm, okey, R.q, cnt);
+    R.base[p] = make_float4(r.value.x, r.value.y, r.value.z, 0.0f);
+    if (cnt.hits) {
+        float4 t = R.thr[p];
+        t.w = __uint_as_float(__float_as_uint(t.w) + cnt.hits);
+        R.thr[p] = t;
+    }
+    mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
+    mcgd::warp_add(R.stats + kStatHits, cnt.hits);
+    mcgd::warp_add(R.stats + kStatWon, cnt.won);
+    mcgd::warp_add(R.stats + kStatFull, cnt.full);
+    mcgd::warp_add(R.stats + kStatStores, cnt.stores);
+    mcgd::warp_add(R.stats + kStatInstrs, cnt.instrs);
+    mcgd::warp_add(R.stats + kStatShade, 1u);
+}
+
+// Adds the finished pass into the framebuffers, samples in order, so the
+// double accumulators see exactly the oracle's summation order.
+__global__ void k_accumulate(RenderView R, uint32_t k) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= R.n_pix) return;
+    const uint32_t pixel = R.pix[q];
+    double r = R.radiance[3ull * pixel], g = R.radiance[3ull * pixel + 1],
+           bl = R.radiance[3ull * pixel + 2], nf = R.nodes_found[pixel];
+    for (uint32_t j = 0; j < k; ++j) {
+        const uint32_t i = j * R.n_pix + q;
+        const float4 L = R.L[i];
+        const uint32_t nodes = __float_as_uint(R.thr[i].w);
+        r += static_cast<double>(L.x);
+        g += static_cast<double>(L.y);
+        bl += static_cast<double>(L.z);
+        nf += static_cast<double>(nodes);
+        if (R.hps) atomicAdd(R.hps + R.hps_base + j, static_cast<unsigned long long>(nodes));
+    }
+    R.radiance[3ull * pixel] = r;
+    R.radiance[3ull * pixel + 1] = g;
+    R.radiance[3ull * pixel + 2] = bl;
+    R.nodes_found[pixel] = nf;
+    R.samples[pixel] += k;
+}
+
+__global__ void k_iota(uint32_t* v, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
+    if (p.shard_count <= 1) return true;
+    if (p.shard_mode == MCG_SHARD_INTERLEAVED) return tile % p.shard_count == p.shard_rank;
+    const int lo = static_cast<int>(static_cast<int64_t>(n_tiles) * p.shard_rank / p.shard_count);
+    const int hi = static_cast<int>(static_cast<int64_t>(n_tiles) * (p.shard_rank + 1) / p.shard_count);
+    return tile >= lo && tile < hi;
+}
+
+void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external,
+                   double* d_rad, double* d_nodes, uint32_t* d_samples, mcg_render_stats* stats) {
+    const DeviceScene& D = ctx->scene;
+    if (!D.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
+    const int W = P.width ? P.width : D.cam.cam_width;
+    const int H = P.height ? P.height : D.cam.cam_height;
+    if (W <= 0 || H <= 0) fail(MCG_ERR_INVALID_ARGUMENT, "image size must be positive");
+    if (P.spp < 1) fail(MCG_ERR_INVALID_ARGUMENT, "spp must be >= 1");
+    if (P.max_bounces < 0) fail(MCG_ERR_INVALID_ARGUMENT, "max_bounces must be >= 0");
+    if (D.view.n_rlights > 31) fail(MCG_ERR_INVALID_ARGUMENT, "at most 31 rect lights");
+    if (P.shard_count > 1 && (P.shard_rank < 0 || P.shard_rank >= P.shard_count)) {
+        fail(MCG_ERR_INVALID_ARGUMENT, "shard_rank out of range");
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const bool cache_on = P.cache_mode != MCG_CACHE_OFF;
+    const bool deferred = P.cache_mode == MCG_CACHE_DETERMINISTIC;
+
+    // Shard pixel list (16x16 tiles, tracer.hpp:19).
+    const int ts = P.tile_size > 0 ? P.tile_size : 16;
+    const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
+    std::vector<uint32_t> pix;
+    pix.reserve(static_cast<size_t>(W) * H);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            if (tile_mine(P, (y / ts) * tiles_x + x / ts, tiles_x * tiles_y))
+                pix.push_back(static_cast<uint32_t>(y * W + x));
+    const uint32_t n_pix = static_cast<uint32_t>(pix.size());
+
+    uint32_t k = P.samples_per_pass > 0 ? static_cast<uint32_t>(P.samples_per_pass) : 0;
+    if (k == 0) {
+        const uint64_t target = 1u << 21;  // ~2M paths in flight fill 148 SMs
+        k = static_cast<uint32_t>(std::max<uint64_t>(1, (target + n_pix - 1) / std::max<uint32_t>(n_pix, 1)));
+    }
+    k = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp));
+    const uint64_t wh = static_cast<uint64_t>(W) * H;
+    if (deferred && (static_cast<uint64_t>(k) * wh) >= (1ull << 26)) {
+        fail(MCG_ERR_INVALID_ARGUMENT, "deterministic mode: samples_per_pass * pixels must be < 2^26");
+    }
+    const uint64_t max_paths = static_cast<uint64_t>(n_pix) * k;
+
+    // Cache: external table, or the context's own one (tracer.hpp:67-68).
+    mcg_cache* cache = nullptr;
+    if (cache_on) {
+        cache = external;
+        if (!cache) {
+            if (!ctx->own_cache || ctx->own_cache->n_cells != P.n_cells ||
+                ctx->own_cache->n_entries != P.n_entries) {
+                if (ctx->own_cache) mcg_cache_destroy(ctx->own_cache);
+                ctx->own_cache = nullptr;
+                const mcg_status s = mcg_cache_create(ctx, P.n_cells, P.n_entries, &ctx->own_cache);
+                if (s != MCG_OK) fail(s, mcg_last_error());
+            } else {
+                const mcg_status s = mcg_cache_clear(ctx->own_cache);
+                if (s != MCG_OK) fail(s, mcg_last_error());
+            }
+            cache = ctx->own_cache;
+        }
+    }
+
+    // Path state: 10 float4 + 3 u32 per path, plus sort buffers.
+    const size_t f4 = max_paths * sizeof(float4);
+    ctx->path_mem.ensure(f4 * 8 + max_paths * 4 * 4 + n_pix * 4ull + 256);
+    char* base = ctx->path_mem.as<char>();
+    RenderView R{};
+    R.S = D.view;
+    R.C = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1};
+    R.cache_on = cache_on ? 1 : 0;
+    R.mip_offset = P.mip_offset;
+    camera_setup(D.cam, W, H, R.cam);
+    std::memcpy(R.cam_pos, D.cam.cam_position, sizeof(R.cam_pos));
+    R.W = W;
+    R.H = H;
+    R.max_bounces = P.max_bounces;
+    R.seed = P.rng_seed;
+    R.diffuse_spread = P.diffuse_spread;
+    R.n_pix = n_pix;
+    R.ro = reinterpret_cast<float4*>(base);
+    R.rd = R.ro + max_paths;
+    R.thr = R.rd + max_paths;
+    R.L = R.thr + max_paths;
+    R.sh0 = R.L + max_paths;
+    R.sh1 = R.sh0 + max_paths;
+    R.sh2 = R.sh1 + max_paths;
+    R.base = R.sh2 + max_paths;
+    uint32_t* u32 = reinterpret_cast<uint32_t*>(R.base + max_paths);
+    R.key = u32;
+    uint32_t* skey = u32 + max_paths;
+    uint32_t* iota = u32 + 2 * max_paths;
+    uint32_t* order = u32 + 3 * max_paths;
+    uint32_t* d_pix = u32 + 4 * max_paths;
+    R.pix = d_pix;
+    cuda_check(cudaMemcpyAsync(d_pix, pix.data(), n_pix * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D pixels");
+    {
+        LaunchScope ls(ctx, "iota", max_paths * 4.0);
+        k_iota<<<grid_for(max_paths, 256), 256, 0, ctx->stream>>>(iota, static_cast<uint32_t>(max_paths));
+        ls.done();
+    }
+    R.radiance = d_rad;
+    R.nodes_found = d_nodes;
+    R.samples = d_samples;
+    ctx->stats_mem.ensure(4096 + static_cast<size_t>(P.spp) * 8);
+    R.stats = ctx->stats_mem.as<unsigned long long>();
+    R.hps = R.stats + kStatCount;
+    cuda_check(cudaMemsetAsync(R.stats, 0, (kStatCount + P.spp) * 8ull, ctx->stream), "memset stats");
+    unsigned long long* cache_ctr = cache ? cache->counters : nullptr;
+
+    if (deferred) {
+        const uint64_t cap = max_paths * std::max<uint32_t>(1, D.max_cache_points);
+        if (cap >= (1ull << 32)) fail(MCG_ERR_INVALID_ARGUMENT, "store queue too large");
+        ctx->queue_mem.ensure(cap * 32 + 64);
+        R.q.keys = ctx->queue_mem.as<unsigned long long>();
+        R.q.vals = R.q.keys + cap;
+        R.q.count = reinterpret_cast<unsigned int*>(R.q.keys + 4 * cap);
+        R.q.capacity = static_cast<unsigned>(cap);
+    }
+    const int key_bits = std::max(1, bits_for(D.view.n_programs));  // holds kInvalid-remapped slots
+    const int block = 128;
+    const int max_stack = static_cast<int>(D.max_stack);
+    const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
+    if (smem > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "material stack too deep for shared memory");
+    cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+
+    for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k) {
+        const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp) - start);
+        R.n_paths = n_pix * kk;
+        R.sample0 = P.first_sample + start;
+        R.hps_base = start;
+        const unsigned grid = grid_for(R.n_paths, 256);
+        for (int b = 0; b <= P.max_bounces + 1; ++b) {
+            {
+                LaunchScope ls(ctx, "bounce", 0.0);
+                k_bounce<<<grid, 256, 0, ctx->stream>>>(R, b);
+                ls.done();
+            }
+            if (b > P.max_bounces) break;
+            // Stable radix sort of (slot -> path); paths without a hit carry
+            // key n_programs and sort last.
+            sort_pairs_u32(ctx, R.key, skey, iota, order, R.n_paths, key_bits);
+            if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, ctx->stream), "memset");
+            {
+                LaunchScope ls(ctx, "shade", 0.0);
+                if (deferred) {
+                    k_shade<true><<<grid_for(R.n_paths, block), block, smem, ctx->stream>>>(
+                        R, skey, order, max_stack, static_cast<uint32_t>(wh));
+                } else {
+                    k_shade<false><<<grid_for(R.n_paths, block), block, smem, ctx->stream>>>(
+                        R, skey, order, max_stack, static_cast<uint32_t>(wh));
+                }
+                ls.done();
+            }
+            if (deferred) {
+                unsigned int count = 0;
+                cuda_check(cudaMemcpyAsync(&count, R.q.count, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+                cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+                if (count > R.q.capacity) fail(MCG_ERR_CUDA, "store queue overflow");
+                if (count) {
+                    const uint64_t cap = R.q.capacity;
+                    unsigned long long* k1 = R.q.keys + 2 * cap;
+                    unsigned long long* v1 = R.q.keys + 3 * cap;
+                    sort_pairs_u64(ctx, R.q.keys, k1, R.q.vals, v1, count, 64);
+                    // apply_ordered adds won/full at counters[2]/[3] == kStatWon/kStatFull.
+                    apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, R.stats);
+                }
+            }
+        }
+        {
+            LaunchScope ls(ctx, "accumulate", n_pix * (40.0 + 40.0 * kk));
+            k_accumulate<<<grid_for(n_pix, 256), 256, 0, ctx->stream>>>(R, kk);
+            ls.done();
+        }
+    }
+    unsigned long long st[kStatCount];
+    cuda_check(cudaMemcpyAsync(st, R.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream), "D2H stats");
+    if (stats && stats->hits_per_sample) {
+        cuda_check(cudaMemcpyAsync(stats->hits_per_sample, R.hps, P.spp * 8ull, cudaMemcpyDeviceToHost, ctx->stream), "D2H hps");
+    }
+    cuda_check(cudaStreamSynchronize(ctx->stream), "render");
+    if (cache_ctr) {
+        // Mirror the render's lookups/hits/inserts into the table's counters
+        // (MaterialCache::counters after a render, cache.cpp:146-150).
+        unsigned long long add[4] = {st[kStatLookups], st[kStatHits], st[kStatWon], st[kStatFull]};
+        unsigned long long cur[4];
+        cuda_check(cudaMemcpy(cur, cache_ctr, sizeof(cur), cudaMemcpyDeviceToHost), "D2H");
+        for (int q = 0; q < 4; ++q) cur[q] += add[q];
+        cuda_check(cudaMemcpy(cache_ctr, cur, sizeof(cur), cudaMemcpyHostToDevice), "H2D");
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (stats) {
+        uint64_t* hps = stats->hits_per_sample;
+        std::memset(stats, 0, sizeof(*stats));
+        stats->hits_per_sample = hps;
+        stats->wall_time_s = std::chrono::duration<double>(t1 - t0).count();
+        stats->lookups = st[kStatLookups];
+        stats->hits = st[kStatHits];
+        stats->inserts_won = st[kStatWon];
+        stats->inserts_lost_full = st[kStatFull];
+        stats->stores_attempted = st[kStatStores];
+        stats->stores_won = st[kStatWon];
+        stats->instructions_executed = st[kStatInstrs];
+        stats->max_stack_seen = D.max_stack;
+        stats->paths = static_cast<uint64_t>(n_pix) * P.spp;
+        stats->shading_points = st[kStatShade];
+        stats->shadow_rays = st[kStatShadow];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+mcg_status mcg_render_device(mcg_ctx* ctx, const mcg_render_params* params, mcg_cache* cache,
+                             mcg_frame* d_frame, mcg_render_stats* stats) {
+    return guarded([&] {
+        if (!ctx || !params || !d_frame) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        render_device(ctx, *params, cache, d_frame->radiance, d_frame->nodes_found,
+                      d_frame->samples, stats);
+    });
+}
+
+mcg_status mcg_render(mcg_ctx* ctx, const mcg_render_params* params, mcg_cache* cache,
+                      mcg_frame* frame, mcg_render_stats* stats) {
+    return guarded([&] {
+        if (!ctx || !params || !frame || !frame->radiance || !frame->nodes_found || !frame->samples) {
+            fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        }
+        if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
+        const int W = params->width ? params->width : ctx->scene.cam.cam_width;
+        const int H = params->height ? params->height : ctx->scene.cam.cam_height;
+        if (W <= 0 || H <= 0) fail(MCG_ERR_INVALID_ARGUMENT, "image size must be positive");
+        const size_t np = static_cast<size_t>(W) * H;
+        ctx->scratch_e.ensure(np * 44 + 64);
+        double* rad = ctx->scratch_e.as<double>();
+        double* nodes = rad + 3 * np;
+        uint32_t* samples = reinterpret_cast<uint32_t*>(nodes + np);
+        cuda_check(cudaMemcpyAsync(rad, frame->radiance, np * 24, cudaMemcpyHostToDevice, ctx->stream), "H2D frame");
+        cuda_check(cudaMemcpyAsync(nodes, frame->nodes_found, np * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D frame");
+        cuda_check(cudaMemcpyAsync(samples, frame->samples, np * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D frame");
+        render_device(ctx, *params, cache, rad, nodes, samples, stats);
+        cuda_check(cudaMemcpyAsync(frame->radiance, rad, np * 24, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+        cuda_check(cudaMemcpyAsync(frame->nodes_found, nodes, np * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+        cuda_check(cudaMemcpyAsync(frame->samples, samples, np * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "render");
+    });
+}
+
+}  // extern "C"

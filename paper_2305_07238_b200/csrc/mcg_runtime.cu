@@ -1,0 +1,904 @@
+// Device runtime and C ABI: contexts, the HBM material cache, batched
+// descriptor/codec/probe kernels, the probe microbenchmark, per-point VM
+// execution and scene upload. Reference behaviour cited per entry point
+// (paths relative to /root/reference/proj/core).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <fstream>
+#include <vector>
+
+#include "host_scene.hpp"
+#include "mcg_ctx.cuh"
+
+using namespace mcg;
+using mcgd::CacheView;
+
+namespace mcg {
+
+cudaEvent_t take_event(mcg_ctx* ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void resolve_events(mcg_ctx* ctx) {
+    for (EventRec& r : ctx->pending) {
+        cuda_check(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        KernelAcc& acc = ctx->times[r.name];
+        acc.launches += 1;
+        acc.ms += ms;
+        acc.bytes += r.bytes;
+        ctx->event_pool.push_back(r.a);
+        ctx->event_pool.push_back(r.b);
+    }
+    ctx->pending.clear();
+}
+
+void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* ki, unsigned long long* ko,
+                    const unsigned long long* vi, unsigned long long* vo, size_t n, int end_bit) {
+    size_t bytes = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ki, ko, vi, vo, static_cast<int>(n), 0,
+                                               end_bit, ctx->stream),
+               "cub sort (size)");
+    ctx->cub_temp.ensure(std::max<size_t>(bytes, 256));
+    cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
+                                               static_cast<int>(n), 0, end_bit, ctx->stream),
+               "cub sort");
+    ctx->launches += static_cast<uint64_t>((end_bit + 7) / 8) + 1;
+}
+
+void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* ki, uint32_t* ko, const uint32_t* vi,
+                    uint32_t* vo, size_t n, int end_bit) {
+    size_t bytes = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ki, ko, vi, vo, static_cast<int>(n), 0,
+                                               end_bit, ctx->stream),
+               "cub sort (size)");
+    ctx->cub_temp.ensure(std::max<size_t>(bytes, 256));
+    cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
+                                               static_cast<int>(n), 0, end_bit, ctx->stream),
+               "cub sort");
+    ctx->launches += static_cast<uint64_t>((end_bit + 7) / 8) + 1;
+}
+
+}  // namespace mcg
+
+// ===========================================================================
+// Kernels
+// ===========================================================================
+namespace {
+
+using mcgd::Desc;
+
+__device__ __forceinline__ Desc load_desc(const mcg_descriptor* d, size_t i) {
+    // 20-byte records: five 32-bit words.
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(d) + 5 * i;
+    return Desc{__ldg(w), __ldg(w + 1), __ldg(w + 3), __ldg(w + 4), __ldg(w + 2) & 0xffu};
+}
+
+__global__ void k_hash(const mcg_descriptor* d, size_t n, uint64_t* cell, uint32_t* check) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    uint64_t h;
+    uint32_t c;
+    mcgd::hash_desc(load_desc(d, i), h, c);
+    cell[i] = h;
+    check[i] = c;
+}
+
+__global__ void k_encode(const float* rgb, size_t n, uint32_t* out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    out[i] = mcgd::encode_rgbe(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+}
+
+__global__ void k_decode(const uint32_t* in, size_t n, float* rgb) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const float3 c = mcgd::decode_rgbe(in[i]);
+    rgb[3 * i] = c.x;
+    rgb[3 * i + 1] = c.y;
+    rgb[3 * i + 2] = c.z;
+}
+
+__global__ void k_mip_texel(const float* uv, const float* g1, const float* g2, size_t n, int off,
+                            uint8_t* mip, uint32_t* txy) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t m = mcgd::mip_level(g1[2 * i], g1[2 * i + 1], g2[2 * i], g2[2 * i + 1], off);
+    mip[i] = static_cast<uint8_t>(m);
+    txy[2 * i] = mcgd::texel_index(uv[2 * i], m);
+    txy[2 * i + 1] = mcgd::texel_index(uv[2 * i + 1], m);
+}
+
+// Counters: [0] lookups [1] hits [2] inserts_won [3] inserts_lost_full [4] lost_race
+__global__ void k_lookup(CacheView c, const mcg_descriptor* d, size_t n, uint8_t* hit, float* rgb,
+                         unsigned long long* counters) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    uint32_t hits = 0, looks = 0;
+    if (i < n) {
+        uint64_t h;
+        uint32_t chk;
+        mcgd::hash_desc(load_desc(d, i), h, chk);
+        const uint64_t cell = mcgd::fast_mod(h, c.n_cells, c.magic);
+        const mcgd::Probe p = mcgd::probe_cell(c, cell * c.n_entries, chk);
+        looks = 1;
+        hits = p.hit;
+        if (hit) hit[i] = p.hit;
+        if (rgb) {
+            const float3 v = p.hit ? mcgd::decode_rgbe(p.payload) : make_float3(0.f, 0.f, 0.f);
+            rgb[3 * i] = v.x;
+            rgb[3 * i + 1] = v.y;
+            rgb[3 * i + 2] = v.z;
+        }
+    }
+    mcgd::warp_add(counters + 0, looks);
+    mcgd::warp_add(counters + 1, hits);
+}
+
+// Concurrent update(): scan, then a single CAS from zero (cache.cpp:94-119).
+__global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb, size_t n,
+                         uint8_t* outcome, uint64_t* slot_out, uint64_t* packed_out,
+                         unsigned long long* counters) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    uint32_t won = 0, full = 0, lost = 0;
+    if (i < n) {
+        uint64_t h;
+        uint32_t chk;
+        mcgd::hash_desc(load_desc(d, i), h, chk);
+        const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
+        const mcgd::Probe p = mcgd::probe_cell(c, base, chk);
+        int res;
+        uint64_t slot = ~0ull, packed = 0;
+        if (p.hit) {
+            res = MCG_INSERT_ALREADY_PRESENT;
+            slot = base + p.where;
+            packed = (static_cast<uint64_t>(chk) << 32) | p.payload;
+        } else {
+            const uint32_t payload = mcgd::encode_rgbe(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+            res = mcgd::insert_at(c, base, p.where, chk, payload);
+            if (res != MCG_INSERT_CELL_FULL) {
+                slot = base + p.where;
+                packed = (static_cast<uint64_t>(chk) << 32) | payload;
+            }
+        }
+        won = res == MCG_INSERT_WON;
+        full = res == MCG_INSERT_CELL_FULL;
+        lost = res == MCG_INSERT_LOST_RACE;
+        if (outcome) outcome[i] = static_cast<uint8_t>(res);
+        if (slot_out) slot_out[i] = slot;
+        if (packed_out) packed_out[i] = packed;
+    }
+    mcgd::warp_add(counters + 2, won);
+    mcgd::warp_add(counters + 3, full);
+    mcgd::warp_add(counters + 4, lost);
+}
+
+// Builds sortable records for an ordered batch: key = cell << ob | index.
+__global__ void k_prepare_ordered(CacheView c, const mcg_descriptor* d, const float* rgb, size_t n,
+                                  int ob, unsigned long long* keys, unsigned long long* vals) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    uint64_t h;
+    uint32_t chk;
+    mcgd::hash_desc(load_desc(d, i), h, chk);
+    const uint64_t cell = mcgd::fast_mod(h, c.n_cells, c.magic);
+    keys[i] = (cell << ob) | i;
+    vals[i] = (static_cast<unsigned long long>(chk) << 32) |
+              mcgd::encode_rgbe(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+}
+
+// One thread per cell segment of the sorted records applies them in order
+// with update() semantics; a single writer per cell, so no atomics.
+__global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
+                                const unsigned long long* vals, size_t n, int ob, uint8_t* outcome,
+                                uint64_t* slot_out, uint64_t* packed_out,
+                                unsigned long long* counters) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    uint32_t won = 0, full = 0;
+    if (i < n) {
+        const uint64_t cell = keys[i] >> ob;
+        if (i == 0 || (keys[i - 1] >> ob) != cell) {
+            uint64_t* words = c.slots + cell * c.n_entries;
+            const unsigned long long omask = ob >= 64 ? ~0ull : ((1ull << ob) - 1ull);
+            for (size_t j = i; j < n && (keys[j] >> ob) == cell; ++j) {
+                const uint32_t chk = static_cast<uint32_t>(vals[j] >> 32);
+                const unsigned long long packed = vals[j];
+                int res = MCG_INSERT_CELL_FULL;
+                uint64_t slot = ~0ull, pk = 0;
+                for (uint32_t s = 0; s < c.n_entries; ++s) {
+                    const uint64_t cur = words[s];
+                    if (static_cast<uint32_t>(cur >> 32) == chk) {
+                        res = MCG_INSERT_ALREADY_PRESENT;
+                        slot = cell * c.n_entries + s;
+                        pk = cur;
+                        break;
+                    }
+                    if (cur == 0ull) {
+                        words[s] = packed;
+                        res = MCG_INSERT_WON;
+                        slot = cell * c.n_entries + s;
+                        pk = packed;
+                        break;
+                    }
+                }
+                won += res == MCG_INSERT_WON;
+                full += res == MCG_INSERT_CELL_FULL;
+                const size_t idx = keys[j] & omask;
+                if (outcome) outcome[idx] = static_cast<uint8_t>(res);
+                if (slot_out) slot_out[idx] = slot;
+                if (packed_out) packed_out[idx] = pk;
+            }
+        }
+    }
+    mcgd::warp_add(counters + 2, won);
+    mcgd::warp_add(counters + 3, full);
+}
+
+__global__ void k_occupied(const uint64_t* slots, uint64_t n, unsigned long long* out) {
+    uint32_t cnt = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        cnt += slots[i] != 0ull;
+    }
+    mcgd::warp_add(out, cnt);
+}
+
+// Probe microbenchmark: descriptors are generated in registers
+// (mat < 8, node < 256, mip <= 16, texels uniform in 2^mip) so the kernel's
+// DRAM traffic is the table's alone.
+__device__ __forceinline__ Desc bench_desc(uint64_t seed, uint64_t i) {
+    const uint64_t h = mcgd::mix64(seed + 0x9e3779b97f4a7c15ull * (i + 1));
+    const uint64_t h2 = mcgd::mix64(h ^ 0x5851f42d4c957f2dull);
+    const uint32_t mip = static_cast<uint32_t>((h >> 11) % 17u);
+    const uint32_t mask = (1u << mip) - 1u;
+    return Desc{static_cast<uint32_t>(h & 7u), static_cast<uint32_t>((h >> 3) & 255u),
+                static_cast<uint32_t>(h2) & mask, static_cast<uint32_t>(h2 >> 32) & mask, mip};
+}
+
+__global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, uint64_t seed,
+                                                     int phase, unsigned long long* counters) {
+    uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t h;
+        uint32_t chk;
+        mcgd::hash_desc(bench_desc(seed, i), h, chk);
+        const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
+        const mcgd::Probe p = mcgd::probe_cell(c, base, chk);
+        const bool insert = phase == 0 || (phase == 2 && (i & 1u));
+        if (!insert) {
+            ++looks;
+            hits += p.hit;
+        } else {
+            ++inserts;
+            if (!p.hit) {
+                const int r = mcgd::insert_at(c, base, p.where, chk,
+                                              static_cast<uint32_t>(h) | 0x80000000u);
+                won += r == MCG_INSERT_WON;
+                full += r == MCG_INSERT_CELL_FULL;
+            }
+        }
+    }
+    mcgd::warp_add(counters + 0, looks);
+    mcgd::warp_add(counters + 1, hits);
+    mcgd::warp_add(counters + 2, won);
+    mcgd::warp_add(counters + 3, full);
+    mcgd::warp_add(counters + 5, inserts);
+}
+
+// Per-point VM execution for mcg_execute_batch: every lane runs the same slot.
+template <bool kDeferred>
+__global__ void k_execute(mcgd::SceneView S, CacheView C, int cache_on, int mip_offset,
+                          uint32_t slot, const float* sp, size_t n, int max_stack, float* values,
+                          uint32_t* nodes, uint32_t* instrs, mcgd::StoreQueue q,
+                          unsigned long long* counters) {
+    extern __shared__ float smem[];
+    __shared__ uint8_t s_perm[256];
+    mcgd::stage_perm(s_perm);
+    __syncthreads();
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned grp = __ballot_sync(mcgd::kFull, valid);
+    if (!valid) return;
+    mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
+                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
+    const float* p = sp + 15 * i;
+    const mcgd::ShadeIn in{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8],
+                           p[9], p[10], p[11], p[12], p[13], p[14]};
+    mcgd::VmCounters cnt;
+    const mcgd::VmResult r = mcgd::run_program<kDeferred>(
+        S, C, cache_on != 0, mip_offset, slot, in, grp, st, s_perm,
+        static_cast<uint32_t>(i) << 6, q, cnt);
+    values[4 * i] = r.value.x;
+    values[4 * i + 1] = r.scalar ? r.value.x : r.value.y;
+    values[4 * i + 2] = r.scalar ? r.value.x : r.value.z;
+    values[4 * i + 3] = __uint_as_float(r.scalar ? 1u : 0u);
+    nodes[i] = cnt.hits;
+    instrs[i] = cnt.instrs;
+    mcgd::warp_add(counters + 0, cnt.lookups);
+    mcgd::warp_add(counters + 1, cnt.hits);
+    mcgd::warp_add(counters + 2, cnt.won);
+    mcgd::warp_add(counters + 3, cnt.full);
+}
+
+}  // namespace
+
+namespace mcg {
+
+void apply_ordered(mcg_ctx* ctx, mcg_cache* cache, const unsigned long long* keys,
+                   const unsigned long long* vals, size_t n, int order_bits, uint8_t* d_outcome,
+                   uint64_t* d_slot, uint64_t* d_packed, unsigned long long* d_stats) {
+    if (n == 0) return;
+    LaunchScope ls(ctx, "apply_ordered", static_cast<double>(n) * 16.0);
+    k_apply_ordered<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), keys, vals, n,
+                                                                order_bits, d_outcome, d_slot,
+                                                                d_packed, d_stats);
+    ls.done();
+}
+
+}  // namespace mcg
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+namespace {
+
+template <typename T>
+T* dev_upload(mcg_ctx* ctx, DevMem& m, const T* host, size_t n) {
+    m.ensure(std::max<size_t>(n * sizeof(T), 16));
+    if (n) cuda_check(cudaMemcpyAsync(m.p, host, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    return m.as<T>();
+}
+
+template <typename T>
+void dev_download(mcg_ctx* ctx, T* host, const void* dev, size_t n) {
+    if (n && host) cuda_check(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+}
+
+void need(bool ok, const char* msg) {
+    if (!ok) fail(MCG_ERR_INVALID_ARGUMENT, msg);
+}
+
+void sync(mcg_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); }
+
+}  // namespace
+
+extern "C" {
+
+mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, "null out");
+        int count = 0;
+        cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        if (count == 0) fail(MCG_ERR_NO_DEVICE, "no CUDA device");
+        const int dev = opt ? opt->device : 0;
+        need(dev >= 0 && dev < count, "device ordinal out of range");
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+        auto* ctx = new mcg_ctx;
+        ctx->device = dev;
+        ctx->profile = opt && opt->profile;
+        if (opt && opt->stream) {
+            ctx->stream = static_cast<cudaStream_t>(opt->stream);
+        } else {
+            cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) {
+                delete ctx;
+                cuda_check(e, "cudaStreamCreate");
+            }
+            ctx->own_stream = true;
+        }
+        ctx->stats_mem.ensure(4096);
+        *out = ctx;
+    });
+}
+
+mcg_status mcg_destroy(mcg_ctx* ctx) {
+    if (!ctx) return MCG_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_cache) mcg_cache_destroy(ctx->own_cache);
+    ctx->scene.clear();
+    for (DevMem* m : {&ctx->cub_temp, &ctx->scratch_a, &ctx->scratch_b, &ctx->scratch_c,
+                      &ctx->scratch_d, &ctx->scratch_e, &ctx->path_mem, &ctx->queue_mem,
+                      &ctx->stats_mem}) {
+        m->release();
+    }
+    for (auto& r : ctx->pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MCG_OK;
+}
+
+mcg_status mcg_synchronize(mcg_ctx* ctx) {
+    return guarded([&] {
+        need(ctx != nullptr, "null ctx");
+        sync(ctx);
+        resolve_events(ctx);
+    });
+}
+
+void* mcg_stream(mcg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+mcg_status mcg_kernel_times(mcg_ctx* ctx, mcg_kernel_time* out, int32_t cap, int32_t* n_out) {
+    return guarded([&] {
+        need(ctx != nullptr, "null ctx");
+        sync(ctx);
+        resolve_events(ctx);
+        int32_t k = 0;
+        for (const auto& [name, acc] : ctx->times) {
+            if (out && k < cap) {
+                std::memset(&out[k], 0, sizeof(mcg_kernel_time));
+                std::snprintf(out[k].name, sizeof(out[k].name), "%s", name.c_str());
+                out[k].launches = acc.launches;
+                out[k].ms = acc.ms;
+                out[k].algorithmic_bytes = acc.bytes;
+            }
+            ++k;
+        }
+        if (n_out) *n_out = k;
+    });
+}
+
+mcg_status mcg_kernel_times_reset(mcg_ctx* ctx) {
+    return guarded([&] {
+        need(ctx != nullptr, "null ctx");
+        sync(ctx);
+        resolve_events(ctx);
+        ctx->times.clear();
+        ctx->launches = 0;
+    });
+}
+
+uint64_t mcg_launch_count(mcg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+mcg_status mcg_hash_batch(mcg_ctx* ctx, const mcg_descriptor* d, size_t n, uint64_t* cell_hash,
+                          uint32_t* check) {
+    return guarded([&] {
+        need(ctx && d && cell_hash && check, "null argument");
+        if (!n) return;
+        auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
+        ctx->scratch_b.ensure(n * 8);
+        ctx->scratch_c.ensure(n * 4);
+        LaunchScope ls(ctx, "hash", n * 20.0 + n * 12.0);
+        k_hash<<<grid_for(n, 256), 256, 0, ctx->stream>>>(dd, n, ctx->scratch_b.as<uint64_t>(),
+                                                         ctx->scratch_c.as<uint32_t>());
+        ls.done();
+        dev_download(ctx, cell_hash, ctx->scratch_b.p, n);
+        dev_download(ctx, check, ctx->scratch_c.p, n);
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_encode_batch(mcg_ctx* ctx, const float* rgb, size_t n, uint32_t* packed) {
+    return guarded([&] {
+        need(ctx && rgb && packed, "null argument");
+        if (!n) return;
+        auto* d = dev_upload(ctx, ctx->scratch_a, rgb, 3 * n);
+        ctx->scratch_b.ensure(n * 4);
+        LaunchScope ls(ctx, "encode", n * 16.0);
+        k_encode<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d, n, ctx->scratch_b.as<uint32_t>());
+        ls.done();
+        dev_download(ctx, packed, ctx->scratch_b.p, n);
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_decode_batch(mcg_ctx* ctx, const uint32_t* packed, size_t n, float* rgb) {
+    return guarded([&] {
+        need(ctx && rgb && packed, "null argument");
+        if (!n) return;
+        auto* d = dev_upload(ctx, ctx->scratch_a, packed, n);
+        ctx->scratch_b.ensure(n * 12);
+        LaunchScope ls(ctx, "decode", n * 16.0);
+        k_decode<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d, n, ctx->scratch_b.as<float>());
+        ls.done();
+        dev_download(ctx, rgb, ctx->scratch_b.p, 3 * n);
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_mip_texel_batch(mcg_ctx* ctx, const float* uv, const float* g1, const float* g2,
+                               size_t n, int32_t mip_offset, uint8_t* mip, uint32_t* texel_xy) {
+    return guarded([&] {
+        need(ctx && uv && g1 && g2 && mip && texel_xy, "null argument");
+        if (!n) return;
+        auto* duv = dev_upload(ctx, ctx->scratch_a, uv, 2 * n);
+        auto* dg1 = dev_upload(ctx, ctx->scratch_b, g1, 2 * n);
+        auto* dg2 = dev_upload(ctx, ctx->scratch_c, g2, 2 * n);
+        ctx->scratch_d.ensure(n);
+        ctx->scratch_e.ensure(n * 8);
+        LaunchScope ls(ctx, "mip_texel", n * 33.0);
+        k_mip_texel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(duv, dg1, dg2, n, mip_offset,
+                                                              ctx->scratch_d.as<uint8_t>(),
+                                                              ctx->scratch_e.as<uint32_t>());
+        ls.done();
+        dev_download(ctx, mip, ctx->scratch_d.p, n);
+        dev_download(ctx, texel_xy, ctx->scratch_e.p, 2 * n);
+        sync(ctx);
+    });
+}
+
+// ---- cache -----------------------------------------------------------------
+
+mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, mcg_cache** out) {
+    return guarded([&] {
+        need(ctx && out, "null argument");
+        if (n_cells == 0 || n_entries == 0) {
+            fail(MCG_ERR_INVALID_ARGUMENT, "cache dimensions must be nonzero");
+        }
+        uint64_t bytes = 0;
+        const mcg_status s = mcg_memory_bytes(n_cells, n_entries, &bytes);
+        if (s != MCG_OK) fail(s, mcg_last_error());
+        if (n_cells >= (1ull << 32)) fail(MCG_ERR_INVALID_ARGUMENT, "n_cells must be < 2^32");
+        auto* c = new mcg_cache;
+        c->ctx = ctx;
+        c->n_cells = n_cells;
+        c->n_entries = n_entries;
+        c->magic = mod_magic(n_cells);
+        cudaError_t e = cudaMalloc(&c->slots, bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
+        if (e != cudaSuccess) {
+            if (c->slots) cudaFree(c->slots);
+            delete c;
+            cuda_check(e, "cudaMalloc(cache)");
+        }
+        cuda_check(cudaMemsetAsync(c->slots, 0, bytes, ctx->stream), "memset cache");
+        cuda_check(cudaMemsetAsync(c->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
+        sync(ctx);
+        *out = c;
+    });
+}
+
+mcg_status mcg_cache_destroy(mcg_cache* cache) {
+    if (!cache) return MCG_OK;
+    cudaStreamSynchronize(cache->ctx->stream);
+    cudaFree(cache->slots);
+    cudaFree(cache->counters);
+    delete cache;
+    return MCG_OK;
+}
+
+mcg_status mcg_cache_clear(mcg_cache* cache) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->n_cells * cache->n_entries * 8,
+                                   cache->ctx->stream), "memset cache");
+        cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
+                                   cache->ctx->stream), "memset counters");
+    });
+}
+
+mcg_status mcg_cache_shape(const mcg_cache* cache, uint64_t* n_cells, uint32_t* n_entries) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        if (n_cells) *n_cells = cache->n_cells;
+        if (n_entries) *n_entries = cache->n_entries;
+    });
+}
+
+uint64_t* mcg_cache_device_slots(mcg_cache* cache) { return cache ? cache->slots : nullptr; }
+
+static void update_device(mcg_cache* cache, const mcg_descriptor* dd, const float* drgb, size_t n,
+                          int32_t mode, uint8_t* d_out, uint64_t* d_slot, uint64_t* d_packed) {
+    mcg_ctx* ctx = cache->ctx;
+    if (!n) return;
+    if (mode == MCG_APPLY_CONCURRENT) {
+        LaunchScope ls(ctx, "cache_update", n * (8.0 * cache->n_entries));
+        k_update<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), dd, drgb, n, d_out,
+                                                           d_slot, d_packed, cache->counters);
+        ls.done();
+        return;
+    }
+    need(mode == MCG_APPLY_ORDERED, "unknown apply mode");
+    const int ob = std::max(1, bits_for(n - 1));
+    const int end_bit = ob + bits_for(cache->n_cells - 1);
+    need(end_bit <= 64, "ordered batch too large for 64-bit keys");
+    ctx->queue_mem.ensure(n * 32);
+    auto* k0 = ctx->queue_mem.as<unsigned long long>();
+    auto* v0 = k0 + n;
+    auto* k1 = k0 + 2 * n;
+    auto* v1 = k0 + 3 * n;
+    {
+        LaunchScope ls(ctx, "prepare_ordered", n * 48.0);
+        k_prepare_ordered<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), dd, drgb, n,
+                                                                    ob, k0, v0);
+        ls.done();
+    }
+    sort_pairs_u64(ctx, k0, k1, v0, v1, n, end_bit);
+    apply_ordered(ctx, cache, k1, v1, n, ob, d_out, d_slot, d_packed, cache->counters);
+}
+
+mcg_status mcg_cache_update_batch(mcg_cache* cache, const mcg_descriptor* d, const float* rgb,
+                                  size_t n, int32_t apply_mode, uint8_t* outcome, uint64_t* slot,
+                                  uint64_t* packed) {
+    return guarded([&] {
+        need(cache && d && rgb, "null argument");
+        if (!n) return;
+        mcg_ctx* ctx = cache->ctx;
+        auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
+        auto* dr = dev_upload(ctx, ctx->scratch_b, rgb, 3 * n);
+        ctx->scratch_c.ensure(n);
+        ctx->scratch_d.ensure(n * 8);
+        ctx->scratch_e.ensure(n * 8);
+        update_device(cache, dd, dr, n, apply_mode, ctx->scratch_c.as<uint8_t>(),
+                      ctx->scratch_d.as<uint64_t>(), ctx->scratch_e.as<uint64_t>());
+        dev_download(ctx, outcome, ctx->scratch_c.p, n);
+        dev_download(ctx, slot, ctx->scratch_d.p, n);
+        dev_download(ctx, packed, ctx->scratch_e.p, n);
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_cache_update_device(mcg_cache* cache, const mcg_descriptor* d_desc,
+                                   const float* d_rgb, size_t n, int32_t apply_mode,
+                                   uint8_t* d_outcome) {
+    return guarded([&] {
+        need(cache && d_desc && d_rgb, "null argument");
+        update_device(cache, d_desc, d_rgb, n, apply_mode, d_outcome, nullptr, nullptr);
+    });
+}
+
+mcg_status mcg_cache_lookup_batch(mcg_cache* cache, const mcg_descriptor* d, size_t n,
+                                  uint8_t* hit, float* rgb) {
+    return guarded([&] {
+        need(cache && d && hit && rgb, "null argument");
+        if (!n) return;
+        mcg_ctx* ctx = cache->ctx;
+        auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
+        ctx->scratch_b.ensure(n);
+        ctx->scratch_c.ensure(n * 12);
+        LaunchScope ls(ctx, "cache_lookup", n * (8.0 * cache->n_entries));
+        k_lookup<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), dd, n,
+                                                           ctx->scratch_b.as<uint8_t>(),
+                                                           ctx->scratch_c.as<float>(), cache->counters);
+        ls.done();
+        dev_download(ctx, hit, ctx->scratch_b.p, n);
+        dev_download(ctx, rgb, ctx->scratch_c.p, 3 * n);
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_cache_lookup_device(mcg_cache* cache, const mcg_descriptor* d_desc, size_t n,
+                                   uint8_t* d_hit, float* d_rgb) {
+    return guarded([&] {
+        need(cache && d_desc, "null argument");
+        if (!n) return;
+        mcg_ctx* ctx = cache->ctx;
+        LaunchScope ls(ctx, "cache_lookup", n * (8.0 * cache->n_entries));
+        k_lookup<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), d_desc, n, d_hit,
+                                                           d_rgb, cache->counters);
+        ls.done();
+    });
+}
+
+mcg_status mcg_cache_read_slots(mcg_cache* cache, uint64_t first, size_t n, uint64_t* words) {
+    return guarded([&] {
+        need(cache && words, "null argument");
+        need(first + n <= cache->n_cells * cache->n_entries, "slot range out of bounds");
+        if (!n) return;
+        dev_download(cache->ctx, words, cache->slots + first, n);
+        sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
+    return guarded([&] {
+        need(cache && occupied, "null argument");
+        mcg_ctx* ctx = cache->ctx;
+        cuda_check(cudaMemsetAsync(cache->counters + 7, 0, 8, ctx->stream), "memset");
+        const uint64_t n = cache->n_cells * cache->n_entries;
+        LaunchScope ls(ctx, "occupied", n * 8.0);
+        k_occupied<<<148 * 8, 256, 0, ctx->stream>>>(cache->slots, n, cache->counters + 7);
+        ls.done();
+        unsigned long long v = 0;
+        dev_download(ctx, &v, cache->counters + 7, 1);
+        sync(ctx);
+        *occupied = v;
+    });
+}
+
+mcg_status mcg_cache_counters_get(mcg_cache* cache, mcg_cache_counters* out) {
+    return guarded([&] {
+        need(cache && out, "null argument");
+        unsigned long long v[8];
+        dev_download(cache->ctx, v, cache->counters, 8);
+        sync(cache->ctx);
+        out->lookups = v[0];
+        out->hits = v[1];
+        out->inserts_won = v[2];
+        out->inserts_lost_full = v[3];
+    });
+}
+
+mcg_status mcg_cache_counters_reset(mcg_cache* cache) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
+                                   cache->ctx->stream), "memset");
+        sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_cache_dump(mcg_cache* cache, const char* path) {
+    return guarded([&] {
+        need(cache && path, "null argument");
+        std::ofstream out(path, std::ios::binary);
+        if (!out) fail(MCG_ERR_IO, std::string("cannot open cache dump for writing: ") + path);
+        const uint64_t header[2] = {cache->n_cells, cache->n_entries};
+        out.write(reinterpret_cast<const char*>(header), sizeof(header));
+        const uint64_t total = cache->n_cells * cache->n_entries;
+        const size_t chunk = 1u << 24;
+        std::vector<uint64_t> buf(std::min<uint64_t>(total, chunk));
+        for (uint64_t off = 0; off < total; off += chunk) {
+            const size_t n = static_cast<size_t>(std::min<uint64_t>(chunk, total - off));
+            dev_download(cache->ctx, buf.data(), cache->slots + off, n);
+            sync(cache->ctx);
+            out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(n * 8));
+        }
+        if (!out) fail(MCG_ERR_IO, std::string("short write on cache dump: ") + path);
+    });
+}
+
+mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t phase,
+                           int32_t iters, double* ms_out, double* bytes_out) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        need(phase >= 0 && phase <= 2, "phase must be 0, 1 or 2");
+        mcg_ctx* ctx = cache->ctx;
+        cudaEvent_t a = take_event(ctx), b = take_event(ctx);
+        cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
+        cudaEventRecord(a, ctx->stream);
+        const int reps = std::max(1, iters);
+        for (int r = 0; r < reps; ++r) {
+            LaunchScope ls(ctx, "probe_bench", 0.0);
+            k_probe_bench<<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, phase,
+                                                           cache->counters);
+            ls.done();
+        }
+        cudaEventRecord(b, ctx->stream);
+        cuda_check(cudaEventSynchronize(b), "probe bench");
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        ctx->event_pool.push_back(a);
+        ctx->event_pool.push_back(b);
+        unsigned long long v[8];
+        dev_download(ctx, v, cache->counters, 8);
+        sync(ctx);
+        // 8*Ne bytes per lookup and per insert attempt, +8 per won CAS.
+        const double cellb = 8.0 * cache->n_entries;
+        if (ms_out) *ms_out = ms / reps;
+        if (bytes_out) *bytes_out = (static_cast<double>(v[0]) * cellb + static_cast<double>(v[5]) * cellb +
+                                     static_cast<double>(v[2]) * 8.0) / reps;
+    });
+}
+
+// ---- scene upload & per-point execution -----------------------------------
+
+mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
+    return guarded([&] {
+        need(ctx && scene, "null argument");
+        mcg_flat_scene f;
+        const mcg_status s = mcg_scene_flat(scene, &f);
+        if (s != MCG_OK) fail(s, mcg_last_error());
+        DeviceScene& D = ctx->scene;
+        D.clear();
+        D.bufs.resize(16);
+        auto up = [&](int k, const void* p, size_t bytes) -> const void* {
+            D.bufs[k].ensure(std::max<size_t>(bytes, 16));
+            if (bytes) cuda_check(cudaMemcpyAsync(D.bufs[k].p, p, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D scene");
+            return D.bufs[k].p;
+        };
+        mcgd::SceneView& v = D.view;
+        v.prim_geom = static_cast<const float4*>(up(0, f.prim_geom, f.n_prims * 48ull));
+        v.prim_uv = static_cast<const float2*>(up(1, f.prim_uv, f.n_prims * 24ull));
+        v.prim_info = static_cast<const uint32_t*>(up(2, f.prim_info, f.n_prims * 4ull));
+        v.nodes = static_cast<const float4*>(up(3, f.nodes, f.n_nodes * sizeof(mcg_bvh_node)));
+        v.n_nodes = f.n_nodes;
+        v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
+        v.n_plights = f.n_point_lights;
+        v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));
+        v.n_rlights = f.n_rect_lights;
+        v.programs = static_cast<const mcg_program*>(up(6, f.programs, f.n_programs * sizeof(mcg_program)));
+        v.n_programs = f.n_programs;
+        v.code = static_cast<const mcg_insn*>(up(7, f.code, f.n_code * sizeof(mcg_insn)));
+        v.consts = static_cast<const mcg_const*>(up(8, f.consts, f.n_consts * sizeof(mcg_const)));
+        v.noise = static_cast<const mcg_noise*>(up(9, f.noise, f.n_noise * sizeof(mcg_noise)));
+        v.ramps = static_cast<const mcg_ramp*>(up(10, f.ramps, f.n_ramps * sizeof(mcg_ramp)));
+        v.stops = static_cast<const mcg_ramp_stop*>(up(11, f.ramp_stops, f.n_ramp_stops * sizeof(mcg_ramp_stop)));
+        v.textures = static_cast<const mcg_texture*>(up(12, f.textures, f.n_textures * sizeof(mcg_texture)));
+        v.texels = static_cast<const float4*>(up(13, f.texels, f.n_texels * 16ull));
+        std::memcpy(v.env, f.env, sizeof(v.env));
+        D.max_stack = 1;
+        D.max_cache_points = 0;
+        for (uint32_t i = 0; i < f.n_programs; ++i) {
+            D.max_stack = std::max(D.max_stack, f.programs[i].max_stack);
+            D.max_cache_points = std::max(D.max_cache_points, f.programs[i].cache_point_count);
+        }
+        D.cam = f;
+        D.cam.prim_geom = nullptr;  // only camera/env fields are used later
+        D.loaded = true;
+        sync(ctx);
+    });
+}
+
+mcg_status mcg_execute_batch(mcg_ctx* ctx, uint32_t slot, const float* sp, size_t n,
+                             mcg_cache* cache, int32_t cache_mode, int32_t mip_offset,
+                             float* values, uint32_t* nodes_found, uint32_t* instructions) {
+    return guarded([&] {
+        need(ctx && sp && values && nodes_found && instructions, "null argument");
+        need(ctx->scene.loaded, "no scene uploaded");
+        need(slot < ctx->scene.view.n_programs, "material slot out of range");
+        if (!n) return;
+        const bool cache_on = cache != nullptr && cache_mode != MCG_CACHE_OFF;
+        const bool deferred = cache_on && cache_mode == MCG_CACHE_DETERMINISTIC;
+        auto* dsp = dev_upload(ctx, ctx->scratch_a, sp, 15 * n);
+        ctx->scratch_b.ensure(n * 16);
+        ctx->scratch_c.ensure(n * 4);
+        ctx->scratch_d.ensure(n * 4);
+        const int block = 128;
+        const int max_stack = static_cast<int>(ctx->scene.max_stack);
+        const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
+        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1};
+        unsigned long long* counters = cache ? cache->counters : ctx->stats_mem.as<unsigned long long>();
+        mcgd::StoreQueue q{nullptr, nullptr, nullptr, 0};
+        const uint64_t cap = deferred ? n * std::max<uint32_t>(1, ctx->scene.max_cache_points) : 0;
+        if (deferred) {
+            ctx->queue_mem.ensure(cap * 32 + 64);
+            q.keys = ctx->queue_mem.as<unsigned long long>();
+            q.vals = q.keys + cap;
+            q.count = reinterpret_cast<unsigned int*>(q.keys + 4 * cap);
+            q.capacity = static_cast<unsigned>(cap);
+            cuda_check(cudaMemsetAsync(q.count, 0, 4, ctx->stream), "memset");
+        }
+        {
+            LaunchScope ls(ctx, "execute", 0.0);
+            if (deferred) {
+                cudaFuncSetAttribute(k_execute<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k_execute<true><<<grid_for(n, block), block, smem, ctx->stream>>>(
+                    ctx->scene.view, cv, 1, mip_offset, slot, dsp, n, max_stack,
+                    ctx->scratch_b.as<float>(), ctx->scratch_c.as<uint32_t>(),
+                    ctx->scratch_d.as<uint32_t>(), q, counters);
+            } else {
+                cudaFuncSetAttribute(k_execute<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k_execute<false><<<grid_for(n, block), block, smem, ctx->stream>>>(
+                    ctx->scene.view, cv, cache_on ? 1 : 0, mip_offset, slot, dsp, n, max_stack,
+                    ctx->scratch_b.as<float>(), ctx->scratch_c.as<uint32_t>(),
+                    ctx->scratch_d.as<uint32_t>(), q, counters);
+            }
+            ls.done();
+        }
+        if (deferred) {
+            unsigned int count = 0;
+            dev_download(ctx, &count, q.count, 1);
+            sync(ctx);
+            need(count <= cap, "store queue overflow");
+            const int ob = std::max(1, bits_for((static_cast<uint64_t>(n) << 6) - 1));
+            // Re-key (cell << 32 | order) -> (cell << ob | order) is implicit:
+            // order keys already fit in the low 32 bits, cells in the high 32.
+            auto* k1 = q.keys + 2 * cap;
+            auto* v1 = q.keys + 3 * cap;
+            sort_pairs_u64(ctx, q.keys, k1, q.vals, v1, count, 64);
+            apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, cache->counters);
+            (void)ob;
+        }
+        dev_download(ctx, values, ctx->scratch_b.p, 4 * n);
+        dev_download(ctx, nodes_found, ctx->scratch_c.p, n);
+        dev_download(ctx, instructions, ctx->scratch_d.p, n);
+        sync(ctx);
+    });
+}
+
+}  // extern "C"
