@@ -1,0 +1,209 @@
+"""CUDA path vs the CPU oracle, through the C ABI (libmcg.so), on a B200.
+
+Bar (BASELINE.json north_star): bit-exact for integer work (hashes, cell and
+entry indices, hit/miss decisions, per-pixel hit counts, table contents) and,
+because the device evaluates the same IEEE operations in the same order
+(--fmad=false), bit-exact for the floating-point values as well; the
+tolerances the north star allows (1e-5 relative) are asserted on top where
+the quantity is floating point."""
+import numpy as np
+import pytest
+
+from paper_2305_07238_b200 import (CACHE_CONCURRENT, CACHE_DETERMINISTIC, MaterialCache,
+                                   RenderConfig, audit_dump, descriptors, load_scene, render,
+                                   scenes)
+
+import _oracle
+import make_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view({4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
+
+
+def test_descriptor_pipeline_matches_golden(ctx, golden):
+    R = make_golden.random_inputs()
+    Z = golden["npz"]
+    cell, chk = ctx.hash_batch(R["desc"])
+    np.testing.assert_array_equal(cell, Z["cell"])
+    np.testing.assert_array_equal(chk, Z["check"])
+    enc = ctx.encode_batch(R["rgb"])
+    np.testing.assert_array_equal(enc, Z["enc"])
+    np.testing.assert_array_equal(bits(ctx.decode_batch(enc)), bits(Z["dec"]))
+    for off, mk, tk in ((0, "mip", "txy"), (2, "mip2", "txy2")):
+        mip, txy = ctx.mip_texel_batch(R["uv"], R["g1"], R["g2"], off)
+        np.testing.assert_array_equal(mip, Z[mk])
+        np.testing.assert_array_equal(txy, Z[tk])
+
+
+def test_descriptor_pipeline_matches_oracle_1e6(ctx, oracle):
+    r = np.random.default_rng(1)
+    n = 1 << 20
+    d = descriptors(r.integers(0, 64, n), r.integers(0, 1 << 16, n), r.integers(0, 25, n),
+                    r.integers(0, 1 << 24, n), r.integers(0, 1 << 24, n))
+    c1, k1 = ctx.hash_batch(d)
+    c2, k2 = oracle.hash(d)
+    np.testing.assert_array_equal(c1, c2)
+    np.testing.assert_array_equal(k1, k2)
+    rgb = (r.standard_normal((n, 3)) * np.exp(r.uniform(-30, 30, (n, 1)))).astype(np.float32)
+    rgb[::97] = np.nan
+    rgb[::89, 1] = np.inf
+    np.testing.assert_array_equal(ctx.encode_batch(rgb), oracle.encode(rgb))
+    words = r.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    np.testing.assert_array_equal(bits(ctx.decode_batch(words)), bits(oracle.decode(words)))
+    uv = r.uniform(-1e3, 1e3, (n, 2)).astype(np.float32)
+    g1 = (np.exp(r.uniform(-40, 3, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
+    g2 = (np.exp(r.uniform(-40, 3, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
+    g1[::101] = 0
+    for off in (-3, 0, 5):
+        m1, t1 = ctx.mip_texel_batch(uv, g1, g2, off)
+        m2, t2 = oracle.mip_texel(uv, g1, g2, off)
+        np.testing.assert_array_equal(m1, m2)
+        np.testing.assert_array_equal(t1, t2)
+
+
+def _desc_stream(n, seed, distinct):
+    r = np.random.default_rng(seed)
+    k = r.integers(0, distinct, n)
+    d = descriptors(k % 8, (k // 8) % 300, k % 17, k * 7919 % (1 << 16), k // 3)
+    rgb = r.uniform(0, 4, (n, 3)).astype(np.float32)
+    return d, rgb
+
+
+@pytest.mark.parametrize("nc,ne", [(997, 4), (1000, 10), (1 << 12, 3)])
+def test_ordered_updates_match_oracle_table(ctx, oracle, nc, ne):
+    d, rgb = _desc_stream(200_000, nc + ne, 20_000)
+    cache = MaterialCache(nc, ne, ctx)
+    o1, s1, p1 = cache.update_batch(d, rgb, ordered=True)
+    oc = oracle.cache_new(nc, ne)
+    o2, s2, p2 = oracle.cache_update(oc, d, rgb)
+    np.testing.assert_array_equal(o1, o2)
+    np.testing.assert_array_equal(s1, s2)
+    np.testing.assert_array_equal(p1, p2)
+    np.testing.assert_array_equal(cache.slot_words(), oracle.cache_slots(oc, nc, ne))
+    hit1, v1 = cache.lookup_batch(d)
+    hit2, v2 = oracle.cache_lookup(oc, d)
+    np.testing.assert_array_equal(hit1, hit2)
+    np.testing.assert_array_equal(bits(v1), bits(v2))
+    assert cache.occupied_slots() == int(oracle.cache_counters(oc)[4])
+    oracle.cache_free(oc)
+
+
+def test_concurrent_updates_keep_table_invariants(ctx, tmp_path):
+    """First-insert-wins under contention: single CAS
+    from zero, no duplicate check-hash in a cell, occupied slots form a prefix,
+    every stored word is the encoding of a value some update offered."""
+    nc, ne = 10_000, 4
+    d, rgb = _desc_stream(1_000_000, 3, 200_000)
+    cache = MaterialCache(nc, ne, ctx)
+    o, s, p = cache.update_batch(d, rgb, ordered=False)
+    words = cache.slot_words().reshape(nc, ne)
+    occupied = words != 0
+    assert (occupied[:, 1:] <= occupied[:, :-1]).all(), "occupied slots must form a prefix"
+    path = str(tmp_path / "dump.bin")
+    cache.dump(path)
+    rep = audit_dump(path)
+    assert rep.clean, rep.problem
+    assert rep.occupied == int(occupied.sum()) == int((o == 0).sum())
+    cnt = cache.counters()
+    assert cnt["inserts_won"] == int((o == 0).sum())
+    assert cnt["inserts_lost_full"] == int((o == 3).sum())
+    won = o == 0
+    np.testing.assert_array_equal(np.sort(p[won]), np.sort(words[occupied]))
+
+
+def test_execute_cache_off_matches_oracle(ctx, oracle, scene_dir):
+    path = scenes.materials_only_scene(scene_dir + "/vm_off", 40, seed=5, libm_ops=True)
+    s = load_scene(path)
+    ctx.upload(s)
+    sp = scenes.random_shading_points(4096, 21)
+    for slot in range(s.n_materials):
+        v1, n1, i1 = ctx.execute_batch(slot, sp)
+        v2, n2, i2 = oracle.execute(s.flat, slot, sp)
+        np.testing.assert_array_equal(bits(v1), bits(v2), err_msg=f"slot {slot}")
+        np.testing.assert_array_equal(i1, i2)
+        assert (n1 == 0).all()
+
+
+def test_execute_deterministic_cache_matches_oracle(ctx, oracle, scene_dir):
+    path = scenes.materials_only_scene(scene_dir + "/vm_det", 12, seed=6, libm_ops=True)
+    s = load_scene(path)
+    ctx.upload(s)
+    sp = scenes.random_shading_points(8192, 22, uv_range=1.0)
+    sp[:, 11:15] = np.float32(0.03)
+    for slot in range(s.n_materials):
+        nc, ne = 2003, 4
+        cache = MaterialCache(nc, ne, ctx)
+        oc = oracle.cache_new(nc, ne)
+        for rnd in range(3):
+            v1, n1, i1 = ctx.execute_batch(slot, sp, cache, CACHE_DETERMINISTIC)
+            v2, n2, i2 = oracle.execute(s.flat, slot, sp, cache=oc, deferred=True)
+            np.testing.assert_array_equal(n1, n2, err_msg=f"slot {slot} round {rnd}")
+            np.testing.assert_array_equal(i1, i2)
+            np.testing.assert_array_equal(bits(v1), bits(v2))
+        np.testing.assert_array_equal(cache.slot_words(), oracle.cache_slots(oc, nc, ne))
+        oracle.cache_free(oc)
+        cache.close()
+
+
+def _params(w, h, spp, mode, spp_pass, nc=997, ne=4, mip=0):
+    return _oracle.RenderParamsC(w, h, spp, 4, mode, mip, nc, ne, 0, 1, 0.2, 16, 0, 1, 0, 0, spp_pass)
+
+
+@pytest.mark.parametrize("kind,libm", [("cornell", False), ("classroom", True), ("monster", True)])
+def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm):
+    w, h, spp = 64, 48, 4
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=libm),
+                              f"{scene_dir}/r_{kind}")
+    s = load_scene(path)
+    res = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=False), ctx=ctx)
+    rad, nodes, samples, hps, st = oracle.render(s.flat, _params(w, h, spp, 0, 1))
+    np.testing.assert_array_equal(bits(res.frame.radiance), bits(rad))
+    np.testing.assert_array_equal(res.frame.samples, samples)
+    assert res.stats.instructions_executed == st.instructions_executed
+    assert res.stats.shading_points == st.shading_points
+
+
+@pytest.mark.parametrize("kind,k", [("cornell", 1), ("junkshop", 2), ("italianflat", 3)])
+def test_render_deterministic_matches_oracle(ctx, oracle, scene_dir, kind, k):
+    w, h, spp, nc, ne = 64, 48, 6, 4099, 4
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=True),
+                              f"{scene_dir}/d_{kind}")
+    s = load_scene(path)
+    cache = MaterialCache(nc, ne, ctx)
+    cfg = RenderConfig(width=w, height=h, spp=spp, cache_enabled=True, deterministic=True,
+                       n_cells=nc, n_entries=ne, samples_per_pass=k)
+    res = render(s, cfg, external_cache=cache, ctx=ctx)
+    oc = oracle.cache_new(nc, ne)
+    rad, nodes, samples, hps, st = oracle.render(s.flat, _params(w, h, spp, 3, k, nc, ne), cache=oc)
+    # bit-exact hit decisions and per-pixel hit counts, identical table
+    np.testing.assert_array_equal(res.frame.nodes_found, nodes)
+    assert res.stats.hits_per_sample == [int(x) for x in hps]
+    np.testing.assert_array_equal(cache.slot_words(), oracle.cache_slots(oc, nc, ne))
+    assert res.stats.lookups == st.lookups and res.stats.hits == st.hits
+    assert res.stats.inserts_won == st.stores_won
+    # radiance: bit-exact (and therefore within the 1e-5 relative bound)
+    np.testing.assert_array_equal(bits(res.frame.radiance), bits(rad))
+    oracle.cache_free(oc)
+
+
+def test_render_concurrent_rmse_bound(ctx, oracle, scene_dir):
+    """Concurrent mode: RMSE vs the no-cache image within the reference's own
+    cached-vs-uncached RMSE + 1e-4 (north star)."""
+    w, h, spp, nc, ne = 96, 64, 8, 20011, 8
+    path = scenes.build_scene(scenes.SceneSpec("classroom", w, h, tris_per_side=6, libm_ops=True),
+                              f"{scene_dir}/c_classroom")
+    s = load_scene(path)
+    off = render(s, RenderConfig(width=w, height=h, spp=spp), ctx=ctx).frame.radiance_image()
+    conc = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=True, n_cells=nc,
+                                  n_entries=ne), ctx=ctx)
+    oc = oracle.cache_new(nc, ne)
+    rad, *_ = oracle.render(s.flat, _params(w, h, spp, 1, 1, nc, ne), cache=oc)
+    ref_cached = (rad / spp).astype(np.float32)
+    rmse = lambda a, b: float(np.sqrt(np.mean((a.astype(np.float64) - b) ** 2)))
+    assert rmse(conc.frame.radiance_image(), off) <= rmse(ref_cached, off) + 1e-4
+    assert conc.stats.hits > 0
+    oracle.cache_free(oc)
