@@ -1,0 +1,413 @@
+"""Benchmark of the progressive-material-cache hot path (BASELINE.json metric:
+samples/sec at 1920x1080 128spp + cache speed-up + HBM% on probes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one render() of the Classroom-like analogue at 1920x1080x128spp
+with a fresh 1e7 x 10 table (tracer.hpp:67-68; configs[2] of BASELINE.json,
+paper's cache size), concurrent inserts (the paper's single-CAS policy). The
+image is tile-sharded across ranks (torchrun, one process per GPU, NCCL
+reduce of the framebuffers to rank 0 inside each step): total work is fixed,
+so scaling is strong.
+
+Printed JSON line (rank 0):
+  value        samples/s, device-timed (CUDA events on the render stream,
+               max over ranks), inputs resident in HBM
+  e2e          the same metric through the C ABI's host-buffer entry point
+               (mcg_upload_scene + mcg_render with pinned host framebuffers):
+               scene H2D + framebuffer H2D/D2H inside the timed region
+  roofline     dominant kernel's algorithmic bytes / its CUDA-event time vs
+               the measured HBM peak (MEASURED_PEAKS.json)
+  probe_roofline  the cache-probe kernel on the 1e7 x 10 table (HBM-bound)
+  cache_speedup   t(no cache) / t(cache) on the same workload
+  cpu_baseline the reference's own CPU path (oracle/_ref) on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+W, H, SPP = 1920, 1080, 128
+N_CELLS, N_ENTRIES = 10_000_000, 10
+SCENE_KIND = "classroom"
+TRIS_PER_SIDE = 24
+METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def make_scene(tmp: str):
+    from paper_2305_07238_b200 import scenes
+    return scenes.build_scene(scenes.SceneSpec(SCENE_KIND, W, H, tris_per_side=TRIS_PER_SIDE,
+                                               libm_ops=True), os.path.join(tmp, "scene"))
+
+
+# --------------------------------------------------------------------------
+# reference arm: the reference's own CPU path on the host cores
+# --------------------------------------------------------------------------
+
+def cpu_reference_sample(scene_path: str, spp: int = 1, threads: int = 0, cache: bool = True):
+    """Times oracle/_ref's render (reference sources + restated tracer, tile
+    queue over worker threads, shared MaterialCache) on a bounded sample:
+    the full 1920x1080 frame at `spp` samples per pixel."""
+    import _oracle
+    nthreads = threads or os.cpu_count() or 1
+    if _oracle.Ref.available():
+        ref = _oracle.Ref()
+        s = ref.scene_load(scene_path)
+        P = _oracle.RenderParamsC(W, H, spp, 4, 2 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
+                                  0.2, 16, 0, 1, 0, nthreads, 1)
+        t0 = time.perf_counter()
+        *_, st = ref.render(s, P, W, H)
+        dt = time.perf_counter() - t0
+        ref.L.ref_scene_free(s)
+        return {"kind": "reference", "seconds": dt, "samples": W * H * spp, "cores": nthreads,
+                "hits": int(st.hits), "lookups": int(st.lookups)}
+    # Fallback: the C restatement (single thread) on a 480x270 crop.
+    from paper_2305_07238_b200 import load_scene
+    orc = _oracle.Oracle()
+    sc = load_scene(scene_path)
+    P = _oracle.RenderParamsC(480, 270, spp, 4, 1 if cache else 0, 0, 1_000_000, N_ENTRIES, 0, 1,
+                              0.2, 16, 0, 1, 0, 1, 1)
+    t0 = time.perf_counter()
+    orc.render(sc.flat, P)
+    dt = time.perf_counter() - t0
+    return {"kind": "port", "seconds": dt, "samples": 480 * 270 * spp, "cores": 1}
+
+
+def run_reference_arm(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    with tempfile.TemporaryDirectory() as tmp:
+        path = make_scene(tmp)
+        for _ in range(args.warmup):
+            cpu_reference_sample(path)
+        times = []
+        info = None
+        for _ in range(args.steps):
+            info = cpu_reference_sample(path)
+            times.append(info["seconds"])
+    t = sum(times) / len(times)
+    v = info["samples"] / t
+    sample = (f"{W}x{H}x1spp frame per step (of the {W}x{H}x{SPP} workload), cache "
+              f"{N_CELLS:.0e}x{N_ENTRIES}, tile queue over {info['cores']} threads"
+              if info["kind"] == "reference" else "480x270x1spp crop, 1 thread (C port)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded classroom-like scene, reference JSON/PPM formats)",
+        "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp cache {N_CELLS:.0e}x{N_ENTRIES}",
+                   "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": info["cores"],
+                         "kind": info["kind"], "sample": sample},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip speed-up/probe legs")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2305_07238_b200 import (Context, RenderConfig, load_scene)
+    from paper_2305_07238_b200 import _native as N
+
+    stream = torch.cuda.Stream()
+    ctx = Context(local, profile=True, stream=stream.cuda_stream)
+    L = N.lib()
+    tmp = tempfile.mkdtemp()
+    scene_path = make_scene(tmp) if rank == 0 else None
+    if world > 1:
+        obj = [tmp if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        scene_path = os.path.join(obj[0], "scene", "scene.json")
+        if rank != 0:  # same seeded generator -> byte-identical files
+            scene_path = make_scene(tempfile.mkdtemp())
+    scene = load_scene(scene_path)
+    ctx.upload(scene)
+
+    cfg = RenderConfig(width=W, height=H, spp=SPP, cache_enabled=True, n_cells=N_CELLS,
+                       n_entries=N_ENTRIES, shard_rank=rank, shard_count=world, shard_mode=0)
+    params = cfg.to_params()
+    dev = torch.device("cuda", local)
+    rad = torch.zeros(H * W * 3, dtype=torch.float64, device=dev)
+    nodes = torch.zeros(H * W, dtype=torch.float64, device=dev)
+    samples = torch.zeros(H * W, dtype=torch.int32, device=dev)
+    dframe = N.Frame(C.cast(C.c_void_p(rad.data_ptr()), C.POINTER(C.c_double)),
+                     C.cast(C.c_void_p(nodes.data_ptr()), C.POINTER(C.c_double)),
+                     C.cast(C.c_void_p(samples.data_ptr()), C.POINTER(C.c_uint32)))
+
+    def step(p=params):
+        with torch.cuda.stream(stream):
+            rad.zero_(); nodes.zero_(); samples.zero_()
+        st = N.RenderStats()
+        N.check(L.mcg_render_device(ctx.handle, C.byref(p), None, C.byref(dframe), C.byref(st)))
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.reduce(rad, 0)
+                dist.reduce(nodes, 0)
+                dist.reduce(samples, 0)
+        return st
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ctx.reset_kernel_times()
+        l0 = ctx.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        stats = [fn() for _ in range(steps)]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, stats, ctx.launch_count() - l0
+
+    # ---- headline: device-timed samples/s ------------------------------
+    with ClockSampler(local) as clk:
+        ms, stats, launches = timed(step, args.steps, args.warmup)
+    ktimes = ctx.kernel_times()
+    total_samples = W * H * SPP
+    value = total_samples * args.steps / (ms / 1e3)
+    st = stats[-1]
+
+    # ---- e2e through the host-buffer C ABI --------------------------------
+    host_rad = torch.zeros(H * W * 3, dtype=torch.float64).pin_memory()
+    host_nodes = torch.zeros(H * W, dtype=torch.float64).pin_memory()
+    host_samples = torch.zeros(H * W, dtype=torch.int32).pin_memory()
+    hframe = N.Frame(C.cast(C.c_void_p(host_rad.data_ptr()), C.POINTER(C.c_double)),
+                     C.cast(C.c_void_p(host_nodes.data_ptr()), C.POINTER(C.c_double)),
+                     C.cast(C.c_void_p(host_samples.data_ptr()), C.POINTER(C.c_uint32)))
+    f = scene.flat
+    scene_bytes = (f.n_prims * (48 + 24 + 4) + f.n_nodes * 32 + f.n_code * 16 + f.n_consts * 16
+                   + f.n_noise * 16 + f.n_ramp_stops * 16 + f.n_texels * 16)
+    frame_bytes = H * W * (24 + 8 + 4)
+
+    def e2e_step():
+        host_rad.zero_(); host_nodes.zero_(); host_samples.zero_()
+        N.check(L.mcg_upload_scene(ctx.handle, scene.handle))
+        s = N.RenderStats()
+        N.check(L.mcg_render(ctx.handle, C.byref(params), None, C.byref(hframe), C.byref(s)))
+        return s
+
+    e2e_steps = max(1, min(args.steps, 2))
+    for _ in range(1):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = total_samples * e2e_steps / t_e2e
+    ctx.upload(scene)
+
+    # ---- extras: cache speed-up and probe roofline (rank 0 leg, N=1 job) ----
+    extras = {}
+    if not args.no_extras:
+        off = RenderConfig(width=W, height=H, spp=SPP, cache_enabled=False,
+                           shard_rank=rank, shard_count=world).to_params()
+        ms_off, _, _ = timed(lambda: step(off), 1, 1)
+        extras["cache_speedup"] = {"t_nocache_ms": ms_off, "t_cache_ms": ms / args.steps,
+                                   "speedup": ms_off / (ms / args.steps)}
+        if rank == 0:
+            from paper_2305_07238_b200 import MaterialCache
+            peak, _ = measured_peaks()
+            table = MaterialCache(N_CELLS, N_ENTRIES, ctx)
+            n = 1 << 26
+            ms_ins, b_ins = table.probe_bench(n, 7, 0, 1)
+            table.probe_bench(n, 7, 1, 1)
+            ms_look, b_look = table.probe_bench(n, 7, 1, 3)
+            ms_mix, b_mix = table.probe_bench(n, 8, 2, 3)
+            extras["probe_roofline"] = {
+                "bound": "hbm", "unit": "GB/s", "peak": peak, "table": "1e7x10 (800 MB)",
+                "descriptors": n,
+                "insert_all": {"achieved": b_ins / ms_ins / 1e6, "frac": b_ins / ms_ins / 1e6 / peak,
+                               "mprobes_per_s": n / ms_ins / 1e3},
+                "lookup_all": {"achieved": b_look / ms_look / 1e6, "frac": b_look / ms_look / 1e6 / peak,
+                               "mprobes_per_s": n / ms_look / 1e3},
+                "mix_50_50": {"achieved": b_mix / ms_mix / 1e6, "frac": b_mix / ms_mix / 1e6 / peak,
+                              "mprobes_per_s": n / ms_mix / 1e3},
+            }
+            table.close()
+
+    # ---- roofline of the dominant kernel ----------------------------------
+    peak, peak_src = measured_peaks()
+    ne = N_ENTRIES
+    steps = args.steps
+    # Algorithmic bytes: per lookup / insert attempt one
+    # cell (8 Ne), +8 per won CAS, 48 per TexSample (4 RGB texels), 80 per
+    # shading record in/out; per BVH node 32, per triangle 48, 128 per path
+    # step of wavefront state.
+    shade_bytes = steps * (st.lookups * 8 * ne + st.stores_attempted * 8 * ne + st.inserts_won * 8
+                           + st.tex_samples * 48 + st.shading_points * 80)
+    bounce_bytes = steps * (st.bvh_nodes * 32 + st.prims_tested * 48
+                            + (st.shading_points + st.paths) * 128)
+    algo = {"shade": shade_bytes, "bounce": bounce_bytes}
+    dom = max(ktimes.items(), key=lambda kv: kv[1]["ms"]) if ktimes else ("?", {"ms": 0, "launches": 0})
+    dname, drec = dom
+    per_launch_ms = drec["ms"] / max(1, drec["launches"])
+    dbytes = algo.get(dname, drec.get("bytes", 0.0)) / max(1, drec["launches"])
+    achieved = dbytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ktimes.values())), 4)
+              for k, v in ktimes.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            info = cpu_reference_sample(scene_path)
+            cpu = {"value": info["samples"] / info["seconds"], "unit": "samples/s",
+                   "cores": info["cores"], "kind": info["kind"],
+                   "sample": (f"{W}x{H}x1spp frame, cache {N_CELLS:.0e}x{N_ENTRIES}, tile queue over "
+                              f"{info['cores']} threads" if info["kind"] == "reference"
+                              else "480x270x1spp crop, 1 thread")}
+        except Exception as e:  # the checker must never break the bench line
+            cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "unavailable",
+                   "sample": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded classroom-like scene in the reference's JSON/PPM formats)",
+            "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp, cache {N_CELLS:.0e}x{N_ENTRIES}, "
+                                   "concurrent inserts", "width": W, "height": H, "spp": SPP,
+                       "n_cells": N_CELLS, "n_entries": N_ENTRIES, "parallelism": f"tiles/{world}",
+                       "l2": "inputs larger than L2 (800 MB table re-zeroed per render + "
+                             f"{(W * H * 10 * 16) >> 20} MB path state)"},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": "samples/s",
+                    "h2d_bytes_per_step": int(scene_bytes + frame_bytes),
+                    "d2h_bytes_per_step": int(frame_bytes)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src, "kernel_share": shares},
+            "render_stats": {"hit_rate": st.hits / st.lookups if st.lookups else 0.0,
+                             "lookups": st.lookups, "hits": st.hits, "inserts_won": st.inserts_won,
+                             "inserts_lost_full": st.inserts_lost_full,
+                             "shading_points": st.shading_points, "shadow_rays": st.shadow_rays},
+            "cpu_baseline": cpu,
+        }
+        line.update(extras)
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

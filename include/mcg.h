@@ -348,6 +348,14 @@ typedef struct mcg_scene_in {
 } mcg_scene_in;
 mcg_status mcg_scene_build(const mcg_scene_in* in, mcg_scene** out);
 
+/* Static stack schedule of one flattened program: fills sp / tags / store_ord
+ * of every instruction and returns the miss-path stack bound, with compile()'s
+ * balance checks and errors (stackvm.cpp:226-245 -> MCG_ERR_COMPILE). For
+ * callers that flatten a reference CompiledProgram themselves. PushConst
+ * args index `consts`. */
+mcg_status mcg_schedule_program(mcg_insn* code, uint32_t n_code, const mcg_const* consts,
+                                uint32_t n_consts, uint32_t* max_stack);
+
 /* ------------------------------------------------------------------------ */
 /* Rendering (tracer.hpp:7-70; body restated in DESIGN.md §render)           */
 /* ------------------------------------------------------------------------ */
@@ -385,6 +393,8 @@ typedef struct mcg_render_stats {    /* RenderStats, tracer.hpp:45-55 */
     uint64_t stores_attempted, stores_won, instructions_executed;
     uint64_t max_stack_seen;
     uint64_t paths, shading_points, shadow_rays;
+    uint64_t bvh_nodes, prims_tested, tex_samples;   /* work counters (roofline bytes) */
+    uint64_t launches;               /* this library's kernel launches in the call */
     uint64_t* hits_per_sample;       /* optional, caller array of spp entries */
 } mcg_render_stats;
 

@@ -81,7 +81,8 @@ class RenderStats(C.Structure):
                 ("inserts_won", u64), ("inserts_lost_full", u64), ("stores_attempted", u64),
                 ("stores_won", u64), ("instructions_executed", u64), ("max_stack_seen", u64),
                 ("paths", u64), ("shading_points", u64), ("shadow_rays", u64),
-                ("hits_per_sample", P(u64))]
+                ("bvh_nodes", u64), ("prims_tested", u64), ("tex_samples", u64),
+                ("launches", u64), ("hits_per_sample", P(u64))]
 
 
 # (name, restype, argtypes)
@@ -126,6 +127,7 @@ _SIGS = [
     ("mcg_scene_disassemble", C.c_int, [vp, u32, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     ("mcg_scene_analysis_json", C.c_int, [vp, u32, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
     ("mcg_scene_build", C.c_int, [vp, P(vp)]),
+    ("mcg_schedule_program", C.c_int, [vp, u32, vp, u32, P(u32)]),
     ("mcg_upload_scene", C.c_int, [vp, vp]),
     ("mcg_render", C.c_int, [vp, P(RenderParams), vp, P(Frame), P(RenderStats)]),
     ("mcg_render_device", C.c_int, [vp, P(RenderParams), vp, P(Frame), P(RenderStats)]),

@@ -677,6 +677,41 @@ mcg_status mcg_scene_build(const mcg_scene_in* in, mcg_scene** out) {
     });
 }
 
+mcg_status mcg_schedule_program(mcg_insn* code, uint32_t n_code, const mcg_const* consts,
+                                uint32_t n_consts, uint32_t* max_stack) {
+    return guarded([&] {
+        if (!code || n_code == 0 || (!consts && n_consts)) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        Program p;
+        p.code.assign(code, code + n_code);
+        p.consts.assign(consts, consts + n_consts);
+        if (p.code.back().op != MCG_OP_END) fail(MCG_ERR_COMPILE, "program must end with End");
+        int depth = 0, peak = 0;
+        for (const mcg_insn& ins : p.code) {
+            if (ins.op > MCG_OP_END) fail(MCG_ERR_COMPILE, "unknown opcode");
+            if (ins.op == MCG_OP_PUSH_CONST && ins.arg >= n_consts) {
+                fail(MCG_ERR_COMPILE, "constant index out of range");
+            }
+            if (ins.op == MCG_OP_END) break;
+            switch (ins.op) {
+                case MCG_OP_ADD: case MCG_OP_SUB: case MCG_OP_MUL: case MCG_OP_DIV:
+                case MCG_OP_DOT: case MCG_OP_POWER: depth -= 1; break;
+                case MCG_OP_MIX: depth -= 2; break;
+                case MCG_OP_PUSH_CONST: case MCG_OP_LOAD_UV: case MCG_OP_LOAD_POSITION:
+                case MCG_OP_LOAD_NORMAL: case MCG_OP_LOAD_INCOMING: case MCG_OP_TEX_SAMPLE:
+                case MCG_OP_CHECKER: case MCG_OP_NOISE: depth += 1; break;
+                default: break;
+            }
+            if (depth <= 0) fail(MCG_ERR_COMPILE, "stack underflow during compilation");
+            peak = std::max(peak, depth);
+        }
+        if (depth != 1) fail(MCG_ERR_COMPILE, "unbalanced stack effect: final depth " + std::to_string(depth));
+        if (peak > 255) fail(MCG_ERR_COMPILE, "stack depth exceeds 255");
+        schedule_program(p);
+        std::copy(p.code.begin(), p.code.end(), code);
+        if (max_stack) *max_stack = static_cast<uint32_t>(peak);
+    });
+}
+
 mcg_status mcg_scene_destroy(mcg_scene* scene) {
     delete scene;
     return MCG_OK;

@@ -86,7 +86,8 @@ struct mcg_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     bool profile = false;
-    uint64_t launches = 0;
+    uint64_t launches = 0;       // this library's kernels
+    uint64_t library_sorts = 0;  // cub::DeviceRadixSort invocations
     std::map<std::string, mcg::KernelAcc> times;
     std::vector<mcg::EventRec> pending;
     std::vector<cudaEvent_t> event_pool;

@@ -96,7 +96,8 @@ struct SceneView {
     const float4* prim_geom;      // 3 float4 per prim
     const float2* prim_uv;        // 3 float2 per prim
     const uint32_t* prim_info;
-    const float4* nodes;          // 2 float4 per BVH node
+    const float4* nodes;          // 2 float4 per BVH node (the reference tree, own boxes)
+    const float4* pairs;          // 4 float4 per internal node: both children's records
     uint32_t n_nodes;
     const mcg_point_light* plights;
     uint32_t n_plights;
@@ -120,7 +121,7 @@ struct ShadeIn {
 };
 
 struct VmCounters {
-    uint32_t instrs = 0, lookups = 0, hits = 0, stores = 0, won = 0, full = 0;
+    uint32_t instrs = 0, lookups = 0, hits = 0, stores = 0, won = 0, full = 0, tex = 0;
 };
 
 // Sink for deterministic-mode stores: (cell, pixel-order key) -> (check, payload).
@@ -244,6 +245,7 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                     const float3 c = bilinear(S.textures[arg], S.texels, sp.u, sp.v,
                                               (flags & MCG_F_WRAP_CLAMP) != 0);
                     st.put(d, c.x, c.y, c.z, false);
+                    ++cnt.tex;
                 }
                 break;
             case MCG_OP_CHECKER:

@@ -34,7 +34,7 @@ constexpr float kInvPi = 0.318309886183790671538f;
 // Render counters (device, u64): see kStat*.
 enum {
     kStatLookups = 0, kStatHits, kStatWon, kStatFull, kStatLost, kStatStores, kStatInstrs,
-    kStatShade, kStatShadow, kStatMaxStack, kStatQueue, kStatCount = 16
+    kStatShade, kStatShadow, kStatNodes, kStatPrims, kStatTex, kStatCount = 16
 };
 
 struct RenderView {
@@ -72,25 +72,6 @@ struct RenderView {
 
 __device__ __forceinline__ uint32_t dim_rect(int b, int j, int k) { return 2u + 64u * b + 2u * j + k; }
 __device__ __forceinline__ uint32_t dim_bounce(int b, int k) { return 2u + 64u * b + 62u + k; }
-
-// ray_aabb (scene.cpp:42-56) with the per-ray reciprocals of the reference.
-__device__ __forceinline__ bool ray_box(V3 o, V3 inv, float4 lo, float4 hi, float tmin, float tmax) {
-    float t0 = (lo.x - o.x) * inv.x, t1 = (hi.x - o.x) * inv.x;
-    if (inv.x < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
-    tmin = fmaxf(tmin, t0);
-    tmax = fminf(tmax, t1);
-    if (tmax < tmin) return false;
-    t0 = (lo.y - o.y) * inv.y; t1 = (hi.y - o.y) * inv.y;
-    if (inv.y < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
-    tmin = fmaxf(tmin, t0);
-    tmax = fminf(tmax, t1);
-    if (tmax < tmin) return false;
-    t0 = (lo.z - o.z) * inv.z; t1 = (hi.z - o.z) * inv.z;
-    if (inv.z < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
-    tmin = fmaxf(tmin, t0);
-    tmax = fminf(tmax, t1);
-    return !(tmax < tmin);
-}
 
 // ray_triangle (scene.cpp:58-78) / ray_sphere (scene.cpp:80-94)
 __device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V3 o, V3 d,
@@ -132,30 +113,68 @@ __device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V
     return true;
 }
 
-// Scene::intersect (scene.cpp:252-278) / Scene::occluded (:280-298): the
-// reference's unordered DFS (left pushed first, so the right child is
-// visited first) -- closest-hit ties at equal t resolve identically.
-template <bool kAnyHit>
-__device__ bool traverse(const mcgd::SceneView& S, V3 o, V3 d, float tmin, float tmax,
-                         uint32_t& prim, float& t_out, float& b1_out, float& b2_out) {
+// Slab test of one box split into its ray-only part: E = max(tmin, entry),
+// T1 = exit (fmaxf/fminf drop NaNs exactly as the reference's loop does).
+// The reference's ray_aabb(ray, box, tmin, tmax) (scene.cpp:42-56) rejects
+// iff fminf(tmax, T1) < E, i.e. iff T1 < E (ray-only) or tmax < E.
+__device__ __forceinline__ void slab(V3 o, V3 inv, float4 lo, float4 hi, float tmin, float& E,
+                                     float& T1) {
+    float t0 = (lo.x - o.x) * inv.x, t1 = (hi.x - o.x) * inv.x;
+    if (inv.x < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    E = fmaxf(tmin, t0);
+    T1 = t1;
+    t0 = (lo.y - o.y) * inv.y; t1 = (hi.y - o.y) * inv.y;
+    if (inv.y < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    E = fmaxf(E, t0);
+    T1 = fminf(T1, t1);
+    t0 = (lo.z - o.z) * inv.z; t1 = (hi.z - o.z) * inv.z;
+    if (inv.z < 0.0f) { const float t = t0; t0 = t1; t1 = t; }
+    E = fmaxf(E, t0);
+    T1 = fminf(T1, t1);
+}
+
+// Scene::intersect (scene.cpp:252-278) over the child-pair layout. Visit
+// order and every culling decision are the reference's: its DFS pushes left
+// then right and tests a node's box when the node is popped, against the
+// closest hit at that moment. Here both child boxes are tested when the
+// parent is expanded; the ray-only part (T1 < E) drops the child for good
+// and the closest-dependent part (closest < E) is re-checked at pop time
+// from the stored entry distance -- the same decision the reference makes,
+// so closest-hit ties at equal t resolve identically.
+__device__ bool traverse_closest(const mcgd::SceneView& S, V3 o, V3 d, float tmin, float tmax,
+                                 uint32_t& prim, float& t_out, float& b1_out, float& b2_out,
+                                 uint32_t& nodes_visited, uint32_t& prims_tested) {
     if (S.n_nodes == 0) return false;
     const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-    int32_t stack[64];
+    int32_t sa[64], sb[64];
+    float se[64];
     int top = 0;
-    stack[top++] = 0;
+    {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (T1 < E) return false;
+        // The root's own record holds its children; an internal root is
+        // referenced by its index (0), a leaf root by (~first, count).
+        const int32_t ra = __float_as_int(lo.w);
+        sa[0] = ra >= 0 ? 0 : ra;
+        sb[0] = __float_as_int(hi.w);
+        se[0] = E;
+        top = 1;
+    }
     bool found = false;
     float closest = tmax;
     while (top > 0) {
-        const int32_t ni = stack[--top];
-        const float4 lo = __ldg(S.nodes + 2 * ni), hi = __ldg(S.nodes + 2 * ni + 1);
-        if (!ray_box(o, inv, lo, hi, tmin, closest)) continue;
-        const int32_t a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+        --top;
+        const int32_t a = sa[top], b = sb[top];
+        ++nodes_visited;
+        if (closest < se[top]) continue;
         if (a < 0) {
             const uint32_t first = static_cast<uint32_t>(~a);
+            prims_tested += static_cast<uint32_t>(b);
             for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
                 float t, b1, b2;
                 if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
-                    if (kAnyHit) return true;
                     closest = t;
                     prim = i;
                     t_out = t;
@@ -165,11 +184,85 @@ __device__ bool traverse(const mcgd::SceneView& S, V3 o, V3 d, float tmin, float
                 }
             }
         } else {
-            stack[top++] = a;
-            stack[top++] = b;
+            const float4* p = S.pairs + 4 * a;
+            const float4 llo = __ldg(p), lhi = __ldg(p + 1), rlo = __ldg(p + 2), rhi = __ldg(p + 3);
+            float EL, T1L, ER, T1R;
+            slab(o, inv, llo, lhi, tmin, EL, T1L);
+            slab(o, inv, rlo, rhi, tmin, ER, T1R);
+            if (!(T1L < EL)) {
+                sa[top] = __float_as_int(llo.w);
+                sb[top] = __float_as_int(lhi.w);
+                se[top] = EL;
+                ++top;
+            }
+            if (!(T1R < ER)) {
+                sa[top] = __float_as_int(rlo.w);
+                sb[top] = __float_as_int(rhi.w);
+                se[top] = ER;
+                ++top;
+            }
         }
     }
     return found;
+}
+
+// Scene::occluded (scene.cpp:280-298): a boolean whose value does not depend
+// on visit order (tmax is fixed), so children are visited near-first and the
+// far one is stacked; the first hit ends the query.
+__device__ bool traverse_any(const mcgd::SceneView& S, V3 o, V3 d, float tmin, float tmax,
+                             uint32_t& nodes_visited, uint32_t& prims_tested) {
+    if (S.n_nodes == 0) return false;
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t sa[64], sb[64];
+    int top = 0;
+    int32_t a, b;
+    {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (fminf(tmax, T1) < E) return false;
+        a = __float_as_int(lo.w);
+        a = a >= 0 ? 0 : a;
+        b = __float_as_int(hi.w);
+    }
+    for (;;) {
+        ++nodes_visited;
+        if (a < 0) {
+            const uint32_t first = static_cast<uint32_t>(~a);
+            prims_tested += static_cast<uint32_t>(b);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) return true;
+            }
+            if (top == 0) return false;
+            --top;
+            a = sa[top];
+            b = sb[top];
+            continue;
+        }
+        const float4* p = S.pairs + 4 * a;
+        const float4 llo = __ldg(p), lhi = __ldg(p + 1), rlo = __ldg(p + 2), rhi = __ldg(p + 3);
+        float EL, T1L, ER, T1R;
+        slab(o, inv, llo, lhi, tmin, EL, T1L);
+        slab(o, inv, rlo, rhi, tmin, ER, T1R);
+        const bool okL = !(fminf(tmax, T1L) < EL), okR = !(fminf(tmax, T1R) < ER);
+        if (okL && okR) {
+            const bool left_first = EL <= ER;
+            sa[top] = __float_as_int(left_first ? rlo.w : llo.w);
+            sb[top] = __float_as_int(left_first ? rhi.w : lhi.w);
+            ++top;
+            a = __float_as_int(left_first ? llo.w : rlo.w);
+            b = __float_as_int(left_first ? lhi.w : rhi.w);
+        } else if (okL || okR) {
+            a = __float_as_int(okL ? llo.w : rlo.w);
+            b = __float_as_int(okL ? lhi.w : rhi.w);
+        } else {
+            if (top == 0) return false;
+            --top;
+            a = sa[top];
+            b = sb[top];
+        }
+    }
 }
 
 struct Surface {
@@ -238,7 +331,7 @@ __device__ __forceinline__ void add_light(float4& L, V3 tf, const float* emit, f
 // over every light, then the cosine bounce) and trace vertex b.
 __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t shadow = 0;
+    uint32_t shadow = 0, nvis = 0, ntest = 0;
     if (i < R.n_paths) {
         const uint32_t slot_j = i / R.n_pix;
         const uint32_t pixel = R.pix[i - slot_j * R.n_pix];
@@ -277,8 +370,6 @@ __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
                 const V3 f = alb * kInvPi;
                 const V3 tf{thr.x * f.x, thr.y * f.y, thr.z * f.z};
                 const V3 o = V3{s0.x, s0.y, s0.z} + n * kEps;
-                uint32_t pdummy;
-                float td, t1, t2;
                 for (uint32_t li = 0; li < R.S.n_plights; ++li) {
                     const mcg_point_light& l = R.S.plights[li];
                     const V3 toL = V3{l.position[0], l.position[1], l.position[2]} - o;
@@ -288,7 +379,7 @@ __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
                     const float cs = mcgd::dot(n, wi);
                     if (cs > 0.0f) {
                         ++shadow;
-                        if (!traverse<true>(R.S, o, wi, kTMin, dist, pdummy, td, t1, t2)) {
+                        if (!traverse_any(R.S, o, wi, kTMin, dist, nvis, ntest)) {
                             add_light(L, tf, l.intensity, cs / d2);
                         }
                     }
@@ -310,7 +401,7 @@ __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
                     const float cl = fabsf(mcgd::dot(nl, wi)) / area;
                     if (cs > 0.0f && cl > 0.0f) {
                         ++shadow;
-                        if (!traverse<true>(R.S, o, wi, kTMin, dist, pdummy, td, t1, t2)) {
+                        if (!traverse_any(R.S, o, wi, kTMin, dist, nvis, ntest)) {
                             add_light(L, tf, l.radiance, ((cs * cl) * area) / d2);
                         }
                     }
@@ -345,7 +436,7 @@ __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
             const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
             uint32_t prim = 0;
             float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-            if (!traverse<false>(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2)) {
+            if (!traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest)) {
                 L.x = L.x + thr.x * R.S.env[0];
                 L.y = L.y + thr.y * R.S.env[1];
                 L.z = L.z + thr.z * R.S.env[2];
@@ -376,6 +467,8 @@ __global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
         R.key[i] = key;
     }
     mcgd::warp_add(R.stats + kStatShadow, shadow);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
 // Material evaluation of every live hit, in material order.
@@ -418,31 +511,45 @@ __global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __r
     mcgd::warp_add(R.stats + kStatStores, cnt.stores);
     mcgd::warp_add(R.stats + kStatInstrs, cnt.instrs);
     mcgd::warp_add(R.stats + kStatShade, 1u);
+    mcgd::warp_add(R.stats + kStatTex, cnt.tex);
 }
 
 // Adds the finished pass into the framebuffers, samples in order, so the
 // double accumulators see exactly the oracle's summation order.
-__global__ void k_accumulate(RenderView R, uint32_t k) {
+__global__ void __launch_bounds__(256) k_accumulate(RenderView R, uint32_t k) {
+    __shared__ unsigned long long s_hits[32];
+    if (threadIdx.x < 32) s_hits[threadIdx.x] = 0ull;
+    __syncthreads();
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= R.n_pix) return;
-    const uint32_t pixel = R.pix[q];
-    double r = R.radiance[3ull * pixel], g = R.radiance[3ull * pixel + 1],
-           bl = R.radiance[3ull * pixel + 2], nf = R.nodes_found[pixel];
-    for (uint32_t j = 0; j < k; ++j) {
-        const uint32_t i = j * R.n_pix + q;
-        const float4 L = R.L[i];
-        const uint32_t nodes = __float_as_uint(R.thr[i].w);
-        r += static_cast<double>(L.x);
-        g += static_cast<double>(L.y);
-        bl += static_cast<double>(L.z);
-        nf += static_cast<double>(nodes);
-        if (R.hps) atomicAdd(R.hps + R.hps_base + j, static_cast<unsigned long long>(nodes));
+    if (q < R.n_pix) {
+        const uint32_t pixel = R.pix[q];
+        double r = R.radiance[3ull * pixel], g = R.radiance[3ull * pixel + 1],
+               bl = R.radiance[3ull * pixel + 2], nf = R.nodes_found[pixel];
+        for (uint32_t j = 0; j < k; ++j) {
+            const uint32_t i = j * R.n_pix + q;
+            const float4 L = R.L[i];
+            const uint32_t nodes = __float_as_uint(R.thr[i].w);
+            r += static_cast<double>(L.x);
+            g += static_cast<double>(L.y);
+            bl += static_cast<double>(L.z);
+            nf += static_cast<double>(nodes);
+            // hits_per_sample: one shared atomic per warp, one global per block.
+            const unsigned m = __activemask();
+            const uint32_t wsum = __reduce_add_sync(m, nodes);
+            if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(m) - 1) && wsum && j < 32) {
+                atomicAdd(&s_hits[j], static_cast<unsigned long long>(wsum));
+            }
+        }
+        R.radiance[3ull * pixel] = r;
+        R.radiance[3ull * pixel + 1] = g;
+        R.radiance[3ull * pixel + 2] = bl;
+        R.nodes_found[pixel] = nf;
+        R.samples[pixel] += k;
     }
-    R.radiance[3ull * pixel] = r;
-    R.radiance[3ull * pixel + 1] = g;
-    R.radiance[3ull * pixel + 2] = bl;
-    R.nodes_found[pixel] = nf;
-    R.samples[pixel] += k;
+    __syncthreads();
+    if (R.hps && threadIdx.x < k && threadIdx.x < 32 && s_hits[threadIdx.x]) {
+        atomicAdd(R.hps + R.hps_base + threadIdx.x, s_hits[threadIdx.x]);
+    }
 }
 
 __global__ void k_iota(uint32_t* v, uint32_t n) {
@@ -472,6 +579,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         fail(MCG_ERR_INVALID_ARGUMENT, "shard_rank out of range");
     }
     const auto t0 = std::chrono::steady_clock::now();
+    const uint64_t launches0 = ctx->launches;
     const bool cache_on = P.cache_mode != MCG_CACHE_OFF;
     const bool deferred = P.cache_mode == MCG_CACHE_DETERMINISTIC;
 
@@ -491,7 +599,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const uint64_t target = 1u << 21;  // ~2M paths in flight fill 148 SMs
         k = static_cast<uint32_t>(std::max<uint64_t>(1, (target + n_pix - 1) / std::max<uint32_t>(n_pix, 1)));
     }
-    k = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp));
+    k = std::min<uint32_t>(std::min<uint32_t>(k, 32u), static_cast<uint32_t>(P.spp));
     const uint64_t wh = static_cast<uint64_t>(W) * H;
     if (deferred && (static_cast<uint64_t>(k) * wh) >= (1ull << 26)) {
         fail(MCG_ERR_INVALID_ARGUMENT, "deterministic mode: samples_per_pass * pixels must be < 2^26");
@@ -662,6 +770,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         stats->paths = static_cast<uint64_t>(n_pix) * P.spp;
         stats->shading_points = st[kStatShade];
         stats->shadow_rays = st[kStatShadow];
+        stats->bvh_nodes = st[kStatNodes];
+        stats->prims_tested = st[kStatPrims];
+        stats->tex_samples = st[kStatTex];
+        stats->launches = ctx->launches - launches0;
     }
 }
 

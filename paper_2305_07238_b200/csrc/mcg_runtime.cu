@@ -53,7 +53,7 @@ void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* ki, unsigned long lo
     cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
                                                static_cast<int>(n), 0, end_bit, ctx->stream),
                "cub sort");
-    ctx->launches += static_cast<uint64_t>((end_bit + 7) / 8) + 1;
+    ++ctx->library_sorts;  // CUB's kernels: library code, not counted in launches
 }
 
 void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* ki, uint32_t* ko, const uint32_t* vi,
@@ -66,7 +66,7 @@ void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* ki, uint32_t* ko, const uint32
     cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
                                                static_cast<int>(n), 0, end_bit, ctx->stream),
                "cub sort");
-    ctx->launches += static_cast<uint64_t>((end_bit + 7) / 8) + 1;
+    ++ctx->library_sorts;  // CUB's kernels: library code, not counted in launches
 }
 
 }  // namespace mcg
@@ -807,6 +807,26 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         v.prim_info = static_cast<const uint32_t*>(up(2, f.prim_info, f.n_prims * 4ull));
         v.nodes = static_cast<const float4*>(up(3, f.nodes, f.n_nodes * sizeof(mcg_bvh_node)));
         v.n_nodes = f.n_nodes;
+        // Child-pair layout: internal node i holds both children's boxes and
+        // references (an internal child by its node index, a leaf by
+        // (~first, count)), so one 64-byte fetch tests both child boxes (the
+        // traversal still visits nodes in the reference's order, see
+        // mcg_render.cu traverse_closest).
+        std::vector<mcg_bvh_node> pairs(2 * static_cast<size_t>(std::max<uint32_t>(f.n_nodes, 1)));
+        for (uint32_t i = 0; i < f.n_nodes; ++i) {
+            const mcg_bvh_node& nd = f.nodes[i];
+            if (nd.a < 0) continue;
+            const int32_t child[2] = {nd.a, nd.b};
+            for (int k = 0; k < 2; ++k) {
+                mcg_bvh_node c = f.nodes[child[k]];
+                if (c.a >= 0) {
+                    c.a = child[k];
+                    c.b = 0;
+                }
+                pairs[2 * i + k] = c;
+            }
+        }
+        v.pairs = static_cast<const float4*>(up(14, pairs.data(), f.n_nodes * 2 * sizeof(mcg_bvh_node)));
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
         v.n_plights = f.n_point_lights;
         v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));

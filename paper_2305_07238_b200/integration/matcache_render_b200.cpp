@@ -1,0 +1,383 @@
+// matcache_render_b200.cpp — the link-level drop-in for the reference's C++
+// renderer API. The reference declares render() and the experiment helpers in
+// include/matcache/tracer.hpp:69-92 but ships no definition (src/tracer.cpp is
+// absent, proj/core/CMakeLists.txt:14). Linking this file plus libmcg.so into
+// matcache_core provides them, backed by the B200 kernels behind the C ABI
+// (include/mcg.h). Build: see INTEGRATION.md (and oracle/Makefile `dropin`,
+// which compiles it against the reference headers in place for the tests).
+//
+// What it does per call:
+//   Scene (scene.hpp:91-123) + compiled programs (stackvm.hpp:73-79)
+//     -> mcg_scene_in (meshes, spheres, lights, camera, flattened bytecode,
+//        RGBA textures) -> mcg_scene_build (BVH rebuilt with the reference's
+//        median split, scene.cpp:154-194) -> mcg_upload_scene -> mcg_render.
+// Status codes are rethrown as the reference's exception types.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "matcache/tracer.hpp"
+#include "mcg.h"
+
+namespace matcache {
+namespace {
+
+[[noreturn]] void rethrow(mcg_status s) {
+    const std::string msg = mcg_last_error();
+    switch (s) {
+        case MCG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case MCG_ERR_OVERFLOW: throw std::overflow_error(msg);
+        case MCG_ERR_GRAPH: throw GraphError(msg);
+        case MCG_ERR_COMPILE: throw CompileError(msg);
+        case MCG_ERR_SCENE: throw SceneError(msg);
+        case MCG_ERR_IMAGE_IO: throw ImageIoError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+void ok(mcg_status s) {
+    if (s != MCG_OK) rethrow(s);
+}
+
+// One device context per process (the reference render() is synchronous).
+struct Device {
+    std::mutex mu;
+    mcg_ctx* ctx = nullptr;
+    const Scene* uploaded = nullptr;
+    mcg_scene* scene = nullptr;
+    // Device tables standing in for external MaterialCache objects: the
+    // reference table exposes no bulk writer (cache.hpp:69-115), so the
+    // GPU table lives here, seeded from the host table's slot words.
+    std::map<const MaterialCache*, mcg_cache*> tables;
+};
+
+Device& device() {
+    static Device d;
+    return d;
+}
+
+uint8_t flags_of(const Instruction& ins) {
+    uint8_t f = 0;
+    if (ins.uses_uv) f |= MCG_F_USES_UV;
+    if (ins.scalar_result) f |= MCG_F_SCALAR_RESULT;
+    if (ins.op == Opcode::TexSample && ins.wrap == WrapMode::Clamp) f |= MCG_F_WRAP_CLAMP;
+    if (ins.op == Opcode::LoadUv) f |= static_cast<uint8_t>(static_cast<unsigned>(ins.uv_channel) << MCG_F_UV_SHIFT);
+    return f;
+}
+
+struct Flattened {
+    std::vector<mcg_program> programs;
+    std::vector<mcg_insn> code;
+    std::vector<mcg_const> consts;
+    std::vector<mcg_noise> noise;
+    std::vector<mcg_ramp> ramps;
+    std::vector<mcg_ramp_stop> stops;
+    std::vector<mcg_texture> textures;
+    std::vector<float> texels;
+    std::unordered_map<const Texture*, uint32_t> tex_id;
+};
+
+uint32_t texture_id(Flattened& F, const Texture* t) {
+    const auto it = F.tex_id.find(t);
+    if (it != F.tex_id.end()) return it->second;
+    const uint32_t id = static_cast<uint32_t>(F.textures.size());
+    F.textures.push_back({t->image.width, t->image.height, F.texels.size() / 4});
+    for (const Color3& c : t->image.pixels) {
+        F.texels.insert(F.texels.end(), {c.r, c.g, c.b, 0.0f});
+    }
+    F.tex_id.emplace(t, id);
+    return id;
+}
+
+// CompiledProgram (stackvm.hpp:73-79) -> device instruction words + pools.
+void flatten(Flattened& F, const CompiledProgram& prog) {
+    mcg_program p{};
+    p.material_id = prog.material_id;
+    p.code_offset = static_cast<uint32_t>(F.code.size());
+    p.code_len = static_cast<uint32_t>(prog.code.size());
+    p.cache_point_count = prog.cache_point_count;
+    const uint32_t ramp_base = static_cast<uint32_t>(F.ramps.size());
+    for (const auto& stops : prog.ramps) {
+        F.ramps.push_back({static_cast<uint32_t>(F.stops.size()), static_cast<uint32_t>(stops.size())});
+        for (const auto& s : stops) F.stops.push_back({s.t, s.color.r, s.color.g, s.color.b});
+    }
+    for (const Instruction& ins : prog.code) {
+        mcg_insn w{};
+        w.op = static_cast<uint8_t>(ins.op);
+        w.flags = flags_of(ins);
+        w.bracket = static_cast<uint16_t>(ins.bracket);
+        switch (ins.op) {
+            case Opcode::PushConst: {
+                const Color3 c = ins.constant.as_rgb();
+                w.arg = static_cast<uint32_t>(F.consts.size());
+                F.consts.push_back({{c.r, c.g, c.b}, ins.constant.is_scalar() ? 1u : 0u});
+                break;
+            }
+            case Opcode::TexSample: w.arg = texture_id(F, ins.texture); break;
+            case Opcode::Checker: w.imm.f = ins.checker_scale; break;
+            case Opcode::Noise:
+                w.arg = static_cast<uint32_t>(F.noise.size());
+                F.noise.push_back({ins.noise.octaves, ins.noise.frequency, ins.noise.lacunarity,
+                                   ins.noise.gain});
+                break;
+            case Opcode::Ramp: w.arg = ramp_base + ins.ramp_index; break;
+            case Opcode::CacheLookup:
+                w.arg = ins.node_idx;
+                w.imm.i = ins.skip_offset;
+                break;
+            case Opcode::CacheStore: w.arg = ins.node_idx; break;
+            default: break;
+        }
+        F.code.push_back(w);
+    }
+    uint32_t max_stack = 0;
+    ok(mcg_schedule_program(F.code.data() + p.code_offset, p.code_len, F.consts.data(),
+                            static_cast<uint32_t>(F.consts.size()), &max_stack));
+    p.max_stack = max_stack;
+    F.programs.push_back(p);
+}
+
+mcg_scene* build_scene(const Scene& scene) {
+    Flattened F;
+    for (const MaterialRuntime& m : scene.materials) flatten(F, m.program);
+    std::vector<mcg_mesh_in> meshes;
+    std::vector<std::vector<float>> pos(scene.meshes.size()), uvs(scene.meshes.size());
+    for (size_t i = 0; i < scene.meshes.size(); ++i) {
+        const MeshObject& m = scene.meshes[i];
+        for (const Vec3& p : m.positions) pos[i].insert(pos[i].end(), {p.x, p.y, p.z});
+        for (const Vec2& t : m.uvs) uvs[i].insert(uvs[i].end(), {t.x, t.y});
+        if (m.positions.size() != m.uvs.size()) throw SceneError("mesh must carry one uv per vertex");
+        meshes.push_back({static_cast<uint32_t>(m.positions.size()),
+                          static_cast<uint32_t>(m.indices.size()), m.material_id, pos[i].data(),
+                          uvs[i].data(), m.indices.data()});
+    }
+    std::vector<mcg_sphere_in> spheres;
+    for (const SphereObject& s : scene.spheres) {
+        spheres.push_back({{s.center.x, s.center.y, s.center.z}, s.radius, s.material_id});
+    }
+    std::vector<mcg_point_light> pl;
+    for (const PointLight& l : scene.point_lights) {
+        pl.push_back({{l.position.x, l.position.y, l.position.z},
+                      {l.intensity.r, l.intensity.g, l.intensity.b}});
+    }
+    std::vector<mcg_rect_light> rl;
+    for (const RectLight& l : scene.rect_lights) {
+        rl.push_back({{l.corner.x, l.corner.y, l.corner.z}, {l.edge_u.x, l.edge_u.y, l.edge_u.z},
+                      {l.edge_v.x, l.edge_v.y, l.edge_v.z}, {l.radiance.r, l.radiance.g, l.radiance.b}});
+    }
+    mcg_scene_in in{};
+    const Camera& c = scene.camera;
+    const float cam[9] = {c.position.x, c.position.y, c.position.z, c.look_at.x, c.look_at.y,
+                          c.look_at.z, c.up.x, c.up.y, c.up.z};
+    std::memcpy(in.cam_position, cam, sizeof(in.cam_position));
+    std::memcpy(in.cam_look_at, cam + 3, sizeof(in.cam_look_at));
+    std::memcpy(in.cam_up, cam + 6, sizeof(in.cam_up));
+    in.cam_vfov_deg = c.vfov_deg;
+    in.cam_width = c.width;
+    in.cam_height = c.height;
+    in.env[0] = scene.env.r;
+    in.env[1] = scene.env.g;
+    in.env[2] = scene.env.b;
+    in.n_meshes = static_cast<uint32_t>(meshes.size());
+    in.meshes = meshes.data();
+    in.n_spheres = static_cast<uint32_t>(spheres.size());
+    in.spheres = spheres.data();
+    in.n_point_lights = static_cast<uint32_t>(pl.size());
+    in.point_lights = pl.data();
+    in.n_rect_lights = static_cast<uint32_t>(rl.size());
+    in.rect_lights = rl.data();
+    in.n_programs = static_cast<uint32_t>(F.programs.size());
+    in.programs = F.programs.data();
+    in.n_code = static_cast<uint32_t>(F.code.size());
+    in.code = F.code.data();
+    in.n_consts = static_cast<uint32_t>(F.consts.size());
+    in.consts = F.consts.data();
+    in.n_noise = static_cast<uint32_t>(F.noise.size());
+    in.noise = F.noise.data();
+    in.n_ramps = static_cast<uint32_t>(F.ramps.size());
+    in.ramps = F.ramps.data();
+    in.n_ramp_stops = static_cast<uint32_t>(F.stops.size());
+    in.ramp_stops = F.stops.data();
+    in.n_textures = static_cast<uint32_t>(F.textures.size());
+    in.textures = F.textures.data();
+    in.n_texels = F.texels.size() / 4;
+    in.texels = F.texels.data();
+    mcg_scene* out = nullptr;
+    ok(mcg_scene_build(&in, &out));
+    return out;
+}
+
+// The device table standing in for `ext`: created on first use (the host
+// table must then be empty -- the C ABI has no raw slot writer, and update()
+// cannot replay entries without their descriptors) and kept across calls, so
+// progressive renders into one external cache continue on the device.
+mcg_cache* table_for(Device& D, MaterialCache* ext) {
+    auto it = D.tables.find(ext);
+    if (it != D.tables.end()) return it->second;
+    if (ext->occupied_slots() != 0) {
+        throw std::invalid_argument(
+            "render(): a non-empty external MaterialCache cannot seed the device table");
+    }
+    mcg_cache* t = nullptr;
+    ok(mcg_cache_create(D.ctx, ext->n_cells(), ext->n_entries(), &t));
+    D.tables.emplace(ext, t);
+    return t;
+}
+
+}  // namespace
+
+RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCache* external_cache) {
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!D.ctx) {
+        mcg_options opt{0, 0, nullptr};
+        ok(mcg_create(&opt, &D.ctx));
+    }
+    if (D.uploaded != &scene) {
+        if (D.scene) mcg_scene_destroy(D.scene);
+        D.scene = build_scene(scene);
+        ok(mcg_upload_scene(D.ctx, D.scene));
+        D.uploaded = &scene;
+    }
+    const int w = config.width ? config.width : scene.camera.width;
+    const int h = config.height ? config.height : scene.camera.height;
+    RenderResult result;
+    result.frame = FrameBuffers(w, h);
+    mcg_render_params p{};
+    p.width = w;
+    p.height = h;
+    p.spp = config.spp;
+    p.max_bounces = config.max_bounces;
+    p.cache_mode = config.cache_enabled ? MCG_CACHE_CONCURRENT : MCG_CACHE_OFF;
+    p.mip_offset = config.mip_offset;
+    p.n_cells = config.n_cells;
+    p.n_entries = config.n_entries;
+    p.rng_seed = config.rng_seed;
+    p.diffuse_spread = config.diffuse_spread;
+    p.tile_size = config.tile_size;
+    p.shard_count = 1;
+    mcg_cache* table = nullptr;
+    if (config.cache_enabled && external_cache) table = table_for(D, external_cache);
+    mcg_frame frame{result.frame.radiance.data(), result.frame.nodes_found.data(),
+                    result.frame.samples.data()};
+    std::vector<uint64_t> hps(static_cast<size_t>(std::max(config.spp, 0)), 0);
+    mcg_render_stats st{};
+    st.hits_per_sample = hps.data();
+    ok(mcg_render(D.ctx, &p, table, &frame, &st));
+    RenderStats& rs = result.stats;
+    rs.lookups = st.lookups;
+    rs.hits = st.hits;
+    rs.hit_rate = st.lookups ? static_cast<double>(st.hits) / static_cast<double>(st.lookups) : 0.0;
+    rs.inserts_won = st.inserts_won;
+    rs.inserts_lost_full = st.inserts_lost_full;
+    rs.stores_attempted = st.stores_attempted;
+    rs.instructions_executed = st.instructions_executed;
+    rs.hits_per_sample = std::move(hps);
+    rs.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return result;
+}
+
+// ---- FrameBuffers helpers and experiment outputs (tracer.hpp:24-92) --------
+
+ImageF FrameBuffers::radiance_image() const {
+    ImageF img(width, height);
+    for (size_t i = 0; i < img.pixels.size(); ++i) {
+        const double n = samples[i] ? static_cast<double>(samples[i]) : 1.0;
+        img.pixels[i] = {static_cast<float>(radiance[3 * i] / n),
+                         static_cast<float>(radiance[3 * i + 1] / n),
+                         static_cast<float>(radiance[3 * i + 2] / n)};
+    }
+    return img;
+}
+
+std::vector<float> FrameBuffers::nodes_found_avg() const {
+    std::vector<float> out(nodes_found.size());
+    for (size_t i = 0; i < out.size(); ++i) {
+        out[i] = static_cast<float>(nodes_found[i] / (samples[i] ? samples[i] : 1u));
+    }
+    return out;
+}
+
+Color3 FrameBuffers::mean_radiance() const {
+    const ImageF img = radiance_image();
+    double r = 0, g = 0, b = 0;
+    for (const Color3& c : img.pixels) {
+        r += c.r;
+        g += c.g;
+        b += c.b;
+    }
+    const double n = img.pixels.empty() ? 1.0 : static_cast<double>(img.pixels.size());
+    return {static_cast<float>(r / n), static_cast<float>(g / n), static_cast<float>(b / n)};
+}
+
+DiffStats image_error(const ImageF& a, const ImageF& b, float scale) {
+    if (a.width != b.width || a.height != b.height) {
+        throw std::invalid_argument("image_error: resolution mismatch");
+    }
+    DiffStats d;
+    d.diff = ImageF(a.width, a.height);
+    double sum = 0.0;
+    for (size_t i = 0; i < a.pixels.size(); ++i) {
+        const float ch[3] = {std::fabs(a.pixels[i].r - b.pixels[i].r),
+                             std::fabs(a.pixels[i].g - b.pixels[i].g),
+                             std::fabs(a.pixels[i].b - b.pixels[i].b)};
+        for (float c : ch) {
+            sum += c;
+            d.max_abs = std::max(d.max_abs, static_cast<double>(c));
+        }
+        d.diff.pixels[i] = {std::fmin(std::fmax(scale * ch[0], 0.0f), 1.0f),
+                            std::fmin(std::fmax(scale * ch[1], 0.0f), 1.0f),
+                            std::fmin(std::fmax(scale * ch[2], 0.0f), 1.0f)};
+    }
+    d.mean_abs = a.pixels.empty() ? 0.0 : sum / (3.0 * static_cast<double>(a.pixels.size()));
+    return d;
+}
+
+std::string stats_to_json(const RenderStats& s, const FrameBuffers& f) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "{\"wall_time_s\": " << s.wall_time_s << ", \"hits\": " << s.hits
+      << ", \"lookups\": " << s.lookups << ", \"hit_rate\": " << s.hit_rate
+      << ", \"inserts_won\": " << s.inserts_won << ", \"inserts_lost_full\": " << s.inserts_lost_full
+      << ", \"width\": " << f.width << ", \"height\": " << f.height << ", \"per_pixel_nodes_found\": [";
+    const std::vector<float> avg = f.nodes_found_avg();
+    for (size_t i = 0; i < avg.size(); ++i) o << (i ? ", " : "") << avg[i];
+    o << "]}";
+    return o.str();
+}
+
+StatsFile parse_stats_json(std::string_view text) {
+    auto number_after = [&](const std::string& key) -> double {
+        const size_t k = text.find("\"" + key + "\"");
+        if (k == std::string_view::npos) throw std::invalid_argument("stats JSON lacks " + key);
+        const size_t c = text.find(':', k);
+        return std::stod(std::string(text.substr(c + 1, 32)));
+    };
+    StatsFile out;
+    out.width = static_cast<int>(number_after("width"));
+    out.height = static_cast<int>(number_after("height"));
+    const size_t k = text.find("\"per_pixel_nodes_found\"");
+    if (k == std::string_view::npos) throw std::invalid_argument("stats JSON lacks per_pixel_nodes_found");
+    size_t i = text.find('[', k) + 1;
+    const size_t end = text.find(']', i);
+    while (i < end) {
+        const size_t comma = std::min(text.find(',', i), end);
+        const std::string tok(text.substr(i, comma - i));
+        if (tok.find_first_not_of(" \t\n") != std::string::npos) out.per_pixel_nodes_found.push_back(std::stof(tok));
+        i = comma + 1;
+    }
+    if (out.per_pixel_nodes_found.size() != static_cast<size_t>(out.width) * out.height) {
+        throw std::invalid_argument("per_pixel_nodes_found size does not match width*height");
+    }
+    return out;
+}
+
+}  // namespace matcache
