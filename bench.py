@@ -399,7 +399,9 @@ def main() -> None:
             "render_stats": {"hit_rate": st.hits / st.lookups if st.lookups else 0.0,
                              "lookups": st.lookups, "hits": st.hits, "inserts_won": st.inserts_won,
                              "inserts_lost_full": st.inserts_lost_full,
-                             "shading_points": st.shading_points, "shadow_rays": st.shadow_rays},
+                             "shading_points": st.shading_points, "shadow_rays": st.shadow_rays,
+                             "bvh_nodes": st.bvh_nodes, "prims_tested": st.prims_tested,
+                             "tex_samples": st.tex_samples},
             "cpu_baseline": cpu,
         }
         line.update(extras)

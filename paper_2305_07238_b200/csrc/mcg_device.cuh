@@ -32,50 +32,113 @@ struct Probe {
     bool hit;
 };
 
-// Scans a cell. The first 16 bytes are loaded first: in a sparse table the
-// scan ends there (one DRAM sector); otherwise the remaining words are
-// fetched together. Loads bypass L1 (ld.global.cg) so concurrent inserts
-// from other SMs are seen as early as L2 sees them.
-__device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, uint32_t check) {
+// One step of the reference scan (cache.cpp:127-134 / :99-116): an empty slot
+// ends it (miss, update() would CAS there), a matching check-hash is a hit.
+__device__ __forceinline__ bool scan_word(uint64_t w, int32_t idx, uint32_t check, Probe& r) {
+    if (w == 0ull) {
+        r.where = idx;
+        return true;
+    }
+    if (static_cast<uint32_t>(w >> 32) == check) {
+        r.hit = true;
+        r.where = idx;
+        r.payload = static_cast<uint32_t>(w);
+        return true;
+    }
+    return false;
+}
+
+// Scans a cell with 128-bit loads. kFirstPairs 16-byte pairs are fetched
+// before the first decision and the rest (cells up to Ne = 10 live in
+// registers) in one more round trip: kFirstPairs = 1 reads one DRAM sector
+// when the scan ends early (sparse tables), kFirstPairs = 5 fetches the whole
+// 80-byte cell at once (one round trip, full tables). Loads bypass L1
+// (ld.global.cg) so concurrent inserts from other SMs are seen as soon as L2
+// sees them.
+template <int kFirstPairs>
+__device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t base, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
     const uint64_t* cell = c.slots + base;
     uint32_t i = 0;
-    const bool aligned = ((base & 1ull) == 0ull);
-    if (aligned && ne >= 2) {
-        const ulonglong2 w = __ldcg(reinterpret_cast<const ulonglong2*>(cell));
-        if (w.x == 0ull) { r.where = 0; return r; }
-        if (static_cast<uint32_t>(w.x >> 32) == check) { r.hit = true; r.where = 0; r.payload = static_cast<uint32_t>(w.x); return r; }
-        if (w.y == 0ull) { r.where = 1; return r; }
-        if (static_cast<uint32_t>(w.y >> 32) == check) { r.hit = true; r.where = 1; r.payload = static_cast<uint32_t>(w.y); return r; }
-        i = 2;
-        // Remaining pairs, issued back to back (up to Ne = 16 in registers).
-        if (ne <= 16) {
-            ulonglong2 rest[7];
-            const uint32_t npairs = (ne - 2) / 2;
+    if ((base & 1ull) == 0ull && ne >= 2 && ne <= 10) {
+        const uint32_t npairs = ne >> 1;
+        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
+        ulonglong2 w[5];
 #pragma unroll
-            for (uint32_t k = 0; k < 7; ++k) {
-                if (k < npairs) rest[k] = __ldcg(reinterpret_cast<const ulonglong2*>(cell + 2 + 2 * k));
-            }
-#pragma unroll
-            for (uint32_t k = 0; k < 7; ++k) {
-                if (k >= npairs) break;
-                const uint64_t a = rest[k].x, b = rest[k].y;
-                const int32_t sa = static_cast<int32_t>(2 + 2 * k);
-                if (a == 0ull) { r.where = sa; return r; }
-                if (static_cast<uint32_t>(a >> 32) == check) { r.hit = true; r.where = sa; r.payload = static_cast<uint32_t>(a); return r; }
-                if (b == 0ull) { r.where = sa + 1; return r; }
-                if (static_cast<uint32_t>(b >> 32) == check) { r.hit = true; r.where = sa + 1; r.payload = static_cast<uint32_t>(b); return r; }
-            }
-            i = 2 + 2 * npairs;
+        for (int k = 0; k < 5; ++k) {
+            if (k < kFirstPairs && k < static_cast<int>(npairs)) w[k] = __ldcg(p + k);
         }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            if (k >= static_cast<int>(npairs)) break;
+            if (k == kFirstPairs) {
+#pragma unroll
+                for (int j = kFirstPairs; j < 5; ++j) {
+                    if (j < static_cast<int>(npairs)) w[j] = __ldcg(p + j);
+                }
+            }
+            if (scan_word(w[k].x, 2 * k, check, r) || scan_word(w[k].y, 2 * k + 1, check, r)) return r;
+        }
+        i = 2 * npairs;
     }
     for (; i < ne; ++i) {
-        const uint64_t w = __ldcg(cell + i);
-        if (w == 0ull) { r.where = static_cast<int32_t>(i); return r; }
-        if (static_cast<uint32_t>(w >> 32) == check) { r.hit = true; r.where = static_cast<int32_t>(i); r.payload = static_cast<uint32_t>(w); return r; }
+        if (scan_word(__ldcg(cell + i), static_cast<int32_t>(i), check, r)) return r;
     }
     return r;  // full, no match
+}
+
+__device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, uint32_t check) {
+    return probe_cell_t<1>(c, base, check);
+}
+
+// Warp-cooperative probe of up to 32 cells (one per lane of `mask`, n_entries
+// <= 32): each round the warp reads floor(32/Ne) whole cells with one 8-byte
+// load per lane (each cell one coalesced 8*Ne-byte access), all rounds issued
+// before any decision; per cell, ballots over its lanes give the first empty
+// slot and the first matching check-hash, i.e. the reference scan.
+template <int kNe>
+__device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, uint32_t check,
+                                            bool valid) {
+    constexpr int kPer = 32 / kNe;
+    constexpr int kRounds = (32 + kPer - 1) / kPer;
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int g = lane / kNe, word = lane - g * kNe;
+    uint64_t w[kRounds];
+#pragma unroll
+    for (int rd = 0; rd < kRounds; ++rd) {
+        const int owner = rd * kPer + g;
+        const uint64_t ob = __shfl_sync(kFull, base, owner & 31);
+        const bool ov = __shfl_sync(kFull, valid, owner & 31);
+        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(c.slots + ob + word) : ~0ull;
+    }
+    Probe mine{0u, -1, false};
+#pragma unroll
+    for (int rd = 0; rd < kRounds; ++rd) {
+#pragma unroll
+        for (int gg = 0; gg < kPer; ++gg) {
+            const int owner = rd * kPer + gg;
+            if (owner >= 32) break;
+            const uint32_t chk = __shfl_sync(kFull, check, owner);
+            const unsigned gm = ((1u << kNe) - 1u) << (gg * kNe);
+            const unsigned empty = __ballot_sync(kFull, w[rd] == 0ull) & gm;
+            const unsigned match = __ballot_sync(kFull, static_cast<uint32_t>(w[rd] >> 32) == chk) & gm;
+            const uint32_t pay = __shfl_sync(kFull, static_cast<uint32_t>(w[rd]),
+                                             match ? __ffs(match) - 1 : 0);
+            if (lane == owner) {
+                const int fe = empty ? __ffs(empty) - 1 - gg * kNe : kNe;
+                const int fm = match ? __ffs(match) - 1 - gg * kNe : kNe;
+                if (fm < fe) {
+                    mine.hit = true;
+                    mine.where = fm;
+                    mine.payload = pay;
+                } else {
+                    mine.where = fe < kNe ? fe : -1;
+                }
+            }
+        }
+    }
+    return mine;
 }
 
 // One CAS from zero on the slot the scan found empty (cache.cpp:108-114).

@@ -16,6 +16,8 @@
 // and k_accumulate adds each finished pass into the double framebuffers in
 // sample order (FrameBuffers, tracer.hpp:24-43).
 #include <chrono>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <vector>
 
@@ -61,7 +63,16 @@ struct RenderView {
     float4* sh1;              // normal.xyz, v
     float4* sh2;              // g1.xy, g2.xy
     float4* base;             // base colour from the VM
-    uint32_t* key;            // material slot, kInvalid if no hit this bounce
+    uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
+    uint32_t* vals;           // unsorted path ids
+    const uint32_t* skey;     // sorted keys: hits first, in material order
+    const uint32_t* order;    // sorted path ids
+    float4* sro;              // shadow ray per (path, light): origin.xyz, t_max
+    float4* srd;              // direction.xyz
+    float4* scon;             // contribution.rgb, candidate flag
+    uint8_t* vis;             // 1 = light visible
+    uint32_t* squeue;         // compacted shadow-ray slots
+    unsigned int* shadow_count;
     double* radiance;
     double* nodes_found;
     uint32_t* samples;
@@ -321,154 +332,762 @@ __device__ Surface surface(const mcgd::SceneView& S, V3 o, V3 d, uint32_t prim, 
     return s;
 }
 
-__device__ __forceinline__ void add_light(float4& L, V3 tf, const float* emit, float w) {
-    L.x = L.x + tf.x * (emit[0] * w);
-    L.y = L.y + tf.y * (emit[1] * w);
-    L.z = L.z + tf.z * (emit[2] * w);
+// Camera ray of path i (camera).
+__device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, uint64_t rkey,
+                                           V3& o, V3& d) {
+    const int x = static_cast<int>(pixel % static_cast<uint32_t>(R.W));
+    const int y = static_cast<int>(pixel / static_cast<uint32_t>(R.W));
+    const float jx = mcgd::path_sample(rkey, 0), jy = mcgd::path_sample(rkey, 1);
+    const float sx = ((static_cast<float>(x) + jx) / static_cast<float>(R.W)) * 2.0f - 1.0f;
+    const float sy = 1.0f - ((static_cast<float>(y) + jy) / static_cast<float>(R.H)) * 2.0f;
+    const float a = (sx * R.cam[9]) * R.cam[10];
+    const float bq = sy * R.cam[9];
+    const V3 fwd{R.cam[0], R.cam[1], R.cam[2]}, right{R.cam[3], R.cam[4], R.cam[5]},
+        up{R.cam[6], R.cam[7], R.cam[8]};
+    o = V3{R.cam_pos[0], R.cam_pos[1], R.cam_pos[2]};
+    d = mcgd::normalize((fwd + right * a) + up * bq);
 }
 
-// One wavefront step for path i: finish vertex b-1 (next-event estimation
-// over every light, then the cosine bounce) and trace vertex b.
-__global__ void __launch_bounds__(256) k_bounce(RenderView R, int b) {
+// Closest hit from (ro, rd) for path p; on a hit writes the shading record
+// (position, normal, uv, footprint gradients) and the propagated cone width
+// and returns the material slot, on a miss adds throughput * env to L and
+// returns n_programs (the "no hit" sort key).
+__device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p, float4& ro,
+                                                 const float4& rd, const float4& thr, float4& L,
+                                                 uint32_t& nvis, uint32_t& ntest) {
+    const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
+    uint32_t prim = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    if (!traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest)) {
+        L.x = L.x + thr.x * R.S.env[0];
+        L.y = L.y + thr.y * R.S.env[1];
+        L.z = L.z + thr.z * R.S.env[2];
+        return R.S.n_programs;
+    }
+    const Surface s = surface(R.S, o, d, prim, t, b1, b2);
+    const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+    float2 g1, g2;
+    mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+    R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+    R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+    R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+    ro.w = width;
+    return s.slot;
+}
+
+// Pass start: primary rays of every path of the pass, traced to vertex 0.
+__global__ void __launch_bounds__(256) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t shadow = 0, nvis = 0, ntest = 0;
+    uint32_t nvis = 0, ntest = 0;
     if (i < R.n_paths) {
         const uint32_t slot_j = i / R.n_pix;
         const uint32_t pixel = R.pix[i - slot_j * R.n_pix];
         const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
-        float4 ro, rd, thr, L;
-        bool alive = true;
-        if (b == 0) {
-            // Primary ray (camera).
-            const int x = static_cast<int>(pixel % static_cast<uint32_t>(R.W));
-            const int y = static_cast<int>(pixel / static_cast<uint32_t>(R.W));
-            const float jx = mcgd::path_sample(rkey, 0), jy = mcgd::path_sample(rkey, 1);
-            const float sx = ((static_cast<float>(x) + jx) / static_cast<float>(R.W)) * 2.0f - 1.0f;
-            const float sy = 1.0f - ((static_cast<float>(y) + jy) / static_cast<float>(R.H)) * 2.0f;
-            const float a = (sx * R.cam[9]) * R.cam[10];
-            const float bq = sy * R.cam[9];
-            const V3 fwd{R.cam[0], R.cam[1], R.cam[2]}, right{R.cam[3], R.cam[4], R.cam[5]},
-                up{R.cam[6], R.cam[7], R.cam[8]};
-            const V3 dir = mcgd::normalize((fwd + right * a) + up * bq);
-            ro = make_float4(R.cam_pos[0], R.cam_pos[1], R.cam_pos[2], 0.0f);
-            rd = make_float4(dir.x, dir.y, dir.z, R.cam[11]);
-            thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
-            L = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(1u));
+        V3 o, d;
+        camera_ray(R, pixel, rkey, o, d);
+        float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
+        const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
+        const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
+        float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const uint32_t key = trace_vertex(R, i, ro, rd, thr, L, nvis, ntest);
+        R.ro[i] = ro;
+        R.rd[i] = rd;
+        R.thr[i] = thr;
+        R.L[i] = L;
+        R.keys[i] = key;
+        R.vals[i] = i;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Next-event estimation and the cosine bounce of every shaded vertex b:
+// one shadow-ray candidate per (path, light) -- its contribution computed
+// now, applied in light order by k_resolve once visibility is known -- and
+// the continuation ray.
+__global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R.n_paths) return;
+    const uint32_t slot = R.skey[i];
+    if (slot >= R.S.n_programs) return;
+    const uint32_t p = R.order[i];
+    const uint32_t slot_j = p / R.n_pix;
+    const uint32_t pixel = R.pix[p - slot_j * R.n_pix];
+    const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
+    float4 thr = R.thr[p];
+    const float4 s0 = R.sh0[p], s1 = R.sh1[p], bc = R.base[p];
+    const V3 n{s1.x, s1.y, s1.z};
+    const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
+                 fminf(fmaxf(bc.z, 0.0f), 1.0f)};
+    const V3 f = alb * kInvPi;
+    const V3 tf{thr.x * f.x, thr.y * f.y, thr.z * f.z};
+    const V3 o = V3{s0.x, s0.y, s0.z} + n * kEps;
+    const uint32_t nl = R.S.n_plights + R.S.n_rlights;
+    const unsigned lane = threadIdx.x & 31u;
+    for (uint32_t j = 0; j < nl; ++j) {
+        const uint32_t s = p * nl + j;
+        bool cand = false;
+        V3 wi{0.0f, 0.0f, 0.0f};
+        float dist = 0.0f, w = 0.0f;
+        const float* emit;
+        if (j < R.S.n_plights) {
+            const mcg_point_light& l = R.S.plights[j];
+            const V3 toL = V3{l.position[0], l.position[1], l.position[2]} - o;
+            const float d2 = mcgd::dot(toL, toL);
+            dist = sqrtf(d2);
+            wi = toL * (1.0f / dist);
+            const float cs = mcgd::dot(n, wi);
+            cand = cs > 0.0f;
+            w = cs / d2;
+            emit = l.intensity;
         } else {
-            L = R.L[i];
-            if (__float_as_uint(L.w) == 0u) {
-                alive = false;
-            } else {
-                ro = R.ro[i];
-                rd = R.rd[i];
-                thr = R.thr[i];
-                const int pb = b - 1;
-                const float4 s0 = R.sh0[i], s1 = R.sh1[i], bc = R.base[i];
-                const V3 n{s1.x, s1.y, s1.z};
-                const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
-                             fminf(fmaxf(bc.z, 0.0f), 1.0f)};
-                const V3 f = alb * kInvPi;
-                const V3 tf{thr.x * f.x, thr.y * f.y, thr.z * f.z};
-                const V3 o = V3{s0.x, s0.y, s0.z} + n * kEps;
-                for (uint32_t li = 0; li < R.S.n_plights; ++li) {
-                    const mcg_point_light& l = R.S.plights[li];
-                    const V3 toL = V3{l.position[0], l.position[1], l.position[2]} - o;
-                    const float d2 = mcgd::dot(toL, toL);
-                    const float dist = sqrtf(d2);
-                    const V3 wi = toL * (1.0f / dist);
-                    const float cs = mcgd::dot(n, wi);
-                    if (cs > 0.0f) {
-                        ++shadow;
-                        if (!traverse_any(R.S, o, wi, kTMin, dist, nvis, ntest)) {
-                            add_light(L, tf, l.intensity, cs / d2);
+            const uint32_t jr = j - R.S.n_plights;
+            const mcg_rect_light& l = R.S.rlights[jr];
+            const float u = mcgd::path_sample(rkey, dim_rect(b, static_cast<int>(jr), 0));
+            const float vv = mcgd::path_sample(rkey, dim_rect(b, static_cast<int>(jr), 1));
+            const V3 eu{l.edge_u[0], l.edge_u[1], l.edge_u[2]};
+            const V3 ev{l.edge_v[0], l.edge_v[1], l.edge_v[2]};
+            const V3 pl = (V3{l.corner[0], l.corner[1], l.corner[2]} + eu * u) + ev * vv;
+            const V3 nlv = mcgd::cross(eu, ev);
+            const float area = mcgd::length(nlv);
+            const V3 toL = pl - o;
+            const float d2 = mcgd::dot(toL, toL);
+            dist = sqrtf(d2);
+            wi = toL * (1.0f / dist);
+            const float cs = mcgd::dot(n, wi);
+            const float cl = fabsf(mcgd::dot(nlv, wi)) / area;
+            cand = cs > 0.0f && cl > 0.0f;
+            w = ((cs * cl) * area) / d2;
+            emit = l.radiance;
+        }
+        if (cand) {
+            R.sro[s] = make_float4(o.x, o.y, o.z, dist);
+            R.srd[s] = make_float4(wi.x, wi.y, wi.z, 0.0f);
+            R.scon[s] = make_float4(tf.x * (emit[0] * w), tf.y * (emit[1] * w), tf.z * (emit[2] * w), 1.0f);
+        } else {
+            R.scon[s] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+        // Append to the shadow-ray queue: one atomic per warp.
+        const unsigned m = __ballot_sync(__activemask(), cand);
+        if (m) {
+            const int ldr = __ffs(m) - 1;
+            unsigned basepos = 0;
+            if (static_cast<int>(lane) == ldr) basepos = atomicAdd(R.shadow_count, static_cast<unsigned>(__popc(m)));
+            basepos = __shfl_sync(__activemask(), basepos, ldr);
+            if (cand) R.squeue[basepos + __popc(m & ((1u << lane) - 1u))] = s;
+        }
+    }
+    if (b < R.max_bounces) {
+        // Cosine-weighted bounce in Duff et al.'s branchless frame.
+        const float r1 = mcgd::path_sample(rkey, dim_bounce(b, 0));
+        const float r2 = mcgd::path_sample(rkey, dim_bounce(b, 1));
+        float sphi, cphi;
+        mcgd::det_sincosf(r1 * mcgd::kTwoPi, sphi, cphi);
+        const float r = sqrtf(r2);
+        const float lx = r * cphi, ly = r * sphi;
+        const float lz = sqrtf(fmaxf(0.0f, 1.0f - r2));
+        const float sign = copysignf(1.0f, n.z);
+        const float a = -1.0f / (sign + n.z);
+        const float bb = (n.x * n.y) * a;
+        const V3 t{1.0f + ((sign * n.x) * n.x) * a, sign * bb, -sign * n.x};
+        const V3 bt{bb, sign + ((n.y * n.y) * a), -n.y};
+        const V3 nd = mcgd::normalize((t * lx + bt * ly) + n * lz);
+        thr.x = thr.x * alb.x;
+        thr.y = thr.y * alb.y;
+        thr.z = thr.z * alb.z;
+        R.thr[p] = thr;
+        R.ro[p] = make_float4(o.x, o.y, o.z, R.ro[p].w);
+        const float4 rd = R.rd[p];
+        R.rd[p] = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
+    }
+}
+
+// Any-hit queries of the queued shadow rays (Scene::occluded, scene.cpp:280-298).
+__global__ void __launch_bounds__(256) k_shadow(RenderView R) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0, rays = 0;
+    if (q < *R.shadow_count) {
+        const uint32_t s = R.squeue[q];
+        const float4 so = R.sro[s], sd = R.srd[s];
+        R.vis[s] = traverse_any(R.S, V3{so.x, so.y, so.z}, V3{sd.x, sd.y, sd.z}, kTMin, so.w, nvis,
+                                ntest) ? 0 : 1;
+        rays = 1;
+    }
+    mcgd::warp_add(R.stats + kStatShadow, rays);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Finishes vertex b (adds the visible light contributions in light order,
+// exactly the oracle's summation order) and traces vertex b+1 of the paths
+// that continue; writes the next sort's (slot, path) pairs.
+__global__ void __launch_bounds__(256) k_resolve(RenderView R, int b) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    if (i < R.n_paths) {
+        const uint32_t slot = R.skey[i];
+        uint32_t key = R.S.n_programs;
+        uint32_t p = 0;
+        if (slot < R.S.n_programs) {
+            p = R.order[i];
+            float4 L = R.L[p];
+            const uint32_t nl = R.S.n_plights + R.S.n_rlights;
+            for (uint32_t j = 0; j < nl; ++j) {
+                const uint32_t s = p * nl + j;
+                const float4 c = R.scon[s];
+                if (c.w != 0.0f && R.vis[s]) {
+                    L.x = L.x + c.x;
+                    L.y = L.y + c.y;
+                    L.z = L.z + c.z;
+                }
+            }
+            if (b < R.max_bounces) {
+                float4 ro = R.ro[p];
+                const float4 rd = R.rd[p], thr = R.thr[p];
+                key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest);
+                if (key < R.S.n_programs) R.ro[p] = ro;
+            }
+            R.L[p] = L;
+        }
+        R.keys[i] = key;
+        R.vals[i] = p;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent ray traversal. Each resident warp keeps its lanes busy: whenever
+// at least kRefill lanes have finished their rays (or all have), the idle
+// lanes fetch the next rays from the job's queue with one atomic per warp.
+// Every lane walks its own ray exactly as traverse_closest / traverse_any do
+// -- same node order, same culling decisions -- one stack pop per loop
+// iteration, so short and long rays no longer hold each other's lanes idle.
+// ---------------------------------------------------------------------------
+constexpr int kRefill = 8;
+
+struct TraceJob {
+    const uint32_t* count;   // rays in the queue (device)
+    unsigned int* next;      // fetch cursor (device, zeroed before the launch)
+};
+
+// Closest hits of the paths continuing to vertex b (queue = the sorted hit
+// list of the previous vertex): writes the shading record and the next sort
+// pair (slot | n_programs, path).
+__global__ void __launch_bounds__(128) k_trace_closest(RenderView R, TraceJob J) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t count = *J.count;
+    uint32_t nvis = 0, ntest = 0, nhit = 0;
+    bool has = false, exhausted = false;
+    uint32_t q = 0, p = 0;
+    V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
+    float4 ro{}, rd{};
+    int32_t sa[64], sb[64];
+    float se[64];
+    int top = 0;
+    float closest = 0.0f, tt = 0.0f, tb1 = 0.0f, tb2 = 0.0f;
+    uint32_t prim = 0;
+    bool found = false;
+    for (;;) {
+        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
+        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
+            const int ldr = __ffs(idle) - 1;
+            unsigned base = 0;
+            if (static_cast<int>(lane) == ldr) base = atomicAdd(J.next, static_cast<unsigned>(__popc(idle)));
+            base = __shfl_sync(mcgd::kFull, base, ldr);
+            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
+            if (!has) {
+                q = base + __popc(idle & ((1u << lane) - 1u));
+                if (q < count) {
+                    has = true;
+                    p = R.order[q];
+                    ro = R.ro[p];
+                    rd = R.rd[p];
+                    o = V3{ro.x, ro.y, ro.z};
+                    d = V3{rd.x, rd.y, rd.z};
+                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+                    closest = __int_as_float(0x7f800000);
+                    found = false;
+                    top = 0;
+                    if (R.S.n_nodes) {
+                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
+                        float E, T1;
+                        slab(o, inv, lo, hi, kTMin, E, T1);
+                        if (!(T1 < E)) {
+                            const int32_t ra = __float_as_int(lo.w);
+                            sa[0] = ra >= 0 ? 0 : ra;
+                            sb[0] = __float_as_int(hi.w);
+                            se[0] = E;
+                            top = 1;
                         }
                     }
-                }
-                for (uint32_t j = 0; j < R.S.n_rlights; ++j) {
-                    const mcg_rect_light& l = R.S.rlights[j];
-                    const float u = mcgd::path_sample(rkey, dim_rect(pb, static_cast<int>(j), 0));
-                    const float vv = mcgd::path_sample(rkey, dim_rect(pb, static_cast<int>(j), 1));
-                    const V3 eu{l.edge_u[0], l.edge_u[1], l.edge_u[2]};
-                    const V3 ev{l.edge_v[0], l.edge_v[1], l.edge_v[2]};
-                    const V3 pl = (V3{l.corner[0], l.corner[1], l.corner[2]} + eu * u) + ev * vv;
-                    const V3 nl = mcgd::cross(eu, ev);
-                    const float area = mcgd::length(nl);
-                    const V3 toL = pl - o;
-                    const float d2 = mcgd::dot(toL, toL);
-                    const float dist = sqrtf(d2);
-                    const V3 wi = toL * (1.0f / dist);
-                    const float cs = mcgd::dot(n, wi);
-                    const float cl = fabsf(mcgd::dot(nl, wi)) / area;
-                    if (cs > 0.0f && cl > 0.0f) {
-                        ++shadow;
-                        if (!traverse_any(R.S, o, wi, kTMin, dist, nvis, ntest)) {
-                            add_light(L, tf, l.radiance, ((cs * cl) * area) / d2);
-                        }
-                    }
-                }
-                if (pb == R.max_bounces) {
-                    alive = false;
-                } else {
-                    // Cosine-weighted bounce in Duff et al.'s branchless frame.
-                    const float r1 = mcgd::path_sample(rkey, dim_bounce(pb, 0));
-                    const float r2 = mcgd::path_sample(rkey, dim_bounce(pb, 1));
-                    float sphi, cphi;
-                    mcgd::det_sincosf(r1 * mcgd::kTwoPi, sphi, cphi);
-                    const float r = sqrtf(r2);
-                    const float lx = r * cphi, ly = r * sphi;
-                    const float lz = sqrtf(fmaxf(0.0f, 1.0f - r2));
-                    const float sign = copysignf(1.0f, n.z);
-                    const float a = -1.0f / (sign + n.z);
-                    const float bb = (n.x * n.y) * a;
-                    const V3 t{1.0f + ((sign * n.x) * n.x) * a, sign * bb, -sign * n.x};
-                    const V3 bt{bb, sign + ((n.y * n.y) * a), -n.y};
-                    const V3 nd = mcgd::normalize((t * lx + bt * ly) + n * lz);
-                    thr.x = thr.x * alb.x;
-                    thr.y = thr.y * alb.y;
-                    thr.z = thr.z * alb.z;
-                    rd = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
-                    ro = make_float4(o.x, o.y, o.z, ro.w);
                 }
             }
         }
-        uint32_t key = R.S.n_programs;  // sorts after every material slot
-        if (alive) {
-            const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
-            uint32_t prim = 0;
-            float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-            if (!traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest)) {
+        if (__ballot_sync(mcgd::kFull, has) == 0) {
+            if (exhausted) break;
+            continue;
+        }
+        if (has && top > 0) {
+            --top;
+            const int32_t a = sa[top], b = sb[top];
+            ++nvis;
+            if (!(closest < se[top])) {
+                if (a < 0) {
+                    const uint32_t first = static_cast<uint32_t>(~a);
+                    ntest += static_cast<uint32_t>(b);
+                    for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
+                        float t, b1, b2;
+                        if (hit_prim(R.S, i, o, d, kTMin, closest, t, b1, b2)) {
+                            closest = t;
+                            prim = i;
+                            tt = t;
+                            tb1 = b1;
+                            tb2 = b2;
+                            found = true;
+                        }
+                    }
+                } else {
+                    const float4* pp = R.S.pairs + 4 * a;
+                    const float4 llo = __ldg(pp), lhi = __ldg(pp + 1), rlo = __ldg(pp + 2), rhi = __ldg(pp + 3);
+                    float EL, T1L, ER, T1R;
+                    slab(o, inv, llo, lhi, kTMin, EL, T1L);
+                    slab(o, inv, rlo, rhi, kTMin, ER, T1R);
+                    if (!(T1L < EL)) {
+                        sa[top] = __float_as_int(llo.w);
+                        sb[top] = __float_as_int(lhi.w);
+                        se[top] = EL;
+                        ++top;
+                    }
+                    if (!(T1R < ER)) {
+                        sa[top] = __float_as_int(rlo.w);
+                        sb[top] = __float_as_int(rhi.w);
+                        se[top] = ER;
+                        ++top;
+                    }
+                }
+            }
+        }
+        if (has && top == 0) {
+            // Ray finished: the vertex's shading record, or the environment.
+            uint32_t key = R.S.n_programs;
+            float4 L = R.L[p];
+            const float4 thr = R.thr[p];
+            if (!found) {
                 L.x = L.x + thr.x * R.S.env[0];
                 L.y = L.y + thr.y * R.S.env[1];
                 L.z = L.z + thr.z * R.S.env[2];
-                alive = false;
+                R.L[p] = L;
             } else {
-                const Surface s = surface(R.S, o, d, prim, t, b1, b2);
-                const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+                const Surface s = surface(R.S, o, d, prim, tt, tb1, tb2);
+                const float width = ro.w + tt * rd.w;  // propagate (raycone.cpp:15-18)
                 float2 g1, g2;
                 mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-                R.sh0[i] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-                R.sh1[i] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-                R.sh2[i] = make_float4(g1.x, g1.y, g2.x, g2.y);
-                ro.w = width;
+                R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+                R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+                R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+                R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
                 key = s.slot;
+                ++nhit;
             }
+            R.keys[q] = key;
+            R.vals[q] = p;
+            has = false;
         }
-        if (b == 0 || alive || __float_as_uint(L.w) != 0u) {
-            L.w = __uint_as_float(alive ? 1u : 0u);
-            R.L[i] = L;
-            if (alive) {
-                R.ro[i] = ro;
-                R.rd[i] = rd;
-                R.thr[i] = thr;
-            } else if (b == 0) {
-                R.thr[i] = thr;  // nodes_found = 0
-            }
-        }
-        R.key[i] = key;
     }
-    mcgd::warp_add(R.stats + kStatShadow, shadow);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Any-hit queries of the queued shadow rays (Scene::occluded,
+// scene.cpp:280-298), near child first, the first hit ends a ray.
+__global__ void __launch_bounds__(128) k_trace_shadow(RenderView R, TraceJob J) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t count = *J.count;
+    uint32_t nvis = 0, ntest = 0, nrays = 0;
+    bool has = false, exhausted = false;
+    uint32_t s = 0;
+    V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
+    float tmax = 0.0f;
+    int32_t sa[64], sb[64];
+    int top = 0;
+    bool hit = false;
+    for (;;) {
+        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
+        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
+            const int ldr = __ffs(idle) - 1;
+            unsigned base = 0;
+            if (static_cast<int>(lane) == ldr) base = atomicAdd(J.next, static_cast<unsigned>(__popc(idle)));
+            base = __shfl_sync(mcgd::kFull, base, ldr);
+            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
+            if (!has) {
+                const uint32_t qq = base + __popc(idle & ((1u << lane) - 1u));
+                if (qq < count) {
+                    has = true;
+                    ++nrays;
+                    s = R.squeue[qq];
+                    const float4 so = R.sro[s], sd = R.srd[s];
+                    o = V3{so.x, so.y, so.z};
+                    d = V3{sd.x, sd.y, sd.z};
+                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+                    tmax = so.w;
+                    hit = false;
+                    top = 0;
+                    if (R.S.n_nodes) {
+                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
+                        float E, T1;
+                        slab(o, inv, lo, hi, kTMin, E, T1);
+                        if (!(fminf(tmax, T1) < E)) {
+                            const int32_t ra = __float_as_int(lo.w);
+                            sa[0] = ra >= 0 ? 0 : ra;
+                            sb[0] = __float_as_int(hi.w);
+                            top = 1;
+                        }
+                    }
+                }
+            }
+        }
+        if (__ballot_sync(mcgd::kFull, has) == 0) {
+            if (exhausted) break;
+            continue;
+        }
+        if (has && top > 0) {
+            --top;
+            const int32_t a = sa[top], b = sb[top];
+            ++nvis;
+            if (a < 0) {
+                const uint32_t first = static_cast<uint32_t>(~a);
+                ntest += static_cast<uint32_t>(b);
+                for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
+                    float t, b1, b2;
+                    if (hit_prim(R.S, i, o, d, kTMin, tmax, t, b1, b2)) {
+                        hit = true;
+                        break;
+                    }
+                }
+                if (hit) top = 0;
+            } else {
+                const float4* pp = R.S.pairs + 4 * a;
+                const float4 llo = __ldg(pp), lhi = __ldg(pp + 1), rlo = __ldg(pp + 2), rhi = __ldg(pp + 3);
+                float EL, T1L, ER, T1R;
+                slab(o, inv, llo, lhi, kTMin, EL, T1L);
+                slab(o, inv, rlo, rhi, kTMin, ER, T1R);
+                const bool okL = !(fminf(tmax, T1L) < EL), okR = !(fminf(tmax, T1R) < ER);
+                const bool left_first = EL <= ER;
+                // push the far child first so the near one is popped next
+                if (left_first) {
+                    if (okR) { sa[top] = __float_as_int(rlo.w); sb[top] = __float_as_int(rhi.w); ++top; }
+                    if (okL) { sa[top] = __float_as_int(llo.w); sb[top] = __float_as_int(lhi.w); ++top; }
+                } else {
+                    if (okL) { sa[top] = __float_as_int(llo.w); sb[top] = __float_as_int(lhi.w); ++top; }
+                    if (okR) { sa[top] = __float_as_int(rlo.w); sb[top] = __float_as_int(rhi.w); ++top; }
+                }
+            }
+        }
+        if (has && top == 0) {
+            R.vis[s] = hit ? 0 : 1;
+            has = false;
+        }
+    }
+    mcgd::warp_add(R.stats + kStatShadow, nrays);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Non-persistent closest-hit over the live list (one thread per ray).
+__global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const uint32_t* count) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    if (q < *count) {
+        const uint32_t p = R.order[q];
+        float4 ro = R.ro[p];
+        const float4 rd = R.rd[p], thr = R.thr[p];
+        float4 L = R.L[p];
+        const uint32_t key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest);
+        if (key < R.S.n_programs) R.ro[p] = ro;
+        else R.L[p] = L;
+        R.keys[q] = key;
+        R.vals[q] = p;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-synchronous "while-while" traversal. Each lane walks its own ray in
+// exactly the order traverse_closest / traverse_any use; a lane that pops a
+// leaf parks on it until every lane of the warp holds a leaf or is done,
+// then all parked lanes test their triangles together. Leaf tests (the
+// expensive part) therefore run with most lanes active instead of a couple,
+// and no lane ever runs ahead of its own reference order. Every lane of the
+// warp must call these (inactive lanes pass active = false).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool closest_ww(const mcgd::SceneView& S, bool active, V3 o, V3 d,
+                                           float tmin, float tmax, uint32_t& prim, float& t_out,
+                                           float& b1_out, float& b2_out, uint32_t& nodes_visited,
+                                           uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t sa[64], sb[64];
+    float se[64];
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(T1 < E)) {
+            const int32_t ra = __float_as_int(lo.w);
+            sa[0] = ra >= 0 ? 0 : ra;
+            sb[0] = __float_as_int(hi.w);
+            se[0] = E;
+            top = 1;
+        }
+    }
+    bool found = false;
+    float closest = tmax;
+    int32_t la = 0, lb = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        // Phase 1: pop and expand until this lane holds a leaf (or is done).
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nodes_visited;
+                    if (!(closest < se[top])) {
+                        if (a < 0) {
+                            leaf = true;
+                            la = a;
+                            lb = b;
+                        } else {
+                            const float4* p = S.pairs + 4 * a;
+                            const float4 llo = __ldg(p), lhi = __ldg(p + 1), rlo = __ldg(p + 2), rhi = __ldg(p + 3);
+                            float EL, T1L, ER, T1R;
+                            slab(o, inv, llo, lhi, tmin, EL, T1L);
+                            slab(o, inv, rlo, rhi, tmin, ER, T1R);
+                            if (!(T1L < EL)) {
+                                sa[top] = __float_as_int(llo.w);
+                                sb[top] = __float_as_int(lhi.w);
+                                se[top] = EL;
+                                ++top;
+                            }
+                            if (!(T1R < ER)) {
+                                sa[top] = __float_as_int(rlo.w);
+                                sb[top] = __float_as_int(rhi.w);
+                                se[top] = ER;
+                                ++top;
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        // Phase 2: every parked lane tests its leaf (the reference's order).
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            prims_tested += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                    closest = t;
+                    prim = i;
+                    t_out = t;
+                    b1_out = b1;
+                    b2_out = b2;
+                    found = true;
+                }
+            }
+            leaf = false;
+            done = top == 0;
+        }
+    }
+    return found;
+}
+
+__device__ __forceinline__ bool any_ww(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                       float tmax, uint32_t& nodes_visited, uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t sa[64], sb[64];
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(fminf(tmax, T1) < E)) {
+            const int32_t ra = __float_as_int(lo.w);
+            sa[0] = ra >= 0 ? 0 : ra;
+            sb[0] = __float_as_int(hi.w);
+            top = 1;
+        }
+    }
+    bool hit = false;
+    int32_t la = 0, lb = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nodes_visited;
+                    if (a < 0) {
+                        leaf = true;
+                        la = a;
+                        lb = b;
+                    } else {
+                        const float4* p = S.pairs + 4 * a;
+                        const float4 llo = __ldg(p), lhi = __ldg(p + 1), rlo = __ldg(p + 2), rhi = __ldg(p + 3);
+                        float EL, T1L, ER, T1R;
+                        slab(o, inv, llo, lhi, tmin, EL, T1L);
+                        slab(o, inv, rlo, rhi, tmin, ER, T1R);
+                        const bool okL = !(fminf(tmax, T1L) < EL), okR = !(fminf(tmax, T1R) < ER);
+                        // far child first so the near one is popped next
+                        const bool lf = EL <= ER;
+                        if (lf ? okR : okL) {
+                            sa[top] = __float_as_int(lf ? rlo.w : llo.w);
+                            sb[top] = __float_as_int(lf ? rhi.w : lhi.w);
+                            ++top;
+                        }
+                        if (lf ? okL : okR) {
+                            sa[top] = __float_as_int(lf ? llo.w : rlo.w);
+                            sb[top] = __float_as_int(lf ? lhi.w : rhi.w);
+                            ++top;
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            prims_tested += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            done = hit || top == 0;
+        }
+    }
+    return hit;
+}
+
+// Shadow rays, one per thread over the queue, warp-synchronous traversal.
+__global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    const bool active = q < *R.shadow_count;
+    uint32_t s = 0;
+    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
+    float tmax = 0.0f;
+    if (active) {
+        s = R.squeue[q];
+        const float4 so = R.sro[s], sd = R.srd[s];
+        o = V3{so.x, so.y, so.z};
+        d = V3{sd.x, sd.y, sd.z};
+        tmax = so.w;
+    }
+    const bool occ = any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
+    if (active) R.vis[s] = occ ? 0 : 1;
+    mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Closest hits of the live paths, one per thread, warp-synchronous traversal.
+__global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const uint32_t* count) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    const bool active = q < *count;
+    uint32_t p = 0;
+    float4 ro{}, rd{};
+    if (active) {
+        p = R.order[q];
+        ro = R.ro[p];
+        rd = R.rd[p];
+    }
+    const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
+    uint32_t prim = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    const bool found = closest_ww(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
+                                  nvis, ntest);
+    if (active) {
+        uint32_t key = R.S.n_programs;
+        if (!found) {
+            float4 L = R.L[p];
+            const float4 thr = R.thr[p];
+            L.x = L.x + thr.x * R.S.env[0];
+            L.y = L.y + thr.y * R.S.env[1];
+            L.z = L.z + thr.z * R.S.env[2];
+            R.L[p] = L;
+        } else {
+            const Surface s = surface(R.S, o, d, prim, t, b1, b2);
+            const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+            float2 g1, g2;
+            mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+            R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+            R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+            R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+            R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
+            key = s.slot;
+        }
+        R.keys[q] = key;
+        R.vals[q] = p;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// Finishes vertex b: adds the visible light contributions in light order
+// (the oracle's summation order); writes "no hit" sort keys for the slots
+// past the live list and for every path at the last vertex.
+__global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R.n_paths) return;
+    const uint32_t slot = R.skey[i];
+    const bool live = slot < R.S.n_programs;
+    if (live) {
+        const uint32_t p = R.order[i];
+        const uint32_t nl = R.S.n_plights + R.S.n_rlights;
+        if (nl) {
+            float4 L = R.L[p];
+            for (uint32_t j = 0; j < nl; ++j) {
+                const uint32_t s = p * nl + j;
+                const float4 c = R.scon[s];
+                if (c.w != 0.0f && R.vis[s]) {
+                    L.x = L.x + c.x;
+                    L.y = L.y + c.y;
+                    L.z = L.z + c.z;
+                }
+            }
+            R.L[p] = L;
+        }
+    }
+    if (!live || b >= R.max_bounces) {
+        R.keys[i] = R.S.n_programs;
+        R.vals[i] = 0;
+    }
+}
+
+// Number of live paths after a sort (hits sort first): the first index whose
+// key is "no hit", found by the warp that straddles the boundary.
+__global__ void k_count_live(RenderView R, uint32_t* live) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R.n_paths) return;
+    const bool v = R.skey[i] < R.S.n_programs;
+    const bool prev = i == 0 ? true : R.skey[i - 1] < R.S.n_programs;
+    if (!v && prev) *live = i;
+    if (v && i + 1 == R.n_paths) *live = R.n_paths;
 }
 
 // Material evaluation of every live hit, in material order.
@@ -625,9 +1244,12 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         }
     }
 
-    // Path state: 10 float4 + 3 u32 per path, plus sort buffers.
+    // Path state: 8 float4 per path; shadow rays: 3 float4 + 1 byte per
+    // (path, light); sort keys/values and the shadow queue as u32.
+    const uint32_t n_lights = D.view.n_plights + D.view.n_rlights;
+    const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
-    ctx->path_mem.ensure(f4 * 8 + max_paths * 4 * 4 + n_pix * 4ull + 256);
+    ctx->path_mem.ensure(f4 * 8 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 4 + n_pix * 4ull + 1024);
     char* base = ctx->path_mem.as<char>();
     RenderView R{};
     R.S = D.view;
@@ -650,19 +1272,22 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.sh1 = R.sh0 + max_paths;
     R.sh2 = R.sh1 + max_paths;
     R.base = R.sh2 + max_paths;
-    uint32_t* u32 = reinterpret_cast<uint32_t*>(R.base + max_paths);
-    R.key = u32;
-    uint32_t* skey = u32 + max_paths;
-    uint32_t* iota = u32 + 2 * max_paths;
+    R.sro = R.base + max_paths;
+    R.srd = R.sro + n_shadow;
+    R.scon = R.srd + n_shadow;
+    uint32_t* u32 = reinterpret_cast<uint32_t*>(R.scon + n_shadow);
+    R.keys = u32;
+    R.vals = u32 + max_paths;
+    uint32_t* skey = u32 + 2 * max_paths;
     uint32_t* order = u32 + 3 * max_paths;
-    uint32_t* d_pix = u32 + 4 * max_paths;
+    R.skey = skey;
+    R.order = order;
+    R.squeue = u32 + 4 * max_paths;
+    uint32_t* d_pix = R.squeue + n_shadow;
     R.pix = d_pix;
+    R.shadow_count = reinterpret_cast<unsigned int*>(d_pix + n_pix);
+    R.vis = reinterpret_cast<uint8_t*>(R.shadow_count + 64);
     cuda_check(cudaMemcpyAsync(d_pix, pix.data(), n_pix * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D pixels");
-    {
-        LaunchScope ls(ctx, "iota", max_paths * 4.0);
-        k_iota<<<grid_for(max_paths, 256), 256, 0, ctx->stream>>>(iota, static_cast<uint32_t>(max_paths));
-        ls.done();
-    }
     R.radiance = d_rad;
     R.nodes_found = d_nodes;
     R.samples = d_samples;
@@ -681,7 +1306,16 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.q.count = reinterpret_cast<unsigned int*>(R.q.keys + 4 * cap);
         R.q.capacity = static_cast<unsigned>(cap);
     }
-    const int key_bits = std::max(1, bits_for(D.view.n_programs));  // holds kInvalid-remapped slots
+    const int key_bits = std::max(1, bits_for(D.view.n_programs));
+    int occ_any = 1, occ_closest = 1, n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_any, k_trace_shadow, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_closest, k_trace_closest, 128, 0);
+    const unsigned persist_grid_any = static_cast<unsigned>(n_sm * std::max(1, occ_any));
+    const unsigned persist_grid_closest = static_cast<unsigned>(n_sm * std::max(1, occ_closest));
+    const char* trace_env = std::getenv("MCG_TRACE");
+    const bool persistent = trace_env && std::string(trace_env) == "persistent";
+    const bool plain = trace_env && std::string(trace_env) == "plain";  // holds kInvalid-remapped slots
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
@@ -695,16 +1329,22 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.sample0 = P.first_sample + start;
         R.hps_base = start;
         const unsigned grid = grid_for(R.n_paths, 256);
-        for (int b = 0; b <= P.max_bounces + 1; ++b) {
+        {
+            LaunchScope ls(ctx, "primary", 0.0);
+            k_primary<<<grid, 256, 0, ctx->stream>>>(R);
+            ls.done();
+        }
+        for (int b = 0; b <= P.max_bounces; ++b) {
+            // Stable radix sort of (slot -> path): hits in material order
+            // first, paths without a hit (key n_programs) last.
+            sort_pairs_u32(ctx, R.keys, skey, R.vals, order, R.n_paths, key_bits);
+            // counters: [0] shadow rays queued, [1] shadow cursor, [2] live paths, [3] trace cursor
+            cuda_check(cudaMemsetAsync(R.shadow_count, 0, 16, ctx->stream), "memset");
             {
-                LaunchScope ls(ctx, "bounce", 0.0);
-                k_bounce<<<grid, 256, 0, ctx->stream>>>(R, b);
+                LaunchScope ls(ctx, "count_live", 0.0);
+                k_count_live<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
                 ls.done();
             }
-            if (b > P.max_bounces) break;
-            // Stable radix sort of (slot -> path); paths without a hit carry
-            // key n_programs and sort last.
-            sort_pairs_u32(ctx, R.key, skey, iota, order, R.n_paths, key_bits);
             if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, ctx->stream), "memset");
             {
                 LaunchScope ls(ctx, "shade", 0.0);
@@ -730,6 +1370,38 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                     // apply_ordered adds won/full at counters[2]/[3] == kStatWon/kStatFull.
                     apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, R.stats);
                 }
+            }
+            {
+                LaunchScope ls(ctx, "nee", 0.0);
+                k_nee<<<grid, 256, 0, ctx->stream>>>(R, b);
+                ls.done();
+            }
+            if (n_lights) {
+                LaunchScope ls(ctx, "trace_shadow", 0.0);
+                if (persistent) {
+                    k_trace_shadow<<<persist_grid_any, 128, 0, ctx->stream>>>(R, TraceJob{R.shadow_count, R.shadow_count + 1});
+                } else if (plain) {
+                    k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                } else {
+                    k_shadow_ww<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                }
+                ls.done();
+            }
+            {
+                LaunchScope ls(ctx, "resolve_lights", 0.0);
+                k_resolve_lights<<<grid, 256, 0, ctx->stream>>>(R, b);
+                ls.done();
+            }
+            if (b < P.max_bounces) {
+                LaunchScope ls(ctx, "trace_closest", 0.0);
+                if (persistent) {
+                    k_trace_closest<<<persist_grid_closest, 128, 0, ctx->stream>>>(R, TraceJob{R.shadow_count + 2, R.shadow_count + 3});
+                } else if (plain) {
+                    k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
+                } else {
+                    k_trace_closest_ww<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
+                }
+                ls.done();
             }
         }
         {

