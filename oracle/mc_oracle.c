@@ -224,18 +224,17 @@ uint8_t mco_mip_level(const float g1[2], const float g2[2], int off) {
     V2 a = {g1[0], g1[1]}, b = {g2[0], g2[1]};
     const float m = fminf(v2_len(a), v2_len(b));
     if (!(m > 0.0f)) return 24;
-    int level;
+    int32_t lv;
     if (isinf(m)) {
-        level = 0;
+        /* floor(-log2(inf)) = -inf converts to INT_MIN on x86-64 (cvttsd2si),
+         * and the reference's `+ mip_offset` then wraps: mirror that. */
+        lv = (int32_t)(0x80000000u + (uint32_t)off);
     } else {
         int e;
         const double f = frexp((double)m, &e);
-        const int fl = f == 0.5 ? 1 - e : -e;
-        long long lv = (long long)fl + off;
-        level = lv < 0 ? 0 : (lv > 24 ? 24 : (int)lv);
-        return (uint8_t)level;
+        lv = (f == 0.5 ? 1 - e : -e) + off;
     }
-    return (uint8_t)level;
+    return (uint8_t)(lv < 0 ? 0 : (lv > 24 ? 24 : lv));
 }
 
 /* texel_indices: src/raycone.cpp:75-83 */

@@ -106,10 +106,16 @@ __device__ __forceinline__ uint32_t mip_level(float g1x, float g1y, float g2x, f
                                               int offset) {
     const float m = fminf(len2(g1x, g1y), len2(g2x, g2y));
     if (!(m > 0.0f)) return kMaxMip;
-    if (isinf(m)) return 0;
-    int e;
-    const double f = frexp(static_cast<double>(m), &e);
-    const long long lv = static_cast<long long>(f == 0.5 ? 1 - e : -e) + offset;
+    int32_t lv;
+    if (isinf(m)) {
+        // The reference converts floor(-inf) to INT_MIN (x86-64 cvttsd2si)
+        // and adds the offset with wrap-around.
+        lv = static_cast<int32_t>(0x80000000u + static_cast<uint32_t>(offset));
+    } else {
+        int e;
+        const double f = frexp(static_cast<double>(m), &e);
+        lv = (f == 0.5 ? 1 - e : -e) + offset;
+    }
     return static_cast<uint32_t>(lv < 0 ? 0 : (lv > kMaxMip ? kMaxMip : lv));
 }
 

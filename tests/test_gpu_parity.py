@@ -55,10 +55,13 @@ def test_descriptor_pipeline_matches_oracle_1e6(ctx, oracle):
     words = r.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
     np.testing.assert_array_equal(bits(ctx.decode_batch(words)), bits(oracle.decode(words)))
     uv = r.uniform(-1e3, 1e3, (n, 2)).astype(np.float32)
-    g1 = (np.exp(r.uniform(-40, 3, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
-    g2 = (np.exp(r.uniform(-40, 3, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
+    uv[::211] = np.float32(np.nan)
+    g1 = (np.exp(r.uniform(-104, 88, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
+    g2 = (np.exp(r.uniform(-104, 88, (n, 2))) * r.choice([-1, 1], (n, 2))).astype(np.float32)
     g1[::101] = 0
-    for off in (-3, 0, 5):
+    g2[::103] = np.float32(np.inf)
+    g1[::107] = np.float32(np.nan)
+    for off in (-30, -3, 0, 5):
         m1, t1 = ctx.mip_texel_batch(uv, g1, g2, off)
         m2, t2 = oracle.mip_texel(uv, g1, g2, off)
         np.testing.assert_array_equal(m1, m2)
