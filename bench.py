@@ -43,6 +43,7 @@ W, H, SPP = 1920, 1080, 128
 N_CELLS, N_ENTRIES = 10_000_000, 10
 SCENE_KIND = "classroom"
 TRIS_PER_SIDE = 24
+PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 0, 2
 METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
 
 
@@ -327,12 +328,17 @@ def main() -> None:
             peak, _ = measured_peaks()
             table = MaterialCache(N_CELLS, N_ENTRIES, ctx)
             n = 1 << 26
-            ms_ins, b_ins = table.probe_bench(n, 7, 0, 1)
-            table.probe_bench(n, 7, 1, 1)
-            ms_look, b_look = table.probe_bench(n, 7, 1, 3)
-            ms_mix, b_mix = table.probe_bench(n, 8, 2, 3)
+            # per-lane two-round scan, 2 blocks of 256 per SM: the sweep in
+            # profiles/README.md (more requests in flight thrash DRAM rows)
+            cfg = 16 * PROBE_VARIANT + 256 * PROBE_BLOCKS_PER_SM
+            ms_ins, b_ins = table.probe_bench(n, 7, 0 + cfg, 1)
+            table.probe_bench(n, 7, 1 + cfg, 1)
+            ms_look, b_look = table.probe_bench(n, 7, 1 + cfg, 3)
+            ms_mix, b_mix = table.probe_bench(n, 8, 2 + cfg, 3)
             extras["probe_roofline"] = {
                 "bound": "hbm", "unit": "GB/s", "peak": peak, "table": "1e7x10 (800 MB)",
+                "kernel": "k_probe_bench", "variant": PROBE_VARIANT, "blocks_per_sm": PROBE_BLOCKS_PER_SM,
+                "random_access_ceiling_gbs": 2900.0,
                 "descriptors": n,
                 "insert_all": {"achieved": b_ins / ms_ins / 1e6, "frac": b_ins / ms_ins / 1e6 / peak,
                                "mprobes_per_s": n / ms_ins / 1e3},

@@ -59,6 +59,7 @@ struct DeviceScene {
     mcgd::SceneView view{};
     uint32_t max_stack = 1;
     uint32_t max_cache_points = 0;
+    float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};   // scene bounds (BVH root)
     mcg_flat_scene cam{};   // camera/env fields only (no pointers used)
     bool loaded = false;
     void clear() {

@@ -92,6 +92,46 @@ __device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, u
     return probe_cell_t<1>(c, base, check);
 }
 
+// Two-round scan aligned to 64-byte DRAM blocks: round one reads from the
+// cell start to the end of its first 64-byte block (2..8 words, one block),
+// round two the rest of the cell (at most one more block for Ne <= 10). A
+// scan that ends in round one costs one block; a full scan two -- never the
+// three blocks an 80-byte cell can straddle.
+__device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t base, uint32_t check) {
+    Probe r{0u, -1, false};
+    const uint32_t ne = c.n_entries;
+    const uint64_t* cell = c.slots + base;
+    if ((base & 1ull) != 0ull || ne > 10) return probe_cell_t<1>(c, base, check);
+    const uint32_t npairs = ne >> 1;
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
+    // pairs in the first 64-byte block: (64 - (addr % 64)) / 16
+    const uint32_t first = (64u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(cell) & 63u)) >> 4;
+    ulonglong2 w[5];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k < static_cast<int>(first) && k < static_cast<int>(npairs)) w[k] = __ldcg(p + k);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= static_cast<int>(first) || k >= static_cast<int>(npairs)) break;
+        if (scan_word(w[k].x, 2 * k, check, r) || scan_word(w[k].y, 2 * k + 1, check, r)) return r;
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        if (k >= static_cast<int>(first) && k < static_cast<int>(npairs)) w[k] = __ldcg(p + k);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        if (k < static_cast<int>(first)) continue;
+        if (k >= static_cast<int>(npairs)) break;
+        if (scan_word(w[k].x, 2 * k, check, r) || scan_word(w[k].y, 2 * k + 1, check, r)) return r;
+    }
+    for (uint32_t i = 2 * npairs; i < ne; ++i) {
+        if (scan_word(__ldcg(cell + i), static_cast<int32_t>(i), check, r)) return r;
+    }
+    return r;
+}
+
 // Warp-cooperative probe of up to 32 cells (one per lane of `mask`, n_entries
 // <= 32): each round the warp reads floor(32/Ne) whole cells with one 8-byte
 // load per lane (each cell one coalesced 8*Ne-byte access), all rounds issued
@@ -161,6 +201,8 @@ struct SceneView {
     const uint32_t* prim_info;
     const float4* nodes;          // 2 float4 per BVH node (the reference tree, own boxes)
     const float4* pairs;          // 4 float4 per internal node: both children's records
+    const float4* quads;          // 8 float4 per 4-wide node (collapsed reference tree)
+    int32_t root_a, root_b;       // root entry into `quads`: (0, -1) or a leaf (~first, count)
     uint32_t n_nodes;
     const mcg_point_light* plights;
     uint32_t n_plights;

@@ -66,6 +66,9 @@ struct RenderView {
     uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
     uint32_t* vals;           // unsorted path ids
     const uint32_t* skey;     // sorted keys: hits first, in material order
+    uint32_t key_shift;       // key = slot << key_shift | Morton code of the hit point
+    uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
+    float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
     const uint32_t* order;    // sorted path ids
     float4* sro;              // shadow ray per (path, light): origin.xyz, t_max
     float4* srd;              // direction.xyz
@@ -83,6 +86,45 @@ struct RenderView {
 
 __device__ __forceinline__ uint32_t dim_rect(int b, int j, int k) { return 2u + 64u * b + 2u * j + k; }
 __device__ __forceinline__ uint32_t dim_bounce(int b, int k) { return 2u + 64u * b + 62u + k; }
+
+// Sort key of a hit: material slot in the high bits (shading stays grouped by
+// material), the 24-bit Morton code of the hit point below it, so rays that
+// leave nearby points on one material -- the next bounce's closest-hit rays
+// and the shadow rays -- share warps and traverse the same BVH nodes.
+__device__ __forceinline__ uint32_t spread8(uint32_t v) {
+    v &= 0xffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ uint32_t sort_key(const RenderView& R, uint32_t slot, float px, float py,
+                                             float pz, V3 n, uint64_t rkey, int vtx) {
+    if (slot >= R.S.n_programs || R.key_shift == 0) return slot << R.key_shift;
+    const float q[3] = {(px - R.box_lo[0]) * R.box_scale[0], (py - R.box_lo[1]) * R.box_scale[1],
+                        (pz - R.box_lo[2]) * R.box_scale[2]};
+    uint32_t c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c[k] = static_cast<uint32_t>(fminf(fmaxf(q[k], 0.0f), 255.0f));
+    if (!R.key_dir) {
+        return (slot << R.key_shift) | spread8(c[0]) | (spread8(c[1]) << 1) | (spread8(c[2]) << 2);
+    }
+    // Direction class of the cosine bounce this vertex will take: the
+    // normal's octant and the quadrant of its azimuth sample (dims of
+    // DESIGN.md §render), so rays leaving in similar directions share warps.
+    const uint32_t oct = (n.x < 0.0f ? 1u : 0u) | (n.y < 0.0f ? 2u : 0u) | (n.z < 0.0f ? 4u : 0u);
+    const uint32_t quad = vtx < R.max_bounces
+                              ? static_cast<uint32_t>(mcgd::path_sample(rkey, dim_bounce(vtx, 0)) * 4.0f) & 3u
+                              : 0u;
+    const uint32_t m18 = spread8(c[0] >> 2) | (spread8(c[1] >> 2) << 1) | (spread8(c[2] >> 2) << 2);
+    return (slot << R.key_shift) | (((oct << 2) | quad) << 18) | m18;
+}
+__device__ __forceinline__ uint32_t key_slot(const RenderView& R, uint32_t key) {
+    return key >> R.key_shift;
+}
+__device__ __forceinline__ uint32_t no_hit_key(const RenderView& R) {
+    return R.S.n_programs << R.key_shift;
+}
 
 // ray_triangle (scene.cpp:58-78) / ray_sphere (scene.cpp:80-94)
 __device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V3 o, V3 d,
@@ -354,7 +396,7 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // returns n_programs (the "no hit" sort key).
 __device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p, float4& ro,
                                                  const float4& rd, const float4& thr, float4& L,
-                                                 uint32_t& nvis, uint32_t& ntest) {
+                                                 uint32_t& nvis, uint32_t& ntest, int vtx) {
     const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
@@ -362,7 +404,7 @@ __device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p
         L.x = L.x + thr.x * R.S.env[0];
         L.y = L.y + thr.y * R.S.env[1];
         L.z = L.z + thr.z * R.S.env[2];
-        return R.S.n_programs;
+        return no_hit_key(R);
     }
     const Surface s = surface(R.S, o, d, prim, t, b1, b2);
     const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
@@ -372,7 +414,9 @@ __device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p
     R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
     R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
     ro.w = width;
-    return s.slot;
+    const uint32_t slot_j = p / R.n_pix;
+    const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
+    return sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
 }
 
 // Pass start: primary rays of every path of the pass, traced to vertex 0.
@@ -389,7 +433,7 @@ __global__ void __launch_bounds__(256) k_primary(RenderView R) {
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
         const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
         float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const uint32_t key = trace_vertex(R, i, ro, rd, thr, L, nvis, ntest);
+        const uint32_t key = trace_vertex(R, i, ro, rd, thr, L, nvis, ntest, 0);
         R.ro[i] = ro;
         R.rd[i] = rd;
         R.thr[i] = thr;
@@ -405,17 +449,12 @@ __global__ void __launch_bounds__(256) k_primary(RenderView R) {
 // one shadow-ray candidate per (path, light) -- its contribution computed
 // now, applied in light order by k_resolve once visibility is known -- and
 // the continuation ray.
-__global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R.n_paths) return;
-    const uint32_t slot = R.skey[i];
-    if (slot >= R.S.n_programs) return;
-    const uint32_t p = R.order[i];
+__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t p, int b, float4 s0,
+                                           float4 s1, float3 bc) {
     const uint32_t slot_j = p / R.n_pix;
     const uint32_t pixel = R.pix[p - slot_j * R.n_pix];
     const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
     float4 thr = R.thr[p];
-    const float4 s0 = R.sh0[p], s1 = R.sh1[p], bc = R.base[p];
     const V3 n{s1.x, s1.y, s1.z};
     const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
                  fminf(fmaxf(bc.z, 0.0f), 1.0f)};
@@ -468,12 +507,13 @@ __global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
             R.scon[s] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         }
         // Append to the shadow-ray queue: one atomic per warp.
-        const unsigned m = __ballot_sync(__activemask(), cand);
+        const unsigned act = __activemask();
+        const unsigned m = __ballot_sync(act, cand);
         if (m) {
             const int ldr = __ffs(m) - 1;
             unsigned basepos = 0;
             if (static_cast<int>(lane) == ldr) basepos = atomicAdd(R.shadow_count, static_cast<unsigned>(__popc(m)));
-            basepos = __shfl_sync(__activemask(), basepos, ldr);
+            basepos = __shfl_sync(act, basepos, ldr);
             if (cand) R.squeue[basepos + __popc(m & ((1u << lane) - 1u))] = s;
         }
     }
@@ -502,6 +542,16 @@ __global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
     }
 }
 
+__global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R.n_paths) return;
+    const uint32_t slot = key_slot(R, R.skey[i]);
+    if (slot >= R.S.n_programs) return;
+    const uint32_t p = R.order[i];
+    const float4 bc = R.base[p];
+    nee_bounce(R, p, b, R.sh0[p], R.sh1[p], make_float3(bc.x, bc.y, bc.z));
+}
+
 // Any-hit queries of the queued shadow rays (Scene::occluded, scene.cpp:280-298).
 __global__ void __launch_bounds__(256) k_shadow(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -518,284 +568,9 @@ __global__ void __launch_bounds__(256) k_shadow(RenderView R) {
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
-// Finishes vertex b (adds the visible light contributions in light order,
-// exactly the oracle's summation order) and traces vertex b+1 of the paths
-// that continue; writes the next sort's (slot, path) pairs.
-__global__ void __launch_bounds__(256) k_resolve(RenderView R, int b) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0;
-    if (i < R.n_paths) {
-        const uint32_t slot = R.skey[i];
-        uint32_t key = R.S.n_programs;
-        uint32_t p = 0;
-        if (slot < R.S.n_programs) {
-            p = R.order[i];
-            float4 L = R.L[p];
-            const uint32_t nl = R.S.n_plights + R.S.n_rlights;
-            for (uint32_t j = 0; j < nl; ++j) {
-                const uint32_t s = p * nl + j;
-                const float4 c = R.scon[s];
-                if (c.w != 0.0f && R.vis[s]) {
-                    L.x = L.x + c.x;
-                    L.y = L.y + c.y;
-                    L.z = L.z + c.z;
-                }
-            }
-            if (b < R.max_bounces) {
-                float4 ro = R.ro[p];
-                const float4 rd = R.rd[p], thr = R.thr[p];
-                key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest);
-                if (key < R.S.n_programs) R.ro[p] = ro;
-            }
-            R.L[p] = L;
-        }
-        R.keys[i] = key;
-        R.vals[i] = p;
-    }
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
-}
-
-// ---------------------------------------------------------------------------
-// Persistent ray traversal. Each resident warp keeps its lanes busy: whenever
-// at least kRefill lanes have finished their rays (or all have), the idle
-// lanes fetch the next rays from the job's queue with one atomic per warp.
-// Every lane walks its own ray exactly as traverse_closest / traverse_any do
-// -- same node order, same culling decisions -- one stack pop per loop
-// iteration, so short and long rays no longer hold each other's lanes idle.
-// ---------------------------------------------------------------------------
-constexpr int kRefill = 8;
-
-struct TraceJob {
-    const uint32_t* count;   // rays in the queue (device)
-    unsigned int* next;      // fetch cursor (device, zeroed before the launch)
-};
-
-// Closest hits of the paths continuing to vertex b (queue = the sorted hit
-// list of the previous vertex): writes the shading record and the next sort
-// pair (slot | n_programs, path).
-__global__ void __launch_bounds__(128) k_trace_closest(RenderView R, TraceJob J) {
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t count = *J.count;
-    uint32_t nvis = 0, ntest = 0, nhit = 0;
-    bool has = false, exhausted = false;
-    uint32_t q = 0, p = 0;
-    V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
-    float4 ro{}, rd{};
-    int32_t sa[64], sb[64];
-    float se[64];
-    int top = 0;
-    float closest = 0.0f, tt = 0.0f, tb1 = 0.0f, tb2 = 0.0f;
-    uint32_t prim = 0;
-    bool found = false;
-    for (;;) {
-        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
-        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
-            const int ldr = __ffs(idle) - 1;
-            unsigned base = 0;
-            if (static_cast<int>(lane) == ldr) base = atomicAdd(J.next, static_cast<unsigned>(__popc(idle)));
-            base = __shfl_sync(mcgd::kFull, base, ldr);
-            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
-            if (!has) {
-                q = base + __popc(idle & ((1u << lane) - 1u));
-                if (q < count) {
-                    has = true;
-                    p = R.order[q];
-                    ro = R.ro[p];
-                    rd = R.rd[p];
-                    o = V3{ro.x, ro.y, ro.z};
-                    d = V3{rd.x, rd.y, rd.z};
-                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-                    closest = __int_as_float(0x7f800000);
-                    found = false;
-                    top = 0;
-                    if (R.S.n_nodes) {
-                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
-                        float E, T1;
-                        slab(o, inv, lo, hi, kTMin, E, T1);
-                        if (!(T1 < E)) {
-                            const int32_t ra = __float_as_int(lo.w);
-                            sa[0] = ra >= 0 ? 0 : ra;
-                            sb[0] = __float_as_int(hi.w);
-                            se[0] = E;
-                            top = 1;
-                        }
-                    }
-                }
-            }
-        }
-        if (__ballot_sync(mcgd::kFull, has) == 0) {
-            if (exhausted) break;
-            continue;
-        }
-        if (has && top > 0) {
-            --top;
-            const int32_t a = sa[top], b = sb[top];
-            ++nvis;
-            if (!(closest < se[top])) {
-                if (a < 0) {
-                    const uint32_t first = static_cast<uint32_t>(~a);
-                    ntest += static_cast<uint32_t>(b);
-                    for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
-                        float t, b1, b2;
-                        if (hit_prim(R.S, i, o, d, kTMin, closest, t, b1, b2)) {
-                            closest = t;
-                            prim = i;
-                            tt = t;
-                            tb1 = b1;
-                            tb2 = b2;
-                            found = true;
-                        }
-                    }
-                } else {
-                    const float4* pp = R.S.pairs + 4 * a;
-                    const float4 llo = __ldg(pp), lhi = __ldg(pp + 1), rlo = __ldg(pp + 2), rhi = __ldg(pp + 3);
-                    float EL, T1L, ER, T1R;
-                    slab(o, inv, llo, lhi, kTMin, EL, T1L);
-                    slab(o, inv, rlo, rhi, kTMin, ER, T1R);
-                    if (!(T1L < EL)) {
-                        sa[top] = __float_as_int(llo.w);
-                        sb[top] = __float_as_int(lhi.w);
-                        se[top] = EL;
-                        ++top;
-                    }
-                    if (!(T1R < ER)) {
-                        sa[top] = __float_as_int(rlo.w);
-                        sb[top] = __float_as_int(rhi.w);
-                        se[top] = ER;
-                        ++top;
-                    }
-                }
-            }
-        }
-        if (has && top == 0) {
-            // Ray finished: the vertex's shading record, or the environment.
-            uint32_t key = R.S.n_programs;
-            float4 L = R.L[p];
-            const float4 thr = R.thr[p];
-            if (!found) {
-                L.x = L.x + thr.x * R.S.env[0];
-                L.y = L.y + thr.y * R.S.env[1];
-                L.z = L.z + thr.z * R.S.env[2];
-                R.L[p] = L;
-            } else {
-                const Surface s = surface(R.S, o, d, prim, tt, tb1, tb2);
-                const float width = ro.w + tt * rd.w;  // propagate (raycone.cpp:15-18)
-                float2 g1, g2;
-                mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-                R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-                R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-                R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
-                R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
-                key = s.slot;
-                ++nhit;
-            }
-            R.keys[q] = key;
-            R.vals[q] = p;
-            has = false;
-        }
-    }
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
-}
-
-// Any-hit queries of the queued shadow rays (Scene::occluded,
-// scene.cpp:280-298), near child first, the first hit ends a ray.
-__global__ void __launch_bounds__(128) k_trace_shadow(RenderView R, TraceJob J) {
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t count = *J.count;
-    uint32_t nvis = 0, ntest = 0, nrays = 0;
-    bool has = false, exhausted = false;
-    uint32_t s = 0;
-    V3 o{0, 0, 0}, d{0, 0, 0}, inv{0, 0, 0};
-    float tmax = 0.0f;
-    int32_t sa[64], sb[64];
-    int top = 0;
-    bool hit = false;
-    for (;;) {
-        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
-        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
-            const int ldr = __ffs(idle) - 1;
-            unsigned base = 0;
-            if (static_cast<int>(lane) == ldr) base = atomicAdd(J.next, static_cast<unsigned>(__popc(idle)));
-            base = __shfl_sync(mcgd::kFull, base, ldr);
-            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
-            if (!has) {
-                const uint32_t qq = base + __popc(idle & ((1u << lane) - 1u));
-                if (qq < count) {
-                    has = true;
-                    ++nrays;
-                    s = R.squeue[qq];
-                    const float4 so = R.sro[s], sd = R.srd[s];
-                    o = V3{so.x, so.y, so.z};
-                    d = V3{sd.x, sd.y, sd.z};
-                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-                    tmax = so.w;
-                    hit = false;
-                    top = 0;
-                    if (R.S.n_nodes) {
-                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
-                        float E, T1;
-                        slab(o, inv, lo, hi, kTMin, E, T1);
-                        if (!(fminf(tmax, T1) < E)) {
-                            const int32_t ra = __float_as_int(lo.w);
-                            sa[0] = ra >= 0 ? 0 : ra;
-                            sb[0] = __float_as_int(hi.w);
-                            top = 1;
-                        }
-                    }
-                }
-            }
-        }
-        if (__ballot_sync(mcgd::kFull, has) == 0) {
-            if (exhausted) break;
-            continue;
-        }
-        if (has && top > 0) {
-            --top;
-            const int32_t a = sa[top], b = sb[top];
-            ++nvis;
-            if (a < 0) {
-                const uint32_t first = static_cast<uint32_t>(~a);
-                ntest += static_cast<uint32_t>(b);
-                for (uint32_t i = first; i < first + static_cast<uint32_t>(b); ++i) {
-                    float t, b1, b2;
-                    if (hit_prim(R.S, i, o, d, kTMin, tmax, t, b1, b2)) {
-                        hit = true;
-                        break;
-                    }
-                }
-                if (hit) top = 0;
-            } else {
-                const float4* pp = R.S.pairs + 4 * a;
-                const float4 llo = __ldg(pp), lhi = __ldg(pp + 1), rlo = __ldg(pp + 2), rhi = __ldg(pp + 3);
-                float EL, T1L, ER, T1R;
-                slab(o, inv, llo, lhi, kTMin, EL, T1L);
-                slab(o, inv, rlo, rhi, kTMin, ER, T1R);
-                const bool okL = !(fminf(tmax, T1L) < EL), okR = !(fminf(tmax, T1R) < ER);
-                const bool left_first = EL <= ER;
-                // push the far child first so the near one is popped next
-                if (left_first) {
-                    if (okR) { sa[top] = __float_as_int(rlo.w); sb[top] = __float_as_int(rhi.w); ++top; }
-                    if (okL) { sa[top] = __float_as_int(llo.w); sb[top] = __float_as_int(lhi.w); ++top; }
-                } else {
-                    if (okL) { sa[top] = __float_as_int(llo.w); sb[top] = __float_as_int(lhi.w); ++top; }
-                    if (okR) { sa[top] = __float_as_int(rlo.w); sb[top] = __float_as_int(rhi.w); ++top; }
-                }
-            }
-        }
-        if (has && top == 0) {
-            R.vis[s] = hit ? 0 : 1;
-            has = false;
-        }
-    }
-    mcgd::warp_add(R.stats + kStatShadow, nrays);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
-}
 
 // Non-persistent closest-hit over the live list (one thread per ray).
-__global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const uint32_t* count) {
+__global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     if (q < *count) {
@@ -803,8 +578,8 @@ __global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const
         float4 ro = R.ro[p];
         const float4 rd = R.rd[p], thr = R.thr[p];
         float4 L = R.L[p];
-        const uint32_t key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest);
-        if (key < R.S.n_programs) R.ro[p] = ro;
+        const uint32_t key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest, vtx);
+        if (key_slot(R, key) < R.S.n_programs) R.ro[p] = ro;
         else R.L[p] = L;
         R.keys[q] = key;
         R.vals[q] = p;
@@ -982,7 +757,187 @@ __device__ __forceinline__ bool any_ww(const mcgd::SceneView& S, bool active, V3
     return hit;
 }
 
-// Shadow rays, one per thread over the queue, warp-synchronous traversal.
+// ---------------------------------------------------------------------------
+// 4-wide variants over the collapsed tree (SceneView::quads). A popped
+// 4-wide node pushes its (up to four) entries -- the reference's
+// grandchildren -- in left-to-right order, so the LIFO visit order is the
+// reference's; each entry's box test is split into its ray-only part (at
+// push) and the closest-dependent part (at pop), as in closest_ww.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool closest_ww4(const mcgd::SceneView& S, bool active, V3 o, V3 d,
+                                            float tmin, float tmax, uint32_t& prim, float& t_out,
+                                            float& b1_out, float& b2_out, uint32_t& nodes_visited,
+                                            uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t sa[64], sb[64];
+    float se[64];
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(T1 < E)) {
+            sa[0] = S.root_a;
+            sb[0] = S.root_b;
+            se[0] = E;
+            top = 1;
+        }
+    }
+    bool found = false;
+    float closest = tmax;
+    int32_t la = 0, lb = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nodes_visited;
+                    if (!(closest < se[top])) {
+                        if (b > 0) {
+                            leaf = true;
+                            la = a;
+                            lb = b;
+                        } else {
+                            const float4* p = S.quads + 8 * a;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                                const int32_t eb = __float_as_int(hi.w);
+                                if (eb == 0) continue;  // empty entry
+                                float E, T1;
+                                slab(o, inv, lo, hi, tmin, E, T1);
+                                if (!(T1 < E)) {
+                                    sa[top] = __float_as_int(lo.w);
+                                    sb[top] = eb;
+                                    se[top] = E;
+                                    ++top;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            prims_tested += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                    closest = t;
+                    prim = i;
+                    t_out = t;
+                    b1_out = b1;
+                    b2_out = b2;
+                    found = true;
+                }
+            }
+            leaf = false;
+            done = top == 0;
+        }
+    }
+    return found;
+}
+
+__device__ __forceinline__ bool any_ww4(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                        float tmax, uint32_t& nodes_visited, uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t sa[64], sb[64];
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(fminf(tmax, T1) < E)) {
+            sa[0] = S.root_a;
+            sb[0] = S.root_b;
+            top = 1;
+        }
+    }
+    bool hit = false;
+    int32_t la = 0, lb = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nodes_visited;
+                    if (b > 0) {
+                        leaf = true;
+                        la = a;
+                        lb = b;
+                    } else {
+                        // Surviving entries, pushed far-to-near so the nearest pops first.
+                        const float4* p = S.quads + 8 * a;
+                        float ke[4];
+                        int32_t ka[4], kb[4];
+                        int n = 0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                            const int32_t eb = __float_as_int(hi.w);
+                            float E, T1;
+                            slab(o, inv, lo, hi, tmin, E, T1);
+                            const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
+                            ke[k] = ok ? E : __int_as_float(0x7f800000);
+                            ka[k] = __float_as_int(lo.w);
+                            kb[k] = ok ? eb : 0;
+                            n += ok;
+                        }
+                        // sort 4 (E descending) with a fixed network
+#define MCG_CSWAP(i, j)                                                              \
+    if (ke[i] < ke[j]) {                                                             \
+        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
+        const int32_t ta = ka[i]; ka[i] = ka[j]; ka[j] = ta;                         \
+        const int32_t tb = kb[i]; kb[i] = kb[j]; kb[j] = tb;                         \
+    }
+                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
+#undef MCG_CSWAP
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (kb[k] != 0) {
+                                sa[top] = ka[k];
+                                sb[top] = kb[k];
+                                ++top;
+                            }
+                        }
+                        (void)n;
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            prims_tested += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            done = hit || top == 0;
+        }
+    }
+    return hit;
+}
+
+// Shadow rays, one per thread over the queue, warp-synchronous traversal
+// over the binary (kWide = false) or the 4-wide (kWide = true) tree.
+template <bool kWide>
 __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -997,7 +952,8 @@ __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    const bool occ = any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
+    const bool occ = kWide ? any_ww4(R.S, active, o, d, kTMin, tmax, nvis, ntest)
+                           : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
@@ -1005,7 +961,8 @@ __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
 }
 
 // Closest hits of the live paths, one per thread, warp-synchronous traversal.
-__global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const uint32_t* count) {
+template <bool kWide>
+__global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *count;
@@ -1019,10 +976,11 @@ __global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const ui
     const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    const bool found = closest_ww(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
-                                  nvis, ntest);
+    const float inf = __int_as_float(0x7f800000);
+    const bool found = kWide ? closest_ww4(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
+                             : closest_ww(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest);
     if (active) {
-        uint32_t key = R.S.n_programs;
+        uint32_t key = no_hit_key(R);
         if (!found) {
             float4 L = R.L[p];
             const float4 thr = R.thr[p];
@@ -1039,7 +997,9 @@ __global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const ui
             R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
             R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
             R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
-            key = s.slot;
+            const uint32_t slot_j = p / R.n_pix;
+            const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
+            key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
         }
         R.keys[q] = key;
         R.vals[q] = p;
@@ -1054,7 +1014,7 @@ __global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const ui
 __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R.n_paths) return;
-    const uint32_t slot = R.skey[i];
+    const uint32_t slot = key_slot(R, R.skey[i]);
     const bool live = slot < R.S.n_programs;
     if (live) {
         const uint32_t p = R.order[i];
@@ -1074,7 +1034,7 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
         }
     }
     if (!live || b >= R.max_bounces) {
-        R.keys[i] = R.S.n_programs;
+        R.keys[i] = no_hit_key(R);
         R.vals[i] = 0;
     }
 }
@@ -1084,23 +1044,23 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 __global__ void k_count_live(RenderView R, uint32_t* live) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R.n_paths) return;
-    const bool v = R.skey[i] < R.S.n_programs;
-    const bool prev = i == 0 ? true : R.skey[i - 1] < R.S.n_programs;
+    const bool v = key_slot(R, R.skey[i]) < R.S.n_programs;
+    const bool prev = i == 0 ? true : key_slot(R, R.skey[i - 1]) < R.S.n_programs;
     if (!v && prev) *live = i;
     if (v && i + 1 == R.n_paths) *live = R.n_paths;
 }
 
 // Material evaluation of every live hit, in material order.
-template <bool kDeferred>
+template <bool kDeferred, bool kNee>
 __global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __restrict__ skey,
                                                const uint32_t* __restrict__ order, int max_stack,
-                                               uint32_t wh) {
+                                               uint32_t wh, int b) {
     extern __shared__ float smem[];
     __shared__ uint8_t s_perm[256];
     mcgd::stage_perm(s_perm);
     __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t slot = i < R.n_paths ? skey[i] : R.S.n_programs;
+    const uint32_t slot = i < R.n_paths ? key_slot(R, skey[i]) : R.S.n_programs;
     const bool valid = slot < R.S.n_programs;
     const unsigned live = __ballot_sync(mcgd::kFull, valid);
     if (!valid) return;
@@ -1117,11 +1077,17 @@ __global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __r
     mcgd::VmCounters cnt;
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt);
-    R.base[p] = make_float4(r.value.x, r.value.y, r.value.z, 0.0f);
     if (cnt.hits) {
         float4 t = R.thr[p];
         t.w = __uint_as_float(__float_as_uint(t.w) + cnt.hits);
         R.thr[p] = t;
+    }
+    if (kNee) {
+        // Fused next-event estimation + bounce: the shading record is
+        // already in registers.
+        nee_bounce(R, p, b, s0, s1, r.value);
+    } else {
+        R.base[p] = make_float4(r.value.x, r.value.y, r.value.z, 0.0f);
     }
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
@@ -1306,22 +1272,32 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.q.count = reinterpret_cast<unsigned int*>(R.q.keys + 4 * cap);
         R.q.capacity = static_cast<unsigned>(cap);
     }
-    const int key_bits = std::max(1, bits_for(D.view.n_programs));
-    int occ_any = 1, occ_closest = 1, n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_any, k_trace_shadow, 128, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_closest, k_trace_closest, 128, 0);
-    const unsigned persist_grid_any = static_cast<unsigned>(n_sm * std::max(1, occ_any));
-    const unsigned persist_grid_closest = static_cast<unsigned>(n_sm * std::max(1, occ_closest));
+    // Sort key: slot << key_shift | 24-bit Morton code of the hit point
+    // (MCG_SORT=material: slot only).
+    const char* sort_env = std::getenv("MCG_SORT");
+    const bool morton = !(sort_env && std::string(sort_env) == "material");
+    const int slot_bits = std::max(1, bits_for(D.view.n_programs));
+    R.key_shift = (morton && slot_bits <= 8) ? 24u : 0u;
+    R.key_dir = (sort_env && std::string(sort_env) == "dir") ? 1u : 0u;
+    for (int a = 0; a < 3; ++a) {
+        const float ext = D.root_hi[a] - D.root_lo[a];
+        R.box_lo[a] = D.root_lo[a];
+        R.box_scale[a] = ext > 0.0f ? 255.999f / ext : 0.0f;
+    }
+    const int key_bits = static_cast<int>(R.key_shift) + slot_bits;
     const char* trace_env = std::getenv("MCG_TRACE");
-    const bool persistent = trace_env && std::string(trace_env) == "persistent";
-    const bool plain = trace_env && std::string(trace_env) == "plain";  // holds kInvalid-remapped slots
+    const bool plain = trace_env && std::string(trace_env) == "plain";
+    const bool binary = trace_env && std::string(trace_env) == "ww2";  // else the 4-wide tree
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
     if (smem > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "material stack too deep for shared memory");
-    cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const char* nee_env = std::getenv("MCG_NEE");
+    const bool fuse_nee = !(nee_env && std::string(nee_env) == "separate");
 
     for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k) {
         const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp) - start);
@@ -1348,12 +1324,17 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, ctx->stream), "memset");
             {
                 LaunchScope ls(ctx, "shade", 0.0);
+                const unsigned sg = grid_for(R.n_paths, block);
+                const uint32_t wh32 = static_cast<uint32_t>(wh);
                 if (deferred) {
-                    k_shade<true><<<grid_for(R.n_paths, block), block, smem, ctx->stream>>>(
-                        R, skey, order, max_stack, static_cast<uint32_t>(wh));
+                    // deterministic mode: stores are applied after the shade,
+                    // NEE needs none of them -- but keep the kernels separate
+                    // so the store queue is complete before any later step.
+                    if (fuse_nee) k_shade<true, true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
+                    else k_shade<true, false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
                 } else {
-                    k_shade<false><<<grid_for(R.n_paths, block), block, smem, ctx->stream>>>(
-                        R, skey, order, max_stack, static_cast<uint32_t>(wh));
+                    if (fuse_nee) k_shade<false, true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
+                    else k_shade<false, false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
                 }
                 ls.done();
             }
@@ -1371,19 +1352,18 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                     apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, R.stats);
                 }
             }
-            {
+            if (!fuse_nee) {
                 LaunchScope ls(ctx, "nee", 0.0);
                 k_nee<<<grid, 256, 0, ctx->stream>>>(R, b);
                 ls.done();
             }
             if (n_lights) {
                 LaunchScope ls(ctx, "trace_shadow", 0.0);
-                if (persistent) {
-                    k_trace_shadow<<<persist_grid_any, 128, 0, ctx->stream>>>(R, TraceJob{R.shadow_count, R.shadow_count + 1});
-                } else if (plain) {
+                if (plain) {
                     k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 } else {
-                    k_shadow_ww<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    if (binary) k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    else k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 }
                 ls.done();
             }
@@ -1394,12 +1374,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
-                if (persistent) {
-                    k_trace_closest<<<persist_grid_closest, 128, 0, ctx->stream>>>(R, TraceJob{R.shadow_count + 2, R.shadow_count + 3});
-                } else if (plain) {
-                    k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
+                if (plain) {
+                    k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 } else {
-                    k_trace_closest_ww<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
+                    if (binary) k_trace_closest_ww<false><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                    else k_trace_closest_ww<true><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 }
                 ls.done();
             }

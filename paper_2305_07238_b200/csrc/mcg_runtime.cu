@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <vector>
 
 #include "host_scene.hpp"
@@ -63,10 +64,20 @@ void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* ki, uint32_t* ko, const uint32
                                                end_bit, ctx->stream),
                "cub sort (size)");
     ctx->cub_temp.ensure(std::max<size_t>(bytes, 256));
+    cudaEvent_t a = nullptr;
+    if (ctx->profile) {
+        a = take_event(ctx);
+        cudaEventRecord(a, ctx->stream);
+    }
     cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
                                                static_cast<int>(n), 0, end_bit, ctx->stream),
                "cub sort");
-    ++ctx->library_sorts;  // CUB's kernels: library code, not counted in launches
+    if (ctx->profile) {  // timed with the kernels, but CUB's launches are not counted as ours
+        cudaEvent_t b = take_event(ctx);
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending.push_back({"sort (cub)", a, b, static_cast<double>(n) * 16.0 * ((end_bit + 7) / 8)});
+    }
+    ++ctx->library_sorts;
 }
 
 }  // namespace mcg
@@ -281,6 +292,7 @@ __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, ui
         mcgd::Probe p;
         if (kVariant == 2) p = mcgd::probe_warp<10>(c, base, chk, valid);
         else if (kVariant == 1) p = valid ? mcgd::probe_cell_t<5>(c, base, chk) : mcgd::Probe{0u, -1, false};
+        else if (kVariant == 3) p = valid ? mcgd::probe_cell_blk(c, base, chk) : mcgd::Probe{0u, -1, false};
         else p = valid ? mcgd::probe_cell_t<1>(c, base, chk) : mcgd::Probe{0u, -1, false};
         if (!valid) continue;
         const bool insert = phase == 0 || (phase == 2 && (i & 1u));
@@ -765,7 +777,8 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        need((phase & 15) <= 2 && (phase >> 4) <= 2, "phase must be 0, 1 or 2 (+16 * variant)");
+        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 3,
+             "phase must be 0, 1 or 2 (+16 * variant, +256 * blocks per SM)");
         mcg_ctx* ctx = cache->ctx;
         cudaEvent_t a = take_event(ctx), b = take_event(ctx);
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
@@ -773,13 +786,17 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
         const int reps = std::max(1, iters);
         for (int r = 0; r < reps; ++r) {
             LaunchScope ls(ctx, "probe_bench", 0.0);
-            const int variant = phase >> 4, ph = phase & 15;
+            const int variant = (phase >> 4) & 15, ph = phase & 15;
+            const int per_sm = (phase >> 8) ? (phase >> 8) : 8;   // blocks per SM
+            const unsigned grid = 148u * static_cast<unsigned>(per_sm);
             if (variant == 2 && cache->n_entries == 10) {
-                k_probe_bench<2><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+                k_probe_bench<2><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 1) {
-                k_probe_bench<1><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+                k_probe_bench<1><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 3) {
+                k_probe_bench<3><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else {
-                k_probe_bench<0><<<148 * 8, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+                k_probe_bench<0><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             }
             ls.done();
         }
@@ -842,6 +859,51 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             }
         }
         v.pairs = static_cast<const float4*>(up(14, pairs.data(), f.n_nodes * 2 * sizeof(mcg_bvh_node)));
+        // 4-wide nodes: each holds the grandchildren of a reference node (a
+        // child that is a leaf stands for itself), left part before right
+        // part, so a LIFO stack still visits in the reference's order; the
+        // skipped child boxes contain their children's boxes, so their
+        // culling is implied.
+        std::vector<mcg_bvh_node> quads;
+        std::function<int32_t(int32_t)> collapse = [&](int32_t x) -> int32_t {
+            const int32_t q = static_cast<int32_t>(quads.size() / 4);
+            quads.resize(quads.size() + 4, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
+            int k = 0;
+            const int32_t kids[2] = {f.nodes[x].a, f.nodes[x].b};
+            std::vector<int32_t> entries;
+            for (int32_t c : kids) {
+                if (f.nodes[c].a < 0) {
+                    entries.push_back(c);
+                } else {
+                    entries.push_back(f.nodes[c].a);
+                    entries.push_back(f.nodes[c].b);
+                }
+            }
+            for (int32_t e : entries) {
+                mcg_bvh_node rec = f.nodes[e];
+                if (rec.a >= 0) {
+                    rec.a = collapse(e);
+                    rec.b = -1;
+                }
+                quads[4 * static_cast<size_t>(q) + k++] = rec;
+            }
+            return q;
+        };
+        v.root_a = 0;
+        v.root_b = 0;
+        if (f.n_nodes) {
+            std::memcpy(D.root_lo, f.nodes[0].lo, sizeof(D.root_lo));
+            std::memcpy(D.root_hi, f.nodes[0].hi, sizeof(D.root_hi));
+            if (f.nodes[0].a < 0) {
+                v.root_a = f.nodes[0].a;
+                v.root_b = f.nodes[0].b;
+            } else {
+                collapse(0);
+                v.root_a = 0;
+                v.root_b = -1;
+            }
+        }
+        v.quads = static_cast<const float4*>(up(15, quads.data(), quads.size() * sizeof(mcg_bvh_node)));
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
         v.n_plights = f.n_point_lights;
         v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));
