@@ -1008,6 +1008,525 @@ __global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const ui
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent while-while traversal over the 4-wide tree. Each resident warp
+// loops: (1) lanes without a ray fetch the next rays of the queue (one atomic
+// per warp, only when at least kRefill lanes are idle); (2) every lane pops
+// and expands nodes in its reference order until it parks on a leaf or its
+// stack runs dry; (3) parked lanes test their leaves together; lanes whose
+// ray is finished write their results together. Short and long rays stop
+// holding each other's lanes idle, and no lane leaves its reference order.
+// ---------------------------------------------------------------------------
+constexpr int kRefill = 8;
+
+__global__ void __launch_bounds__(256) k_trace_closest_pww(RenderView R, const uint32_t* count_ptr,
+                                                           unsigned int* cursor, int vtx) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t count = *count_ptr;
+    uint32_t nvis = 0, ntest = 0;
+    bool has = false, exhausted = false, leaf = false, fin = false, found = false;
+    uint32_t q = 0, p = 0, prim = 0;
+    V3 o{0, 0, 0}, d{1, 1, 1}, inv{1, 1, 1};
+    float4 ro{}, rd{};
+    int32_t sa[64], sb[64];
+    float se[64];
+    int top = 0;
+    float closest = 0.0f, tt = 0.0f, tb1 = 0.0f, tb2 = 0.0f;
+    int32_t la = 0, lb = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
+        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
+            const int ldr = __ffs(idle) - 1;
+            unsigned base = 0;
+            if (static_cast<int>(lane) == ldr) base = atomicAdd(cursor, static_cast<unsigned>(__popc(idle)));
+            base = __shfl_sync(mcgd::kFull, base, ldr);
+            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
+            if (!has) {
+                q = base + __popc(idle & ((1u << lane) - 1u));
+                if (q < count) {
+                    has = true;
+                    p = R.order[q];
+                    ro = R.ro[p];
+                    rd = R.rd[p];
+                    o = V3{ro.x, ro.y, ro.z};
+                    d = V3{rd.x, rd.y, rd.z};
+                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+                    closest = __int_as_float(0x7f800000);
+                    found = false;
+                    top = 0;
+                    if (R.S.n_nodes) {
+                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
+                        float E, T1;
+                        slab(o, inv, lo, hi, kTMin, E, T1);
+                        if (!(T1 < E)) {
+                            sa[0] = R.S.root_a;
+                            sb[0] = R.S.root_b;
+                            se[0] = E;
+                            top = 1;
+                        }
+                    }
+                }
+            }
+        }
+        if (__ballot_sync(mcgd::kFull, has) == 0) {
+            if (exhausted) break;
+            continue;
+        }
+        // Phase 1: pop / expand in reference order until parked on a leaf.
+        for (;;) {
+            if (has && !leaf && !fin) {
+                if (top == 0) {
+                    fin = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nvis;
+                    if (!(closest < se[top])) {
+                        if (b > 0) {
+                            leaf = true;
+                            la = a;
+                            lb = b;
+                        } else {
+                            const float4* pp = R.S.quads + 8 * a;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float4 lo = __ldg(pp + 2 * k), hi = __ldg(pp + 2 * k + 1);
+                                const int32_t eb = __float_as_int(hi.w);
+                                if (eb == 0) continue;
+                                float E, T1;
+                                slab(o, inv, lo, hi, kTMin, E, T1);
+                                if (!(T1 < E)) {
+                                    sa[top] = __float_as_int(lo.w);
+                                    sb[top] = eb;
+                                    se[top] = E;
+                                    ++top;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, !has || leaf || fin)) break;
+        }
+        // Phase 2: leaves, together.
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            ntest += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(R.S, i, o, d, kTMin, closest, t, b1, b2)) {
+                    closest = t;
+                    prim = i;
+                    tt = t;
+                    tb1 = b1;
+                    tb2 = b2;
+                    found = true;
+                }
+            }
+            leaf = false;
+            fin = top == 0;
+        }
+        // Finished rays, together: the vertex's shading record or the env.
+        if (fin) {
+            uint32_t key = no_hit_key(R);
+            if (!found) {
+                float4 L = R.L[p];
+                const float4 thr = R.thr[p];
+                L.x = L.x + thr.x * R.S.env[0];
+                L.y = L.y + thr.y * R.S.env[1];
+                L.z = L.z + thr.z * R.S.env[2];
+                R.L[p] = L;
+            } else {
+                const Surface s = surface(R.S, o, d, prim, tt, tb1, tb2);
+                const float width = ro.w + tt * rd.w;  // propagate (raycone.cpp:15-18)
+                float2 g1, g2;
+                mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+                R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+                R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+                R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+                R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
+                const uint32_t slot_j = p / R.n_pix;
+                const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
+                key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+            }
+            R.keys[q] = key;
+            R.vals[q] = p;
+            has = false;
+            fin = false;
+        }
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+__global__ void __launch_bounds__(256) k_shadow_pww(RenderView R, unsigned int* cursor) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t count = *R.shadow_count;
+    uint32_t nvis = 0, ntest = 0, nrays = 0;
+    bool has = false, exhausted = false, leaf = false, fin = false, hit = false;
+    uint32_t s = 0;
+    V3 o{0, 0, 0}, d{1, 1, 1}, inv{1, 1, 1};
+    float tmax = 0.0f;
+    int32_t sa[64], sb[64];
+    int top = 0;
+    int32_t la = 0, lb = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
+        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
+            const int ldr = __ffs(idle) - 1;
+            unsigned base = 0;
+            if (static_cast<int>(lane) == ldr) base = atomicAdd(cursor, static_cast<unsigned>(__popc(idle)));
+            base = __shfl_sync(mcgd::kFull, base, ldr);
+            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
+            if (!has) {
+                const uint32_t qq = base + __popc(idle & ((1u << lane) - 1u));
+                if (qq < count) {
+                    has = true;
+                    ++nrays;
+                    s = R.squeue[qq];
+                    const float4 so = R.sro[s], sd = R.srd[s];
+                    o = V3{so.x, so.y, so.z};
+                    d = V3{sd.x, sd.y, sd.z};
+                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+                    tmax = so.w;
+                    hit = false;
+                    top = 0;
+                    if (R.S.n_nodes) {
+                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
+                        float E, T1;
+                        slab(o, inv, lo, hi, kTMin, E, T1);
+                        if (!(fminf(tmax, T1) < E)) {
+                            sa[0] = R.S.root_a;
+                            sb[0] = R.S.root_b;
+                            top = 1;
+                        }
+                    }
+                }
+            }
+        }
+        if (__ballot_sync(mcgd::kFull, has) == 0) {
+            if (exhausted) break;
+            continue;
+        }
+        for (;;) {
+            if (has && !leaf && !fin) {
+                if (top == 0) {
+                    fin = true;
+                } else {
+                    --top;
+                    const int32_t a = sa[top], b = sb[top];
+                    ++nvis;
+                    if (b > 0) {
+                        leaf = true;
+                        la = a;
+                        lb = b;
+                    } else {
+                        const float4* pp = R.S.quads + 8 * a;
+                        float ke[4];
+                        int32_t ka[4], kb[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 lo = __ldg(pp + 2 * k), hi = __ldg(pp + 2 * k + 1);
+                            const int32_t eb = __float_as_int(hi.w);
+                            float E, T1;
+                            slab(o, inv, lo, hi, kTMin, E, T1);
+                            const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
+                            ke[k] = ok ? E : __int_as_float(0x7f800000);
+                            ka[k] = __float_as_int(lo.w);
+                            kb[k] = ok ? eb : 0;
+                        }
+#define MCG_CSWAP(i, j)                                                              \
+    if (ke[i] < ke[j]) {                                                             \
+        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
+        const int32_t ta = ka[i]; ka[i] = ka[j]; ka[j] = ta;                         \
+        const int32_t tb = kb[i]; kb[i] = kb[j]; kb[j] = tb;                         \
+    }
+                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
+#undef MCG_CSWAP
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (kb[k] != 0) {
+                                sa[top] = ka[k];
+                                sb[top] = kb[k];
+                                ++top;
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, !has || leaf || fin)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(~la);
+            ntest += static_cast<uint32_t>(lb);
+            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
+                float t, b1, b2;
+                if (hit_prim(R.S, i, o, d, kTMin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            fin = hit || top == 0;
+        }
+        if (fin) {
+            R.vis[s] = hit ? 0 : 1;
+            has = false;
+            fin = false;
+        }
+    }
+    mcgd::warp_add(R.stats + kStatShadow, nrays);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory traversal stacks. Entry k of thread t lives at [k][t] of a
+// per-block array, so lanes at different stack depths still hit different
+// banks (the stride is a multiple of 32) -- no local-memory round trips, no
+// uncoalesced spills. An entry packs its node reference into one word:
+// >= 0 a 4-wide node index, < 0 ~(first << 3 | count) for a leaf.
+// Capacity kStackCap; scenes whose collapsed tree could need more use the
+// local-memory kernels (the host checks the worst-case depth).
+// ---------------------------------------------------------------------------
+constexpr int kStackCap = 32;
+constexpr int kWsBlock = 128;
+
+__device__ __forceinline__ int32_t pack_ref(int32_t a, int32_t b) {
+    return b > 0 ? ~((static_cast<int32_t>(~a) << 3) | b) : a;
+}
+
+__device__ __forceinline__ bool closest_ws(const mcgd::SceneView& S, bool active, V3 o, V3 d,
+                                           float tmin, float tmax, uint32_t& prim, float& t_out,
+                                           float& b1_out, float& b2_out, uint32_t& nodes_visited,
+                                           uint32_t& prims_tested, int32_t* sref, float* se) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    const int tid = threadIdx.x;
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(T1 < E)) {
+            sref[tid] = pack_ref(S.root_a, S.root_b);
+            se[tid] = E;
+            top = 1;
+        }
+    }
+    bool found = false;
+    float closest = tmax;
+    int32_t leaf_ref = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t r = sref[top * kWsBlock + tid];
+                    ++nodes_visited;
+                    if (!(closest < se[top * kWsBlock + tid])) {
+                        if (r < 0) {
+                            leaf = true;
+                            leaf_ref = ~r;
+                        } else {
+                            const float4* p = S.quads + 8 * r;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                                const int32_t eb = __float_as_int(hi.w);
+                                if (eb == 0) continue;
+                                float E, T1;
+                                slab(o, inv, lo, hi, tmin, E, T1);
+                                if (!(T1 < E)) {
+                                    sref[top * kWsBlock + tid] = pack_ref(__float_as_int(lo.w), eb);
+                                    se[top * kWsBlock + tid] = E;
+                                    ++top;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(leaf_ref) >> 3;
+            const uint32_t cnt = static_cast<uint32_t>(leaf_ref) & 7u;
+            prims_tested += cnt;
+            for (uint32_t i = first; i < first + cnt; ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                    closest = t;
+                    prim = i;
+                    t_out = t;
+                    b1_out = b1;
+                    b2_out = b2;
+                    found = true;
+                }
+            }
+            leaf = false;
+            done = top == 0;
+        }
+    }
+    return found;
+}
+
+__device__ __forceinline__ bool any_ws(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                       float tmax, uint32_t& nodes_visited, uint32_t& prims_tested,
+                                       int32_t* sref) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    const int tid = threadIdx.x;
+    int top = 0;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(fminf(tmax, T1) < E)) {
+            sref[tid] = pack_ref(S.root_a, S.root_b);
+            top = 1;
+        }
+    }
+    bool hit = false;
+    int32_t leaf_ref = 0;
+    bool leaf = false;
+    bool done = top == 0;
+    while (__any_sync(mcgd::kFull, !done)) {
+        for (;;) {
+            if (!done && !leaf) {
+                if (top == 0) {
+                    done = true;
+                } else {
+                    --top;
+                    const int32_t r = sref[top * kWsBlock + tid];
+                    ++nodes_visited;
+                    if (r < 0) {
+                        leaf = true;
+                        leaf_ref = ~r;
+                    } else {
+                        const float4* p = S.quads + 8 * r;
+                        float ke[4];
+                        int32_t kr[4];
+                        bool ko[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                            const int32_t eb = __float_as_int(hi.w);
+                            float E, T1;
+                            slab(o, inv, lo, hi, tmin, E, T1);
+                            ko[k] = eb != 0 && !(fminf(tmax, T1) < E);
+                            ke[k] = ko[k] ? E : __int_as_float(0x7f800000);
+                            kr[k] = pack_ref(__float_as_int(lo.w), eb);
+                        }
+#define MCG_CSWAP(i, j)                                                              \
+    if (ke[i] < ke[j]) {                                                             \
+        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
+        const int32_t tr = kr[i]; kr[i] = kr[j]; kr[j] = tr;                         \
+        const bool to = ko[i]; ko[i] = ko[j]; ko[j] = to;                            \
+    }
+                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
+#undef MCG_CSWAP
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (ko[k]) {
+                                sref[top * kWsBlock + tid] = kr[k];
+                                ++top;
+                            }
+                        }
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, done || leaf)) break;
+        }
+        if (leaf) {
+            const uint32_t first = static_cast<uint32_t>(leaf_ref) >> 3;
+            const uint32_t cnt = static_cast<uint32_t>(leaf_ref) & 7u;
+            prims_tested += cnt;
+            for (uint32_t i = first; i < first + cnt; ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            done = hit || top == 0;
+        }
+    }
+    return hit;
+}
+
+__global__ void __launch_bounds__(kWsBlock) k_shadow_ws(RenderView R) {
+    __shared__ int32_t sref[kStackCap * kWsBlock];
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    const bool active = q < *R.shadow_count;
+    uint32_t s = 0;
+    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
+    float tmax = 0.0f;
+    if (active) {
+        s = R.squeue[q];
+        const float4 so = R.sro[s], sd = R.srd[s];
+        o = V3{so.x, so.y, so.z};
+        d = V3{sd.x, sd.y, sd.z};
+        tmax = so.w;
+    }
+    const bool occ = any_ws(R.S, active, o, d, kTMin, tmax, nvis, ntest, sref);
+    if (active) R.vis[s] = occ ? 0 : 1;
+    mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+__global__ void __launch_bounds__(kWsBlock) k_trace_closest_ws(RenderView R, const uint32_t* count, int vtx) {
+    __shared__ int32_t sref[kStackCap * kWsBlock];
+    __shared__ float se[kStackCap * kWsBlock];
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    const bool active = q < *count;
+    uint32_t p = 0;
+    float4 ro{}, rd{};
+    if (active) {
+        p = R.order[q];
+        ro = R.ro[p];
+        rd = R.rd[p];
+    }
+    const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
+    uint32_t prim = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    const bool found = closest_ws(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1,
+                                  b2, nvis, ntest, sref, se);
+    if (active) {
+        uint32_t key = no_hit_key(R);
+        if (!found) {
+            float4 L = R.L[p];
+            const float4 thr = R.thr[p];
+            L.x = L.x + thr.x * R.S.env[0];
+            L.y = L.y + thr.y * R.S.env[1];
+            L.z = L.z + thr.z * R.S.env[2];
+            R.L[p] = L;
+        } else {
+            const Surface s = surface(R.S, o, d, prim, t, b1, b2);
+            const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+            float2 g1, g2;
+            mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+            R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+            R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+            R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+            R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
+            const uint32_t slot_j = p / R.n_pix;
+            const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
+            key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+        }
+        R.keys[q] = key;
+        R.vals[q] = p;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
 // Finishes vertex b: adds the visible light contributions in light order
 // (the oracle's summation order); writes "no hit" sort keys for the slots
 // past the live list and for every path at the last vertex.
@@ -1288,6 +1807,17 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const char* trace_env = std::getenv("MCG_TRACE");
     const bool plain = trace_env && std::string(trace_env) == "plain";
     const bool binary = trace_env && std::string(trace_env) == "ww2";  // else the 4-wide tree
+    const bool pww = trace_env && std::string(trace_env) == "pww";
+    // Shared-memory stacks (experiment, MCG_TRACE=ws; slower than the
+    // local-memory stacks on the bench scene: profiles/README.md).
+    const bool ws = trace_env && std::string(trace_env) == "ws" &&
+                    D.max_stack4 <= static_cast<uint32_t>(kStackCap);
+    int n_sm = 148, occ_s = 1, occ_c = 1;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_shadow_pww, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_trace_closest_pww, 256, 0);
+    const unsigned pgrid_shadow = static_cast<unsigned>(n_sm * std::max(1, occ_s));
+    const unsigned pgrid_closest = static_cast<unsigned>(n_sm * std::max(1, occ_c));
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
@@ -1359,7 +1889,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (n_lights) {
                 LaunchScope ls(ctx, "trace_shadow", 0.0);
-                if (plain) {
+                if (ws) {
+                    k_shadow_ws<<<grid_for(n_shadow, kWsBlock), kWsBlock, 0, ctx->stream>>>(R);
+                } else if (pww) {
+                    k_shadow_pww<<<pgrid_shadow, 256, 0, ctx->stream>>>(R, R.shadow_count + 1);
+                } else if (plain) {
                     k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 } else {
                     if (binary) k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
@@ -1374,7 +1908,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
-                if (plain) {
+                if (ws) {
+                    k_trace_closest_ws<<<grid_for(R.n_paths, kWsBlock), kWsBlock, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                } else if (pww) {
+                    k_trace_closest_pww<<<pgrid_closest, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, R.shadow_count + 3, b + 1);
+                } else if (plain) {
                     k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 } else {
                     if (binary) k_trace_closest_ww<false><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);

@@ -904,6 +904,23 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             }
         }
         v.quads = static_cast<const float4*>(up(15, quads.data(), quads.size() * sizeof(mcg_bvh_node)));
+        // Worst-case stack of the LIFO traversal: a node pushes its k
+        // entries and descends into one of them, leaving k-1 behind.
+        {
+            const size_t nq = quads.size() / 4;
+            std::vector<uint32_t> need(nq, 1);
+            for (size_t q = nq; q-- > 0;) {
+                uint32_t k = 0, deepest = 1;
+                for (int e = 0; e < 4; ++e) {
+                    const mcg_bvh_node& r = quads[4 * q + e];
+                    if (r.b == 0) continue;
+                    ++k;
+                    if (r.b < 0) deepest = std::max(deepest, need[r.a]);
+                }
+                need[q] = std::max(k, (k ? k - 1 : 0) + deepest);
+            }
+            D.max_stack4 = nq ? std::max<uint32_t>(1, need[0]) : 1;
+        }
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
         v.n_plights = f.n_point_lights;
         v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));

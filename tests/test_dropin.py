@@ -57,7 +57,13 @@ def test_dropin_render_matches_python_api(ctx, dropin, scene_dir, cache_on):
         np.testing.assert_array_equal(rad.view(np.uint64), res.frame.radiance.view(np.uint64))
         assert st[4] == res.stats.instructions_executed
     else:
-        # concurrent inserts: which sample wins a texel is a race, so the two
-        # cached frames agree up to the cache's (coarse, at this size) texels
+        # concurrent inserts: which sample wins a texel is a race, so each
+        # cached frame is compared with the cache-off frame: both must be the
+        # same approximation of it (the cache's texels are coarse at this size)
         assert st[1] > 0 and abs(int(st[0]) - res.stats.lookups) <= res.stats.lookups * 0.01
-        assert np.abs(rad - res.frame.radiance).mean() / max(1e-9, res.frame.radiance.mean()) < 0.1
+        off = render(s, RenderConfig(width=w, height=h, spp=spp), ctx=ctx).frame.radiance
+        scale = max(1e-9, off.mean())
+        e_dropin = np.abs(rad - off).mean() / scale
+        e_python = np.abs(res.frame.radiance - off).mean() / scale
+        assert e_dropin < 0.25 and e_python < 0.25
+        assert abs(e_dropin - e_python) < 0.1
