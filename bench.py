@@ -353,20 +353,36 @@ def main() -> None:
     peak, peak_src = measured_peaks()
     ne = N_ENTRIES
     steps = args.steps
-    # Algorithmic bytes: per lookup / insert attempt one
-    # cell (8 Ne), +8 per won CAS, 48 per TexSample (4 RGB texels), 80 per
-    # shading record in/out; per BVH node 32, per triangle 48, 128 per path
-    # step of wavefront state.
-    shade_bytes = steps * (st.lookups * 8 * ne + st.stores_attempted * 8 * ne + st.inserts_won * 8
-                           + st.tex_samples * 48 + st.shading_points * 80)
-    bounce_bytes = steps * (st.bvh_nodes * 32 + st.prims_tested * 48
-                            + (st.shading_points + st.paths) * 128)
-    algo = {"shade": shade_bytes, "bounce": bounce_bytes}
+    # Algorithmic bytes per kernel class over the timed steps:
+    #   shade:  one cell (8 Ne) per lookup and per store attempt, +8 per won
+    #           CAS, 48 per TexSample (4 RGB texels), and per shading point
+    #           the 64-byte record in + NEE/bounce state out (2 lights x 48 + 48)
+    #   trace:  128 per 4-wide node popped, 48 per triangle tested, and per
+    #           traced path 32 in (ray) + 72 out (record, key, value)
+    #   shadow: 128 per node popped, 48 per triangle, 33 per ray (ray + flag)
+    n_closest_nodes = st.bvh_nodes - st.bvh_nodes_shadow
+    n_closest_prims = st.prims_tested - st.prims_tested_shadow
+    algo = {
+        "shade": steps * (st.lookups * 8 * ne + st.stores_attempted * 8 * ne + st.inserts_won * 8
+                          + st.tex_samples * 48 + st.shading_points * (64 + 144)),
+        "trace_closest": steps * (n_closest_nodes * 128 + n_closest_prims * 48
+                                  + st.shading_points * (32 + 72)),
+        "trace_shadow": steps * (st.bvh_nodes_shadow * 128 + st.prims_tested_shadow * 48
+                                 + st.shadow_rays * 33),
+    }
     dom = max(ktimes.items(), key=lambda kv: kv[1]["ms"]) if ktimes else ("?", {"ms": 0, "launches": 0})
     dname, drec = dom
     per_launch_ms = drec["ms"] / max(1, drec["launches"])
     dbytes = algo.get(dname, drec.get("bytes", 0.0)) / max(1, drec["launches"])
     achieved = dbytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    # ncu-measured DRAM traffic per launch of the same kernel (profiles/, one
+    # --set full capture) -- read back here, never measured under the bench.
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
+            traffic = json.load(f).get(dname)
+    except Exception:
+        traffic = None
     shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ktimes.values())), 4)
               for k, v in ktimes.items()}
 
@@ -400,7 +416,9 @@ def main() -> None:
                     "d2h_bytes_per_step": int(frame_bytes)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": dbytes,
+                         "per_launch_ms": per_launch_ms,
                          "peak_source": peak_src, "kernel_share": shares},
             "render_stats": {"hit_rate": st.hits / st.lookups if st.lookups else 0.0,
                              "lookups": st.lookups, "hits": st.hits, "inserts_won": st.inserts_won,

@@ -36,7 +36,8 @@ constexpr float kInvPi = 0.318309886183790671538f;
 // Render counters (device, u64): see kStat*.
 enum {
     kStatLookups = 0, kStatHits, kStatWon, kStatFull, kStatLost, kStatStores, kStatInstrs,
-    kStatShade, kStatShadow, kStatNodes, kStatPrims, kStatTex, kStatCount = 16
+    kStatShade, kStatShadow, kStatNodes, kStatPrims, kStatTex, kStatNodesShadow, kStatPrimsShadow,
+    kStatCount = 16
 };
 
 struct RenderView {
@@ -564,8 +565,8 @@ __global__ void __launch_bounds__(256) k_shadow(RenderView R) {
         rays = 1;
     }
     mcgd::warp_add(R.stats + kStatShadow, rays);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
+    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
 }
 
 
@@ -956,8 +957,8 @@ __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
                            : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
+    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
 }
 
 // Closest hits of the live paths, one per thread, warp-synchronous traversal.
@@ -1276,8 +1277,8 @@ __global__ void __launch_bounds__(256) k_shadow_pww(RenderView R, unsigned int* 
         }
     }
     mcgd::warp_add(R.stats + kStatShadow, nrays);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
+    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
 }
 
 // ---------------------------------------------------------------------------
@@ -1476,8 +1477,8 @@ __global__ void __launch_bounds__(kWsBlock) k_shadow_ws(RenderView R) {
     const bool occ = any_ws(R.S, active, o, d, kTMin, tmax, nvis, ntest, sref);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
+    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
 }
 
 __global__ void __launch_bounds__(kWsBlock) k_trace_closest_ws(RenderView R, const uint32_t* count, int vtx) {
@@ -1959,9 +1960,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         stats->paths = static_cast<uint64_t>(n_pix) * P.spp;
         stats->shading_points = st[kStatShade];
         stats->shadow_rays = st[kStatShadow];
-        stats->bvh_nodes = st[kStatNodes];
-        stats->prims_tested = st[kStatPrims];
+        stats->bvh_nodes = st[kStatNodes] + st[kStatNodesShadow];
+        stats->prims_tested = st[kStatPrims] + st[kStatPrimsShadow];
         stats->tex_samples = st[kStatTex];
+        stats->bvh_nodes_shadow = st[kStatNodesShadow];
+        stats->prims_tested_shadow = st[kStatPrimsShadow];
         stats->launches = ctx->launches - launches0;
     }
 }
