@@ -423,6 +423,19 @@ mcg_status mcg_render_device(mcg_ctx* ctx, const mcg_render_params* params, mcg_
 mcg_status mcg_camera_setup(const mcg_flat_scene* scene, int32_t width, int32_t height,
                             float out[12]);
 
+/* Scene queries on the uploaded scene for a batch of rays (host buffers):
+ * Scene::intersect (scene.cpp:252-278) -> 24 floats per ray (found, t,
+ * position, normal, uv, slot, e1, e2, duv1, duv2; zeros on a miss) and
+ * Scene::occluded (scene.cpp:280-298) -> 1 byte per ray, t_max per ray.
+ * rays: 6 floats (origin, direction). variant selects the traversal the
+ * renderer can use: 0 per-thread DFS over the reference's nodes,
+ * 1 warp-synchronous child pairs, 2 4-wide, 3 speculative 4-wide (default).
+ * Every variant returns the reference's answer. */
+mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min, float t_max,
+                               int32_t variant, float* out);
+mcg_status mcg_occluded_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min,
+                              const float* t_max, int32_t variant, uint8_t* out);
+
 /* Per-shading-point material evaluation (execute, stackvm.cpp:248-368) on the
  * device for a batch of shading points of one material slot of the uploaded
  * scene. sp: 15 floats per point (position, normal, incoming, uv, g1, g2).

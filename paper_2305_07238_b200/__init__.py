@@ -229,6 +229,28 @@ class Context:
                                         mip_offset, _ptr(vals), _ptr(nodes), _ptr(instrs)))
         return vals, nodes, instrs
 
+    def intersect_batch(self, rays: np.ndarray, t_min: float = 1e-4, t_max: float = np.inf,
+                        variant: int = 3) -> np.ndarray:
+        """Scene::intersect (scene.cpp:252-278) on the uploaded scene for n
+        rays (n x 6: origin, direction) -> n x 24 floats (found, t, position,
+        normal, uv, slot, e1, e2, duv1, duv2). variant: the traversal
+        (0 per-thread DFS, 1 child pairs, 2 4-wide, 3 speculative 4-wide)."""
+        rays = np.ascontiguousarray(rays, np.float32).reshape(-1, 6)
+        out = np.zeros((rays.shape[0], 24), np.float32)
+        check(N.lib().mcg_intersect_batch(self.handle, _ptr(rays), rays.shape[0], t_min, t_max,
+                                          variant, _ptr(out)))
+        return out
+
+    def occluded_batch(self, rays: np.ndarray, t_min: float, t_max: np.ndarray,
+                       variant: int = 3) -> np.ndarray:
+        """Scene::occluded (scene.cpp:280-298) per ray with its own t_max."""
+        rays = np.ascontiguousarray(rays, np.float32).reshape(-1, 6)
+        t_max = np.ascontiguousarray(t_max, np.float32).reshape(-1)
+        out = np.zeros(rays.shape[0], np.uint8)
+        check(N.lib().mcg_occluded_batch(self.handle, _ptr(rays), rays.shape[0], t_min, _ptr(t_max),
+                                         variant, _ptr(out)))
+        return out
+
 
 # --------------------------------------------------------------------------
 # Material cache (cache.hpp:69-115), resident in HBM

@@ -7,7 +7,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libmcg.so")
+# MCG_LIB_PATH: an alternative in-tree build (kernel A/B experiments,
+# profiles/scripts/build_variant.sh); default the normal build.
+LIB_PATH = os.environ.get("MCG_LIB_PATH") or os.path.join(HERE, "_lib", "libmcg.so")
 
 u8, u32, u64, i32, i64, f32, f64 = C.c_uint8, C.c_uint32, C.c_uint64, C.c_int32, C.c_int64, C.c_float, C.c_double
 P = C.POINTER
@@ -134,6 +136,8 @@ _SIGS = [
     ("mcg_render_device", C.c_int, [vp, P(RenderParams), vp, P(Frame), P(RenderStats)]),
     ("mcg_camera_setup", C.c_int, [P(FlatScene), i32, i32, P(f32)]),
     ("mcg_execute_batch", C.c_int, [vp, u32, vp, C.c_size_t, vp, i32, i32, vp, vp, vp]),
+    ("mcg_intersect_batch", C.c_int, [vp, vp, C.c_size_t, f32, f32, i32, vp]),
+    ("mcg_occluded_batch", C.c_int, [vp, vp, C.c_size_t, f32, vp, i32, vp]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

@@ -395,13 +395,11 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // (position, normal, uv, footprint gradients) and the propagated cone width
 // and returns the material slot, on a miss adds throughput * env to L and
 // returns n_programs (the "no hit" sort key).
-__device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p, float4& ro,
-                                                 const float4& rd, const float4& thr, float4& L,
-                                                 uint32_t& nvis, uint32_t& ntest, int vtx) {
+__device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t p, float4& ro,
+                                               const float4& rd, const float4& thr, float4& L, bool found,
+                                               uint32_t prim, float t, float b1, float b2, int vtx) {
     const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
-    uint32_t prim = 0;
-    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    if (!traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest)) {
+    if (!found) {
         L.x = L.x + thr.x * R.S.env[0];
         L.y = L.y + thr.y * R.S.env[1];
         L.z = L.z + thr.z * R.S.env[2];
@@ -420,30 +418,14 @@ __device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p
     return sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
 }
 
-// Pass start: primary rays of every path of the pass, traced to vertex 0.
-__global__ void __launch_bounds__(256) k_primary(RenderView R) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0;
-    if (i < R.n_paths) {
-        const uint32_t slot_j = i / R.n_pix;
-        const uint32_t pixel = R.pix[i - slot_j * R.n_pix];
-        const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
-        V3 o, d;
-        camera_ray(R, pixel, rkey, o, d);
-        float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
-        const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
-        const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
-        float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const uint32_t key = trace_vertex(R, i, ro, rd, thr, L, nvis, ntest, 0);
-        R.ro[i] = ro;
-        R.rd[i] = rd;
-        R.thr[i] = thr;
-        R.L[i] = L;
-        R.keys[i] = key;
-        R.vals[i] = i;
-    }
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+__device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p, float4& ro,
+                                                 const float4& rd, const float4& thr, float4& L,
+                                                 uint32_t& nvis, uint32_t& ntest, int vtx) {
+    const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
+    uint32_t prim = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    const bool found = traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest);
+    return hit_record(R, p, ro, rd, thr, L, found, prim, t, b1, b2, vtx);
 }
 
 // Next-event estimation and the cosine bounce of every shaded vertex b:
@@ -936,10 +918,309 @@ __device__ __forceinline__ bool any_ww4(const mcgd::SceneView& S, bool active, V
     return hit;
 }
 
+// ---------------------------------------------------------------------------
+// 4-wide traversal with speculative expansion and one-word stack entries.
+// An entry is (code, E): code >= 0 a 4-wide node, code < 0 a leaf
+// ~(first << 3 | count) (reference leaves hold <= 4 primitives,
+// scene.cpp:168). The entry to be popped next stays in registers (the last
+// child pushed), so most pops never touch the local-memory stack.
+//
+// Speculation: a lane that already holds a leaf keeps popping while other
+// lanes of its warp are still searching for theirs -- internal entries are
+// expanded, the next leaf is left in place until the leaf tests ran. This
+// is exact. An internal entry passes its cull test (closest < E) against a
+// closest that is at least the reference's at that point, so it may be
+// expanded where the reference would have culled it; but each child box lies
+// inside its parent's, so every child's entry distance is >= the parent's
+// (slab arithmetic is monotone under IEEE rounding) and every
+// one of them is then culled when popped, against a closest that is by then
+// at most the reference's. Leaves are only tested after a cull test against
+// the up-to-date closest, in the reference's LIFO order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t entry_code(int32_t a, int32_t b) {
+    // quads entry (a, b): b > 0 leaf (a = ~first, b = count), b < 0 node a
+    return b > 0 ? static_cast<int32_t>(~((static_cast<uint32_t>(~a) << 3) | static_cast<uint32_t>(b))) : a;
+}
+
+__device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool active, V3 o, V3 d,
+                                             float tmin, float tmax, uint32_t& prim, float& t_out,
+                                             float& b1_out, float& b2_out, uint32_t& nodes_visited,
+                                             uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int2 st[64];
+    int top = 0;
+    int32_t nc = 0;  // register-held next entry
+    float ne = 0.0f;
+    bool has_n = false;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(T1 < E)) {
+            nc = entry_code(S.root_a, S.root_b);
+            ne = E;
+            has_n = true;
+        }
+    }
+    bool found = false;
+    float closest = tmax;
+    int32_t lc = 0;
+    bool leaf = false;
+    while (__any_sync(mcgd::kFull, has_n || leaf)) {
+        // Phase 1: pop/expand until every lane holds a leaf or is done;
+        // lanes holding one keep expanding internal entries (speculation).
+        for (;;) {
+            if (has_n) {
+                if (closest < ne) {  // culled (the reference's test at pop)
+                    ++nodes_visited;
+                    has_n = false;
+                } else if (nc < 0) {
+                    if (!leaf) {
+                        ++nodes_visited;
+                        leaf = true;
+                        lc = nc;
+                        has_n = false;
+                    }
+                } else {
+                    ++nodes_visited;
+                    has_n = false;
+                    const float4* p = S.quads + 8 * nc;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                        const int32_t eb = __float_as_int(hi.w);
+                        if (eb == 0) continue;  // empty entry
+                        float E, T1;
+                        slab(o, inv, lo, hi, tmin, E, T1);
+                        if (!(T1 < E)) {
+                            if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
+                            nc = entry_code(__float_as_int(lo.w), eb);
+                            ne = E;
+                            has_n = true;
+                        }
+                    }
+                }
+            }
+            if (!has_n && top > 0) {
+                --top;
+                const int2 e = st[top];
+                nc = e.x;
+                ne = __int_as_float(e.y);
+                has_n = true;
+            }
+            if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
+        }
+        // Phase 2: every lane holding a leaf tests it (the reference's order).
+        if (leaf) {
+            const uint32_t v = static_cast<uint32_t>(~lc);
+            const uint32_t first = v >> 3, cnt = v & 7u;
+            prims_tested += cnt;
+            for (uint32_t i = first; i < first + cnt; ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                    closest = t;
+                    prim = i;
+                    t_out = t;
+                    b1_out = b1;
+                    b2_out = b2;
+                    found = true;
+                }
+            }
+            leaf = false;
+        }
+    }
+    return found;
+}
+
+// Any-hit with the same entries and speculation; children pushed far to
+// near so the nearest pops first (any order is exact for a boolean query).
+__device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                         float tmax, uint32_t& nodes_visited, uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t st[64];
+    int top = 0;
+    int32_t nc = 0;
+    bool has_n = false;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(fminf(tmax, T1) < E)) {
+            nc = entry_code(S.root_a, S.root_b);
+            has_n = true;
+        }
+    }
+    bool hit = false;
+    int32_t lc = 0;
+    bool leaf = false;
+    while (__any_sync(mcgd::kFull, has_n || leaf)) {
+        for (;;) {
+            if (has_n) {
+                if (nc < 0) {
+                    if (!leaf) {
+                        ++nodes_visited;
+                        leaf = true;
+                        lc = nc;
+                        has_n = false;
+                    }
+                } else {
+                    ++nodes_visited;
+                    has_n = false;
+                    const float4* p = S.quads + 8 * nc;
+                    float ke[4];
+                    int32_t kc[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                        const int32_t eb = __float_as_int(hi.w);
+                        float E, T1;
+                        slab(o, inv, lo, hi, tmin, E, T1);
+                        const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
+                        ke[k] = ok ? E : __int_as_float(0x7f800000);
+                        kc[k] = ok ? entry_code(__float_as_int(lo.w), eb) : 0x7fffffff;
+                    }
+#define MCG_CSWAP(i, j)                                                              \
+    if (ke[i] < ke[j]) {                                                             \
+        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
+        const int32_t tc = kc[i]; kc[i] = kc[j]; kc[j] = tc;                         \
+    }
+                    MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
+#undef MCG_CSWAP
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (kc[k] != 0x7fffffff) {
+                            if (has_n) st[top++] = nc;
+                            nc = kc[k];
+                            has_n = true;
+                        }
+                    }
+                }
+            }
+            if (!has_n && top > 0) {
+                nc = st[--top];
+                has_n = true;
+            }
+            if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
+        }
+        if (leaf) {
+            const uint32_t v = static_cast<uint32_t>(~lc);
+            const uint32_t first = v >> 3, cnt = v & 7u;
+            prims_tested += cnt;
+            for (uint32_t i = first; i < first + cnt; ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            if (hit) has_n = false, top = 0;
+        }
+    }
+    return hit;
+}
+
+// Pass start: primary rays of every path of the pass, traced to vertex 0
+// (warp-synchronous speculative traversal, like k_trace_closest_ww<2>).
+__global__ void __launch_bounds__(256) k_primary(RenderView R) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nvis = 0, ntest = 0;
+    const bool active = i < R.n_paths;
+    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
+    if (active) {
+        const uint32_t slot_j = i / R.n_pix;
+        const uint32_t pixel = R.pix[i - slot_j * R.n_pix];
+        const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
+        camera_ray(R, pixel, rkey, o, d);
+    }
+    uint32_t prim = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
+                                    nvis, ntest);
+    if (active) {
+        float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
+        const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
+        const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
+        float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const uint32_t key = hit_record(R, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
+        R.ro[i] = ro;
+        R.rd[i] = rd;
+        R.thr[i] = thr;
+        R.L[i] = L;
+        R.keys[i] = key;
+        R.vals[i] = i;
+    }
+    mcgd::warp_add(R.stats + kStatNodes, nvis);
+    mcgd::warp_add(R.stats + kStatPrims, ntest);
+}
+
+// ---------------------------------------------------------------------------
+// Scene queries for a batch of rays (Scene::intersect / Scene::occluded,
+// scene.cpp:252-298) through any of the traversal variants the renderer
+// uses -- the parity tests check each one against the oracle's DFS.
+// variant: 0 per-thread binary DFS, 1 while-while child pairs, 2 4-wide,
+// 3 speculative 4-wide (the default of render()).
+// ---------------------------------------------------------------------------
+template <int kVar>
+__global__ void __launch_bounds__(256) k_intersect_batch(mcgd::SceneView S, const float* rays, uint32_t n,
+                                                         float tmin, float tmax, float* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = i < n;
+    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
+    if (active) {
+        o = V3{rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
+        d = V3{rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
+    }
+    uint32_t prim = 0, nv = 0, nt = 0;
+    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+    bool found;
+    if (kVar == 0) found = active && traverse_closest(S, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    else if (kVar == 1) found = closest_ww(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    else if (kVar == 2) found = closest_ww4(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    else found = closest_ww4s(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    if (!active) return;
+    float* w = out + 24ull * i;
+    float v[24] = {};
+    if (found) {
+        const Surface sf = surface(S, o, d, prim, t, b1, b2);
+        const float vals[21] = {1.0f, t, sf.p.x, sf.p.y, sf.p.z, sf.n.x, sf.n.y, sf.n.z, sf.u, sf.v,
+                                static_cast<float>(sf.slot), sf.e1.x, sf.e1.y, sf.e1.z, sf.e2.x, sf.e2.y,
+                                sf.e2.z, sf.d1.x, sf.d1.y, sf.d2.x, sf.d2.y};
+#pragma unroll
+        for (int k = 0; k < 21; ++k) v[k] = vals[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 24; ++k) w[k] = v[k];
+}
+
+template <int kVar>
+__global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const float* rays, uint32_t n,
+                                                        float tmin, const float* tmax, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = i < n;
+    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
+    float tm = 0.0f;
+    if (active) {
+        o = V3{rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
+        d = V3{rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
+        tm = tmax[i];
+    }
+    uint32_t nv = 0, nt = 0;
+    bool occ;
+    if (kVar == 0) occ = active && traverse_any(S, o, d, tmin, tm, nv, nt);
+    else if (kVar == 1) occ = any_ww(S, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 2) occ = any_ww4(S, active, o, d, tmin, tm, nv, nt);
+    else occ = any_ww4s(S, active, o, d, tmin, tm, nv, nt);
+    if (active) out[i] = occ ? 1 : 0;
+}
+
 // Shadow rays, one per thread over the queue, warp-synchronous traversal
-// over the binary (kWide = false) or the 4-wide (kWide = true) tree.
-template <bool kWide>
-__global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
+// over the binary (kTree = 0), 4-wide (1) or speculative 4-wide (2) tree.
+template <int kTree>
+#ifndef MCG_TRACE_MINB
+#define MCG_TRACE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *R.shadow_count;
@@ -953,8 +1234,9 @@ __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    const bool occ = kWide ? any_ww4(R.S, active, o, d, kTMin, tmax, nvis, ntest)
-                           : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
+    const bool occ = kTree == 2   ? any_ww4s(R.S, active, o, d, kTMin, tmax, nvis, ntest)
+                     : kTree == 1 ? any_ww4(R.S, active, o, d, kTMin, tmax, nvis, ntest)
+                                  : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
@@ -962,8 +1244,8 @@ __global__ void __launch_bounds__(256) k_shadow_ww(RenderView R) {
 }
 
 // Closest hits of the live paths, one per thread, warp-synchronous traversal.
-template <bool kWide>
-__global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
+template <int kTree>
+__global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *count;
@@ -978,8 +1260,10 @@ __global__ void __launch_bounds__(256) k_trace_closest_ww(RenderView R, const ui
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
     const float inf = __int_as_float(0x7f800000);
-    const bool found = kWide ? closest_ww4(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
-                             : closest_ww(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest);
+    const bool found =
+        kTree == 2   ? closest_ww4s(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
+        : kTree == 1 ? closest_ww4(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
+                     : closest_ww(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest);
     if (active) {
         uint32_t key = no_hit_key(R);
         if (!found) {
@@ -1807,7 +2091,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const int key_bits = static_cast<int>(R.key_shift) + slot_bits;
     const char* trace_env = std::getenv("MCG_TRACE");
     const bool plain = trace_env && std::string(trace_env) == "plain";
-    const bool binary = trace_env && std::string(trace_env) == "ww2";  // else the 4-wide tree
+    const bool binary = trace_env && std::string(trace_env) == "ww2";
+    const bool wide_nospec = trace_env && std::string(trace_env) == "ww4";  // else speculative 4-wide
     const bool pww = trace_env && std::string(trace_env) == "pww";
     // Shared-memory stacks (experiment, MCG_TRACE=ws; slower than the
     // local-memory stacks on the bench scene: profiles/README.md).
@@ -1897,8 +2182,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 } else if (plain) {
                     k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 } else {
-                    if (binary) k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                    else k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    if (binary) k_shadow_ww<0><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    else if (wide_nospec) k_shadow_ww<1><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    else k_shadow_ww<2><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 }
                 ls.done();
             }
@@ -1916,8 +2202,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 } else if (plain) {
                     k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 } else {
-                    if (binary) k_trace_closest_ww<false><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                    else k_trace_closest_ww<true><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                    if (binary) k_trace_closest_ww<0><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                    else if (wide_nospec) k_trace_closest_ww<1><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                    else k_trace_closest_ww<2><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 }
                 ls.done();
             }
@@ -1972,6 +2259,67 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
 }  // namespace
 
 extern "C" {
+
+mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min, float t_max,
+                               int32_t variant, float* out) {
+    return guarded([&] {
+        if (!ctx || (n && (!rays || !out))) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
+        if (variant < 0 || variant > 3) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+        if (n >= (1ull << 31)) fail(MCG_ERR_INVALID_ARGUMENT, "batch too large");
+        if (!n) return;
+        ctx->scratch_a.ensure(n * 24);
+        ctx->scratch_b.ensure(n * 96);
+        float* dr = ctx->scratch_a.as<float>();
+        float* dout = ctx->scratch_b.as<float>();
+        cuda_check(cudaMemcpyAsync(dr, rays, n * 24, cudaMemcpyHostToDevice, ctx->stream), "H2D rays");
+        const mcgd::SceneView& S = ctx->scene.view;
+        const uint32_t n32 = static_cast<uint32_t>(n);
+        const unsigned g = grid_for(n, 256);
+        {
+            LaunchScope ls(ctx, "intersect_batch", 0.0);
+            if (variant == 0) k_intersect_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
+            else if (variant == 1) k_intersect_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
+            else if (variant == 2) k_intersect_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
+            else k_intersect_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
+            ls.done();
+        }
+        cuda_check(cudaMemcpyAsync(out, dout, n * 96, cudaMemcpyDeviceToHost, ctx->stream), "D2H hits");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "intersect_batch");
+    });
+}
+
+mcg_status mcg_occluded_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min, const float* t_max,
+                              int32_t variant, uint8_t* out) {
+    return guarded([&] {
+        if (!ctx || (n && (!rays || !t_max || !out))) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
+        if (variant < 0 || variant > 3) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+        if (n >= (1ull << 31)) fail(MCG_ERR_INVALID_ARGUMENT, "batch too large");
+        if (!n) return;
+        ctx->scratch_a.ensure(n * 24);
+        ctx->scratch_b.ensure(n * 4);
+        ctx->scratch_c.ensure(n);
+        float* dr = ctx->scratch_a.as<float>();
+        float* dt = ctx->scratch_b.as<float>();
+        uint8_t* dout = ctx->scratch_c.as<uint8_t>();
+        cuda_check(cudaMemcpyAsync(dr, rays, n * 24, cudaMemcpyHostToDevice, ctx->stream), "H2D rays");
+        cuda_check(cudaMemcpyAsync(dt, t_max, n * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D tmax");
+        const mcgd::SceneView& S = ctx->scene.view;
+        const uint32_t n32 = static_cast<uint32_t>(n);
+        const unsigned g = grid_for(n, 256);
+        {
+            LaunchScope ls(ctx, "occluded_batch", 0.0);
+            if (variant == 0) k_occluded_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
+            else if (variant == 1) k_occluded_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
+            else if (variant == 2) k_occluded_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
+            else k_occluded_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
+            ls.done();
+        }
+        cuda_check(cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, ctx->stream), "D2H occluded");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "occluded_batch");
+    });
+}
 
 mcg_status mcg_render_device(mcg_ctx* ctx, const mcg_render_params* params, mcg_cache* cache,
                              mcg_frame* d_frame, mcg_render_stats* stats) {

@@ -1,6 +1,6 @@
 """Short render of the bench workload (1920x1080, classroom-like, cache 1e7x10)
 for ncu captures: spp is small so a `--set full` capture of a few launches
-finishes quickly. Usage: python profiles/scripts/prof_render.py [spp] [cache 0|1]"""
+finishes quickly. Usage: python profiles/scripts/prof_render.py [spp] [cache 0|1] [renders]"""
 import os
 import sys
 import tempfile
@@ -16,6 +16,6 @@ ctx = Context(0)
 scene = load_scene(bench.make_scene(tempfile.mkdtemp()))
 cfg = RenderConfig(width=bench.W, height=bench.H, spp=spp, cache_enabled=cache,
                    n_cells=bench.N_CELLS, n_entries=bench.N_ENTRIES)
-for _ in range(2):
+for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     r = render(scene, cfg, ctx=ctx)
 print("ok", r.stats.shading_points, r.stats.hits)

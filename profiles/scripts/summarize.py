@@ -2,6 +2,7 @@
 
     python profiles/scripts/summarize.py rep  gpurun_out/x.ncu-rep  > profiles/x.txt
     python profiles/scripts/summarize.py launches gpurun_out/launches.csv > profiles/y.txt
+    python profiles/scripts/summarize.py traffic gpurun_out/traffic.csv > profiles/dram_traffic.json
 """
 import collections
 import csv
@@ -55,5 +56,34 @@ def launches(path):
         print(f"{k[:70]:70s} {v[0]:8d} {v[1] / 1e3:12.1f} {v[1] / tot:7.3f}")
 
 
+# kernel-name prefix -> the class name bench.py times it under
+CLASSES = {"k_trace_closest": "trace_closest", "k_shadow": "trace_shadow", "k_shade": "shade",
+           "k_primary": "primary", "k_probe_bench": "probe"}
+
+
+def traffic(path):
+    """dram read+write bytes per launch, averaged over every launch of each
+    kernel class in the capture (one whole render), as JSON."""
+    import json
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    hdr = rows[hi]
+    ki, vi, mi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name"),
+                      hdr.index("Metric Unit"))
+    idi = hdr.index("ID")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    per = collections.defaultdict(lambda: collections.defaultdict(float))
+    for r in rows[hi + 1:]:
+        if len(r) <= vi or r[mi] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            continue
+        name = r[ki].split("(")[0].split("::")[-1].split("<")[0]
+        cls = next((v for k, v in CLASSES.items() if name.startswith(k)), None)
+        if cls:
+            per[cls][r[idi]] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    out = {k: sum(v.values()) / len(v) for k, v in per.items()}
+    out["_launches"] = {k: len(v) for k, v in per.items()}
+    print(json.dumps(out, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    {"rep": rep, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"rep": rep, "launches": launches, "traffic": traffic}[sys.argv[1]](sys.argv[2])

@@ -210,3 +210,44 @@ def test_render_concurrent_rmse_bound(ctx, oracle, scene_dir):
     assert rmse(conc.frame.radiance_image(), off) <= rmse(ref_cached, off) + 1e-4
     assert conc.stats.hits > 0
     oracle.cache_free(oc)
+
+
+def _edge_rays(s, r, n):
+    """Rays aimed at triangle vertices and edge midpoints (shared edges give
+    closest-hit ties, resolved by visit order) and axis-aligned rays."""
+    geom = np.asarray(np.ctypeslib.as_array(s.flat.prim_geom, (s.flat.n_prims * 12,))).reshape(-1, 3, 4)
+    p0 = geom[:, 0, :3]
+    e1, e2 = geom[:, 1, :3], geom[:, 2, :3]
+    pts = np.concatenate([p0, p0 + e1, p0 + e2, p0 + 0.5 * e1, p0 + 0.5 * e2, p0 + 0.5 * (e1 + e2)])
+    tgt = pts[r.integers(0, pts.shape[0], n)]
+    lo, hi = pts.min(0), pts.max(0)
+    o = r.uniform(lo + 0.05 * (hi - lo), hi - 0.05 * (hi - lo), (n, 3))
+    d = tgt - o
+    d /= np.maximum(np.linalg.norm(d, axis=1, keepdims=True), 1e-20)
+    d[: n // 20] = np.eye(3)[r.integers(0, 3, n // 20)] * r.choice([-1.0, 1.0], (n // 20, 1))
+    return np.concatenate([o, d], 1).astype(np.float32)
+
+
+@pytest.mark.parametrize("kind,tps", [("cornell", 8), ("classroom", 24)])
+def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, kind, tps):
+    """Closest hit and any hit through each traversal variant (per-thread DFS,
+    child pairs, 4-wide, speculative 4-wide) == the oracle's reference DFS,
+    bit for bit, on random rays and on rays aimed at vertices and edges."""
+    path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=tps), f"{scene_dir}/q_{kind}")
+    s = load_scene(path)
+    ctx.upload(s)
+    r = np.random.default_rng(11)
+    n = 60_000
+    o = r.uniform([-7.9, 0.01, -9.9], [7.9, 4.99, 9.9], (n, 3))
+    d = r.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rays = np.concatenate([np.concatenate([o, d], 1).astype(np.float32), _edge_rays(s, r, n)])
+    want = oracle.intersect(s.flat, rays)
+    assert want[:, 0].sum() > 0.5 * rays.shape[0]
+    tm = r.uniform(0.01, 20, rays.shape[0]).astype(np.float32)
+    want_occ = oracle.occluded(s.flat, rays, 1e-4, tm)
+    for variant in range(4):
+        got = ctx.intersect_batch(rays, 1e-4, np.inf, variant)
+        np.testing.assert_array_equal(bits(got), bits(want), err_msg=f"variant {variant}")
+        np.testing.assert_array_equal(ctx.occluded_batch(rays, 1e-4, tm, variant), want_occ,
+                                      err_msg=f"variant {variant}")
