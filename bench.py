@@ -16,8 +16,10 @@ Printed JSON line (rank 0):
   e2e          the same metric through the C ABI's host-buffer entry point
                (mcg_upload_scene + mcg_render with pinned host framebuffers):
                scene H2D + framebuffer H2D/D2H inside the timed region
-  roofline     dominant kernel's algorithmic bytes / its CUDA-event time vs
-               the measured HBM peak (MEASURED_PEAKS.json)
+  roofline     dominant kernel's compulsory HBM bytes / its CUDA-event time vs
+               the measured HBM peak (MEASURED_PEAKS.json), the ncu DRAM
+               traffic per launch, and the L1/L2-served BVH/triangle bytes
+  roofline_shade  the same for the material-VM + cache-probe kernel
   probe_roofline  the cache-probe kernel on the 1e7 x 10 table (HBM-bound)
   cache_speedup   t(no cache) / t(cache) on the same workload
   cpu_baseline the reference's own CPU path (oracle/_ref) on the host cores
@@ -353,38 +355,77 @@ def main() -> None:
     peak, peak_src = measured_peaks()
     ne = N_ENTRIES
     steps = args.steps
-    # Algorithmic bytes per kernel class over the timed steps:
+    f = scene.flat
+    n_lights = f.n_point_lights + f.n_rect_lights
+    # Compulsory HBM bytes per kernel class over the timed steps (DESIGN.md
+    # §5): what the kernel must move between HBM and the SMs at least once.
     #   shade:  one cell (8 Ne) per lookup and per store attempt, +8 per won
-    #           CAS, 48 per TexSample (4 RGB texels), and per shading point
-    #           the 64-byte record in + NEE/bounce state out (2 lights x 48 + 48)
-    #   trace:  128 per 4-wide node popped, 48 per triangle tested, and per
-    #           traced path 32 in (ray) + 72 out (record, key, value)
-    #   shadow: 128 per node popped, 48 per triangle, 33 per ray (ray + flag)
+    #           CAS, 48 per TexSample (4 RGB texels); per shading point the
+    #           record + path state in (104 B) and the continuation out (48 B);
+    #           per shadow-ray candidate 52 B out, per rejected light 16 B
+    #   trace_closest: per ray 36 B in (order, ray), 72 B out per hit
+    #           (record, cone, key, value), 48 B per miss (radiance update)
+    #   trace_shadow: per ray 37 B (queue slot, ray, visibility byte)
+    # plus the scene's nodes and triangles once per launch. BVH node and
+    # triangle reads beyond that are served by L1/L2 (the bench scene's BVH
+    # is a few hundred KB); SURVEY §8d's per-visit units (40 B per reference
+    # node, here 128 B per 4-wide node, 48 B per triangle) are reported as
+    # `cache_served_bytes_per_launch` next to them.
+    scene_once = f.n_prims * (48 + 24 + 4) + f.n_nodes * 64
+    closest_rays = st.closest_rays
+    # hits of continuation rays = shading points after the primary vertex
+    # (every primary ray hits in the closed bench room)
+    closest_hits = min(closest_rays, max(0, st.shading_points - st.paths))
     n_closest_nodes = st.bvh_nodes - st.bvh_nodes_shadow
     n_closest_prims = st.prims_tested - st.prims_tested_shadow
-    algo = {
+    compulsory = {
         "shade": steps * (st.lookups * 8 * ne + st.stores_attempted * 8 * ne + st.inserts_won * 8
-                          + st.tex_samples * 48 + st.shading_points * (64 + 144)),
-        "trace_closest": steps * (n_closest_nodes * 128 + n_closest_prims * 48
-                                  + st.shading_points * (32 + 72)),
-        "trace_shadow": steps * (st.bvh_nodes_shadow * 128 + st.prims_tested_shadow * 48
-                                 + st.shadow_rays * 33),
+                          + st.tex_samples * 48 + st.shading_points * (104 + 48)
+                          + st.shadow_rays * 52 + (n_lights * st.shading_points - st.shadow_rays) * 16),
+        "trace_closest": steps * (closest_rays * 36 + closest_hits * 72 + (closest_rays - closest_hits) * 48),
+        "trace_shadow": steps * st.shadow_rays * 37,
     }
-    dom = max(ktimes.items(), key=lambda kv: kv[1]["ms"]) if ktimes else ("?", {"ms": 0, "launches": 0})
-    dname, drec = dom
-    per_launch_ms = drec["ms"] / max(1, drec["launches"])
-    dbytes = algo.get(dname, drec.get("bytes", 0.0)) / max(1, drec["launches"])
-    achieved = dbytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
-    # ncu-measured DRAM traffic per launch of the same kernel (profiles/, one
-    # --set full capture) -- read back here, never measured under the bench.
-    traffic = None
+    cache_served = {
+        "trace_closest": steps * (n_closest_nodes * 128 + n_closest_prims * 48),
+        "trace_shadow": steps * (st.bvh_nodes_shadow * 128 + st.prims_tested_shadow * 48),
+    }
+
+    def kernel_roofline(kname):
+        rec = ktimes.get(kname, {"ms": 0.0, "launches": 0})
+        launches = max(1, rec["launches"])
+        per_ms = rec["ms"] / launches
+        nbytes = compulsory.get(kname, rec.get("bytes", 0.0)) / launches
+        if kname in ("trace_closest", "trace_shadow"):
+            nbytes += scene_once
+        ach = nbytes / (per_ms / 1e3) / 1e9 if per_ms > 0 else 0.0
+        out = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak, "unit": "GB/s",
+               "frac": ach / peak, "traffic": traffic_ncu.get(kname),
+               "algorithmic_bytes_per_launch": nbytes, "per_launch_ms": per_ms}
+        if kname in cache_served:
+            cs = cache_served[kname] / launches
+            out["cache_served_bytes_per_launch"] = cs
+            out["cache_served_gbs"] = cs / (per_ms / 1e3) / 1e9 if per_ms > 0 else 0.0
+        return out
+
+    # ncu-measured DRAM traffic per launch (profiles/dram_traffic.json, one
+    # capture of a whole render, averaged per launch) -- read back here,
+    # never measured under the bench.
     try:
-        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
-            traffic = json.load(f).get(dname)
+        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
+            traffic_ncu = {k: v for k, v in json.load(fh).items() if not k.startswith("_")}
     except Exception:
-        traffic = None
+        traffic_ncu = {}
+    dname = max(ktimes.items(), key=lambda kv: kv[1]["ms"])[0] if ktimes else "?"
+    roof = kernel_roofline(dname)
+    roof["limiter"] = ("issue/latency: warp divergence in BVH traversal (L1/L2-resident tree); "
+                       "HBM is not the bound -- see profiles/README.md"
+                       if dname.startswith("trace") else "random HBM access (cache probes)")
+    roof["peak_source"] = peak_src
     shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ktimes.values())), 4)
               for k, v in ktimes.items()}
+    roof["kernel_share"] = shares
+    # The north-star kernel (material VM + cache probes) beside it.
+    roof_shade = kernel_roofline("shade")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -415,17 +456,16 @@ def main() -> None:
                     "h2d_bytes_per_step": int(scene_bytes + frame_bytes),
                     "d2h_bytes_per_step": int(frame_bytes)},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": dbytes,
-                         "per_launch_ms": per_launch_ms,
-                         "peak_source": peak_src, "kernel_share": shares},
+            "roofline": roof,
+            "roofline_shade": roof_shade,
             "render_stats": {"hit_rate": st.hits / st.lookups if st.lookups else 0.0,
                              "lookups": st.lookups, "hits": st.hits, "inserts_won": st.inserts_won,
                              "inserts_lost_full": st.inserts_lost_full,
                              "shading_points": st.shading_points, "shadow_rays": st.shadow_rays,
                              "bvh_nodes": st.bvh_nodes, "prims_tested": st.prims_tested,
-                             "tex_samples": st.tex_samples},
+                             "bvh_nodes_shadow": st.bvh_nodes_shadow,
+                             "prims_tested_shadow": st.prims_tested_shadow,
+                             "closest_rays": st.closest_rays, "tex_samples": st.tex_samples},
             "cpu_baseline": cpu,
         }
         line.update(extras)

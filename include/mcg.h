@@ -398,6 +398,7 @@ typedef struct mcg_render_stats {    /* RenderStats, tracer.hpp:45-55 */
     uint64_t paths, shading_points, shadow_rays;
     uint64_t bvh_nodes, prims_tested, tex_samples;   /* work counters (roofline bytes) */
     uint64_t bvh_nodes_shadow, prims_tested_shadow;  /* of which any-hit (shadow) rays */
+    uint64_t closest_rays;                           /* continuation rays traced (after the primary) */
     uint64_t launches;               /* this library's kernel launches in the call */
     uint64_t* hits_per_sample;       /* optional, caller array of spp entries */
 } mcg_render_stats;
@@ -429,7 +430,9 @@ mcg_status mcg_camera_setup(const mcg_flat_scene* scene, int32_t width, int32_t 
  * Scene::occluded (scene.cpp:280-298) -> 1 byte per ray, t_max per ray.
  * rays: 6 floats (origin, direction). variant selects the traversal the
  * renderer can use: 0 per-thread DFS over the reference's nodes,
- * 1 warp-synchronous child pairs, 2 4-wide, 3 speculative 4-wide (default).
+ * 1 warp-synchronous child pairs, 2 4-wide, 3 speculative 4-wide (default),
+ * 4 warp packets over the 4-wide tree; occluded also 5: speculative 4-wide over
+ * a SAH hierarchy of the reference's leaves (the renderer's shadow rays).
  * Every variant returns the reference's answer. */
 mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min, float t_max,
                                int32_t variant, float* out);

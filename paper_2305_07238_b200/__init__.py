@@ -234,7 +234,7 @@ class Context:
         """Scene::intersect (scene.cpp:252-278) on the uploaded scene for n
         rays (n x 6: origin, direction) -> n x 24 floats (found, t, position,
         normal, uv, slot, e1, e2, duv1, duv2). variant: the traversal
-        (0 per-thread DFS, 1 child pairs, 2 4-wide, 3 speculative 4-wide)."""
+        (0 per-thread DFS, 1 child pairs, 2 4-wide, 3 speculative 4-wide, 4 packets)."""
         rays = np.ascontiguousarray(rays, np.float32).reshape(-1, 6)
         out = np.zeros((rays.shape[0], 24), np.float32)
         check(N.lib().mcg_intersect_batch(self.handle, _ptr(rays), rays.shape[0], t_min, t_max,

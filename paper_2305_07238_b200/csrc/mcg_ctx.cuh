@@ -61,6 +61,7 @@ struct DeviceScene {
     uint32_t max_cache_points = 0;
     float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};   // scene bounds (BVH root)
     uint32_t max_stack4 = 1;   // worst-case LIFO stack of the 4-wide traversal
+    uint32_t max_stack_s = 1;  // same for the shadow (SAH) tree
     mcg_flat_scene cam{};   // camera/env fields only (no pointers used)
     bool loaded = false;
     void clear() {

@@ -203,6 +203,8 @@ struct SceneView {
     const float4* pairs;          // 4 float4 per internal node: both children's records
     const float4* quads;          // 8 float4 per 4-wide node (collapsed reference tree)
     int32_t root_a, root_b;       // root entry into `quads`: (0, -1) or a leaf (~first, count)
+    const float4* squads;         // 4-wide SAH tree over the reference's leaves (any-hit only)
+    int32_t sroot_a, sroot_b;     // root entry into `squads`
     uint32_t n_nodes;
     const mcg_point_light* plights;
     uint32_t n_plights;

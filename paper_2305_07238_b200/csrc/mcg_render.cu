@@ -37,6 +37,7 @@ constexpr float kInvPi = 0.318309886183790671538f;
 enum {
     kStatLookups = 0, kStatHits, kStatWon, kStatFull, kStatLost, kStatStores, kStatInstrs,
     kStatShade, kStatShadow, kStatNodes, kStatPrims, kStatTex, kStatNodesShadow, kStatPrimsShadow,
+    kStatClosestRays,
     kStatCount = 16
 };
 
@@ -69,6 +70,7 @@ struct RenderView {
     const uint32_t* skey;     // sorted keys: hits first, in material order
     uint32_t key_shift;       // key = slot << key_shift | Morton code of the hit point
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
+    int pk_depth;             // packet-traversal stack depth (entries per warp)
     float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
     const uint32_t* order;    // sorted path ids
     float4* sro;              // shadow ray per (path, light): origin.xyz, t_max
@@ -567,6 +569,7 @@ __global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const
         R.keys[q] = key;
         R.vals[q] = p;
     }
+    mcgd::warp_add(R.stats + kStatClosestRays, q < *count ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
@@ -1034,8 +1037,9 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
 
 // Any-hit with the same entries and speculation; children pushed far to
 // near so the nearest pops first (any order is exact for a boolean query).
-__device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
-                                         float tmax, uint32_t& nodes_visited, uint32_t& prims_tested) {
+__device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, const float4* Q, int32_t root_a,
+                                         int32_t root_b, bool active, V3 o, V3 d, float tmin, float tmax,
+                                         uint32_t& nodes_visited, uint32_t& prims_tested) {
     const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
     int32_t st[64];
     int top = 0;
@@ -1046,7 +1050,7 @@ __device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, bool active, 
         float E, T1;
         slab(o, inv, lo, hi, tmin, E, T1);
         if (!(fminf(tmax, T1) < E)) {
-            nc = entry_code(S.root_a, S.root_b);
+            nc = entry_code(root_a, root_b);
             has_n = true;
         }
     }
@@ -1066,7 +1070,7 @@ __device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, bool active, 
                 } else {
                     ++nodes_visited;
                     has_n = false;
-                    const float4* p = S.quads + 8 * nc;
+                    const float4* p = Q + 8 * nc;
                     float ke[4];
                     int32_t kc[4];
 #pragma unroll
@@ -1120,8 +1124,212 @@ __device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, bool active, 
     return hit;
 }
 
+// ---------------------------------------------------------------------------
+// Packet traversal: the warp walks the 4-wide tree together, one entry at a
+// time, each entry carrying the mask of lanes that pushed it. The
+// reference's visit order does not depend on the ray (its DFS always pushes
+// left then right, scene.cpp:259-272), so every lane still sees its own
+// entries in its own LIFO order -- the packet stack is the interleaving of
+// 32 identical-order private stacks -- and each lane makes exactly its own
+// decisions: the ray-only half of a box test when the entry is pushed, the
+// closest-dependent half (closest < E, per lane, E kept in shared memory)
+// when it is popped. Pops and pushes are warp-uniform, so the stack costs
+// one shared-memory word pair per entry instead of per lane, and the box
+// tests run with every interested lane converged. Coherent rays (primary
+// rays, shadow rays toward one light from Morton-sorted points) share most
+// of their entries; the price is that a lane waits through entries that
+// only other lanes need.
+// Per-warp shared memory: code[D], mask[D] (+ E[D][32] for closest hit).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool closest_pk(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                           float tmax, uint32_t& prim, float& t_out, float& b1_out,
+                                           float& b2_out, uint32_t& nodes_visited, uint32_t& prims_tested,
+                                           int32_t* s_code, uint32_t* s_mask, float* s_e) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int top = 0;
+    if (S.n_nodes) {
+        bool ok = false;
+        float E = 0.0f, T1 = 0.0f;
+        if (active) {
+            slab(o, inv, __ldg(S.nodes), __ldg(S.nodes + 1), tmin, E, T1);
+            ok = !(T1 < E);
+        }
+        const uint32_t m = __ballot_sync(mcgd::kFull, ok);
+        if (m) {
+            if (lane == 0) {
+                s_code[0] = entry_code(S.root_a, S.root_b);
+                s_mask[0] = m;
+            }
+            s_e[lane] = E;
+            top = 1;
+        }
+    }
+    __syncwarp();
+    bool found = false;
+    float closest = tmax;
+    while (top > 0) {
+        --top;
+        const int32_t code = s_code[top];
+        const uint32_t m = s_mask[top];
+        bool me = (m >> lane) & 1u;
+        if (me) {
+            ++nodes_visited;
+            if (closest < s_e[top * 32 + lane]) me = false;  // the reference's test at pop
+        }
+        if (__ballot_sync(mcgd::kFull, me) == 0u) {
+            __syncwarp();
+            continue;
+        }
+        if (code < 0) {
+            if (me) {
+                const uint32_t v = static_cast<uint32_t>(~code);
+                const uint32_t first = v >> 3, cnt = v & 7u;
+                prims_tested += cnt;
+                for (uint32_t i = first; i < first + cnt; ++i) {
+                    float t, b1, b2;
+                    if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+                        closest = t;
+                        prim = i;
+                        t_out = t;
+                        b1_out = b1;
+                        b2_out = b2;
+                        found = true;
+                    }
+                }
+            }
+        } else {
+            const float4* p = S.quads + 8 * code;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                const int32_t eb = __float_as_int(hi.w);
+                if (eb == 0) continue;  // empty entry (uniform)
+                float E, T1;
+                slab(o, inv, lo, hi, tmin, E, T1);
+                const uint32_t mk = __ballot_sync(mcgd::kFull, me && !(T1 < E));
+                if (mk) {
+                    if (lane == 0) {
+                        s_code[top] = entry_code(__float_as_int(lo.w), eb);
+                        s_mask[top] = mk;
+                    }
+                    s_e[top * 32 + lane] = E;
+                    ++top;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return found;
+}
+
+__device__ __forceinline__ bool any_pk(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
+                                       float tmax, uint32_t& nodes_visited, uint32_t& prims_tested,
+                                       int32_t* s_code, uint32_t* s_mask) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int top = 0;
+    if (S.n_nodes) {
+        bool ok = false;
+        if (active) {
+            float E, T1;
+            slab(o, inv, __ldg(S.nodes), __ldg(S.nodes + 1), tmin, E, T1);
+            ok = !(fminf(tmax, T1) < E);
+        }
+        const uint32_t m = __ballot_sync(mcgd::kFull, ok);
+        if (m) {
+            if (lane == 0) {
+                s_code[0] = entry_code(S.root_a, S.root_b);
+                s_mask[0] = m;
+            }
+            top = 1;
+        }
+    }
+    __syncwarp();
+    bool hit = false;
+    while (top > 0) {
+        --top;
+        const int32_t code = s_code[top];
+        const uint32_t m = s_mask[top] & ~__ballot_sync(mcgd::kFull, hit);
+        if (m == 0u) {
+            __syncwarp();
+            continue;
+        }
+        const bool me = (m >> lane) & 1u;
+        if (me) ++nodes_visited;
+        if (code < 0) {
+            if (me) {
+                const uint32_t v = static_cast<uint32_t>(~code);
+                const uint32_t first = v >> 3, cnt = v & 7u;
+                prims_tested += cnt;
+                for (uint32_t i = first; i < first + cnt; ++i) {
+                    float t, b1, b2;
+                    if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                        hit = true;
+                        break;
+                    }
+                }
+            }
+            if (__all_sync(mcgd::kFull, hit || !active)) break;
+        } else {
+            const float4* p = S.quads + 8 * code;
+            const int leader = __ffs(m) - 1;
+            float ke[4];
+            uint32_t km[4];
+            int32_t kc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                const int32_t eb = __float_as_int(hi.w);
+                float E, T1;
+                slab(o, inv, lo, hi, tmin, E, T1);
+                const bool ok = me && eb != 0 && !(fminf(tmax, T1) < E);
+                km[k] = __ballot_sync(mcgd::kFull, ok);
+                // order entries by the leader lane's entry distance (any
+                // order is exact for a boolean query; near first exits early)
+                ke[k] = __shfl_sync(mcgd::kFull, ok ? E : __int_as_float(0x7f800000), leader);
+                kc[k] = entry_code(__float_as_int(lo.w), eb);
+            }
+#define MCG_CSWAP(i, j)                                                              \
+    if (ke[i] < ke[j]) {                                                             \
+        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
+        const int32_t tc = kc[i]; kc[i] = kc[j]; kc[j] = tc;                         \
+        const uint32_t tm = km[i]; km[i] = km[j]; km[j] = tm;                        \
+    }
+            MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
+#undef MCG_CSWAP
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (km[k]) {
+                        s_code[top] = kc[k];
+                        s_mask[top] = km[k];
+                        ++top;
+                    }
+                }
+            }
+            top = __shfl_sync(mcgd::kFull, top, 0);
+        }
+        __syncwarp();
+    }
+    return hit;
+}
+
+// Per-warp packet stacks in dynamic shared memory (depth D entries).
+__device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& code, uint32_t*& mask,
+                                          float*& e) {
+    extern __shared__ float pk_smem[];
+    const uint32_t w = threadIdx.x >> 5;
+    const size_t per_warp = static_cast<size_t>(depth) * (closest ? 2 + 32 : 2);
+    float* base = pk_smem + w * per_warp;
+    code = reinterpret_cast<int32_t*>(base);
+    mask = reinterpret_cast<uint32_t*>(base + depth);
+    e = base + 2 * depth;
+}
+
 // Pass start: primary rays of every path of the pass, traced to vertex 0
-// (warp-synchronous speculative traversal, like k_trace_closest_ww<2>).
+// (speculative 4-wide or packet traversal, like k_trace_closest_ww<kTree>).
+template <int kTree>
 __global__ void __launch_bounds__(256) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -1135,8 +1343,17 @@ __global__ void __launch_bounds__(256) k_primary(RenderView R) {
     }
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
-                                    nvis, ntest);
+    bool found;
+    if (kTree == 3) {
+        int32_t* pc;
+        uint32_t* pm;
+        float* pe;
+        pk_stacks(R.pk_depth, true, pc, pm, pe);
+        found = closest_pk(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest,
+                           pc, pm, pe);
+    } else {
+        found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest);
+    }
     if (active) {
         float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
@@ -1163,7 +1380,7 @@ __global__ void __launch_bounds__(256) k_primary(RenderView R) {
 // ---------------------------------------------------------------------------
 template <int kVar>
 __global__ void __launch_bounds__(256) k_intersect_batch(mcgd::SceneView S, const float* rays, uint32_t n,
-                                                         float tmin, float tmax, float* out) {
+                                                         float tmin, float tmax, float* out, int depth) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = i < n;
     V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
@@ -1177,7 +1394,14 @@ __global__ void __launch_bounds__(256) k_intersect_batch(mcgd::SceneView S, cons
     if (kVar == 0) found = active && traverse_closest(S, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
     else if (kVar == 1) found = closest_ww(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
     else if (kVar == 2) found = closest_ww4(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
-    else found = closest_ww4s(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    else if (kVar == 3) found = closest_ww4s(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt);
+    else {
+        int32_t* pc;
+        uint32_t* pm;
+        float* pe;
+        pk_stacks(depth, true, pc, pm, pe);
+        found = closest_pk(S, active, o, d, tmin, tmax, prim, t, b1, b2, nv, nt, pc, pm, pe);
+    }
     if (!active) return;
     float* w = out + 24ull * i;
     float v[24] = {};
@@ -1195,7 +1419,7 @@ __global__ void __launch_bounds__(256) k_intersect_batch(mcgd::SceneView S, cons
 
 template <int kVar>
 __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const float* rays, uint32_t n,
-                                                        float tmin, const float* tmax, uint8_t* out) {
+                                                        float tmin, const float* tmax, uint8_t* out, int depth) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = i < n;
     V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
@@ -1210,7 +1434,15 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
     if (kVar == 0) occ = active && traverse_any(S, o, d, tmin, tm, nv, nt);
     else if (kVar == 1) occ = any_ww(S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 2) occ = any_ww4(S, active, o, d, tmin, tm, nv, nt);
-    else occ = any_ww4s(S, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 3) occ = any_ww4s(S, S.quads, S.root_a, S.root_b, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 5) occ = any_ww4s(S, S.squads, S.sroot_a, S.sroot_b, active, o, d, tmin, tm, nv, nt);
+    else {
+        int32_t* pc;
+        uint32_t* pm;
+        float* pe;
+        pk_stacks(depth, false, pc, pm, pe);
+        occ = any_pk(S, active, o, d, tmin, tm, nv, nt, pc, pm);
+    }
     if (active) out[i] = occ ? 1 : 0;
 }
 
@@ -1234,7 +1466,13 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R)
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    const bool occ = kTree == 2   ? any_ww4s(R.S, active, o, d, kTMin, tmax, nvis, ntest)
+    int32_t* pc = nullptr;
+    uint32_t* pm = nullptr;
+    float* pe = nullptr;
+    if (kTree == 3) pk_stacks(R.pk_depth, false, pc, pm, pe);
+    const bool occ = kTree == 3   ? any_pk(R.S, active, o, d, kTMin, tmax, nvis, ntest, pc, pm)
+                     : kTree == 4 ? any_ww4s(R.S, R.S.squads, R.S.sroot_a, R.S.sroot_b, active, o, d, kTMin, tmax, nvis, ntest)
+                     : kTree == 2 ? any_ww4s(R.S, R.S.quads, R.S.root_a, R.S.root_b, active, o, d, kTMin, tmax, nvis, ntest)
                      : kTree == 1 ? any_ww4(R.S, active, o, d, kTMin, tmax, nvis, ntest)
                                   : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
@@ -1260,8 +1498,13 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(Render
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
     const float inf = __int_as_float(0x7f800000);
+    int32_t* pc = nullptr;
+    uint32_t* pm = nullptr;
+    float* pe = nullptr;
+    if (kTree == 3) pk_stacks(R.pk_depth, true, pc, pm, pe);
     const bool found =
-        kTree == 2   ? closest_ww4s(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
+        kTree == 3   ? closest_pk(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest, pc, pm, pe)
+        : kTree == 2 ? closest_ww4s(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
         : kTree == 1 ? closest_ww4(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
                      : closest_ww(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest);
     if (active) {
@@ -1289,525 +1532,7 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(Render
         R.keys[q] = key;
         R.vals[q] = p;
     }
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
-}
-
-// ---------------------------------------------------------------------------
-// Persistent while-while traversal over the 4-wide tree. Each resident warp
-// loops: (1) lanes without a ray fetch the next rays of the queue (one atomic
-// per warp, only when at least kRefill lanes are idle); (2) every lane pops
-// and expands nodes in its reference order until it parks on a leaf or its
-// stack runs dry; (3) parked lanes test their leaves together; lanes whose
-// ray is finished write their results together. Short and long rays stop
-// holding each other's lanes idle, and no lane leaves its reference order.
-// ---------------------------------------------------------------------------
-constexpr int kRefill = 8;
-
-__global__ void __launch_bounds__(256) k_trace_closest_pww(RenderView R, const uint32_t* count_ptr,
-                                                           unsigned int* cursor, int vtx) {
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t count = *count_ptr;
-    uint32_t nvis = 0, ntest = 0;
-    bool has = false, exhausted = false, leaf = false, fin = false, found = false;
-    uint32_t q = 0, p = 0, prim = 0;
-    V3 o{0, 0, 0}, d{1, 1, 1}, inv{1, 1, 1};
-    float4 ro{}, rd{};
-    int32_t sa[64], sb[64];
-    float se[64];
-    int top = 0;
-    float closest = 0.0f, tt = 0.0f, tb1 = 0.0f, tb2 = 0.0f;
-    int32_t la = 0, lb = 0;
-    for (;;) {
-        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
-        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
-            const int ldr = __ffs(idle) - 1;
-            unsigned base = 0;
-            if (static_cast<int>(lane) == ldr) base = atomicAdd(cursor, static_cast<unsigned>(__popc(idle)));
-            base = __shfl_sync(mcgd::kFull, base, ldr);
-            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
-            if (!has) {
-                q = base + __popc(idle & ((1u << lane) - 1u));
-                if (q < count) {
-                    has = true;
-                    p = R.order[q];
-                    ro = R.ro[p];
-                    rd = R.rd[p];
-                    o = V3{ro.x, ro.y, ro.z};
-                    d = V3{rd.x, rd.y, rd.z};
-                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-                    closest = __int_as_float(0x7f800000);
-                    found = false;
-                    top = 0;
-                    if (R.S.n_nodes) {
-                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
-                        float E, T1;
-                        slab(o, inv, lo, hi, kTMin, E, T1);
-                        if (!(T1 < E)) {
-                            sa[0] = R.S.root_a;
-                            sb[0] = R.S.root_b;
-                            se[0] = E;
-                            top = 1;
-                        }
-                    }
-                }
-            }
-        }
-        if (__ballot_sync(mcgd::kFull, has) == 0) {
-            if (exhausted) break;
-            continue;
-        }
-        // Phase 1: pop / expand in reference order until parked on a leaf.
-        for (;;) {
-            if (has && !leaf && !fin) {
-                if (top == 0) {
-                    fin = true;
-                } else {
-                    --top;
-                    const int32_t a = sa[top], b = sb[top];
-                    ++nvis;
-                    if (!(closest < se[top])) {
-                        if (b > 0) {
-                            leaf = true;
-                            la = a;
-                            lb = b;
-                        } else {
-                            const float4* pp = R.S.quads + 8 * a;
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const float4 lo = __ldg(pp + 2 * k), hi = __ldg(pp + 2 * k + 1);
-                                const int32_t eb = __float_as_int(hi.w);
-                                if (eb == 0) continue;
-                                float E, T1;
-                                slab(o, inv, lo, hi, kTMin, E, T1);
-                                if (!(T1 < E)) {
-                                    sa[top] = __float_as_int(lo.w);
-                                    sb[top] = eb;
-                                    se[top] = E;
-                                    ++top;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-            if (__all_sync(mcgd::kFull, !has || leaf || fin)) break;
-        }
-        // Phase 2: leaves, together.
-        if (leaf) {
-            const uint32_t first = static_cast<uint32_t>(~la);
-            ntest += static_cast<uint32_t>(lb);
-            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
-                float t, b1, b2;
-                if (hit_prim(R.S, i, o, d, kTMin, closest, t, b1, b2)) {
-                    closest = t;
-                    prim = i;
-                    tt = t;
-                    tb1 = b1;
-                    tb2 = b2;
-                    found = true;
-                }
-            }
-            leaf = false;
-            fin = top == 0;
-        }
-        // Finished rays, together: the vertex's shading record or the env.
-        if (fin) {
-            uint32_t key = no_hit_key(R);
-            if (!found) {
-                float4 L = R.L[p];
-                const float4 thr = R.thr[p];
-                L.x = L.x + thr.x * R.S.env[0];
-                L.y = L.y + thr.y * R.S.env[1];
-                L.z = L.z + thr.z * R.S.env[2];
-                R.L[p] = L;
-            } else {
-                const Surface s = surface(R.S, o, d, prim, tt, tb1, tb2);
-                const float width = ro.w + tt * rd.w;  // propagate (raycone.cpp:15-18)
-                float2 g1, g2;
-                mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-                R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-                R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-                R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
-                R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
-                const uint32_t slot_j = p / R.n_pix;
-                const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
-                key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
-            }
-            R.keys[q] = key;
-            R.vals[q] = p;
-            has = false;
-            fin = false;
-        }
-    }
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
-}
-
-__global__ void __launch_bounds__(256) k_shadow_pww(RenderView R, unsigned int* cursor) {
-    const unsigned lane = threadIdx.x & 31u;
-    const uint32_t count = *R.shadow_count;
-    uint32_t nvis = 0, ntest = 0, nrays = 0;
-    bool has = false, exhausted = false, leaf = false, fin = false, hit = false;
-    uint32_t s = 0;
-    V3 o{0, 0, 0}, d{1, 1, 1}, inv{1, 1, 1};
-    float tmax = 0.0f;
-    int32_t sa[64], sb[64];
-    int top = 0;
-    int32_t la = 0, lb = 0;
-    for (;;) {
-        const unsigned idle = __ballot_sync(mcgd::kFull, !has);
-        if (idle && !exhausted && (__popc(idle) >= kRefill || idle == mcgd::kFull)) {
-            const int ldr = __ffs(idle) - 1;
-            unsigned base = 0;
-            if (static_cast<int>(lane) == ldr) base = atomicAdd(cursor, static_cast<unsigned>(__popc(idle)));
-            base = __shfl_sync(mcgd::kFull, base, ldr);
-            exhausted = base + static_cast<unsigned>(__popc(idle)) >= count;
-            if (!has) {
-                const uint32_t qq = base + __popc(idle & ((1u << lane) - 1u));
-                if (qq < count) {
-                    has = true;
-                    ++nrays;
-                    s = R.squeue[qq];
-                    const float4 so = R.sro[s], sd = R.srd[s];
-                    o = V3{so.x, so.y, so.z};
-                    d = V3{sd.x, sd.y, sd.z};
-                    inv = V3{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-                    tmax = so.w;
-                    hit = false;
-                    top = 0;
-                    if (R.S.n_nodes) {
-                        const float4 lo = __ldg(R.S.nodes), hi = __ldg(R.S.nodes + 1);
-                        float E, T1;
-                        slab(o, inv, lo, hi, kTMin, E, T1);
-                        if (!(fminf(tmax, T1) < E)) {
-                            sa[0] = R.S.root_a;
-                            sb[0] = R.S.root_b;
-                            top = 1;
-                        }
-                    }
-                }
-            }
-        }
-        if (__ballot_sync(mcgd::kFull, has) == 0) {
-            if (exhausted) break;
-            continue;
-        }
-        for (;;) {
-            if (has && !leaf && !fin) {
-                if (top == 0) {
-                    fin = true;
-                } else {
-                    --top;
-                    const int32_t a = sa[top], b = sb[top];
-                    ++nvis;
-                    if (b > 0) {
-                        leaf = true;
-                        la = a;
-                        lb = b;
-                    } else {
-                        const float4* pp = R.S.quads + 8 * a;
-                        float ke[4];
-                        int32_t ka[4], kb[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float4 lo = __ldg(pp + 2 * k), hi = __ldg(pp + 2 * k + 1);
-                            const int32_t eb = __float_as_int(hi.w);
-                            float E, T1;
-                            slab(o, inv, lo, hi, kTMin, E, T1);
-                            const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
-                            ke[k] = ok ? E : __int_as_float(0x7f800000);
-                            ka[k] = __float_as_int(lo.w);
-                            kb[k] = ok ? eb : 0;
-                        }
-#define MCG_CSWAP(i, j)                                                              \
-    if (ke[i] < ke[j]) {                                                             \
-        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
-        const int32_t ta = ka[i]; ka[i] = ka[j]; ka[j] = ta;                         \
-        const int32_t tb = kb[i]; kb[i] = kb[j]; kb[j] = tb;                         \
-    }
-                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
-#undef MCG_CSWAP
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (kb[k] != 0) {
-                                sa[top] = ka[k];
-                                sb[top] = kb[k];
-                                ++top;
-                            }
-                        }
-                    }
-                }
-            }
-            if (__all_sync(mcgd::kFull, !has || leaf || fin)) break;
-        }
-        if (leaf) {
-            const uint32_t first = static_cast<uint32_t>(~la);
-            ntest += static_cast<uint32_t>(lb);
-            for (uint32_t i = first; i < first + static_cast<uint32_t>(lb); ++i) {
-                float t, b1, b2;
-                if (hit_prim(R.S, i, o, d, kTMin, tmax, t, b1, b2)) {
-                    hit = true;
-                    break;
-                }
-            }
-            leaf = false;
-            fin = hit || top == 0;
-        }
-        if (fin) {
-            R.vis[s] = hit ? 0 : 1;
-            has = false;
-            fin = false;
-        }
-    }
-    mcgd::warp_add(R.stats + kStatShadow, nrays);
-    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
-    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
-}
-
-// ---------------------------------------------------------------------------
-// Shared-memory traversal stacks. Entry k of thread t lives at [k][t] of a
-// per-block array, so lanes at different stack depths still hit different
-// banks (the stride is a multiple of 32) -- no local-memory round trips, no
-// uncoalesced spills. An entry packs its node reference into one word:
-// >= 0 a 4-wide node index, < 0 ~(first << 3 | count) for a leaf.
-// Capacity kStackCap; scenes whose collapsed tree could need more use the
-// local-memory kernels (the host checks the worst-case depth).
-// ---------------------------------------------------------------------------
-constexpr int kStackCap = 32;
-constexpr int kWsBlock = 128;
-
-__device__ __forceinline__ int32_t pack_ref(int32_t a, int32_t b) {
-    return b > 0 ? ~((static_cast<int32_t>(~a) << 3) | b) : a;
-}
-
-__device__ __forceinline__ bool closest_ws(const mcgd::SceneView& S, bool active, V3 o, V3 d,
-                                           float tmin, float tmax, uint32_t& prim, float& t_out,
-                                           float& b1_out, float& b2_out, uint32_t& nodes_visited,
-                                           uint32_t& prims_tested, int32_t* sref, float* se) {
-    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-    const int tid = threadIdx.x;
-    int top = 0;
-    if (active && S.n_nodes) {
-        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
-        float E, T1;
-        slab(o, inv, lo, hi, tmin, E, T1);
-        if (!(T1 < E)) {
-            sref[tid] = pack_ref(S.root_a, S.root_b);
-            se[tid] = E;
-            top = 1;
-        }
-    }
-    bool found = false;
-    float closest = tmax;
-    int32_t leaf_ref = 0;
-    bool leaf = false;
-    bool done = top == 0;
-    while (__any_sync(mcgd::kFull, !done)) {
-        for (;;) {
-            if (!done && !leaf) {
-                if (top == 0) {
-                    done = true;
-                } else {
-                    --top;
-                    const int32_t r = sref[top * kWsBlock + tid];
-                    ++nodes_visited;
-                    if (!(closest < se[top * kWsBlock + tid])) {
-                        if (r < 0) {
-                            leaf = true;
-                            leaf_ref = ~r;
-                        } else {
-                            const float4* p = S.quads + 8 * r;
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
-                                const int32_t eb = __float_as_int(hi.w);
-                                if (eb == 0) continue;
-                                float E, T1;
-                                slab(o, inv, lo, hi, tmin, E, T1);
-                                if (!(T1 < E)) {
-                                    sref[top * kWsBlock + tid] = pack_ref(__float_as_int(lo.w), eb);
-                                    se[top * kWsBlock + tid] = E;
-                                    ++top;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-            if (__all_sync(mcgd::kFull, done || leaf)) break;
-        }
-        if (leaf) {
-            const uint32_t first = static_cast<uint32_t>(leaf_ref) >> 3;
-            const uint32_t cnt = static_cast<uint32_t>(leaf_ref) & 7u;
-            prims_tested += cnt;
-            for (uint32_t i = first; i < first + cnt; ++i) {
-                float t, b1, b2;
-                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
-                    closest = t;
-                    prim = i;
-                    t_out = t;
-                    b1_out = b1;
-                    b2_out = b2;
-                    found = true;
-                }
-            }
-            leaf = false;
-            done = top == 0;
-        }
-    }
-    return found;
-}
-
-__device__ __forceinline__ bool any_ws(const mcgd::SceneView& S, bool active, V3 o, V3 d, float tmin,
-                                       float tmax, uint32_t& nodes_visited, uint32_t& prims_tested,
-                                       int32_t* sref) {
-    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-    const int tid = threadIdx.x;
-    int top = 0;
-    if (active && S.n_nodes) {
-        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
-        float E, T1;
-        slab(o, inv, lo, hi, tmin, E, T1);
-        if (!(fminf(tmax, T1) < E)) {
-            sref[tid] = pack_ref(S.root_a, S.root_b);
-            top = 1;
-        }
-    }
-    bool hit = false;
-    int32_t leaf_ref = 0;
-    bool leaf = false;
-    bool done = top == 0;
-    while (__any_sync(mcgd::kFull, !done)) {
-        for (;;) {
-            if (!done && !leaf) {
-                if (top == 0) {
-                    done = true;
-                } else {
-                    --top;
-                    const int32_t r = sref[top * kWsBlock + tid];
-                    ++nodes_visited;
-                    if (r < 0) {
-                        leaf = true;
-                        leaf_ref = ~r;
-                    } else {
-                        const float4* p = S.quads + 8 * r;
-                        float ke[4];
-                        int32_t kr[4];
-                        bool ko[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
-                            const int32_t eb = __float_as_int(hi.w);
-                            float E, T1;
-                            slab(o, inv, lo, hi, tmin, E, T1);
-                            ko[k] = eb != 0 && !(fminf(tmax, T1) < E);
-                            ke[k] = ko[k] ? E : __int_as_float(0x7f800000);
-                            kr[k] = pack_ref(__float_as_int(lo.w), eb);
-                        }
-#define MCG_CSWAP(i, j)                                                              \
-    if (ke[i] < ke[j]) {                                                             \
-        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
-        const int32_t tr = kr[i]; kr[i] = kr[j]; kr[j] = tr;                         \
-        const bool to = ko[i]; ko[i] = ko[j]; ko[j] = to;                            \
-    }
-                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
-#undef MCG_CSWAP
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (ko[k]) {
-                                sref[top * kWsBlock + tid] = kr[k];
-                                ++top;
-                            }
-                        }
-                    }
-                }
-            }
-            if (__all_sync(mcgd::kFull, done || leaf)) break;
-        }
-        if (leaf) {
-            const uint32_t first = static_cast<uint32_t>(leaf_ref) >> 3;
-            const uint32_t cnt = static_cast<uint32_t>(leaf_ref) & 7u;
-            prims_tested += cnt;
-            for (uint32_t i = first; i < first + cnt; ++i) {
-                float t, b1, b2;
-                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
-                    hit = true;
-                    break;
-                }
-            }
-            leaf = false;
-            done = hit || top == 0;
-        }
-    }
-    return hit;
-}
-
-__global__ void __launch_bounds__(kWsBlock) k_shadow_ws(RenderView R) {
-    __shared__ int32_t sref[kStackCap * kWsBlock];
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0;
-    const bool active = q < *R.shadow_count;
-    uint32_t s = 0;
-    V3 o{0.0f, 0.0f, 0.0f}, d{1.0f, 1.0f, 1.0f};
-    float tmax = 0.0f;
-    if (active) {
-        s = R.squeue[q];
-        const float4 so = R.sro[s], sd = R.srd[s];
-        o = V3{so.x, so.y, so.z};
-        d = V3{sd.x, sd.y, sd.z};
-        tmax = so.w;
-    }
-    const bool occ = any_ws(R.S, active, o, d, kTMin, tmax, nvis, ntest, sref);
-    if (active) R.vis[s] = occ ? 0 : 1;
-    mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
-    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
-    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
-}
-
-__global__ void __launch_bounds__(kWsBlock) k_trace_closest_ws(RenderView R, const uint32_t* count, int vtx) {
-    __shared__ int32_t sref[kStackCap * kWsBlock];
-    __shared__ float se[kStackCap * kWsBlock];
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0;
-    const bool active = q < *count;
-    uint32_t p = 0;
-    float4 ro{}, rd{};
-    if (active) {
-        p = R.order[q];
-        ro = R.ro[p];
-        rd = R.rd[p];
-    }
-    const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
-    uint32_t prim = 0;
-    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    const bool found = closest_ws(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1,
-                                  b2, nvis, ntest, sref, se);
-    if (active) {
-        uint32_t key = no_hit_key(R);
-        if (!found) {
-            float4 L = R.L[p];
-            const float4 thr = R.thr[p];
-            L.x = L.x + thr.x * R.S.env[0];
-            L.y = L.y + thr.y * R.S.env[1];
-            L.z = L.z + thr.z * R.S.env[2];
-            R.L[p] = L;
-        } else {
-            const Surface s = surface(R.S, o, d, prim, t, b1, b2);
-            const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
-            float2 g1, g2;
-            mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-            R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-            R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-            R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
-            R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
-            const uint32_t slot_j = p / R.n_pix;
-            const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
-            key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
-        }
-        R.keys[q] = key;
-        R.vals[q] = p;
-    }
+    mcgd::warp_add(R.stats + kStatClosestRays, q < *count ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
@@ -1954,6 +1679,16 @@ bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
     return tile >= lo && tile < hi;
 }
 
+// Packet kernels may need more than the default 48 KB of dynamic shared memory.
+void pk_smem_attr(size_t bytes) {
+    const int b = static_cast<int>(bytes);
+    cudaFuncSetAttribute(k_primary<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_shadow_ww<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_trace_closest_ww<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_intersect_batch<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_occluded_batch<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external,
                    double* d_rad, double* d_nodes, uint32_t* d_samples, mcg_render_stats* stats) {
     const DeviceScene& D = ctx->scene;
@@ -2093,17 +1828,21 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const bool plain = trace_env && std::string(trace_env) == "plain";
     const bool binary = trace_env && std::string(trace_env) == "ww2";
     const bool wide_nospec = trace_env && std::string(trace_env) == "ww4";  // else speculative 4-wide
-    const bool pww = trace_env && std::string(trace_env) == "pww";
-    // Shared-memory stacks (experiment, MCG_TRACE=ws; slower than the
-    // local-memory stacks on the bench scene: profiles/README.md).
-    const bool ws = trace_env && std::string(trace_env) == "ws" &&
-                    D.max_stack4 <= static_cast<uint32_t>(kStackCap);
-    int n_sm = 148, occ_s = 1, occ_c = 1;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_shadow_pww, 256, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_trace_closest_pww, 256, 0);
-    const unsigned pgrid_shadow = static_cast<unsigned>(n_sm * std::max(1, occ_s));
-    const unsigned pgrid_closest = static_cast<unsigned>(n_sm * std::max(1, occ_c));
+    // Packet traversal (MCG_TRACE=pk: primary, shadow and closest-hit rays;
+    // pks: primary and shadow rays only).
+    const bool pk_all = trace_env && std::string(trace_env) == "pk";
+    const bool pk_coherent = pk_all || (trace_env && std::string(trace_env) == "pks");
+    R.pk_depth = static_cast<int>(D.max_stack4) + 1;
+    // Shadow rays over the SAH tree of the reference's leaves (exact for
+    // any-hit); MCG_SHADOW_TREE=ref keeps the reference's own tree.
+    const char* stree_env = std::getenv("MCG_SHADOW_TREE");
+    const bool sah_shadow = !(stree_env && std::string(stree_env) == "ref");
+    const size_t pk_bytes_closest = 8ull * R.pk_depth * (2 + 32) * sizeof(float);
+    const size_t pk_bytes_any = 8ull * R.pk_depth * 2 * sizeof(float);
+    if (pk_coherent) {
+        if (pk_bytes_closest > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "BVH too deep for packet traversal");
+        pk_smem_attr(pk_bytes_closest);
+    }
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
@@ -2123,7 +1862,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0);
-            k_primary<<<grid, 256, 0, ctx->stream>>>(R);
+            if (pk_coherent) k_primary<3><<<grid, 256, pk_bytes_closest, ctx->stream>>>(R);
+            else k_primary<2><<<grid, 256, 0, ctx->stream>>>(R);
             ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
@@ -2175,15 +1915,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (n_lights) {
                 LaunchScope ls(ctx, "trace_shadow", 0.0);
-                if (ws) {
-                    k_shadow_ws<<<grid_for(n_shadow, kWsBlock), kWsBlock, 0, ctx->stream>>>(R);
-                } else if (pww) {
-                    k_shadow_pww<<<pgrid_shadow, 256, 0, ctx->stream>>>(R, R.shadow_count + 1);
-                } else if (plain) {
+                if (plain) {
                     k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 } else {
                     if (binary) k_shadow_ww<0><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                     else if (wide_nospec) k_shadow_ww<1><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                    else if (pk_coherent) k_shadow_ww<3><<<grid_for(n_shadow, 256), 256, pk_bytes_any, ctx->stream>>>(R);
+                    else if (sah_shadow) k_shadow_ww<4><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                     else k_shadow_ww<2><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 }
                 ls.done();
@@ -2195,15 +1933,12 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
-                if (ws) {
-                    k_trace_closest_ws<<<grid_for(R.n_paths, kWsBlock), kWsBlock, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                } else if (pww) {
-                    k_trace_closest_pww<<<pgrid_closest, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, R.shadow_count + 3, b + 1);
-                } else if (plain) {
+                if (plain) {
                     k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 } else {
                     if (binary) k_trace_closest_ww<0><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                     else if (wide_nospec) k_trace_closest_ww<1><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                    else if (pk_all) k_trace_closest_ww<3><<<grid, 256, pk_bytes_closest, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                     else k_trace_closest_ww<2><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 }
                 ls.done();
@@ -2252,6 +1987,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         stats->tex_samples = st[kStatTex];
         stats->bvh_nodes_shadow = st[kStatNodesShadow];
         stats->prims_tested_shadow = st[kStatPrimsShadow];
+        stats->closest_rays = st[kStatClosestRays];
         stats->launches = ctx->launches - launches0;
     }
 }
@@ -2265,7 +2001,7 @@ mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float 
     return guarded([&] {
         if (!ctx || (n && (!rays || !out))) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
         if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
-        if (variant < 0 || variant > 3) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+        if (variant < 0 || variant > 4) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..4");
         if (n >= (1ull << 31)) fail(MCG_ERR_INVALID_ARGUMENT, "batch too large");
         if (!n) return;
         ctx->scratch_a.ensure(n * 24);
@@ -2277,11 +2013,15 @@ mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float 
         const uint32_t n32 = static_cast<uint32_t>(n);
         const unsigned g = grid_for(n, 256);
         {
+            const int depth = static_cast<int>(ctx->scene.max_stack4) + 1;
+            const size_t pk_bytes = 8ull * depth * (2 + 32) * sizeof(float);
+            if (variant == 4) pk_smem_attr(pk_bytes);
             LaunchScope ls(ctx, "intersect_batch", 0.0);
-            if (variant == 0) k_intersect_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
-            else if (variant == 1) k_intersect_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
-            else if (variant == 2) k_intersect_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
-            else k_intersect_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout);
+            if (variant == 0) k_intersect_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout, 0);
+            else if (variant == 1) k_intersect_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout, 0);
+            else if (variant == 2) k_intersect_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout, 0);
+            else if (variant == 3) k_intersect_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, t_max, dout, 0);
+            else k_intersect_batch<4><<<g, 256, pk_bytes, ctx->stream>>>(S, dr, n32, t_min, t_max, dout, depth);
             ls.done();
         }
         cuda_check(cudaMemcpyAsync(out, dout, n * 96, cudaMemcpyDeviceToHost, ctx->stream), "D2H hits");
@@ -2294,7 +2034,7 @@ mcg_status mcg_occluded_batch(mcg_ctx* ctx, const float* rays, size_t n, float t
     return guarded([&] {
         if (!ctx || (n && (!rays || !t_max || !out))) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
         if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
-        if (variant < 0 || variant > 3) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..3");
+        if (variant < 0 || variant > 5) fail(MCG_ERR_INVALID_ARGUMENT, "variant must be 0..5");
         if (n >= (1ull << 31)) fail(MCG_ERR_INVALID_ARGUMENT, "batch too large");
         if (!n) return;
         ctx->scratch_a.ensure(n * 24);
@@ -2309,11 +2049,16 @@ mcg_status mcg_occluded_batch(mcg_ctx* ctx, const float* rays, size_t n, float t
         const uint32_t n32 = static_cast<uint32_t>(n);
         const unsigned g = grid_for(n, 256);
         {
+            const int depth = static_cast<int>(ctx->scene.max_stack4) + 1;
+            const size_t pk_bytes = 8ull * depth * 2 * sizeof(float);
+            if (variant == 4) pk_smem_attr(pk_bytes);
             LaunchScope ls(ctx, "occluded_batch", 0.0);
-            if (variant == 0) k_occluded_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
-            else if (variant == 1) k_occluded_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
-            else if (variant == 2) k_occluded_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
-            else k_occluded_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout);
+            if (variant == 0) k_occluded_batch<0><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout, 0);
+            else if (variant == 1) k_occluded_batch<1><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout, 0);
+            else if (variant == 2) k_occluded_batch<2><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout, 0);
+            else if (variant == 3) k_occluded_batch<3><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout, 0);
+            else if (variant == 5) k_occluded_batch<5><<<g, 256, 0, ctx->stream>>>(S, dr, n32, t_min, dt, dout, 0);
+            else k_occluded_batch<4><<<g, 256, pk_bytes, ctx->stream>>>(S, dr, n32, t_min, dt, dout, depth);
             ls.done();
         }
         cuda_check(cudaMemcpyAsync(out, dout, n, cudaMemcpyDeviceToHost, ctx->stream), "D2H occluded");

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <limits>
 #include <vector>
 
 #include "host_scene.hpp"
@@ -392,6 +393,178 @@ void need(bool ok, const char* msg) {
 void sync(mcg_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); }
 
 }  // namespace
+
+// Binned-SAH hierarchy over the reference BVH's leaves, collapsed to the
+// 4-wide entry layout of `quads` (entries: leaf (~first, count) with the
+// leaf's own box, or node (index, -1) with the union of its leaves' boxes).
+static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int32_t& root_a, int32_t& root_b) {
+    const mcg_bvh_node* nodes = static_cast<const mcg_bvh_node*>(f.nodes);
+    std::vector<mcg_bvh_node> leaves;
+    for (uint32_t i = 0; i < f.n_nodes; ++i)
+        if (nodes[i].a < 0) leaves.push_back(nodes[i]);
+    std::vector<mcg_bvh_node> out;
+    root_a = 0;
+    root_b = 0;
+    if (leaves.empty()) return out;
+    if (leaves.size() == 1) {
+        root_a = leaves[0].a;
+        root_b = leaves[0].b;
+        return out;
+    }
+    struct BNode { float lo[3], hi[3]; int32_t l = -1, r = -1, leaf = -1; };
+    std::vector<BNode> bn;
+    std::vector<int32_t> idx(leaves.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int32_t>(i);
+    auto cen = [&](int32_t i, int a) { return 0.5f * (leaves[i].lo[a] + leaves[i].hi[a]); };
+    auto area = [](const float* lo, const float* hi) {
+        const float dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+        return dx * dy + dy * dz + dz * dx;
+    };
+    constexpr int kBins = 32;
+    std::function<int32_t(size_t, size_t)> build = [&](size_t first, size_t count) -> int32_t {
+        const int32_t id = static_cast<int32_t>(bn.size());
+        bn.emplace_back();
+        BNode nd;
+        for (int a = 0; a < 3; ++a) {
+            nd.lo[a] = std::numeric_limits<float>::infinity();
+            nd.hi[a] = -std::numeric_limits<float>::infinity();
+        }
+        float clo[3], chi[3];
+        for (int a = 0; a < 3; ++a) {
+            clo[a] = std::numeric_limits<float>::infinity();
+            chi[a] = -std::numeric_limits<float>::infinity();
+        }
+        for (size_t k = first; k < first + count; ++k) {
+            const mcg_bvh_node& L = leaves[idx[k]];
+            for (int a = 0; a < 3; ++a) {
+                nd.lo[a] = std::min(nd.lo[a], L.lo[a]);
+                nd.hi[a] = std::max(nd.hi[a], L.hi[a]);
+                clo[a] = std::min(clo[a], cen(idx[k], a));
+                chi[a] = std::max(chi[a], cen(idx[k], a));
+            }
+        }
+        if (count == 1) {
+            nd.leaf = idx[first];
+            bn[id] = nd;
+            return id;
+        }
+        // Binned SAH over centroids; fall back to an index median split.
+        double best = std::numeric_limits<double>::infinity();
+        int best_axis = -1, best_bin = 0;
+        for (int a = 0; a < 3; ++a) {
+            const float ext = chi[a] - clo[a];
+            if (!(ext > 0.0f)) continue;
+            int cnt[kBins] = {};
+            float blo[kBins][3], bhi[kBins][3];
+            for (int b = 0; b < kBins; ++b)
+                for (int c = 0; c < 3; ++c) {
+                    blo[b][c] = std::numeric_limits<float>::infinity();
+                    bhi[b][c] = -std::numeric_limits<float>::infinity();
+                }
+            for (size_t k = first; k < first + count; ++k) {
+                int b = static_cast<int>((cen(idx[k], a) - clo[a]) / ext * kBins);
+                b = std::min(std::max(b, 0), kBins - 1);
+                ++cnt[b];
+                const mcg_bvh_node& L = leaves[idx[k]];
+                for (int c = 0; c < 3; ++c) {
+                    blo[b][c] = std::min(blo[b][c], L.lo[c]);
+                    bhi[b][c] = std::max(bhi[b][c], L.hi[c]);
+                }
+            }
+            // prefix/suffix sweeps
+            float rlo[kBins][3], rhi[kBins][3];
+            int rcnt[kBins];
+            float alo[3], ahi[3];
+            int acnt = 0;
+            for (int c = 0; c < 3; ++c) {
+                alo[c] = std::numeric_limits<float>::infinity();
+                ahi[c] = -std::numeric_limits<float>::infinity();
+            }
+            for (int b = kBins - 1; b >= 0; --b) {
+                acnt += cnt[b];
+                for (int c = 0; c < 3; ++c) {
+                    alo[c] = std::min(alo[c], blo[b][c]);
+                    ahi[c] = std::max(ahi[c], bhi[b][c]);
+                    rlo[b][c] = alo[c];
+                    rhi[b][c] = ahi[c];
+                }
+                rcnt[b] = acnt;
+            }
+            for (int c = 0; c < 3; ++c) {
+                alo[c] = std::numeric_limits<float>::infinity();
+                ahi[c] = -std::numeric_limits<float>::infinity();
+            }
+            acnt = 0;
+            for (int b = 0; b < kBins - 1; ++b) {
+                acnt += cnt[b];
+                for (int c = 0; c < 3; ++c) {
+                    alo[c] = std::min(alo[c], blo[b][c]);
+                    ahi[c] = std::max(ahi[c], bhi[b][c]);
+                }
+                if (acnt == 0 || rcnt[b + 1] == 0) continue;
+                const double cost = static_cast<double>(area(alo, ahi)) * acnt +
+                                    static_cast<double>(area(rlo[b + 1], rhi[b + 1])) * rcnt[b + 1];
+                if (cost < best) {
+                    best = cost;
+                    best_axis = a;
+                    best_bin = b;
+                }
+            }
+        }
+        size_t mid;
+        if (best_axis < 0) {
+            mid = first + count / 2;
+        } else {
+            const int a = best_axis;
+            const float ext = chi[a] - clo[a];
+            auto it = std::partition(idx.begin() + first, idx.begin() + first + count, [&](int32_t i) {
+                int b = static_cast<int>((cen(i, a) - clo[a]) / ext * kBins);
+                b = std::min(std::max(b, 0), kBins - 1);
+                return b <= best_bin;
+            });
+            mid = static_cast<size_t>(it - idx.begin());
+            if (mid == first || mid == first + count) mid = first + count / 2;
+        }
+        const int32_t l = build(first, mid - first);
+        const int32_t r = build(mid, first + count - mid);
+        nd.l = l;
+        nd.r = r;
+        bn[id] = nd;
+        return id;
+    };
+    const int32_t root = build(0, leaves.size());
+    std::function<int32_t(int32_t)> collapse = [&](int32_t x) -> int32_t {
+        const int32_t q = static_cast<int32_t>(out.size() / 4);
+        out.resize(out.size() + 4, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
+        std::vector<int32_t> entries;
+        for (int32_t c : {bn[x].l, bn[x].r}) {
+            if (bn[c].leaf >= 0) {
+                entries.push_back(c);
+            } else {
+                entries.push_back(bn[c].l);
+                entries.push_back(bn[c].r);
+            }
+        }
+        int k = 0;
+        for (int32_t e : entries) {
+            mcg_bvh_node rec;
+            if (bn[e].leaf >= 0) {
+                rec = leaves[bn[e].leaf];
+            } else {
+                std::memcpy(rec.lo, bn[e].lo, sizeof(rec.lo));
+                std::memcpy(rec.hi, bn[e].hi, sizeof(rec.hi));
+                rec.a = collapse(e);
+                rec.b = -1;
+            }
+            out[4 * static_cast<size_t>(q) + k++] = rec;
+        }
+        return q;
+    };
+    collapse(root);
+    root_a = 0;
+    root_b = -1;
+    return out;
+}
 
 extern "C" {
 
@@ -827,7 +1000,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         if (s != MCG_OK) fail(s, mcg_last_error());
         DeviceScene& D = ctx->scene;
         D.clear();
-        D.bufs.resize(16);
+        D.bufs.resize(17);
         auto up = [&](int k, const void* p, size_t bytes) -> const void* {
             D.bufs[k].ensure(std::max<size_t>(bytes, 16));
             if (bytes) cuda_check(cudaMemcpyAsync(D.bufs[k].p, p, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D scene");
@@ -906,21 +1079,34 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         v.quads = static_cast<const float4*>(up(15, quads.data(), quads.size() * sizeof(mcg_bvh_node)));
         // Worst-case stack of the LIFO traversal: a node pushes its k
         // entries and descends into one of them, leaving k-1 behind.
-        {
-            const size_t nq = quads.size() / 4;
+        auto stack_need = [](const std::vector<mcg_bvh_node>& qs) -> uint32_t {
+            const size_t nq = qs.size() / 4;
             std::vector<uint32_t> need(nq, 1);
             for (size_t q = nq; q-- > 0;) {
                 uint32_t k = 0, deepest = 1;
                 for (int e = 0; e < 4; ++e) {
-                    const mcg_bvh_node& r = quads[4 * q + e];
+                    const mcg_bvh_node& r = qs[4 * q + e];
                     if (r.b == 0) continue;
                     ++k;
                     if (r.b < 0) deepest = std::max(deepest, need[r.a]);
                 }
                 need[q] = std::max(k, (k ? k - 1 : 0) + deepest);
             }
-            D.max_stack4 = nq ? std::max<uint32_t>(1, need[0]) : 1;
-        }
+            return nq ? std::max<uint32_t>(1, need[0]) : 1;
+        };
+        D.max_stack4 = stack_need(quads);
+        if (D.max_stack4 > 63) fail(MCG_ERR_INVALID_ARGUMENT, "BVH too deep for the traversal stack");
+        // Shadow tree: the reference's leaves (their exact boxes and
+        // primitive ranges) regrouped by a binned SAH build. Any-hit is a
+        // boolean: a triangle is found iff its leaf's box passes and the
+        // triangle test hits (every ancestor box contains the leaf box, and
+        // the slab test is monotone, so ancestors never reject first) -- so
+        // any hierarchy over the same leaves answers exactly as the
+        // reference's tree does.
+        std::vector<mcg_bvh_node> squads = build_shadow_tree(f, v.sroot_a, v.sroot_b);
+        D.max_stack_s = stack_need(squads);
+        if (D.max_stack_s > 63) fail(MCG_ERR_INVALID_ARGUMENT, "shadow BVH too deep for the traversal stack");
+        v.squads = static_cast<const float4*>(up(16, squads.data(), squads.size() * sizeof(mcg_bvh_node)));
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
         v.n_plights = f.n_point_lights;
         v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));

@@ -231,7 +231,7 @@ def _edge_rays(s, r, n):
 @pytest.mark.parametrize("kind,tps", [("cornell", 8), ("classroom", 24)])
 def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, kind, tps):
     """Closest hit and any hit through each traversal variant (per-thread DFS,
-    child pairs, 4-wide, speculative 4-wide) == the oracle's reference DFS,
+    child pairs, 4-wide, speculative 4-wide, packet) == the oracle's reference DFS,
     bit for bit, on random rays and on rays aimed at vertices and edges."""
     path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=tps), f"{scene_dir}/q_{kind}")
     s = load_scene(path)
@@ -246,8 +246,10 @@ def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, ki
     assert want[:, 0].sum() > 0.5 * rays.shape[0]
     tm = r.uniform(0.01, 20, rays.shape[0]).astype(np.float32)
     want_occ = oracle.occluded(s.flat, rays, 1e-4, tm)
-    for variant in range(4):
+    for variant in range(5):
         got = ctx.intersect_batch(rays, 1e-4, np.inf, variant)
         np.testing.assert_array_equal(bits(got), bits(want), err_msg=f"variant {variant}")
+    # any hit also through the SAH tree over the reference's leaves (variant 5)
+    for variant in range(6):
         np.testing.assert_array_equal(ctx.occluded_batch(rays, 1e-4, tm, variant), want_occ,
                                       err_msg=f"variant {variant}")
