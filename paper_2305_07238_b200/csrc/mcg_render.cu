@@ -1,20 +1,27 @@
 // Wavefront path tracer driving the material cache on the GPU: the body of
 // render() (tracer.hpp:69-70, absent in the reference; restated per
 // tracer.hpp:7-94 + SPEC.md:378-434 with the decisions pinned in DESIGN.md
-// §render). One pass = k samples of every pixel of this shard in flight;
-// per bounce:
+// §render). One pass = k samples of every pixel of this shard in flight:
 //
-//   k_bounce   NEE + cosine bounce for the previous vertex, then BVH closest
-//              hit, surface, ray-cone propagation and footprint gradients
-//              (scene.cpp:252-278, raycone.cpp:15-65) -> shading record
-//   sort       hit points by material slot (CUB radix sort, stable)
-//   k_shade    warp-uniform bytecode VM with inline cache lookup/store
-//              (stackvm.cpp:248-368, cache.cpp:94-136)
-//   [deterministic mode: sort queued stores by (cell, sample, pixel, ord)
-//    and apply them cell by cell -- the epoch rule, DESIGN.md §determinism]
+//   k_primary        camera rays, closest hit, shading record, sort key
+//   per vertex b:
+//     sort           (material slot | Morton code of the hit point) -> order
+//     k_shade        warp-uniform bytecode VM with inline cache lookup/store
+//                    (stackvm.cpp:248-368, cache.cpp:94-136), then NEE (one
+//                    shadow ray per light) and the cosine bounce
+//     [deterministic mode: queued stores sorted by (cell, sample, pixel,
+//      ord) and applied cell by cell -- the epoch rule, DESIGN.md]
+//     k_shadow_ww    any-hit of the queued shadow rays
+//     k_resolve      visible light contributions, in light order
+//     k_trace_closest_ww  closest hits of the continuation rays
+//   k_accumulate     finished paths into the double framebuffers, samples in
+//                    order (FrameBuffers, tracer.hpp:24-43)
 //
-// and k_accumulate adds each finished pass into the double framebuffers in
-// sample order (FrameBuffers, tracer.hpp:24-43).
+// Path state moves with the sort: k_shade gathers each path's state from
+// its old position and writes it at its sorted position, so every later
+// kernel of the vertex reads and writes its own index (coalesced). A path's
+// identity travels in `pid` (pass slot j * n_pix + pixel index); its final
+// radiance lands in `fin[pid]` when it ends.
 #include <chrono>
 #include <cstdlib>
 #include <string>
@@ -57,22 +64,30 @@ struct RenderView {
     uint32_t n_paths;         // n_pix * samples in this pass
     uint32_t sample0;         // sample index of pass slot 0
     uint32_t hps_base;        // hits_per_sample index of pass slot 0
+    // Path state at the current layout (index = position in the last sort
+    // output; the primary pass starts at pid order) and the next layout,
+    // written by k_shade at the sorted position.
     float4* ro;               // origin.xyz, cone width
     float4* rd;               // direction.xyz, cone spread
     float4* thr;              // throughput.rgb, nodes_found (uint bits)
-    float4* L;                // radiance.rgb, alive (uint bits)
+    float4* L;                // radiance.rgb
+    uint32_t* pid;            // path id: pass slot j * n_pix + shard pixel index
+    float4* ro2;
+    float4* rd2;
+    float4* thr2;
+    float4* L2;
+    uint32_t* pid2;
+    float4* fin;              // by path id: final radiance.rgb, nodes_found (uint bits)
     float4* sh0;              // position.xyz, u
     float4* sh1;              // normal.xyz, v
     float4* sh2;              // g1.xy, g2.xy
-    float4* base;             // base colour from the VM
     uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
-    uint32_t* vals;           // unsorted path ids
+    uint32_t* vals;           // unsorted layout positions
     const uint32_t* skey;     // sorted keys: hits first, in material order
     uint32_t key_shift;       // key = slot << key_shift | Morton code of the hit point
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
-    int pk_depth;             // packet-traversal stack depth (entries per warp)
     float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
-    const uint32_t* order;    // sorted path ids
+    const uint32_t* order;    // sorted layout positions
     float4* sro;              // shadow ray per (path, light): origin.xyz, t_max
     float4* srd;              // direction.xyz
     float4* scon;             // contribution.rgb, candidate flag
@@ -393,53 +408,42 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
     d = mcgd::normalize((fwd + right * a) + up * bq);
 }
 
-// Closest hit from (ro, rd) for path p; on a hit writes the shading record
-// (position, normal, uv, footprint gradients) and the propagated cone width
-// and returns the material slot, on a miss adds throughput * env to L and
-// returns n_programs (the "no hit" sort key).
-__device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t p, float4& ro,
-                                               const float4& rd, const float4& thr, float4& L, bool found,
-                                               uint32_t prim, float t, float b1, float b2, int vtx) {
+// Shading record of a closest hit for the path at layout position q (path
+// id pid): position, normal, uv, footprint gradients at q, the propagated
+// cone width into ro.w, and the sort key; on a miss the path ends: radiance
+// + throughput * env goes to fin[pid] and the key is "no hit".
+__device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, uint32_t pid, float4& ro,
+                                               const float4& rd, const float4& thr, const float4& L,
+                                               bool found, uint32_t prim, float t, float b1, float b2,
+                                               int vtx) {
     const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
     if (!found) {
-        L.x = L.x + thr.x * R.S.env[0];
-        L.y = L.y + thr.y * R.S.env[1];
-        L.z = L.z + thr.z * R.S.env[2];
+        R.fin[pid] = make_float4(L.x + thr.x * R.S.env[0], L.y + thr.y * R.S.env[1],
+                                 L.z + thr.z * R.S.env[2], thr.w);
         return no_hit_key(R);
     }
     const Surface s = surface(R.S, o, d, prim, t, b1, b2);
     const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
     float2 g1, g2;
     mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-    R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-    R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-    R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
+    R.sh0[q] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
+    R.sh1[q] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
+    R.sh2[q] = make_float4(g1.x, g1.y, g2.x, g2.y);
     ro.w = width;
-    const uint32_t slot_j = p / R.n_pix;
-    const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
+    const uint32_t slot_j = pid / R.n_pix;
+    const uint64_t rkey = mcgd::path_key(R.seed, R.pix[pid - slot_j * R.n_pix], R.sample0 + slot_j);
     return sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
 }
 
-__device__ __forceinline__ uint32_t trace_vertex(const RenderView& R, uint32_t p, float4& ro,
-                                                 const float4& rd, const float4& thr, float4& L,
-                                                 uint32_t& nvis, uint32_t& ntest, int vtx) {
-    const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
-    uint32_t prim = 0;
-    float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    const bool found = traverse_closest(R.S, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest);
-    return hit_record(R, p, ro, rd, thr, L, found, prim, t, b1, b2, vtx);
-}
-
-// Next-event estimation and the cosine bounce of every shaded vertex b:
-// one shadow-ray candidate per (path, light) -- its contribution computed
-// now, applied in light order by k_resolve once visibility is known -- and
-// the continuation ray.
-__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t p, int b, float4 s0,
-                                           float4 s1, float3 bc) {
-    const uint32_t slot_j = p / R.n_pix;
-    const uint32_t pixel = R.pix[p - slot_j * R.n_pix];
+// Next-event estimation and the cosine bounce of vertex b of path pid, whose
+// state goes to sorted position i: one shadow-ray candidate per light -- its
+// contribution computed now, applied in light order by k_resolve once
+// visibility is known -- and the continuation ray.
+__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, int b, float4 s0,
+                                           float4 s1, float3 bc, float4 thr, float4 ro, float4 rd) {
+    const uint32_t slot_j = pid / R.n_pix;
+    const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
-    float4 thr = R.thr[p];
     const V3 n{s1.x, s1.y, s1.z};
     const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
                  fminf(fmaxf(bc.z, 0.0f), 1.0f)};
@@ -449,7 +453,7 @@ __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t p, int 
     const uint32_t nl = R.S.n_plights + R.S.n_rlights;
     const unsigned lane = threadIdx.x & 31u;
     for (uint32_t j = 0; j < nl; ++j) {
-        const uint32_t s = p * nl + j;
+        const uint32_t s = i * nl + j;
         bool cand = false;
         V3 wi{0.0f, 0.0f, 0.0f};
         float dist = 0.0f, w = 0.0f;
@@ -520,58 +524,10 @@ __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t p, int 
         thr.x = thr.x * alb.x;
         thr.y = thr.y * alb.y;
         thr.z = thr.z * alb.z;
-        R.thr[p] = thr;
-        R.ro[p] = make_float4(o.x, o.y, o.z, R.ro[p].w);
-        const float4 rd = R.rd[p];
-        R.rd[p] = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
+        R.ro2[i] = make_float4(o.x, o.y, o.z, ro.w);
+        R.rd2[i] = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
     }
-}
-
-__global__ void __launch_bounds__(256) k_nee(RenderView R, int b) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R.n_paths) return;
-    const uint32_t slot = key_slot(R, R.skey[i]);
-    if (slot >= R.S.n_programs) return;
-    const uint32_t p = R.order[i];
-    const float4 bc = R.base[p];
-    nee_bounce(R, p, b, R.sh0[p], R.sh1[p], make_float3(bc.x, bc.y, bc.z));
-}
-
-// Any-hit queries of the queued shadow rays (Scene::occluded, scene.cpp:280-298).
-__global__ void __launch_bounds__(256) k_shadow(RenderView R) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0, rays = 0;
-    if (q < *R.shadow_count) {
-        const uint32_t s = R.squeue[q];
-        const float4 so = R.sro[s], sd = R.srd[s];
-        R.vis[s] = traverse_any(R.S, V3{so.x, so.y, so.z}, V3{sd.x, sd.y, sd.z}, kTMin, so.w, nvis,
-                                ntest) ? 0 : 1;
-        rays = 1;
-    }
-    mcgd::warp_add(R.stats + kStatShadow, rays);
-    mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
-    mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
-}
-
-
-// Non-persistent closest-hit over the live list (one thread per ray).
-__global__ void __launch_bounds__(256) k_trace_closest_plain(RenderView R, const uint32_t* count, int vtx) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t nvis = 0, ntest = 0;
-    if (q < *count) {
-        const uint32_t p = R.order[q];
-        float4 ro = R.ro[p];
-        const float4 rd = R.rd[p], thr = R.thr[p];
-        float4 L = R.L[p];
-        const uint32_t key = trace_vertex(R, p, ro, rd, thr, L, nvis, ntest, vtx);
-        if (key_slot(R, key) < R.S.n_programs) R.ro[p] = ro;
-        else R.L[p] = L;
-        R.keys[q] = key;
-        R.vals[q] = p;
-    }
-    mcgd::warp_add(R.stats + kStatClosestRays, q < *count ? 1u : 0u);
-    mcgd::warp_add(R.stats + kStatNodes, nvis);
-    mcgd::warp_add(R.stats + kStatPrims, ntest);
+    R.thr2[i] = thr;
 }
 
 // ---------------------------------------------------------------------------
@@ -1327,9 +1283,8 @@ __device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& cod
     e = base + 2 * depth;
 }
 
-// Pass start: primary rays of every path of the pass, traced to vertex 0
-// (speculative 4-wide or packet traversal, like k_trace_closest_ww<kTree>).
-template <int kTree>
+// Pass start: primary rays of every path of the pass, traced to vertex 0,
+// state written at layout position = path id.
 __global__ void __launch_bounds__(256) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -1343,27 +1298,19 @@ __global__ void __launch_bounds__(256) k_primary(RenderView R) {
     }
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    bool found;
-    if (kTree == 3) {
-        int32_t* pc;
-        uint32_t* pm;
-        float* pe;
-        pk_stacks(R.pk_depth, true, pc, pm, pe);
-        found = closest_pk(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest,
-                           pc, pm, pe);
-    } else {
-        found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2, nvis, ntest);
-    }
+    const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
+                                    nvis, ntest);
     if (active) {
         float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
         const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
-        float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const uint32_t key = hit_record(R, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
+        const float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const uint32_t key = hit_record(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
         R.ro[i] = ro;
         R.rd[i] = rd;
         R.thr[i] = thr;
         R.L[i] = L;
+        R.pid[i] = i;
         R.keys[i] = key;
         R.vals[i] = i;
     }
@@ -1446,12 +1393,13 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
     if (active) out[i] = occ ? 1 : 0;
 }
 
-// Shadow rays, one per thread over the queue, warp-synchronous traversal
-// over the binary (kTree = 0), 4-wide (1) or speculative 4-wide (2) tree.
-template <int kTree>
+// Shadow rays, one per thread over the queue, speculative 4-wide traversal
+// of the SAH tree over the reference's leaves (kSah) or of the reference's
+// own tree.
 #ifndef MCG_TRACE_MINB
 #define MCG_TRACE_MINB 1
 #endif
+template <bool kSah>
 __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -1466,105 +1414,74 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R)
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    int32_t* pc = nullptr;
-    uint32_t* pm = nullptr;
-    float* pe = nullptr;
-    if (kTree == 3) pk_stacks(R.pk_depth, false, pc, pm, pe);
-    const bool occ = kTree == 3   ? any_pk(R.S, active, o, d, kTMin, tmax, nvis, ntest, pc, pm)
-                     : kTree == 4 ? any_ww4s(R.S, R.S.squads, R.S.sroot_a, R.S.sroot_b, active, o, d, kTMin, tmax, nvis, ntest)
-                     : kTree == 2 ? any_ww4s(R.S, R.S.quads, R.S.root_a, R.S.root_b, active, o, d, kTMin, tmax, nvis, ntest)
-                     : kTree == 1 ? any_ww4(R.S, active, o, d, kTMin, tmax, nvis, ntest)
-                                  : any_ww(R.S, active, o, d, kTMin, tmax, nvis, ntest);
+    const bool occ = kSah ? any_ww4s(R.S, R.S.squads, R.S.sroot_a, R.S.sroot_b, active, o, d, kTMin, tmax, nvis, ntest)
+                          : any_ww4s(R.S, R.S.quads, R.S.root_a, R.S.root_b, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodesShadow, nvis);
     mcgd::warp_add(R.stats + kStatPrimsShadow, ntest);
 }
 
-// Closest hits of the live paths, one per thread, warp-synchronous traversal.
-template <int kTree>
+// Closest hits of the continuation rays, one per thread at its own layout
+// position, speculative 4-wide traversal in the reference's order.
 __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *count;
-    uint32_t p = 0;
     float4 ro{}, rd{};
     if (active) {
-        p = R.order[q];
-        ro = R.ro[p];
-        rd = R.rd[p];
+        ro = R.ro[q];
+        rd = R.rd[q];
     }
     const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-    const float inf = __int_as_float(0x7f800000);
-    int32_t* pc = nullptr;
-    uint32_t* pm = nullptr;
-    float* pe = nullptr;
-    if (kTree == 3) pk_stacks(R.pk_depth, true, pc, pm, pe);
-    const bool found =
-        kTree == 3   ? closest_pk(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest, pc, pm, pe)
-        : kTree == 2 ? closest_ww4s(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
-        : kTree == 1 ? closest_ww4(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest)
-                     : closest_ww(R.S, active, o, d, kTMin, inf, prim, t, b1, b2, nvis, ntest);
+    const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
+                                    nvis, ntest);
     if (active) {
-        uint32_t key = no_hit_key(R);
-        if (!found) {
-            float4 L = R.L[p];
-            const float4 thr = R.thr[p];
-            L.x = L.x + thr.x * R.S.env[0];
-            L.y = L.y + thr.y * R.S.env[1];
-            L.z = L.z + thr.z * R.S.env[2];
-            R.L[p] = L;
+        const uint32_t pid = R.pid[q];
+        uint32_t key;
+        if (found) {
+            key = hit_record(R, q, pid, ro, rd, make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), true, prim, t,
+                             b1, b2, vtx);
+            R.ro[q] = ro;
         } else {
-            const Surface s = surface(R.S, o, d, prim, t, b1, b2);
-            const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
-            float2 g1, g2;
-            mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-            R.sh0[p] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-            R.sh1[p] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-            R.sh2[p] = make_float4(g1.x, g1.y, g2.x, g2.y);
-            R.ro[p] = make_float4(ro.x, ro.y, ro.z, width);
-            const uint32_t slot_j = p / R.n_pix;
-            const uint64_t rkey = mcgd::path_key(R.seed, R.pix[p - slot_j * R.n_pix], R.sample0 + slot_j);
-            key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+            key = hit_record(R, q, pid, ro, rd, R.thr[q], R.L[q], false, prim, t, b1, b2, vtx);
         }
         R.keys[q] = key;
-        R.vals[q] = p;
+        R.vals[q] = q;
     }
-    mcgd::warp_add(R.stats + kStatClosestRays, q < *count ? 1u : 0u);
+    mcgd::warp_add(R.stats + kStatClosestRays, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
-// Finishes vertex b: adds the visible light contributions in light order
-// (the oracle's summation order); writes "no hit" sort keys for the slots
-// past the live list and for every path at the last vertex.
+// Finishes vertex b at sorted position i: adds the visible light
+// contributions in light order (the oracle's summation order); at the last
+// vertex the path ends (fin[pid]). Writes "no hit" sort keys for the slots
+// past the live list.
 __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R.n_paths) return;
     const uint32_t slot = key_slot(R, R.skey[i]);
     const bool live = slot < R.S.n_programs;
     if (live) {
-        const uint32_t p = R.order[i];
         const uint32_t nl = R.S.n_plights + R.S.n_rlights;
-        if (nl) {
-            float4 L = R.L[p];
-            for (uint32_t j = 0; j < nl; ++j) {
-                const uint32_t s = p * nl + j;
-                const float4 c = R.scon[s];
-                if (c.w != 0.0f && R.vis[s]) {
-                    L.x = L.x + c.x;
-                    L.y = L.y + c.y;
-                    L.z = L.z + c.z;
-                }
+        float4 L = R.L[i];
+        for (uint32_t j = 0; j < nl; ++j) {
+            const uint32_t s = i * nl + j;
+            const float4 c = R.scon[s];
+            if (c.w != 0.0f && R.vis[s]) {
+                L.x = L.x + c.x;
+                L.y = L.y + c.y;
+                L.z = L.z + c.z;
             }
-            R.L[p] = L;
         }
-    }
-    if (!live || b >= R.max_bounces) {
+        if (b >= R.max_bounces) R.fin[R.pid[i]] = make_float4(L.x, L.y, L.z, R.thr[i].w);
+        else R.L[i] = L;
+    } else {
         R.keys[i] = no_hit_key(R);
-        R.vals[i] = 0;
+        R.vals[i] = i;
     }
 }
 
@@ -1579,8 +1496,10 @@ __global__ void k_count_live(RenderView R, uint32_t* live) {
     if (v && i + 1 == R.n_paths) *live = R.n_paths;
 }
 
-// Material evaluation of every live hit, in material order.
-template <bool kDeferred, bool kNee>
+// Material evaluation of every live hit, in sorted (material, Morton)
+// order, then NEE and the bounce; the path's state moves from its old layout
+// position q = order[i] to i in the next layout.
+template <bool kDeferred>
 __global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __restrict__ skey,
                                                const uint32_t* __restrict__ order, int max_stack,
                                                uint32_t wh, int b) {
@@ -1593,31 +1512,25 @@ __global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __r
     const bool valid = slot < R.S.n_programs;
     const unsigned live = __ballot_sync(mcgd::kFull, valid);
     if (!valid) return;
-    const uint32_t p = order[i];
+    const uint32_t q = order[i];
     const unsigned grp = __match_any_sync(live, slot);
-    const float4 s0 = R.sh0[p], s1 = R.sh1[p], s2 = R.sh2[p], rd = R.rd[p];
+    const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
+    const uint32_t pid = R.pid[q];
     const mcgd::ShadeIn in{s0.x, s0.y, s0.z, s1.x, s1.y, s1.z, rd.x, rd.y, rd.z,
                            s0.w, s1.w, s2.x, s2.y, s2.z, s2.w};
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
                    static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
-    const uint32_t slot_j = p / R.n_pix;
-    const uint32_t pixel = R.pix[p - slot_j * R.n_pix];
+    const uint32_t slot_j = pid / R.n_pix;
+    const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt);
-    if (cnt.hits) {
-        float4 t = R.thr[p];
-        t.w = __uint_as_float(__float_as_uint(t.w) + cnt.hits);
-        R.thr[p] = t;
-    }
-    if (kNee) {
-        // Fused next-event estimation + bounce: the shading record is
-        // already in registers.
-        nee_bounce(R, p, b, s0, s1, r.value);
-    } else {
-        R.base[p] = make_float4(r.value.x, r.value.y, r.value.z, 0.0f);
-    }
+    float4 thr = R.thr[q];
+    thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
+    R.L2[i] = R.L[q];
+    R.pid2[i] = pid;
+    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, R.ro[q], rd);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
     mcgd::warp_add(R.stats + kStatWon, cnt.won);
@@ -1640,9 +1553,8 @@ __global__ void __launch_bounds__(256) k_accumulate(RenderView R, uint32_t k) {
         double r = R.radiance[3ull * pixel], g = R.radiance[3ull * pixel + 1],
                bl = R.radiance[3ull * pixel + 2], nf = R.nodes_found[pixel];
         for (uint32_t j = 0; j < k; ++j) {
-            const uint32_t i = j * R.n_pix + q;
-            const float4 L = R.L[i];
-            const uint32_t nodes = __float_as_uint(R.thr[i].w);
+            const float4 L = R.fin[j * R.n_pix + q];
+            const uint32_t nodes = __float_as_uint(L.w);
             r += static_cast<double>(L.x);
             g += static_cast<double>(L.y);
             bl += static_cast<double>(L.z);
@@ -1682,9 +1594,6 @@ bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
 // Packet kernels may need more than the default 48 KB of dynamic shared memory.
 void pk_smem_attr(size_t bytes) {
     const int b = static_cast<int>(bytes);
-    cudaFuncSetAttribute(k_primary<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_shadow_ww<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_trace_closest_ww<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     cudaFuncSetAttribute(k_intersect_batch<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     cudaFuncSetAttribute(k_occluded_batch<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
@@ -1749,12 +1658,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         }
     }
 
-    // Path state: 8 float4 per path; shadow rays: 3 float4 + 1 byte per
+    // Path state: 2 layouts x (4 float4 + pid) + 3 float4 shading record +
+    // 1 float4 final radiance per path; shadow rays: 3 float4 + 1 byte per
     // (path, light); sort keys/values and the shadow queue as u32.
     const uint32_t n_lights = D.view.n_plights + D.view.n_rlights;
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
-    ctx->path_mem.ensure(f4 * 8 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 4 + n_pix * 4ull + 1024);
+    ctx->path_mem.ensure(f4 * 12 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024);
     char* base = ctx->path_mem.as<char>();
     RenderView R{};
     R.S = D.view;
@@ -1773,11 +1683,15 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.rd = R.ro + max_paths;
     R.thr = R.rd + max_paths;
     R.L = R.thr + max_paths;
-    R.sh0 = R.L + max_paths;
+    R.ro2 = R.L + max_paths;
+    R.rd2 = R.ro2 + max_paths;
+    R.thr2 = R.rd2 + max_paths;
+    R.L2 = R.thr2 + max_paths;
+    R.sh0 = R.L2 + max_paths;
     R.sh1 = R.sh0 + max_paths;
     R.sh2 = R.sh1 + max_paths;
-    R.base = R.sh2 + max_paths;
-    R.sro = R.base + max_paths;
+    R.fin = R.sh2 + max_paths;
+    R.sro = R.fin + max_paths;
     R.srd = R.sro + n_shadow;
     R.scon = R.srd + n_shadow;
     uint32_t* u32 = reinterpret_cast<uint32_t*>(R.scon + n_shadow);
@@ -1785,9 +1699,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.vals = u32 + max_paths;
     uint32_t* skey = u32 + 2 * max_paths;
     uint32_t* order = u32 + 3 * max_paths;
+    R.pid = u32 + 4 * max_paths;
+    R.pid2 = u32 + 5 * max_paths;
     R.skey = skey;
     R.order = order;
-    R.squeue = u32 + 4 * max_paths;
+    R.squeue = u32 + 6 * max_paths;
     uint32_t* d_pix = R.squeue + n_shadow;
     R.pix = d_pix;
     R.shadow_count = reinterpret_cast<unsigned int*>(d_pix + n_pix);
@@ -1824,51 +1740,35 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.box_scale[a] = ext > 0.0f ? 255.999f / ext : 0.0f;
     }
     const int key_bits = static_cast<int>(R.key_shift) + slot_bits;
-    const char* trace_env = std::getenv("MCG_TRACE");
-    const bool plain = trace_env && std::string(trace_env) == "plain";
-    const bool binary = trace_env && std::string(trace_env) == "ww2";
-    const bool wide_nospec = trace_env && std::string(trace_env) == "ww4";  // else speculative 4-wide
-    // Packet traversal (MCG_TRACE=pk: primary, shadow and closest-hit rays;
-    // pks: primary and shadow rays only).
-    const bool pk_all = trace_env && std::string(trace_env) == "pk";
-    const bool pk_coherent = pk_all || (trace_env && std::string(trace_env) == "pks");
-    R.pk_depth = static_cast<int>(D.max_stack4) + 1;
     // Shadow rays over the SAH tree of the reference's leaves (exact for
     // any-hit); MCG_SHADOW_TREE=ref keeps the reference's own tree.
     const char* stree_env = std::getenv("MCG_SHADOW_TREE");
     const bool sah_shadow = !(stree_env && std::string(stree_env) == "ref");
-    const size_t pk_bytes_closest = 8ull * R.pk_depth * (2 + 32) * sizeof(float);
-    const size_t pk_bytes_any = 8ull * R.pk_depth * 2 * sizeof(float);
-    if (pk_coherent) {
-        if (pk_bytes_closest > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "BVH too deep for packet traversal");
-        pk_smem_attr(pk_bytes_closest);
-    }
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
     if (smem > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "material stack too deep for shared memory");
-    cudaFuncSetAttribute(k_shade<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_shade<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_shade<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_shade<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const char* nee_env = std::getenv("MCG_NEE");
-    const bool fuse_nee = !(nee_env && std::string(nee_env) == "separate");
+    cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const RenderView R0 = R;
 
     for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k) {
         const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp) - start);
+        // the pass starts on the first layout
+        R.ro = R0.ro; R.rd = R0.rd; R.thr = R0.thr; R.L = R0.L; R.pid = R0.pid;
+        R.ro2 = R0.ro2; R.rd2 = R0.rd2; R.thr2 = R0.thr2; R.L2 = R0.L2; R.pid2 = R0.pid2;
         R.n_paths = n_pix * kk;
         R.sample0 = P.first_sample + start;
         R.hps_base = start;
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0);
-            if (pk_coherent) k_primary<3><<<grid, 256, pk_bytes_closest, ctx->stream>>>(R);
-            else k_primary<2><<<grid, 256, 0, ctx->stream>>>(R);
+            k_primary<<<grid, 256, 0, ctx->stream>>>(R);
             ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
-            // Stable radix sort of (slot -> path): hits in material order
-            // first, paths without a hit (key n_programs) last.
+            // Stable radix sort of (key -> layout position): hits in
+            // material order first, paths without a hit (key n_programs) last.
             sort_pairs_u32(ctx, R.keys, skey, R.vals, order, R.n_paths, key_bits);
             // counters: [0] shadow rays queued, [1] shadow cursor, [2] live paths, [3] trace cursor
             cuda_check(cudaMemsetAsync(R.shadow_count, 0, 16, ctx->stream), "memset");
@@ -1882,18 +1782,18 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 LaunchScope ls(ctx, "shade", 0.0);
                 const unsigned sg = grid_for(R.n_paths, block);
                 const uint32_t wh32 = static_cast<uint32_t>(wh);
-                if (deferred) {
-                    // deterministic mode: stores are applied after the shade,
-                    // NEE needs none of them -- but keep the kernels separate
-                    // so the store queue is complete before any later step.
-                    if (fuse_nee) k_shade<true, true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
-                    else k_shade<true, false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
-                } else {
-                    if (fuse_nee) k_shade<false, true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
-                    else k_shade<false, false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
-                }
+                // deterministic mode: stores are queued and applied after the
+                // shade (NEE and the bounce need none of them)
+                if (deferred) k_shade<true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
+                else k_shade<false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
                 ls.done();
             }
+            // the path state now lives at the sorted positions
+            std::swap(R.ro, R.ro2);
+            std::swap(R.rd, R.rd2);
+            std::swap(R.thr, R.thr2);
+            std::swap(R.L, R.L2);
+            std::swap(R.pid, R.pid2);
             if (deferred) {
                 unsigned int count = 0;
                 cuda_check(cudaMemcpyAsync(&count, R.q.count, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
@@ -1908,22 +1808,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                     apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, R.stats);
                 }
             }
-            if (!fuse_nee) {
-                LaunchScope ls(ctx, "nee", 0.0);
-                k_nee<<<grid, 256, 0, ctx->stream>>>(R, b);
-                ls.done();
-            }
             if (n_lights) {
                 LaunchScope ls(ctx, "trace_shadow", 0.0);
-                if (plain) {
-                    k_shadow<<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                } else {
-                    if (binary) k_shadow_ww<0><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                    else if (wide_nospec) k_shadow_ww<1><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                    else if (pk_coherent) k_shadow_ww<3><<<grid_for(n_shadow, 256), 256, pk_bytes_any, ctx->stream>>>(R);
-                    else if (sah_shadow) k_shadow_ww<4><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                    else k_shadow_ww<2><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                }
+                if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                else k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
                 ls.done();
             }
             {
@@ -1933,14 +1821,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             }
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
-                if (plain) {
-                    k_trace_closest_plain<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                } else {
-                    if (binary) k_trace_closest_ww<0><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                    else if (wide_nospec) k_trace_closest_ww<1><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                    else if (pk_all) k_trace_closest_ww<3><<<grid, 256, pk_bytes_closest, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                    else k_trace_closest_ww<2><<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
-                }
+                k_trace_closest_ww<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
                 ls.done();
             }
         }
