@@ -24,6 +24,7 @@
 #include "matcache/cache.hpp"
 #include "matcache/eval.hpp"
 #include "matcache/graph.hpp"
+#include "matcache/image.hpp"
 #include "matcache/noise.hpp"
 #include "matcache/raycone.hpp"
 #include "matcache/rng.hpp"
@@ -338,6 +339,50 @@ struct RefRenderStats {
     uint64_t stores_attempted, stores_won, instructions_executed;
     uint64_t paths, shading_points;
 };
+
+// ---- image I/O (image.cpp) -------------------------------------------------
+static ImageF to_image(int w, int h, const float* rgb) {
+    ImageF img(w, h);
+    for (size_t i = 0; i < img.pixels.size(); ++i) img.pixels[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+    return img;
+}
+int ref_write_ppm(const char* path, int w, int h, const float* rgb, int gamma) {
+    try {
+        write_ppm(path, to_image(w, h, rgb), gamma != 0);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+int ref_write_pfm(const char* path, int w, int h, const float* rgb) {
+    try {
+        write_pfm(path, to_image(w, h, rgb));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+// out may be null (size query): returns width/height through w/h.
+int ref_read_pfm(const char* path, int* w, int* h, float* out) {
+    try {
+        const ImageF img = read_pfm(path);
+        *w = img.width;
+        *h = img.height;
+        if (out) {
+            for (size_t i = 0; i < img.pixels.size(); ++i) {
+                out[3 * i] = img.pixels[i].r;
+                out[3 * i + 1] = img.pixels[i].g;
+                out[3 * i + 2] = img.pixels[i].b;
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
 
 }  // extern "C"
 

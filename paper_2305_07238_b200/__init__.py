@@ -32,7 +32,7 @@ __all__ = [
     "decode_value", "memory_bytes", "audit_dump", "AuditReport", "image_error", "DiffStats",
     "stats_to_json", "parse_stats_json", "GraphError", "CompileError", "SceneError",
     "ImageIoError", "CudaError", "NoDeviceError", "CACHE_OFF", "CACHE_CONCURRENT",
-    "CACHE_DETERMINISTIC",
+    "CACHE_DETERMINISTIC", "artifacts", "sweep", "SweepRow",
 ]
 
 CACHE_OFF, CACHE_CONCURRENT, CACHE_DETERMINISTIC = 0, 1, 2
@@ -504,6 +504,7 @@ class RenderStats:
     shading_points: int = 0
     shadow_rays: int = 0
     paths: int = 0
+    device_ms: float = 0.0       # CUDA-event time of the render on the context's stream
 
 
 @dataclass
@@ -536,7 +537,8 @@ def render(scene: Scene, config: RenderConfig, external_cache: Optional[Material
     stats = RenderStats(st.wall_time_s, st.lookups, st.hits,
                         (st.hits / st.lookups) if st.lookups else 0.0, st.inserts_won,
                         st.inserts_lost_full, st.stores_attempted, st.instructions_executed,
-                        [int(x) for x in hps], st.shading_points, st.shadow_rays, st.paths)
+                        [int(x) for x in hps], st.shading_points, st.shadow_rays, st.paths,
+                        st.device_ms)
     return RenderResult(fb, stats)
 
 
@@ -591,3 +593,70 @@ def parse_stats_json(text: str) -> StatsFile:
     if v.size != w * h:
         raise ValueError("per_pixel_nodes_found size does not match width*height")
     return StatsFile(w, h, v.reshape(h, w))
+
+
+# --------------------------------------------------------------------------
+# Cache-size sweep (SweepReport SPEC.md:441-444; Fig.
+# "cacheSize" of the paper): baseline without cache, then every (Nc, Ne).
+# --------------------------------------------------------------------------
+
+@dataclass
+class SweepRow:
+    """One SweepReport row; relative_time_pct = 100 * time / no-cache time."""
+    n_cells: int
+    n_entries: int
+    wall_time_s: float
+    relative_time_pct: float
+    hit_rate: float
+    inserts_lost_full: int
+    memory_bytes: int
+
+
+def sweep(scene: "Scene", config: RenderConfig, cells_list: Sequence[int],
+          entries_list: Sequence[int], repeats: int = 1, ctx: Optional[Context] = None,
+          device_time: bool = True) -> list:
+    """cmd_sweep: render once without the cache (the 100% baseline), then
+    every (n_cells, n_entries) combination with a fresh table, `repeats`
+    times each (median). Times are the device's (CUDA events around the
+    render on the context's stream; device_time=False: the call's wall
+    time). Rows sorted by (n_cells, n_entries)."""
+    import dataclasses
+    import statistics
+    if not cells_list or not entries_list:
+        raise ValueError("sweep needs non-empty cells and entries lists")
+    for v in list(cells_list) + list(entries_list):
+        if int(v) <= 0:
+            raise ValueError("cache sizes must be positive")
+    ctx = ctx or Context.default()
+
+    def timed(cfg):
+        ts, last = [], None
+        for _ in range(max(1, repeats)):
+            last = render(scene, cfg, ctx=ctx)
+            ts.append(last.stats.device_ms / 1e3 if device_time else last.stats.wall_time_s)
+        return statistics.median(ts), last
+
+    base_cfg = dataclasses.replace(config, cache_enabled=False)
+    t0, _ = timed(base_cfg)
+    rows = []
+    for nc in sorted(int(c) for c in cells_list):
+        for ne in sorted(int(e) for e in entries_list):
+            cfg = dataclasses.replace(config, cache_enabled=True, n_cells=nc, n_entries=ne)
+            t, res = timed(cfg)
+            rows.append(SweepRow(nc, ne, t, 100.0 * t / t0 if t0 > 0 else 0.0, res.stats.hit_rate,
+                                 res.stats.inserts_lost_full, memory_bytes(nc, ne)))
+    return rows
+
+
+def write_sweep_csv(rows: Sequence[SweepRow], path: str) -> None:
+    """SweepReport as CSV, one row per (n_cells, n_entries), fixed column order."""
+    cols = ["n_cells", "n_entries", "wall_time_s", "relative_time_pct", "hit_rate",
+            "inserts_lost_full", "memory_bytes"]
+    with open(path, "w") as f:
+        f.write(",".join(cols) + "\n")
+        for r in sorted(rows, key=lambda r: (r.n_cells, r.n_entries)):
+            f.write(f"{r.n_cells},{r.n_entries},{r.wall_time_s:.9g},{r.relative_time_pct:.6g},"
+                    f"{r.hit_rate:.9g},{r.inserts_lost_full},{r.memory_bytes}\n")
+
+
+from . import artifacts  # noqa: E402  (image I/O, heatmap, diff)

@@ -1751,6 +1751,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const RenderView R0 = R;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cuda_check(cudaEventCreate(&ev0), "event");
+    cuda_check(cudaEventCreate(&ev1), "event");
+    cuda_check(cudaEventRecord(ev0, ctx->stream), "event record");
 
     for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k) {
         const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp) - start);
@@ -1831,12 +1835,17 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             ls.done();
         }
     }
+    cuda_check(cudaEventRecord(ev1, ctx->stream), "event record");
     unsigned long long st[kStatCount];
     cuda_check(cudaMemcpyAsync(st, R.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream), "D2H stats");
     if (stats && stats->hits_per_sample) {
         cuda_check(cudaMemcpyAsync(stats->hits_per_sample, R.hps, P.spp * 8ull, cudaMemcpyDeviceToHost, ctx->stream), "D2H hps");
     }
     cuda_check(cudaStreamSynchronize(ctx->stream), "render");
+    float dev_ms = 0.0f;
+    cudaEventElapsedTime(&dev_ms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (cache_ctr) {
         // Mirror the render's lookups/hits/inserts into the table's counters
         // (MaterialCache::counters after a render, cache.cpp:146-150).
@@ -1852,6 +1861,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         std::memset(stats, 0, sizeof(*stats));
         stats->hits_per_sample = hps;
         stats->wall_time_s = std::chrono::duration<double>(t1 - t0).count();
+        stats->device_ms = dev_ms;
         stats->lookups = st[kStatLookups];
         stats->hits = st[kStatHits];
         stats->inserts_won = st[kStatWon];

@@ -177,6 +177,25 @@ def material_lowlevel(mid, rng, textures, uv_scale, libm_ops, n_points=6, noise_
     return g.finish(g.add("clamp", [acc]))
 
 
+def material_hostile(mid, rng, textures, uv_scale, libm_ops, n_terms=12, noise_freq=1.0):
+    """Cache-hostile material (acceptance criterion 7): heavy FBM
+    work whose every uv-only subtree is a single node consumed by an
+    Other-class product, below analysis' min_subtree_size (3) -- zero cache
+    points, so the cache can only add overhead."""
+    g = Graph(mid)
+    acc = g.add("mul", [other_gate(g), g.add("const_float", value=0.1)])
+    ex = UvExpr(g, rng, textures, uv_scale, libm_ops, noise_freq)
+    for _ in range(n_terms):
+        leaf = g.add("noise_fbm", octaves=rng.randint(5, 8),
+                     frequency=_f(rng.uniform(2.0, 9.0) * uv_scale * noise_freq),
+                     lacunarity=_f(rng.uniform(1.8, 2.3)), gain=_f(rng.uniform(0.4, 0.6)))
+        pos = g.add("position")
+        w = g.add("clamp", [g.add("dot", [pos, g.add("const_color", rgb=[_f(0.05), _f(0.1), _f(0.02)])])])
+        acc = g.add("add", [acc, g.add("mul", [leaf, w])])
+    _ = ex
+    return g.finish(g.add("clamp", [acc]))
+
+
 def material_depth8(mid, rng, textures, libm_ops=False):
     """The C1 parity material: one depth-8 uv expression behind the gate."""
     g = Graph(mid)
@@ -338,6 +357,10 @@ def build_scene(spec: SceneSpec, out_dir: str) -> str:
     elif kind == "cornell":
         for i in range(3):
             mats.append(material_depth8(i, rng, textures, spec.libm_ops))
+        uv_scale = 0.5
+    elif kind == "hostile":
+        for i in range(4):
+            mats.append(material_hostile(i, rng, textures, 1.0, spec.libm_ops))
         uv_scale = 0.5
     else:
         raise ValueError(f"unknown scene kind {kind!r}")

@@ -233,6 +233,9 @@ class Ref:
         L.ref_checker.argtypes = [C.c_float, vp, C.c_size_t, vp]
         L.ref_bilinear.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_size_t, vp]
         L.ref_memory_bytes.argtypes = [C.c_uint64, C.c_uint64, vp]
+        L.ref_write_ppm.argtypes = [C.c_char_p, C.c_int, C.c_int, vp, C.c_int]
+        L.ref_write_pfm.argtypes = [C.c_char_p, C.c_int, C.c_int, vp]
+        L.ref_read_pfm.argtypes = [C.c_char_p, vp, vp, vp]
         L.ref_cache_new.argtypes = [C.c_uint64, C.c_uint32, C.POINTER(vp)]
         L.ref_cache_free.argtypes = [vp]
         L.ref_cache_update.argtypes = [vp, vp, vp, C.c_size_t, vp, vp, vp]
