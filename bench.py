@@ -45,7 +45,8 @@ W, H, SPP = 1920, 1080, 128
 N_CELLS, N_ENTRIES = 10_000_000, 10
 SCENE_KIND = "classroom"
 TRIS_PER_SIDE = 24
-PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 0, 2
+PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 4, 8          # HBM table: warp-cooperative, one round trip
+PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM = 0, 8    # L2-resident table: per-lane scan (issue-bound)
 METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
 
 
@@ -328,28 +329,31 @@ def main() -> None:
         if rank == 0:
             from paper_2305_07238_b200 import MaterialCache
             peak, _ = measured_peaks()
-            table = MaterialCache(N_CELLS, N_ENTRIES, ctx)
             n = 1 << 26
-            # per-lane two-round scan, 2 blocks of 256 per SM: the sweep in
-            # profiles/README.md (more requests in flight thrash DRAM rows)
-            cfg = 16 * PROBE_VARIANT + 256 * PROBE_BLOCKS_PER_SM
-            ms_ins, b_ins = table.probe_bench(n, 7, 0 + cfg, 1)
-            table.probe_bench(n, 7, 1 + cfg, 1)
-            ms_look, b_look = table.probe_bench(n, 7, 1 + cfg, 3)
-            ms_mix, b_mix = table.probe_bench(n, 8, 2 + cfg, 3)
-            extras["probe_roofline"] = {
-                "bound": "hbm", "unit": "GB/s", "peak": peak, "table": "1e7x10 (800 MB)",
-                "kernel": "k_probe_bench", "variant": PROBE_VARIANT, "blocks_per_sm": PROBE_BLOCKS_PER_SM,
-                "random_access_ceiling_gbs": 2900.0,
-                "descriptors": n,
-                "insert_all": {"achieved": b_ins / ms_ins / 1e6, "frac": b_ins / ms_ins / 1e6 / peak,
-                               "mprobes_per_s": n / ms_ins / 1e3},
-                "lookup_all": {"achieved": b_look / ms_look / 1e6, "frac": b_look / ms_look / 1e6 / peak,
-                               "mprobes_per_s": n / ms_look / 1e3},
-                "mix_50_50": {"achieved": b_mix / ms_mix / 1e6, "frac": b_mix / ms_mix / 1e6 / peak,
-                              "mprobes_per_s": n / ms_mix / 1e3},
-            }
+
+            def legs(table, variant, bps):
+                cfg = 16 * variant + 256 * bps
+                table.probe_bench(n, 7, 0 + cfg, 1)    # warm-up (module load, first touch)
+                table.clear()
+                ms_ins, b_ins = table.probe_bench(n, 7, 0 + cfg, 1)
+                table.probe_bench(n, 7, 1 + cfg, 1)
+                ms_look, b_look = table.probe_bench(n, 7, 1 + cfg, 3)
+                ms_mix, b_mix = table.probe_bench(n, 8, 2 + cfg, 3)
+                leg = lambda b, m: {"achieved": b / m / 1e6, "frac": b / m / 1e6 / peak,  # noqa: E731
+                                    "mprobes_per_s": n / m / 1e3}
+                return {"variant": variant, "blocks_per_sm": bps, "insert_all": leg(b_ins, ms_ins),
+                        "lookup_all": leg(b_look, ms_look), "mix_50_50": leg(b_mix, ms_mix)}
+
+            table = MaterialCache(N_CELLS, N_ENTRIES, ctx)
+            pr = {"bound": "hbm", "unit": "GB/s", "peak": peak, "table": "1e7x10 (800 MB)",
+                  "kernel": "k_probe_bench", "random_access_ceiling_gbs": 2900.0, "descriptors": n}
+            pr.update(legs(table, PROBE_VARIANT, PROBE_BLOCKS_PER_SM))
             table.close()
+            small = MaterialCache(100_000, N_ENTRIES, ctx)
+            pr["l2_resident_1e5x10"] = legs(small, PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM)
+            pr["l2_resident_1e5x10"]["table"] = "1e5x10 (8 MB, L2-resident)"
+            small.close()
+            extras["probe_roofline"] = pr
 
     # ---- roofline of the dominant kernel ----------------------------------
     peak, peak_src = measured_peaks()

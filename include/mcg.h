@@ -182,7 +182,8 @@ mcg_status mcg_audit_dump(const char* path, mcg_audit_report* out);
  * phase over them: 0 insert-all, 1 lookup-all, 2 50/50 mix; phase + 16*v
  * selects the probe variant v: 0 two-round per-lane scan (first 16 B, then
  * the rest), 1 one-round per-lane scan (whole cell), 2 warp-cooperative
- * (coalesced whole cells + ballots; Ne = 10 only). Returns the kernel's
+ * (coalesced whole cells + ballots; Ne = 10 only), 4 warp-cooperative with
+ * 16-byte lanes (one round trip per probe; Ne even <= 10). Returns the kernel's
  * device milliseconds and the algorithmic bytes it moved. */
 mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t phase,
                            int32_t iters, double* ms_out, double* algorithmic_bytes_out);

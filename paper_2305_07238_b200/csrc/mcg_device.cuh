@@ -181,6 +181,81 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, u
     return mine;
 }
 
+// Warp-cooperative probe with one 16-byte load per lane: the cell of each
+// lane's descriptor (Ne even, <= 10) is read by Ne/2 adjacent lanes as one
+// coalesced access, and every round's load is issued before the first
+// decision, so a probe costs one DRAM round trip (the per-lane scans need
+// two, and a random access that comes back to a row after it closed pays the
+// row activation again). Per round one ballot finds, for each cell, the first
+// 16-byte pair that ends the reference's linear scan (an empty slot or the
+// matching check hash, cache.cpp:127-134), and the descriptor's lane reads the
+// outcome from the deciding lane. Every lane of the warp must call it.
+__device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base, uint32_t check,
+                                              bool valid) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lpc = c.n_entries >> 1;   // lanes (pairs) per cell
+    const uint32_t cpr = 32u / lpc;          // cells per round
+    const uint32_t rounds = (32u + cpr - 1u) / cpr;
+    const uint32_t g = lane / lpc, k = lane - g * lpc;
+    ulonglong2 w[6];
+    uint32_t chk[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        w[r] = make_ulonglong2(~0ull, ~0ull);
+        chk[r] = 0u;
+        if (static_cast<uint32_t>(r) < rounds) {
+            const uint32_t owner = static_cast<uint32_t>(r) * cpr + g;
+            const uint64_t ob = __shfl_sync(kFull, base, owner & 31u);
+            const bool ov = __shfl_sync(kFull, valid, owner & 31u);
+            chk[r] = __shfl_sync(kFull, check, owner & 31u);
+            if (g < cpr && owner < 32u && ov) {
+                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(c.slots + ob) + k);
+            }
+        }
+    }
+    Probe mine{0u, -1, false};
+    const uint32_t my_round = lane / cpr, my_g = lane - my_round * cpr;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        if (static_cast<uint32_t>(r) >= rounds) break;
+        const bool e0 = w[r].x == 0ull, m0 = static_cast<uint32_t>(w[r].x >> 32) == chk[r];
+        const bool e1 = w[r].y == 0ull, m1 = static_cast<uint32_t>(w[r].y >> 32) == chk[r];
+        const bool first0 = e0 || m0;
+        const unsigned bal = __ballot_sync(kFull, (first0 || e1 || m1) && g < cpr);
+        const bool hit = first0 ? (m0 && !e0) : (m1 && !e1);
+        const uint32_t meta = ((2u * k + (first0 ? 0u : 1u)) << 1) | (hit ? 1u : 0u);
+        const uint32_t pay = static_cast<uint32_t>(first0 ? w[r].x : w[r].y);
+        uint32_t src = lane;
+        bool found = false;
+        if (my_round == static_cast<uint32_t>(r)) {
+            const uint32_t bits = (bal >> (my_g * lpc)) & ((1u << lpc) - 1u);
+            found = bits != 0u;
+            src = my_g * lpc + (found ? static_cast<uint32_t>(__ffs(bits) - 1) : 0u);
+        }
+        const uint32_t m = __shfl_sync(kFull, meta, src);
+        const uint32_t pl = __shfl_sync(kFull, pay, src);
+        if (my_round == static_cast<uint32_t>(r)) {
+            if (found) {
+                mine.where = static_cast<int32_t>(m >> 1);
+                mine.hit = (m & 1u) != 0u;
+                if (mine.hit) mine.payload = pl;
+            } else {
+                mine.where = -1;
+            }
+        }
+    }
+    return mine;
+}
+
+// The warp's probes: the cooperative one-round-trip scan where the cell
+// shape allows it (Ne even, <= 10), else the per-lane scan. Warp-collective:
+// every lane of the warp calls it (invalid lanes with valid = false).
+__device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t base, uint32_t check,
+                                             bool valid) {
+    if ((c.n_entries & 1u) == 0u && c.n_entries <= 10u) return probe_warp16(c, base, check, valid);
+    return valid ? probe_cell(c, base, check) : Probe{0u, -1, false};
+}
+
 // One CAS from zero on the slot the scan found empty (cache.cpp:108-114).
 // Returns MCG_INSERT_WON / LOST_RACE / CELL_FULL.
 __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t base, int32_t where,

@@ -135,13 +135,14 @@ __global__ void k_mip_texel(const float* uv, const float* g1, const float* g2, s
 __global__ void k_lookup(CacheView c, const mcg_descriptor* d, size_t n, uint8_t* hit, float* rgb,
                          unsigned long long* counters) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const bool valid = i < n;
+    uint64_t h = 0;
+    uint32_t chk = 0;
+    if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
+    const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
+    const mcgd::Probe p = mcgd::probe_lanes(c, cell * c.n_entries, chk, valid);
     uint32_t hits = 0, looks = 0;
-    if (i < n) {
-        uint64_t h;
-        uint32_t chk;
-        mcgd::hash_desc(load_desc(d, i), h, chk);
-        const uint64_t cell = mcgd::fast_mod(h, c.n_cells, c.magic);
-        const mcgd::Probe p = mcgd::probe_cell(c, cell * c.n_entries, chk);
+    if (valid) {
         looks = 1;
         hits = p.hit;
         if (hit) hit[i] = p.hit;
@@ -161,13 +162,14 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
                          uint8_t* outcome, uint64_t* slot_out, uint64_t* packed_out,
                          unsigned long long* counters) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const bool valid = i < n;
+    uint64_t h = 0;
+    uint32_t chk = 0;
+    if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
+    const uint64_t base = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries : 0;
+    const mcgd::Probe p = mcgd::probe_lanes(c, base, chk, valid);
     uint32_t won = 0, full = 0, lost = 0;
-    if (i < n) {
-        uint64_t h;
-        uint32_t chk;
-        mcgd::hash_desc(load_desc(d, i), h, chk);
-        const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
-        const mcgd::Probe p = mcgd::probe_cell(c, base, chk);
+    if (valid) {
         int res;
         uint64_t slot = ~0ull, packed = 0;
         if (p.hit) {
@@ -291,7 +293,8 @@ __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, ui
         mcgd::hash_desc(bench_desc(seed, i), h, chk);
         const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
         mcgd::Probe p;
-        if (kVariant == 2) p = mcgd::probe_warp<10>(c, base, chk, valid);
+        if (kVariant == 4) p = mcgd::probe_warp16(c, base, chk, valid);
+        else if (kVariant == 2) p = mcgd::probe_warp<10>(c, base, chk, valid);
         else if (kVariant == 1) p = valid ? mcgd::probe_cell_t<5>(c, base, chk) : mcgd::Probe{0u, -1, false};
         else if (kVariant == 3) p = valid ? mcgd::probe_cell_blk(c, base, chk) : mcgd::Probe{0u, -1, false};
         else p = valid ? mcgd::probe_cell_t<1>(c, base, chk) : mcgd::Probe{0u, -1, false};
@@ -950,7 +953,7 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 3,
+        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 4,
              "phase must be 0, 1 or 2 (+16 * variant, +256 * blocks per SM)");
         mcg_ctx* ctx = cache->ctx;
         cudaEvent_t a = take_event(ctx), b = take_event(ctx);
@@ -962,7 +965,9 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
             const int variant = (phase >> 4) & 15, ph = phase & 15;
             const int per_sm = (phase >> 8) ? (phase >> 8) : 8;   // blocks per SM
             const unsigned grid = 148u * static_cast<unsigned>(per_sm);
-            if (variant == 2 && cache->n_entries == 10) {
+            if (variant == 4 && cache->n_entries % 2 == 0 && cache->n_entries <= 10) {
+                k_probe_bench<4><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 2 && cache->n_entries == 10) {
                 k_probe_bench<2><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 1) {
                 k_probe_bench<1><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
