@@ -270,6 +270,11 @@ __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t base, int3
 // ---------------------------------------------------------------------------
 // Scene view (device pointers; include/mcg.h layouts)
 // ---------------------------------------------------------------------------
+#ifndef MCG_SHADOW_WIDTH
+#define MCG_SHADOW_WIDTH 4
+#endif
+constexpr int kShadowWidth = MCG_SHADOW_WIDTH;   // entries per node of the shadow tree
+
 struct SceneView {
     const float4* prim_geom;      // 3 float4 per prim
     const float2* prim_uv;        // 3 float2 per prim
@@ -278,7 +283,7 @@ struct SceneView {
     const float4* pairs;          // 4 float4 per internal node: both children's records
     const float4* quads;          // 8 float4 per 4-wide node (collapsed reference tree)
     int32_t root_a, root_b;       // root entry into `quads`: (0, -1) or a leaf (~first, count)
-    const float4* squads;         // 4-wide SAH tree over the reference's leaves (any-hit only)
+    const float4* squads;         // kShadowWidth-wide SAH tree over the reference's leaves (any-hit only)
     int32_t sroot_a, sroot_b;     // root entry into `squads`
     uint32_t n_nodes;
     const mcg_point_light* plights;

@@ -1080,6 +1080,94 @@ __device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, const float4*
     return hit;
 }
 
+// Any hit over a kW-wide tree (the SAH shadow tree over the reference's
+// leaves): speculative while-while like any_ww4s; of the entries a node
+// passes, the nearest stays in registers (popped next), the rest go to the
+// stack in entry order -- any order is exact for a boolean query.
+template <int kW>
+__device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t root_b, const mcgd::SceneView& S,
+                                        bool active, V3 o, V3 d, float tmin, float tmax,
+                                        uint32_t& nodes_visited, uint32_t& prims_tested) {
+    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    int32_t st[64];
+    int top = 0;
+    int32_t nc = 0;
+    bool has_n = false;
+    if (active && S.n_nodes) {
+        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
+        float E, T1;
+        slab(o, inv, lo, hi, tmin, E, T1);
+        if (!(fminf(tmax, T1) < E)) {
+            nc = entry_code(root_a, root_b);
+            has_n = true;
+        }
+    }
+    bool hit = false;
+    int32_t lc = 0;
+    bool leaf = false;
+    while (__any_sync(mcgd::kFull, has_n || leaf)) {
+        for (;;) {
+            if (has_n) {
+                if (nc < 0) {
+                    if (!leaf) {
+                        ++nodes_visited;
+                        leaf = true;
+                        lc = nc;
+                        has_n = false;
+                    }
+                } else {
+                    ++nodes_visited;
+                    has_n = false;
+                    const float4* p = Q + 2 * kW * nc;
+                    float best = __int_as_float(0x7f800000);
+#pragma unroll
+                    for (int k = 0; k < kW; ++k) {
+                        const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                        const int32_t eb = __float_as_int(hi.w);
+                        if (eb == 0) break;  // entries are packed: the first empty ends the node
+                        float E, T1;
+                        slab(o, inv, lo, hi, tmin, E, T1);
+                        if (!(fminf(tmax, T1) < E)) {
+                            const int32_t code = entry_code(__float_as_int(lo.w), eb);
+                            if (!has_n) {
+                                nc = code;
+                                best = E;
+                                has_n = true;
+                            } else if (E < best) {
+                                st[top++] = nc;
+                                nc = code;
+                                best = E;
+                            } else {
+                                st[top++] = code;
+                            }
+                        }
+                    }
+                }
+            }
+            if (!has_n && top > 0) {
+                nc = st[--top];
+                has_n = true;
+            }
+            if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
+        }
+        if (leaf) {
+            const uint32_t v = static_cast<uint32_t>(~lc);
+            const uint32_t first = v >> 3, cnt = v & 7u;
+            prims_tested += cnt;
+            for (uint32_t i = first; i < first + cnt; ++i) {
+                float t, b1, b2;
+                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                    hit = true;
+                    break;
+                }
+            }
+            leaf = false;
+            if (hit) has_n = false, top = 0;
+        }
+    }
+    return hit;
+}
+
 // ---------------------------------------------------------------------------
 // Packet traversal: the warp walks the 4-wide tree together, one entry at a
 // time, each entry carrying the mask of lanes that pushed it. The
@@ -1382,7 +1470,7 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
     else if (kVar == 1) occ = any_ww(S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 2) occ = any_ww4(S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 3) occ = any_ww4s(S, S.quads, S.root_a, S.root_b, active, o, d, tmin, tm, nv, nt);
-    else if (kVar == 5) occ = any_ww4s(S, S.squads, S.sroot_a, S.sroot_b, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 5) occ = any_wws<mcgd::kShadowWidth>(S.squads, S.sroot_a, S.sroot_b, S, active, o, d, tmin, tm, nv, nt);
     else {
         int32_t* pc;
         uint32_t* pm;
@@ -1414,7 +1502,7 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R)
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    const bool occ = kSah ? any_ww4s(R.S, R.S.squads, R.S.sroot_a, R.S.sroot_b, active, o, d, kTMin, tmax, nvis, ntest)
+    const bool occ = kSah ? any_wws<mcgd::kShadowWidth>(R.S.squads, R.S.sroot_a, R.S.sroot_b, R.S, active, o, d, kTMin, tmax, nvis, ntest)
                           : any_ww4s(R.S, R.S.quads, R.S.root_a, R.S.root_b, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
@@ -1727,17 +1815,23 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.q.count = reinterpret_cast<unsigned int*>(R.q.keys + 4 * cap);
         R.q.capacity = static_cast<unsigned>(cap);
     }
-    // Sort key: slot << key_shift | 24-bit Morton code of the hit point
+    // Sort key: slot << key_shift | Morton code of the hit point
     // (MCG_SORT=material: slot only).
     const char* sort_env = std::getenv("MCG_SORT");
     const bool morton = !(sort_env && std::string(sort_env) == "material");
     const int slot_bits = std::max(1, bits_for(D.view.n_programs));
-    R.key_shift = (morton && slot_bits <= 8) ? 24u : 0u;
+    // Morton grid: 2^b cells per axis (MCG_MORTON_BITS = b, 1..8). b = 7
+    // keeps the key within 3 radix passes for up to 4 material slots and
+    // measured best (profiles/README.md: 8 -> 808 ms, 7 -> 799, 6 -> 801).
+    const char* mb_env = std::getenv("MCG_MORTON_BITS");
+    const int mb = mb_env ? std::min(8, std::max(1, std::atoi(mb_env))) : 7;
+    R.key_shift = (morton && slot_bits <= 8) ? static_cast<uint32_t>(3 * mb) : 0u;
     R.key_dir = (sort_env && std::string(sort_env) == "dir") ? 1u : 0u;
+    if (R.key_dir) R.key_shift = 24u;  // the direction-class key keeps its 24-bit layout
     for (int a = 0; a < 3; ++a) {
         const float ext = D.root_hi[a] - D.root_lo[a];
         R.box_lo[a] = D.root_lo[a];
-        R.box_scale[a] = ext > 0.0f ? 255.999f / ext : 0.0f;
+        R.box_scale[a] = ext > 0.0f ? (static_cast<float>(1 << mb) - 0.001f) / ext : 0.0f;
     }
     const int key_bits = static_cast<int>(R.key_shift) + slot_bits;
     // Shadow rays over the SAH tree of the reference's leaves (exact for

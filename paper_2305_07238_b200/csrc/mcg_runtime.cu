@@ -397,10 +397,13 @@ void sync(mcg_ctx* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "cudaSt
 
 }  // namespace
 
-// Binned-SAH hierarchy over the reference BVH's leaves, collapsed to the
-// 4-wide entry layout of `quads` (entries: leaf (~first, count) with the
-// leaf's own box, or node (index, -1) with the union of its leaves' boxes).
-static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int32_t& root_a, int32_t& root_b) {
+// Binned-SAH hierarchy over the reference BVH's leaves, collapsed to
+// `width`-wide nodes in the entry layout of `quads` (entries: leaf
+// (~first, count) with the leaf's own box, or node (index, -1) with the union
+// of its leaves' boxes; unused entries zero). A node opens its largest-area
+// internal entries until it holds `width` entries.
+static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int width, int32_t& root_a,
+                                                   int32_t& root_b) {
     const mcg_bvh_node* nodes = static_cast<const mcg_bvh_node*>(f.nodes);
     std::vector<mcg_bvh_node> leaves;
     for (uint32_t i = 0; i < f.n_nodes; ++i)
@@ -537,16 +540,26 @@ static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int3
     };
     const int32_t root = build(0, leaves.size());
     std::function<int32_t(int32_t)> collapse = [&](int32_t x) -> int32_t {
-        const int32_t q = static_cast<int32_t>(out.size() / 4);
-        out.resize(out.size() + 4, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
-        std::vector<int32_t> entries;
-        for (int32_t c : {bn[x].l, bn[x].r}) {
-            if (bn[c].leaf >= 0) {
-                entries.push_back(c);
-            } else {
-                entries.push_back(bn[c].l);
-                entries.push_back(bn[c].r);
+        const int32_t q = static_cast<int32_t>(out.size() / width);
+        out.resize(out.size() + width, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
+        std::vector<int32_t> entries{bn[x].l, bn[x].r};
+        for (;;) {
+            if (static_cast<int>(entries.size()) >= width) break;
+            int best = -1;
+            float best_area = -1.0f;
+            for (size_t e = 0; e < entries.size(); ++e) {
+                const BNode& b = bn[entries[e]];
+                if (b.leaf >= 0) continue;
+                const float a = area(b.lo, b.hi);
+                if (a > best_area) {
+                    best_area = a;
+                    best = static_cast<int>(e);
+                }
             }
+            if (best < 0) break;
+            const int32_t x2 = entries[best];
+            entries[best] = bn[x2].l;
+            entries.insert(entries.begin() + best + 1, bn[x2].r);
         }
         int k = 0;
         for (int32_t e : entries) {
@@ -559,7 +572,7 @@ static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int3
                 rec.a = collapse(e);
                 rec.b = -1;
             }
-            out[4 * static_cast<size_t>(q) + k++] = rec;
+            out[static_cast<size_t>(width) * q + k++] = rec;
         }
         return q;
     };
@@ -1084,13 +1097,13 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         v.quads = static_cast<const float4*>(up(15, quads.data(), quads.size() * sizeof(mcg_bvh_node)));
         // Worst-case stack of the LIFO traversal: a node pushes its k
         // entries and descends into one of them, leaving k-1 behind.
-        auto stack_need = [](const std::vector<mcg_bvh_node>& qs) -> uint32_t {
-            const size_t nq = qs.size() / 4;
+        auto stack_need = [](const std::vector<mcg_bvh_node>& qs, int width) -> uint32_t {
+            const size_t nq = qs.size() / width;
             std::vector<uint32_t> need(nq, 1);
             for (size_t q = nq; q-- > 0;) {
                 uint32_t k = 0, deepest = 1;
-                for (int e = 0; e < 4; ++e) {
-                    const mcg_bvh_node& r = qs[4 * q + e];
+                for (int e = 0; e < width; ++e) {
+                    const mcg_bvh_node& r = qs[width * q + e];
                     if (r.b == 0) continue;
                     ++k;
                     if (r.b < 0) deepest = std::max(deepest, need[r.a]);
@@ -1099,7 +1112,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             }
             return nq ? std::max<uint32_t>(1, need[0]) : 1;
         };
-        D.max_stack4 = stack_need(quads);
+        D.max_stack4 = stack_need(quads, 4);
         if (D.max_stack4 > 63) fail(MCG_ERR_INVALID_ARGUMENT, "BVH too deep for the traversal stack");
         // Shadow tree: the reference's leaves (their exact boxes and
         // primitive ranges) regrouped by a binned SAH build. Any-hit is a
@@ -1108,8 +1121,8 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         // the slab test is monotone, so ancestors never reject first) -- so
         // any hierarchy over the same leaves answers exactly as the
         // reference's tree does.
-        std::vector<mcg_bvh_node> squads = build_shadow_tree(f, v.sroot_a, v.sroot_b);
-        D.max_stack_s = stack_need(squads);
+        std::vector<mcg_bvh_node> squads = build_shadow_tree(f, mcgd::kShadowWidth, v.sroot_a, v.sroot_b);
+        D.max_stack_s = stack_need(squads, mcgd::kShadowWidth);
         if (D.max_stack_s > 63) fail(MCG_ERR_INVALID_ARGUMENT, "shadow BVH too deep for the traversal stack");
         v.squads = static_cast<const float4*>(up(16, squads.data(), squads.size() * sizeof(mcg_bvh_node)));
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
