@@ -247,6 +247,84 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base,
     return mine;
 }
 
+// Cooperative probe inside a lane group `grp` (the VM's material group,
+// possibly a partial warp): the cells of the group's `leader` lanes are read
+// by Ne/2 consecutive group lanes each, every round's load in flight before
+// the first decision, as in probe_warp16. Falls back to per-lane scans by the
+// leaders when the group is too small or has too many cells. Every lane of
+// `grp` must call it; only leaders' results are meaningful.
+__device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base, uint32_t check,
+                                              bool leader, unsigned grp) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned L = __ballot_sync(grp, leader);
+    const uint32_t nL = __popc(L), nW = __popc(grp);
+    const uint32_t lpc = c.n_entries >> 1;
+    const uint32_t cpr = lpc ? nW / lpc : 0u;
+    const uint32_t rounds = cpr ? (nL + cpr - 1u) / cpr : 99u;
+    if ((c.n_entries & 1u) != 0u || c.n_entries > 10u || cpr == 0u || rounds > 6u) {
+        return leader ? probe_cell(c, base, check) : Probe{0u, -1, false};
+    }
+    const unsigned below = (1u << lane) - 1u;
+    const uint32_t rank = __popc(grp & below);
+    const uint32_t g = rank / lpc, k = rank - g * lpc;
+    ulonglong2 w[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        w[r] = make_ulonglong2(~0ull, ~0ull);
+        if (static_cast<uint32_t>(r) < rounds) {
+            const uint32_t j = static_cast<uint32_t>(r) * cpr + g;
+            const bool work = g < cpr && j < nL;
+            const uint32_t owner = work ? __fns(L, 0u, static_cast<int>(j) + 1) : lane;
+            const uint64_t ob = __shfl_sync(grp, base, owner);
+            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(c.slots + ob) + k);
+        }
+    }
+    Probe mine{0u, -1, false};
+    const uint32_t jm = __popc(L & below);   // my ordinal among the leaders
+    const uint32_t my_round = jm / cpr, gm = jm - my_round * cpr;
+    unsigned range = 0u;
+    if (leader) {
+        const uint32_t lo = __fns(grp, 0u, static_cast<int>(gm * lpc) + 1);
+        const uint32_t hi = __fns(grp, 0u, static_cast<int>(gm * lpc + lpc));
+        const unsigned upto = hi >= 31u ? 0xffffffffu : ((2u << hi) - 1u);
+        range = grp & upto & ~((1u << lo) - 1u);
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        if (static_cast<uint32_t>(r) >= rounds) break;
+        const uint32_t j = static_cast<uint32_t>(r) * cpr + g;
+        const bool work = g < cpr && j < nL;
+        const uint32_t owner = work ? __fns(L, 0u, static_cast<int>(j) + 1) : lane;
+        const uint32_t chk = __shfl_sync(grp, check, owner);
+        const bool e0 = w[r].x == 0ull, m0 = static_cast<uint32_t>(w[r].x >> 32) == chk;
+        const bool e1 = w[r].y == 0ull, m1 = static_cast<uint32_t>(w[r].y >> 32) == chk;
+        const bool first0 = e0 || m0;
+        const unsigned bal = __ballot_sync(grp, work && (first0 || e1 || m1));
+        const bool hit = first0 ? (m0 && !e0) : (m1 && !e1);
+        const uint32_t meta = ((2u * k + (first0 ? 0u : 1u)) << 1) | (hit ? 1u : 0u);
+        const uint32_t pay = static_cast<uint32_t>(first0 ? w[r].x : w[r].y);
+        uint32_t src = lane;
+        bool found = false;
+        if (leader && my_round == static_cast<uint32_t>(r)) {
+            const unsigned bits = bal & range;
+            found = bits != 0u;
+            if (found) src = static_cast<uint32_t>(__ffs(bits) - 1);
+        }
+        const uint32_t mm = __shfl_sync(grp, meta, src);
+        const uint32_t pl = __shfl_sync(grp, pay, src);
+        if (leader && my_round == static_cast<uint32_t>(r)) {
+            if (found) {
+                mine.where = static_cast<int32_t>(mm >> 1);
+                mine.hit = (mm & 1u) != 0u;
+                if (mine.hit) mine.payload = pl;
+            } else {
+                mine.where = -1;
+            }
+        }
+    }
+    return mine;
+}
+
 // The warp's probes: the cooperative one-round-trip scan where the cell
 // shape allows it (Ne even, <= 10), else the per-lane scan. Warp-collective:
 // every lane of the warp calls it (invalid lanes with valid = false).
@@ -547,8 +625,15 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 const unsigned long long key = (cell << 32) ^ p_check;
                 const unsigned peers = __match_any_sync(grp, key);
                 const int leader = __ffs(peers) - 1;
+#ifdef MCG_VM_GROUP_PROBE
+                // cooperative scan by the group (measured slower in the VM:
+                // 115 vs 96 registers, and few leaders per warp after the
+                // Morton sort -- profiles/README.md)
+                Probe pr = probe_group16(C, p_base, p_check, static_cast<int>(lane) == leader, grp);
+#else
                 Probe pr{0u, -1, false};
                 if (static_cast<int>(lane) == leader) pr = probe_cell(C, p_base, p_check);
+#endif
                 pr.payload = __shfl_sync(grp, pr.payload, leader);
                 pr.where = __shfl_sync(grp, pr.where, leader);
                 pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;

@@ -929,11 +929,21 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
         // Phase 1: pop/expand until every lane holds a leaf or is done;
         // lanes holding one keep expanding internal entries (speculation).
         for (;;) {
+            // culled entries (the reference's test at pop) are skipped in a
+            // tight loop rather than one per warp-wide iteration
+            while (has_n && closest < ne) {
+                ++nodes_visited;
+                has_n = false;
+                if (top > 0) {
+                    --top;
+                    const int2 e = st[top];
+                    nc = e.x;
+                    ne = __int_as_float(e.y);
+                    has_n = true;
+                }
+            }
             if (has_n) {
-                if (closest < ne) {  // culled (the reference's test at pop)
-                    ++nodes_visited;
-                    has_n = false;
-                } else if (nc < 0) {
+                if (nc < 0) {
                     if (!leaf) {
                         ++nodes_visited;
                         leaf = true;
@@ -1587,8 +1597,11 @@ __global__ void k_count_live(RenderView R, uint32_t* live) {
 // Material evaluation of every live hit, in sorted (material, Morton)
 // order, then NEE and the bounce; the path's state moves from its old layout
 // position q = order[i] to i in the next layout.
+#ifndef MCG_SHADE_MINB
+#define MCG_SHADE_MINB 1
+#endif
 template <bool kDeferred>
-__global__ void __launch_bounds__(128) k_shade(RenderView R, const uint32_t* __restrict__ skey,
+__global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
                                                const uint32_t* __restrict__ order, int max_stack,
                                                uint32_t wh, int b) {
     extern __shared__ float smem[];
