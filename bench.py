@@ -198,6 +198,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip speed-up/probe legs")
+    ap.add_argument("--shared-cache", action="store_true",
+                    help="N>1: one table striped over the GPUs (SURVEY 8f.3) instead of per-GPU replicas")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -240,11 +242,22 @@ def main() -> None:
                      C.cast(C.c_void_p(nodes.data_ptr()), C.POINTER(C.c_double)),
                      C.cast(C.c_void_p(samples.data_ptr()), C.POINTER(C.c_uint32)))
 
+    shared = None
+    if args.shared_cache and world > 1:
+        from paper_2305_07238_b200 import dist as D
+        shared = D.shared_cache(N_CELLS, N_ENTRIES, ctx, rank, world)
+
     def step(p=params):
         with torch.cuda.stream(stream):
             rad.zero_(); nodes.zero_(); samples.zero_()
         st = N.RenderStats()
-        N.check(L.mcg_render_device(ctx.handle, C.byref(p), None, C.byref(dframe), C.byref(st)))
+        ext = None
+        if shared is not None and p.cache_mode != 0:
+            shared.clear()            # a fresh logical table per render, like the replicas
+            ctx.synchronize()
+            dist.barrier()
+            ext = shared.handle
+        N.check(L.mcg_render_device(ctx.handle, C.byref(p), ext, C.byref(dframe), C.byref(st)))
         if world > 1:
             with torch.cuda.stream(stream):
                 dist.reduce(rad, 0)
@@ -453,6 +466,7 @@ def main() -> None:
             "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp, cache {N_CELLS:.0e}x{N_ENTRIES}, "
                                    "concurrent inserts", "width": W, "height": H, "spp": SPP,
                        "n_cells": N_CELLS, "n_entries": N_ENTRIES, "parallelism": f"tiles/{world}",
+                       "cache": "striped over GPUs" if shared is not None else "per-GPU replica",
                        "l2": "inputs larger than L2 (800 MB table re-zeroed per render + "
                              f"{(W * H * 10 * 16) >> 20} MB path state)"},
             "clocks": clk.summary(),

@@ -168,6 +168,24 @@ mcg_status mcg_cache_dump(mcg_cache* cache, const char* path);
 /* Device pointer of the slot array (n_cells*n_entries u64), for tooling. */
 uint64_t* mcg_cache_device_slots(mcg_cache* cache);
 
+/* Striped shared table (one logical Nc x Ne table over `world`
+ * GPUs instead of per-GPU replicas). The stripe of `rank` holds the cells c
+ * with c % world == rank (local cell c / world); lookups, inserts and renders
+ * address any cell through the stripes' device pointers -- peers' over
+ * NVLink (CUDA IPC within a node), or other stripes of the same process
+ * (mcg_cache_attach_local, which also emulates a striped table on one GPU).
+ * Hashing, cell and entry indices are the logical table's, so results equal
+ * those of one Nc x Ne table; cross-process deterministic mode is not
+ * provided (each process applies its own ordered stores). read_slots,
+ * occupied and clear act on this stripe's words; dump needs world == 1. */
+mcg_status mcg_cache_create_stripe(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, uint32_t rank,
+                                   uint32_t world, mcg_cache** out);
+mcg_status mcg_cache_attach_local(mcg_cache* cache, mcg_cache* const* stripes, uint32_t world);
+mcg_status mcg_cache_ipc_handle(mcg_cache* cache, void* out, size_t cap);   /* 64 bytes */
+mcg_status mcg_cache_attach_ipc(mcg_cache* cache, const void* handles, uint32_t world);
+mcg_status mcg_cache_stripe_info(const mcg_cache* cache, uint32_t* rank, uint32_t* world,
+                                 uint64_t* local_cells);
+
 /* audit_dump (cache.cpp:175-230), host only. */
 typedef struct mcg_audit_report {
     uint64_t n_cells, n_entries, occupied;

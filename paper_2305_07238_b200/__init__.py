@@ -261,12 +261,49 @@ class MaterialCache:
 
     APPLY_CONCURRENT, APPLY_ORDERED = 0, 1
 
-    def __init__(self, n_cells: int, n_entries: int, ctx: Optional[Context] = None):
+    def __init__(self, n_cells: int, n_entries: int, ctx: Optional[Context] = None, *,
+                 rank: int = 0, world: int = 1):
         self.ctx = ctx or Context.default()
         h = C.c_void_p()
-        check(N.lib().mcg_cache_create(self.ctx.handle, int(n_cells), int(n_entries), C.byref(h)))
+        if world == 1:
+            check(N.lib().mcg_cache_create(self.ctx.handle, int(n_cells), int(n_entries), C.byref(h)))
+        else:
+            check(N.lib().mcg_cache_create_stripe(self.ctx.handle, int(n_cells), int(n_entries), int(rank),
+                                                  int(world), C.byref(h)))
         self.handle = h
         self.n_cells, self.n_entries = int(n_cells), int(n_entries)
+        self.rank, self.world = int(rank), int(world)
+
+    # ---- striped shared table (include/mcg.h) ----
+    @classmethod
+    def stripe(cls, n_cells: int, n_entries: int, rank: int, world: int,
+               ctx: Optional[Context] = None) -> "MaterialCache":
+        """This device's stripe of one logical n_cells x n_entries table
+        shared by `world` GPUs (cells c with c % world == rank)."""
+        return cls(n_cells, n_entries, ctx, rank=rank, world=world)
+
+    def local_cells(self) -> int:
+        out = C.c_uint64()
+        check(N.lib().mcg_cache_stripe_info(self.handle, None, None, C.byref(out)))
+        return int(out.value)
+
+    def attach_local(self, stripes: Sequence["MaterialCache"]) -> None:
+        """Address the other stripes directly (same process: peers or, on one
+        GPU, an emulated striped table)."""
+        arr = (C.c_void_p * len(stripes))(*[st.handle.value for st in stripes])
+        check(N.lib().mcg_cache_attach_local(self.handle, arr, len(stripes)))
+
+    def ipc_handle(self) -> bytes:
+        """CUDA IPC handle of this stripe (64 bytes) for the other ranks."""
+        buf = C.create_string_buffer(64)
+        check(N.lib().mcg_cache_ipc_handle(self.handle, buf, 64))
+        return buf.raw
+
+    def attach_ipc(self, handles: Sequence[bytes]) -> None:
+        """Map every rank's stripe (handles in rank order; own entry ignored)."""
+        blob = b"".join(bytes(h).ljust(64, b"\0")[:64] for h in handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        check(N.lib().mcg_cache_attach_ipc(self.handle, buf, len(handles)))
 
     def close(self) -> None:
         if getattr(self, "handle", None):
@@ -280,7 +317,8 @@ class MaterialCache:
             pass
 
     def slot_count(self) -> int:
-        return self.n_cells * self.n_entries
+        """Slots held by this object (this stripe's, for a striped table)."""
+        return (self.n_cells if self.world == 1 else self.local_cells()) * self.n_entries
 
     def bytes(self) -> int:
         return self.slot_count() * 8

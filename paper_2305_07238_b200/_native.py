@@ -122,6 +122,11 @@ _SIGS = [
     ("mcg_cache_counters_reset", C.c_int, [vp]),
     ("mcg_cache_dump", C.c_int, [vp, C.c_char_p]),
     ("mcg_cache_device_slots", vp, [vp]),
+    ("mcg_cache_create_stripe", C.c_int, [vp, u64, u32, u32, u32, P(vp)]),
+    ("mcg_cache_attach_local", C.c_int, [vp, P(vp), u32]),
+    ("mcg_cache_ipc_handle", C.c_int, [vp, vp, C.c_size_t]),
+    ("mcg_cache_attach_ipc", C.c_int, [vp, vp, u32]),
+    ("mcg_cache_stripe_info", C.c_int, [vp, P(u32), P(u32), P(u64)]),
     ("mcg_audit_dump", C.c_int, [C.c_char_p, P(AuditReport)]),
     ("mcg_probe_bench", C.c_int, [vp, u64, u64, i32, i32, P(f64), P(f64)]),
     ("mcg_scene_load", C.c_int, [C.c_char_p, i32, P(vp)]),

@@ -76,12 +76,20 @@ struct DeviceScene {
 
 struct mcg_cache {
     mcg_ctx* ctx = nullptr;
-    uint64_t n_cells = 0;
+    uint64_t n_cells = 0;         // logical cells (all stripes)
     uint32_t n_entries = 0;
     uint64_t magic = 0;
-    uint64_t* slots = nullptr;
+    uint64_t* slots = nullptr;    // this device's cells (all of them when world == 1)
     unsigned long long* counters = nullptr;  // lookups, hits, won, lost_full, lost_race
-    mcgd::CacheView view() const { return {slots, n_cells, magic, n_entries}; }
+    // Striped shared table: this stripe holds cells c with
+    // c % world == rank; `stripes` (device array) points at every stripe,
+    // peers' through CUDA IPC / peer access over NVLink.
+    uint32_t world = 1, rank = 0;
+    uint64_t local_cells = 0;
+    uint64_t** stripes = nullptr;
+    std::vector<void*> ipc_opened;
+    uint64_t local_words() const { return local_cells * n_entries; }
+    mcgd::CacheView view() const { return {slots, n_cells, magic, n_entries, world, stripes}; }
 };
 
 struct mcg_ctx {

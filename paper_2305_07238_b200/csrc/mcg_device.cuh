@@ -21,7 +21,18 @@ struct CacheView {
     uint64_t n_cells;
     uint64_t magic;           // floor((2^64-1) / n_cells) for fast_mod
     uint32_t n_entries;
+    uint32_t world;           // > 1: one logical table striped by cell over `world` devices
+    uint64_t* const* stripes; // device pointers of every stripe (peer memory over NVLink)
 };
+
+// Words of the cell starting at logical slot `base` (= cell * n_entries). A
+// striped table keeps cell c on stripe c % world at local cell c / world, so
+// every device sees the same logical table.
+__device__ __forceinline__ uint64_t* cell_words(const CacheView& c, uint64_t base) {
+    if (c.world <= 1u) return c.slots + base;
+    const uint64_t cell = base / c.n_entries;
+    return c.stripes[cell % c.world] + (cell / c.world) * c.n_entries;
+}
 
 // Result of scanning one cell as lookup() does (cache.cpp:121-136): a match,
 // or the first empty slot (where update() would CAS, cache.cpp:108), or a
@@ -59,7 +70,7 @@ template <int kFirstPairs>
 __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t base, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
-    const uint64_t* cell = c.slots + base;
+    const uint64_t* cell = cell_words(c, base);
     uint32_t i = 0;
     if ((base & 1ull) == 0ull && ne >= 2 && ne <= 10) {
         const uint32_t npairs = ne >> 1;
@@ -100,7 +111,7 @@ __device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, u
 __device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t base, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
-    const uint64_t* cell = c.slots + base;
+    const uint64_t* cell = cell_words(c, base);
     if ((base & 1ull) != 0ull || ne > 10) return probe_cell_t<1>(c, base, check);
     const uint32_t npairs = ne >> 1;
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
@@ -150,7 +161,7 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, u
         const int owner = rd * kPer + g;
         const uint64_t ob = __shfl_sync(kFull, base, owner & 31);
         const bool ov = __shfl_sync(kFull, valid, owner & 31);
-        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(c.slots + ob + word) : ~0ull;
+        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(cell_words(c, ob) + word) : ~0ull;
     }
     Probe mine{0u, -1, false};
 #pragma unroll
@@ -209,7 +220,7 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base,
             const bool ov = __shfl_sync(kFull, valid, owner & 31u);
             chk[r] = __shfl_sync(kFull, check, owner & 31u);
             if (g < cpr && owner < 32u && ov) {
-                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(c.slots + ob) + k);
+                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, ob)) + k);
             }
         }
     }
@@ -276,7 +287,7 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base
             const bool work = g < cpr && j < nL;
             const uint32_t owner = work ? __fns(L, 0u, static_cast<int>(j) + 1) : lane;
             const uint64_t ob = __shfl_sync(grp, base, owner);
-            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(c.slots + ob) + k);
+            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, ob)) + k);
         }
     }
     Probe mine{0u, -1, false};
@@ -341,7 +352,7 @@ __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t base, int3
     if (where < 0) return MCG_INSERT_CELL_FULL;
     const unsigned long long packed = (static_cast<unsigned long long>(check) << 32) | payload;
     const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long*>(c.slots + base + where), 0ull, packed);
+        atomicCAS(reinterpret_cast<unsigned long long*>(cell_words(c, base) + where), 0ull, packed);
     return prev == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
 }
 

@@ -1769,7 +1769,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     char* base = ctx->path_mem.as<char>();
     RenderView R{};
     R.S = D.view;
-    R.C = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1};
+    if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
+    R.C = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, nullptr};
     R.cache_on = cache_on ? 1 : 0;
     R.mip_offset = P.mip_offset;
     camera_setup(D.cam, W, H, R.cam);

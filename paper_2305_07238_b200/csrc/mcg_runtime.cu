@@ -221,7 +221,7 @@ __global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
     if (i < n) {
         const uint64_t cell = keys[i] >> ob;
         if (i == 0 || (keys[i - 1] >> ob) != cell) {
-            uint64_t* words = c.slots + cell * c.n_entries;
+            uint64_t* words = mcgd::cell_words(c, cell * c.n_entries);
             const unsigned long long omask = ob >= 64 ? ~0ull : ((1ull << ob) - 1ull);
             for (size_t j = i; j < n && (keys[j] >> ob) == cell; ++j) {
                 const uint32_t chk = static_cast<uint32_t>(vals[j] >> 32);
@@ -758,6 +758,7 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
         c->n_cells = n_cells;
         c->n_entries = n_entries;
         c->magic = mod_magic(n_cells);
+        c->local_cells = n_cells;
         cudaError_t e = cudaMalloc(&c->slots, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -775,16 +776,118 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
 mcg_status mcg_cache_destroy(mcg_cache* cache) {
     if (!cache) return MCG_OK;
     cudaStreamSynchronize(cache->ctx->stream);
+    for (void* p : cache->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (cache->stripes) cudaFree(cache->stripes);
     cudaFree(cache->slots);
     cudaFree(cache->counters);
     delete cache;
     return MCG_OK;
 }
 
+// ---- striped shared table --------------------------------------
+
+mcg_status mcg_cache_create_stripe(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, uint32_t rank,
+                                   uint32_t world, mcg_cache** out) {
+    return guarded([&] {
+        need(ctx && out, "null argument");
+        need(world >= 1 && rank < world, "rank must be < world");
+        if (n_cells == 0 || n_entries == 0) fail(MCG_ERR_INVALID_ARGUMENT, "cache dimensions must be nonzero");
+        uint64_t bytes = 0;
+        const mcg_status s = mcg_memory_bytes(n_cells, n_entries, &bytes);
+        if (s != MCG_OK) fail(s, mcg_last_error());
+        if (n_cells >= (1ull << 32)) fail(MCG_ERR_INVALID_ARGUMENT, "n_cells must be < 2^32");
+        auto* c = new mcg_cache;
+        c->ctx = ctx;
+        c->n_cells = n_cells;
+        c->n_entries = n_entries;
+        c->magic = mod_magic(n_cells);
+        c->world = world;
+        c->rank = rank;
+        c->local_cells = n_cells > rank ? (n_cells - rank + world - 1) / world : 0;
+        const size_t local_bytes = std::max<uint64_t>(8, c->local_words() * 8);
+        cudaError_t e = cudaMalloc(&c->slots, local_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
+        if (e != cudaSuccess) {
+            if (c->slots) cudaFree(c->slots);
+            delete c;
+            cuda_check(e, "cudaMalloc(cache stripe)");
+        }
+        cuda_check(cudaMemsetAsync(c->slots, 0, local_bytes, ctx->stream), "memset stripe");
+        cuda_check(cudaMemsetAsync(c->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
+        sync(ctx);
+        *out = c;
+    });
+}
+
+static void upload_stripes(mcg_cache* c, const std::vector<uint64_t*>& ptrs) {
+    if (!c->stripes) cuda_check(cudaMalloc(&c->stripes, ptrs.size() * sizeof(uint64_t*)), "cudaMalloc(stripes)");
+    cuda_check(cudaMemcpyAsync(c->stripes, ptrs.data(), ptrs.size() * sizeof(uint64_t*), cudaMemcpyHostToDevice,
+                               c->ctx->stream), "H2D stripes");
+    sync(c->ctx);
+}
+
+mcg_status mcg_cache_attach_local(mcg_cache* cache, mcg_cache* const* stripes, uint32_t world) {
+    return guarded([&] {
+        need(cache && stripes, "null argument");
+        need(world == cache->world, "world does not match the stripe's");
+        std::vector<uint64_t*> ptrs(world);
+        for (uint32_t r = 0; r < world; ++r) {
+            need(stripes[r] && stripes[r]->world == world && stripes[r]->rank == r &&
+                     stripes[r]->n_cells == cache->n_cells && stripes[r]->n_entries == cache->n_entries,
+                 "stripe r must be rank r of the same logical table");
+            ptrs[r] = stripes[r]->slots;
+        }
+        upload_stripes(cache, ptrs);
+    });
+}
+
+mcg_status mcg_cache_ipc_handle(mcg_cache* cache, void* out, size_t cap) {
+    return guarded([&] {
+        need(cache && out, "null argument");
+        need(cap >= sizeof(cudaIpcMemHandle_t), "handle buffer too small (64 bytes)");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, cache->slots), "cudaIpcGetMemHandle");
+        std::memcpy(out, &h, sizeof(h));
+    });
+}
+
+mcg_status mcg_cache_attach_ipc(mcg_cache* cache, const void* handles, uint32_t world) {
+    return guarded([&] {
+        need(cache && handles, "null argument");
+        need(world == cache->world, "world does not match the stripe's");
+        need(cache->ipc_opened.empty(), "stripes already attached");
+        std::vector<uint64_t*> ptrs(world);
+        const auto* hb = static_cast<const unsigned char*>(handles);
+        for (uint32_t r = 0; r < world; ++r) {
+            if (r == cache->rank) {
+                ptrs[r] = cache->slots;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, hb + static_cast<size_t>(r) * sizeof(h), sizeof(h));
+            void* p = nullptr;
+            cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            cache->ipc_opened.push_back(p);
+            ptrs[r] = static_cast<uint64_t*>(p);
+        }
+        upload_stripes(cache, ptrs);
+    });
+}
+
+mcg_status mcg_cache_stripe_info(const mcg_cache* cache, uint32_t* rank, uint32_t* world,
+                                 uint64_t* local_cells) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        if (rank) *rank = cache->rank;
+        if (world) *world = cache->world;
+        if (local_cells) *local_cells = cache->local_cells;
+    });
+}
+
 mcg_status mcg_cache_clear(mcg_cache* cache) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->n_cells * cache->n_entries * 8,
+        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_words() * 8,
                                    cache->ctx->stream), "memset cache");
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
                                    cache->ctx->stream), "memset counters");
@@ -805,6 +908,7 @@ static void update_device(mcg_cache* cache, const mcg_descriptor* dd, const floa
                           int32_t mode, uint8_t* d_out, uint64_t* d_slot, uint64_t* d_packed) {
     mcg_ctx* ctx = cache->ctx;
     if (!n) return;
+    need(cache->world == 1 || cache->stripes, "striped table: attach the stripes first");
     if (mode == MCG_APPLY_CONCURRENT) {
         LaunchScope ls(ctx, "cache_update", n * (8.0 * cache->n_entries));
         k_update<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), dd, drgb, n, d_out,
@@ -836,6 +940,7 @@ mcg_status mcg_cache_update_batch(mcg_cache* cache, const mcg_descriptor* d, con
                                   uint64_t* packed) {
     return guarded([&] {
         need(cache && d && rgb, "null argument");
+        need(cache->world == 1 || cache->stripes, "striped table: attach the stripes first");
         if (!n) return;
         mcg_ctx* ctx = cache->ctx;
         auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
@@ -865,6 +970,7 @@ mcg_status mcg_cache_lookup_batch(mcg_cache* cache, const mcg_descriptor* d, siz
                                   uint8_t* hit, float* rgb) {
     return guarded([&] {
         need(cache && d && hit && rgb, "null argument");
+        need(cache->world == 1 || cache->stripes, "striped table: attach the stripes first");
         if (!n) return;
         mcg_ctx* ctx = cache->ctx;
         auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
@@ -886,6 +992,7 @@ mcg_status mcg_cache_lookup_device(mcg_cache* cache, const mcg_descriptor* d_des
     return guarded([&] {
         need(cache && d_desc, "null argument");
         if (!n) return;
+        need(cache->world == 1 || cache->stripes, "striped table: attach the stripes first");
         mcg_ctx* ctx = cache->ctx;
         LaunchScope ls(ctx, "cache_lookup", n * (8.0 * cache->n_entries));
         k_lookup<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cache->view(), d_desc, n, d_hit,
@@ -897,7 +1004,7 @@ mcg_status mcg_cache_lookup_device(mcg_cache* cache, const mcg_descriptor* d_des
 mcg_status mcg_cache_read_slots(mcg_cache* cache, uint64_t first, size_t n, uint64_t* words) {
     return guarded([&] {
         need(cache && words, "null argument");
-        need(first + n <= cache->n_cells * cache->n_entries, "slot range out of bounds");
+        need(first + n <= cache->local_words(), "slot range out of bounds (this stripe's words)");
         if (!n) return;
         dev_download(cache->ctx, words, cache->slots + first, n);
         sync(cache->ctx);
@@ -909,7 +1016,7 @@ mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
         need(cache && occupied, "null argument");
         mcg_ctx* ctx = cache->ctx;
         cuda_check(cudaMemsetAsync(cache->counters + 7, 0, 8, ctx->stream), "memset");
-        const uint64_t n = cache->n_cells * cache->n_entries;
+        const uint64_t n = cache->local_words();
         LaunchScope ls(ctx, "occupied", n * 8.0);
         k_occupied<<<148 * 8, 256, 0, ctx->stream>>>(cache->slots, n, cache->counters + 7);
         ls.done();
@@ -945,6 +1052,7 @@ mcg_status mcg_cache_counters_reset(mcg_cache* cache) {
 mcg_status mcg_cache_dump(mcg_cache* cache, const char* path) {
     return guarded([&] {
         need(cache && path, "null argument");
+        need(cache->world == 1, "dump of a striped table: dump each stripe's words (mcg_cache_read_slots)");
         std::ofstream out(path, std::ios::binary);
         if (!out) fail(MCG_ERR_IO, std::string("cannot open cache dump for writing: ") + path);
         const uint64_t header[2] = {cache->n_cells, cache->n_entries};
@@ -1169,7 +1277,8 @@ mcg_status mcg_execute_batch(mcg_ctx* ctx, uint32_t slot, const float* sp, size_
         const int block = 128;
         const int max_stack = static_cast<int>(ctx->scene.max_stack);
         const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
-        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1};
+        if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
+        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, nullptr};
         unsigned long long* counters = cache ? cache->counters : ctx->stats_mem.as<unsigned long long>();
         mcgd::StoreQueue q{nullptr, nullptr, nullptr, 0};
         const uint64_t cap = deferred ? n * std::max<uint32_t>(1, ctx->scene.max_cache_points) : 0;

@@ -3,6 +3,11 @@ its 16x16 tiles (tracer.hpp:19) with a private table replica, and one
 reduce(sum) per framebuffer to rank 0 over torch.distributed (NCCL over
 NVLink on GPUs, gloo in the CPU tests). The reduce is exact: every pixel is
 non-zero on exactly one rank and x + 0 = x.
+
+`shared_cache` builds the alternative of SURVEY §8f.3: one logical table
+striped by cell over the ranks (each rank's stripe mapped into every other
+rank through CUDA IPC, inserts are CASes on peer memory over NVLink), so all
+ranks share what any of them cached.
 """
 from __future__ import annotations
 
@@ -51,10 +56,30 @@ def gather_frame(tensors, dst: int = 0, group=None) -> None:
         dist.reduce(t, dst, group=group)
 
 
+def exchange_handles(handle: bytes, world: int, group=None) -> list:
+    """all_gather of the ranks' 64-byte stripe handles (rank order)."""
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, bytes(handle), group=group)
+    return out
+
+
+def shared_cache(n_cells: int, n_entries: int, ctx: Context, rank: int, world: int, group=None):
+    """This rank's stripe of a table shared by all ranks, every stripe
+    attached (collective: every rank calls it)."""
+    from . import MaterialCache
+    import torch.distributed as dist
+    st = MaterialCache.stripe(n_cells, n_entries, rank, world, ctx)
+    st.attach_ipc(exchange_handles(st.ipc_handle(), world, group))
+    dist.barrier(group=group)   # every stripe zeroed and mapped before anyone inserts
+    return st
+
+
 def render_sharded(scene: Scene, config: RenderConfig, ctx: Context, rank: int, world: int,
-                   mode: int = SHARD_INTERLEAVED, gather: bool = True):
+                   mode: int = SHARD_INTERLEAVED, gather: bool = True, cache=None):
     """Renders this rank's tiles into device framebuffers (torch tensors on
-    the context's device) and reduces them to rank 0. Returns
+    the context's device) and reduces them to rank 0; `cache` (e.g. a
+    shared_cache stripe) replaces the rank's private table. Returns
     (radiance, nodes_found, samples, stats) tensors (valid on rank 0)."""
     import torch
     if ctx._scene is not scene:
@@ -71,7 +96,8 @@ def render_sharded(scene: Scene, config: RenderConfig, ctx: Context, rank: int, 
     params = shard_config(config, rank, world, mode).to_params()
     st = N.RenderStats()
     torch.cuda.current_stream(dev).synchronize()
-    N.check(N.lib().mcg_render_device(ctx.handle, C.byref(params), None, C.byref(frame), C.byref(st)))
+    N.check(N.lib().mcg_render_device(ctx.handle, C.byref(params), cache.handle if cache is not None else None,
+                                      C.byref(frame), C.byref(st)))
     ctx.synchronize()
     if gather and world > 1:
         gather_frame([rad, nodes, samples])

@@ -253,3 +253,53 @@ def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, ki
     for variant in range(6):
         np.testing.assert_array_equal(ctx.occluded_batch(rays, 1e-4, tm, variant), want_occ,
                                       err_msg=f"variant {variant}")
+
+
+def test_striped_table_equals_one_table(ctx, scene_dir):
+    """one logical table striped by cell over `world` devices
+    (emulated here by three stripes on one GPU, addressed through the same
+    stripe-pointer path peers use over NVLink) behaves exactly as one Nc x Ne
+    table: same outcomes, slots and payloads, same words cell by cell, same
+    deterministic render."""
+    nc, ne, world = 4099, 4, 3
+    stripes = [MaterialCache.stripe(nc, ne, r, world, ctx) for r in range(world)]
+    for st in stripes:
+        st.attach_local(stripes)
+    assert [st.local_cells() for st in stripes] == [1367, 1366, 1366]
+    one = MaterialCache(nc, ne, ctx)
+    r = np.random.default_rng(17)
+    n = 30_000
+    d = descriptors(r.integers(0, 4, n), r.integers(0, 64, n), r.integers(0, 9, n),
+                    r.integers(0, 64, n), r.integers(0, 64, n))
+    rgb = r.uniform(0, 4, (n, 3)).astype(np.float32)
+    a = one.update_batch(d, rgb, ordered=True)
+    b = stripes[1].update_batch(d, rgb, ordered=True)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    words = one.slot_words().reshape(nc, ne)
+    for k, st in enumerate(stripes):
+        np.testing.assert_array_equal(st.slot_words().reshape(-1, ne), words[k::world])
+    h1, v1 = one.lookup_batch(d)
+    h2, v2 = stripes[2].lookup_batch(d)
+    np.testing.assert_array_equal(h1, h2)
+    np.testing.assert_array_equal(v1, v2)
+    # a deterministic render through the striped table == through one table
+    path = scenes.build_scene(scenes.SceneSpec("junkshop", 48, 32, tris_per_side=4), f"{scene_dir}/stripe")
+    s = load_scene(path)
+    one.clear()
+    for st in stripes:
+        st.clear()
+    cfg = RenderConfig(width=48, height=32, spp=4, cache_enabled=True, deterministic=True, n_cells=nc,
+                       n_entries=ne)
+    ra = render(s, cfg, external_cache=one, ctx=ctx)
+    rb = render(s, cfg, external_cache=stripes[0], ctx=ctx)
+    np.testing.assert_array_equal(bits(ra.frame.radiance), bits(rb.frame.radiance))
+    np.testing.assert_array_equal(ra.frame.nodes_found, rb.frame.nodes_found)
+    assert ra.stats.hits == rb.stats.hits > 0
+    words = one.slot_words().reshape(nc, ne)
+    for k, st in enumerate(stripes):
+        np.testing.assert_array_equal(st.slot_words().reshape(-1, ne), words[k::world])
+    # an unattached stripe refuses to run
+    lone = MaterialCache.stripe(nc, ne, 0, 2, ctx)
+    with pytest.raises(ValueError, match="attach"):
+        lone.lookup_batch(d[:4])

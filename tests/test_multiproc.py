@@ -80,3 +80,28 @@ def test_shard_masks_partition_the_image():
         for world in (1, 2, 3, 4, 8):
             cover = sum(D.shard_mask(1920, 1080, 16, r, world, mode).astype(int) for r in range(world))
             assert (cover == 1).all()
+
+
+def _handle_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = bytes([rank]) * 64          # stands for this rank's 64-byte CUDA IPC handle
+    got = D.exchange_handles(mine, world)
+    with open(os.path.join(out_dir, f"h{rank}.bin"), "wb") as f:
+        f.write(b"".join(got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shared_cache_handle_exchange(built):
+    """The shared (striped) table's set-up step on CPU: every rank ends with
+    every rank's stripe handle, in rank order (dist.shared_cache then maps
+    them with mcg_cache_attach_ipc)."""
+    out = tempfile.mkdtemp()
+    world = 3
+    mp.start_processes(_handle_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    want = b"".join(bytes([r]) * 64 for r in range(world))
+    for r in range(world):
+        with open(os.path.join(out, f"h{r}.bin"), "rb") as f:
+            assert f.read() == want
