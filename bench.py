@@ -362,6 +362,25 @@ def main() -> None:
                   "kernel": "k_probe_bench", "random_access_ceiling_gbs": 2900.0, "descriptors": n}
             pr.update(legs(table, PROBE_VARIANT, PROBE_BLOCKS_PER_SM))
             table.close()
+            # replay of the bench render's own lookups (first 2^26 of them)
+            traced = MaterialCache(N_CELLS, N_ENTRIES, ctx)
+            traced.trace_start(1 << 26)
+            pr_params = cfg.to_params()
+            st_t = N.RenderStats()
+            N.check(L.mcg_render_device(ctx.handle, C.byref(pr_params), traced.handle, C.byref(dframe),
+                                        C.byref(st_t)))
+            n_tr = traced.trace_stop()
+            trace = traced.trace_read(0, n_tr)
+            traced.close()
+            fresh = MaterialCache(N_CELLS, N_ENTRIES, ctx)
+            fresh.probe_replay(trace[: 1 << 20])          # warm-up
+            fresh.clear()
+            ms_r, b_r, c_r = fresh.probe_replay(trace)
+            fresh.close()
+            pr["trace_replay"] = {"descriptors": int(n_tr), "source": "the bench render's first lookups",
+                                  "achieved": b_r / ms_r / 1e6, "frac": b_r / ms_r / 1e6 / peak,
+                                  "mprobes_per_s": n_tr / ms_r / 1e3,
+                                  "hit_rate": c_r["hits"] / max(1, c_r["lookups"])}
             small = MaterialCache(100_000, N_ENTRIES, ctx)
             pr["l2_resident_1e5x10"] = legs(small, PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM)
             pr["l2_resident_1e5x10"]["table"] = "1e5x10 (8 MB, L2-resident)"

@@ -195,6 +195,19 @@ typedef struct mcg_audit_report {
 } mcg_audit_report;
 mcg_status mcg_audit_dump(const char* path, mcg_audit_report* out);
 
+/* Descriptor trace (SURVEY §8d "replay a descriptor trace dumped from a
+ * render"): while recording, every CacheLookup the VM makes through this
+ * table (renders, mcg_execute_batch) appends its descriptor, in lookup order
+ * (warp-aggregated), up to `capacity` records; stop returns the count kept.
+ * mcg_probe_replay runs a descriptor list (host) through the table as the VM
+ * would -- lookup, insert on a miss -- with the warp-cooperative probe, and
+ * returns the device time, the algorithmic bytes and the outcome counts. */
+mcg_status mcg_cache_trace_start(mcg_cache* cache, uint64_t capacity);
+mcg_status mcg_cache_trace_stop(mcg_cache* cache, uint64_t* recorded);
+mcg_status mcg_cache_trace_read(mcg_cache* cache, uint64_t first, size_t n, mcg_descriptor* out);
+mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t n, int32_t blocks_per_sm,
+                            double* ms, double* bytes, mcg_cache_counters* counters);
+
 /* Probe microbenchmark: n descriptors generated on the device
  * from `seed` (mat<8, node<256, mip<=16, texel uniform in 2^mip), then one
  * phase over them: 0 insert-all, 1 lookup-all, 2 50/50 mix; phase + 16*v

@@ -385,6 +385,32 @@ class MaterialCache:
     def dump(self, path: str) -> None:
         check(N.lib().mcg_cache_dump(self.handle, os.fsencode(path)))
 
+    # ---- descriptor trace ----
+    def trace_start(self, capacity: int) -> None:
+        """Record the descriptors of the lookups made through this table."""
+        check(N.lib().mcg_cache_trace_start(self.handle, int(capacity)))
+
+    def trace_stop(self) -> int:
+        out = C.c_uint64()
+        check(N.lib().mcg_cache_trace_stop(self.handle, C.byref(out)))
+        return int(out.value)
+
+    def trace_read(self, first: int = 0, n: Optional[int] = None, recorded: Optional[int] = None) -> np.ndarray:
+        n = (recorded if recorded is not None else 0) - first if n is None else n
+        out = np.zeros(max(0, n), DESC_DTYPE)
+        check(N.lib().mcg_cache_trace_read(self.handle, first, out.shape[0], _ptr(out)))
+        return out
+
+    def probe_replay(self, desc: np.ndarray, blocks_per_sm: int = 8):
+        """Lookup + insert-on-miss of `desc` in order; (ms, algorithmic bytes, counters)."""
+        desc = np.ascontiguousarray(desc, DESC_DTYPE)
+        ms, by = C.c_double(), C.c_double()
+        cc = N.CacheCounters()
+        check(N.lib().mcg_probe_replay(self.handle, _ptr(desc), desc.shape[0], blocks_per_sm, C.byref(ms),
+                                       C.byref(by), C.byref(cc)))
+        return ms.value, by.value, {"lookups": cc.lookups, "hits": cc.hits, "inserts_won": cc.inserts_won,
+                                    "inserts_lost_full": cc.inserts_lost_full}
+
     def probe_bench(self, n: int, seed: int, phase: int, iters: int = 1):
         ms, by = C.c_double(), C.c_double()
         check(N.lib().mcg_probe_bench(self.handle, n, seed, phase, iters, C.byref(ms), C.byref(by)))

@@ -129,6 +129,10 @@ _SIGS = [
     ("mcg_cache_stripe_info", C.c_int, [vp, P(u32), P(u32), P(u64)]),
     ("mcg_audit_dump", C.c_int, [C.c_char_p, P(AuditReport)]),
     ("mcg_probe_bench", C.c_int, [vp, u64, u64, i32, i32, P(f64), P(f64)]),
+    ("mcg_cache_trace_start", C.c_int, [vp, u64]),
+    ("mcg_cache_trace_stop", C.c_int, [vp, P(u64)]),
+    ("mcg_cache_trace_read", C.c_int, [vp, u64, C.c_size_t, vp]),
+    ("mcg_probe_replay", C.c_int, [vp, vp, u64, i32, P(f64), P(f64), P(CacheCounters)]),
     ("mcg_scene_load", C.c_int, [C.c_char_p, i32, P(vp)]),
     ("mcg_scene_destroy", C.c_int, [vp]),
     ("mcg_scene_flat", C.c_int, [vp, P(FlatScene)]),

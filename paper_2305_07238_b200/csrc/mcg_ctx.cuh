@@ -88,8 +88,14 @@ struct mcg_cache {
     uint64_t local_cells = 0;
     uint64_t** stripes = nullptr;
     std::vector<void*> ipc_opened;
+    // descriptor trace of the lookups made through this table (mcg_cache_trace_*)
+    uint32_t* trace = nullptr;
+    unsigned long long* trace_count = nullptr;
+    uint64_t trace_cap = 0;
     uint64_t local_words() const { return local_cells * n_entries; }
-    mcgd::CacheView view() const { return {slots, n_cells, magic, n_entries, world, stripes}; }
+    mcgd::CacheView view() const {
+        return {slots, n_cells, magic, n_entries, world, stripes, trace, trace_count, trace_cap};
+    }
 };
 
 struct mcg_ctx {

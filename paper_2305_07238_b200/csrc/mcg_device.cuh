@@ -23,6 +23,9 @@ struct CacheView {
     uint32_t n_entries;
     uint32_t world;           // > 1: one logical table striped by cell over `world` devices
     uint64_t* const* stripes; // device pointers of every stripe (peer memory over NVLink)
+    uint32_t* trace;          // optional descriptor log: 5 words per lookup (mcg_descriptor)
+    unsigned long long* trace_count;
+    uint64_t trace_cap;
 };
 
 // Words of the cell starting at logical slot `base` (= cell * n_entries). A
@@ -649,6 +652,21 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 pr.where = __shfl_sync(grp, pr.where, leader);
                 pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;
                 ++cnt.lookups;
+                if (C.trace) {
+                    // descriptor log (SURVEY §8d trace replay): warp-aggregated append
+                    const int ldr = __ffs(grp) - 1;
+                    unsigned long long at = 0;
+                    if (static_cast<int>(lane) == ldr) at = atomicAdd(C.trace_count, __popc(grp));
+                    at = __shfl_sync(grp, at, ldr) + __popc(grp & ((1u << lane) - 1u));
+                    if (at < C.trace_cap) {
+                        uint32_t* t = C.trace + 5 * at;
+                        t[0] = desc.mat;
+                        t[1] = desc.node;
+                        t[2] = desc.mip;
+                        t[3] = desc.tx;
+                        t[4] = desc.ty;
+                    }
+                }
                 p_where = pr.where;
                 if (pr.hit) {
                     const float3 v = decode_rgbe(pr.payload);

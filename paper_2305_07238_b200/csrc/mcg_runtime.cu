@@ -320,6 +320,37 @@ __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, ui
     mcgd::warp_add(counters + 5, inserts);
 }
 
+// Replay of a recorded descriptor trace: in trace order, each
+// warp takes 32 consecutive lookups, probes them cooperatively and inserts
+// the misses (payload from the hash), as the VM's lookup + store would.
+__global__ void __launch_bounds__(256) k_probe_replay(CacheView c, const mcg_descriptor* d, uint64_t n,
+                                                      unsigned long long* counters) {
+    uint32_t looks = 0, hits = 0, won = 0, full = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); i0 < n;
+         i0 += stride) {
+        const uint64_t i = i0 + (threadIdx.x & 31u);
+        const bool valid = i < n;
+        uint64_t h = 0;
+        uint32_t chk = 0;
+        if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
+        const uint64_t base = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries : 0;
+        const mcgd::Probe p = mcgd::probe_lanes(c, base, chk, valid);
+        if (!valid) continue;
+        ++looks;
+        hits += p.hit;
+        if (!p.hit) {
+            const int r = mcgd::insert_at(c, base, p.where, chk, static_cast<uint32_t>(h) | 0x80000000u);
+            won += r == MCG_INSERT_WON;
+            full += r == MCG_INSERT_CELL_FULL;
+        }
+    }
+    mcgd::warp_add(counters + 0, looks);
+    mcgd::warp_add(counters + 1, hits);
+    mcgd::warp_add(counters + 2, won);
+    mcgd::warp_add(counters + 3, full);
+}
+
 // Per-point VM execution for mcg_execute_batch: every lane runs the same slot.
 template <bool kDeferred>
 __global__ void k_execute(mcgd::SceneView S, CacheView C, int cache_on, int mip_offset,
@@ -777,6 +808,8 @@ mcg_status mcg_cache_destroy(mcg_cache* cache) {
     if (!cache) return MCG_OK;
     cudaStreamSynchronize(cache->ctx->stream);
     for (void* p : cache->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (cache->trace) cudaFree(cache->trace);
+    if (cache->trace_count) cudaFree(cache->trace_count);
     if (cache->stripes) cudaFree(cache->stripes);
     cudaFree(cache->slots);
     cudaFree(cache->counters);
@@ -1070,6 +1103,86 @@ mcg_status mcg_cache_dump(mcg_cache* cache, const char* path) {
     });
 }
 
+mcg_status mcg_cache_trace_start(mcg_cache* cache, uint64_t capacity) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        need(capacity > 0 && capacity < (1ull << 34), "trace capacity out of range");
+        if (cache->trace) cudaFree(cache->trace);
+        cache->trace = nullptr;
+        cache->trace_cap = 0;
+        cuda_check(cudaMalloc(&cache->trace, capacity * 20), "cudaMalloc(trace)");
+        if (!cache->trace_count) cuda_check(cudaMalloc(&cache->trace_count, 8), "cudaMalloc(trace count)");
+        cuda_check(cudaMemsetAsync(cache->trace_count, 0, 8, cache->ctx->stream), "memset");
+        cache->trace_cap = capacity;
+        sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_cache_trace_stop(mcg_cache* cache, uint64_t* recorded) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        unsigned long long v = 0;
+        if (cache->trace_count) {
+            dev_download(cache->ctx, &v, cache->trace_count, 1);
+            sync(cache->ctx);
+        }
+        if (recorded) *recorded = std::min<uint64_t>(v, cache->trace_cap);
+        cache->trace_cap = 0;   // recording off; the buffer stays readable
+    });
+}
+
+mcg_status mcg_cache_trace_read(mcg_cache* cache, uint64_t first, size_t n, mcg_descriptor* out) {
+    return guarded([&] {
+        need(cache && out, "null argument");
+        need(cache->trace != nullptr, "no trace recorded");
+        unsigned long long v = 0;
+        dev_download(cache->ctx, &v, cache->trace_count, 1);
+        sync(cache->ctx);
+        need(first + n <= v, "trace range out of bounds");
+        if (!n) return;
+        dev_download(cache->ctx, reinterpret_cast<uint32_t*>(out), cache->trace + 5 * first, 5 * n);
+        sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t n, int32_t blocks_per_sm,
+                            double* ms_out, double* bytes_out, mcg_cache_counters* counters) {
+    return guarded([&] {
+        need(cache && d, "null argument");
+        need(cache->world == 1 || cache->stripes, "striped table: attach the stripes first");
+        if (!n) return;
+        mcg_ctx* ctx = cache->ctx;
+        auto* dd = dev_upload(ctx, ctx->scratch_a, d, n);
+        cudaEvent_t a = take_event(ctx), b = take_event(ctx);
+        cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long), ctx->stream), "memset");
+        cudaEventRecord(a, ctx->stream);
+        {
+            LaunchScope ls(ctx, "probe_replay", 0.0);
+            const unsigned grid = 148u * static_cast<unsigned>(blocks_per_sm > 0 ? blocks_per_sm : 8);
+            k_probe_replay<<<grid, 256, 0, ctx->stream>>>(cache->view(), dd, n, cache->counters);
+            ls.done();
+        }
+        cudaEventRecord(b, ctx->stream);
+        cuda_check(cudaEventSynchronize(b), "probe replay");
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        ctx->event_pool.push_back(a);
+        ctx->event_pool.push_back(b);
+        unsigned long long v[8];
+        dev_download(ctx, v, cache->counters, 8);
+        sync(ctx);
+        if (ms_out) *ms_out = ms;
+        // 8*Ne per lookup, 8*Ne per insert attempt (the miss's scan is the lookup's), +8 per won CAS
+        if (bytes_out) *bytes_out = static_cast<double>(v[0]) * 8.0 * cache->n_entries + static_cast<double>(v[2]) * 8.0;
+        if (counters) {
+            counters->lookups = v[0];
+            counters->hits = v[1];
+            counters->inserts_won = v[2];
+            counters->inserts_lost_full = v[3];
+        }
+    });
+}
+
 mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t phase,
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
@@ -1278,7 +1391,7 @@ mcg_status mcg_execute_batch(mcg_ctx* ctx, uint32_t slot, const float* sp, size_
         const int max_stack = static_cast<int>(ctx->scene.max_stack);
         const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
         if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
-        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, nullptr};
+        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, nullptr, nullptr, nullptr, 0};
         unsigned long long* counters = cache ? cache->counters : ctx->stats_mem.as<unsigned long long>();
         mcgd::StoreQueue q{nullptr, nullptr, nullptr, 0};
         const uint64_t cap = deferred ? n * std::max<uint32_t>(1, ctx->scene.max_cache_points) : 0;

@@ -47,3 +47,36 @@ def test_render_artifacts(ctx, scene_dir, tmp_path):
     # pixels with no hits map to viridis(0)
     zero = on.frame.nodes_found_avg() == 0
     assert (heat[zero] == artifacts.viridis(0.0)).all()
+
+
+def test_descriptor_trace_and_replay(ctx, scene_dir):
+    """the lookups of a render are recorded in order and replayed
+    through a fresh table (lookup, insert on a miss)."""
+    from paper_2305_07238_b200 import MaterialCache
+    path = scenes.build_scene(scenes.SceneSpec("classroom", 48, 32, tris_per_side=4), f"{scene_dir}/trace")
+    s = load_scene(path)
+    t = MaterialCache(4099, 4, ctx)
+    t.trace_start(1 << 20)
+    res = render(s, RenderConfig(width=48, height=32, spp=8, cache_enabled=True, n_cells=4099, n_entries=4),
+                 external_cache=t, ctx=ctx)
+    n = t.trace_stop()
+    assert n == res.stats.lookups > 0
+    tr = t.trace_read(0, n)
+    assert (tr["mip_level"] <= 24).all() and (tr["mat_idx"] < s.n_materials).all()
+    assert (tr["texel_x"] < (1 << tr["mip_level"].astype(np.uint64))).all()
+    fresh = MaterialCache(4099, 4, ctx)
+    ms, nbytes, c = fresh.probe_replay(tr)
+    assert c["lookups"] == n and ms > 0 and nbytes >= n * 32
+    keys = {tuple(x) for x in tr[["mat_idx", "node_idx", "mip_level", "texel_x", "texel_y"]].tolist()}
+    assert c["inserts_won"] + c["inserts_lost_full"] >= len(keys) - (n - c["hits"] - c["inserts_won"]
+                                                                     - c["inserts_lost_full"])
+    assert c["hits"] + c["inserts_won"] + c["inserts_lost_full"] <= n
+    # the replayed table answers every traced key that found room
+    hit, _ = fresh.lookup_batch(tr)
+    assert hit.mean() > 0.9
+    # a small capacity keeps the first records only
+    t.clear()
+    t.trace_start(100)
+    render(s, RenderConfig(width=48, height=32, spp=2, cache_enabled=True, n_cells=4099, n_entries=4),
+           external_cache=t, ctx=ctx)
+    assert t.trace_stop() == 100
