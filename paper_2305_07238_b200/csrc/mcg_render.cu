@@ -1730,7 +1730,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
 
     uint32_t k = P.samples_per_pass > 0 ? static_cast<uint32_t>(P.samples_per_pass) : 0;
     if (k == 0) {
-        const uint64_t target = 1u << 21;  // ~2M paths in flight fill 148 SMs
+        // ~4M paths in flight (measured: 1M 866 ms, 2M 773, 4M 751, 8M 769 per
+        // bench render); MCG_PASS_PATHS overrides (experiments)
+        const char* pp_env = std::getenv("MCG_PASS_PATHS");
+        const uint64_t target = pp_env ? std::max<uint64_t>(1, std::strtoull(pp_env, nullptr, 10)) : (1u << 22);
         k = static_cast<uint32_t>(std::max<uint64_t>(1, (target + n_pix - 1) / std::max<uint32_t>(n_pix, 1)));
     }
     k = std::min<uint32_t>(std::min<uint32_t>(k, 32u), static_cast<uint32_t>(P.spp));
