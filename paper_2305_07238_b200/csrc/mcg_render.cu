@@ -1617,6 +1617,10 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     const unsigned grp = __match_any_sync(live, slot);
     const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
     const uint32_t pid = R.pid[q];
+    // the rest of the path's state is loaded now, in the same round trip as
+    // the shading record, not after the VM
+    float4 thr = R.thr[q];
+    const float4 Lq = R.L[q], ro = R.ro[q];
     const mcgd::ShadeIn in{s0.x, s0.y, s0.z, s1.x, s1.y, s1.z, rd.x, rd.y, rd.z,
                            s0.w, s1.w, s2.x, s2.y, s2.z, s2.w};
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
@@ -1627,11 +1631,10 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     mcgd::VmCounters cnt;
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt);
-    float4 thr = R.thr[q];
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
-    R.L2[i] = R.L[q];
+    R.L2[i] = Lq;
     R.pid2[i] = pid;
-    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, R.ro[q], rd);
+    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, ro, rd);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
     mcgd::warp_add(R.stats + kStatWon, cnt.won);
