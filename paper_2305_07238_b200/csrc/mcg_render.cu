@@ -1134,7 +1134,10 @@ __device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, const float4*
 // leaves): speculative while-while like any_ww4s; of the entries a node
 // passes, the nearest stays in registers (popped next), the rest go to the
 // stack in entry order -- any order is exact for a boolean query.
-template <int kW>
+#ifndef MCG_SHADOW_LEAVES
+#define MCG_SHADOW_LEAVES 1
+#endif
+template <int kW, int kLeaves = MCG_SHADOW_LEAVES>
 __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t root_b, const mcgd::SceneView& S,
                                         bool active, V3 o, V3 d, float tmin, float tmax,
                                         uint32_t& nodes_visited, uint32_t& prims_tested) {
@@ -1153,8 +1156,8 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
         }
     }
     bool hit = false;
-    int32_t lc = 0;
-    bool leaf = false;
+    int32_t lc = 0, lc2 = 0;
+    bool leaf = false, leaf2 = false;
     while (__any_sync(mcgd::kFull, has_n || leaf)) {
         for (;;) {
             if (has_n) {
@@ -1163,6 +1166,11 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
                         ++nodes_visited;
                         leaf = true;
                         lc = nc;
+                        has_n = false;
+                    } else if (kLeaves > 1 && !leaf2) {
+                        ++nodes_visited;
+                        leaf2 = true;
+                        lc2 = nc;
                         has_n = false;
                     }
                 } else {
@@ -1201,17 +1209,22 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
             if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
         }
         if (leaf) {
-            const uint32_t v = static_cast<uint32_t>(~lc);
-            const uint32_t first = v >> 3, cnt = v & 7u;
-            prims_tested += cnt;
-            for (uint32_t i = first; i < first + cnt; ++i) {
-                float t, b1, b2;
-                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
-                    hit = true;
-                    break;
+#pragma unroll
+            for (int l = 0; l < kLeaves; ++l) {
+                if (l == 1 && (!leaf2 || hit)) break;
+                const uint32_t v = static_cast<uint32_t>(~(l == 0 ? lc : lc2));
+                const uint32_t first = v >> 3, cnt = v & 7u;
+                prims_tested += cnt;
+                for (uint32_t i = first; i < first + cnt; ++i) {
+                    float t, b1, b2;
+                    if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
+                        hit = true;
+                        break;
+                    }
                 }
             }
             leaf = false;
+            leaf2 = false;
             if (hit) has_n = false, top = 0;
         }
     }
