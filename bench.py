@@ -451,8 +451,17 @@ def main() -> None:
             traffic_ncu = {k: v for k, v in json.load(fh).items() if not k.startswith("_")}
     except Exception:
         traffic_ncu = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_efficiency.json")) as fh:
+            eff = json.load(fh)
+    except Exception:
+        eff = {}
     dname = max(ktimes.items(), key=lambda kv: kv[1]["ms"])[0] if ktimes else "?"
     roof = kernel_roofline(dname)
+    if dname in eff:
+        # what does bound it (ncu, profiles/r1_ncu_h.txt): issue slots and SIMT
+        # efficiency, not HBM bandwidth
+        roof["issue"] = eff[dname]
     roof["limiter"] = ("issue/latency: warp divergence in BVH traversal (L1/L2-resident tree); "
                        "HBM is not the bound -- see profiles/README.md"
                        if dname.startswith("trace") else "random HBM access (cache probes)")
@@ -462,6 +471,14 @@ def main() -> None:
     roof["kernel_share"] = shares
     # The north-star kernel (material VM + cache probes) beside it.
     roof_shade = kernel_roofline("shade")
+    if "shade" in eff:
+        roof_shade["issue"] = eff["shade"]
+    # Render-level: the shade and traversal kernels' compulsory
+    # bytes over the whole step time.
+    total_bytes = sum(compulsory.values())
+    roof["render_level"] = {"compulsory_bytes_per_step": total_bytes / max(1, steps),
+                            "achieved": total_bytes / (ms / 1e3) / 1e9,
+                            "frac": total_bytes / (ms / 1e3) / 1e9 / peak}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
