@@ -106,9 +106,10 @@ __device__ __forceinline__ uint32_t dim_rect(int b, int j, int k) { return 2u + 
 __device__ __forceinline__ uint32_t dim_bounce(int b, int k) { return 2u + 64u * b + 62u + k; }
 
 // Sort key of a hit: material slot in the high bits (shading stays grouped by
-// material), the 24-bit Morton code of the hit point below it, so rays that
-// leave nearby points on one material -- the next bounce's closest-hit rays
-// and the shadow rays -- share warps and traverse the same BVH nodes.
+// material), then the octant of the bounce the vertex will take, then the
+// Morton code of the hit point, so rays that leave nearby points in similar
+// directions -- the next closest-hit rays, and the shadow rays -- share warps
+// and traverse the same BVH nodes.
 __device__ __forceinline__ uint32_t spread8(uint32_t v) {
     v &= 0xffu;
     v = (v | (v << 8)) & 0x0300f00fu;
@@ -126,6 +127,30 @@ __device__ __forceinline__ uint32_t sort_key(const RenderView& R, uint32_t slot,
     for (int k = 0; k < 3; ++k) c[k] = static_cast<uint32_t>(fminf(fmaxf(q[k], 0.0f), 255.0f));
     if (!R.key_dir) {
         return (slot << R.key_shift) | spread8(c[0]) | (spread8(c[1]) << 1) | (spread8(c[2]) << 2);
+    }
+    if (R.key_dir == 2u) {
+        // Octant of the cosine bounce this vertex will take (the formula of
+        // nee_bounce with fast intrinsics -- a grouping heuristic only) above
+        // the Morton code: the next closest-hit rays of a warp leave nearby
+        // points in similar directions.
+        uint32_t oct = 0u;
+        if (vtx < R.max_bounces) {
+            const float r1 = mcgd::path_sample(rkey, dim_bounce(vtx, 0));
+            const float r2 = mcgd::path_sample(rkey, dim_bounce(vtx, 1));
+            float sphi, cphi;
+            __sincosf(r1 * mcgd::kTwoPi, &sphi, &cphi);
+            const float r = sqrtf(r2);
+            const float lx = r * cphi, ly = r * sphi, lz = sqrtf(fmaxf(0.0f, 1.0f - r2));
+            const float sign = copysignf(1.0f, n.z);
+            const float a = -1.0f / (sign + n.z);
+            const float bb = (n.x * n.y) * a;
+            const V3 t{1.0f + ((sign * n.x) * n.x) * a, sign * bb, -sign * n.x};
+            const V3 bt{bb, sign + ((n.y * n.y) * a), -n.y};
+            const V3 dv = (t * lx + bt * ly) + n * lz;
+            oct = (dv.x < 0.0f ? 1u : 0u) | (dv.y < 0.0f ? 2u : 0u) | (dv.z < 0.0f ? 4u : 0u);
+        }
+        const uint32_t mbits = R.key_shift - 3u;
+        return (slot << R.key_shift) | (oct << mbits) | spread8(c[0]) | (spread8(c[1]) << 1) | (spread8(c[2]) << 2);
     }
     // Direction class of the cosine bounce this vertex will take: the
     // normal's octant and the quadrant of its azimuth sample (dims of
@@ -1888,19 +1913,27 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         R.q.count = reinterpret_cast<unsigned int*>(R.q.keys + 4 * cap);
         R.q.capacity = static_cast<unsigned>(cap);
     }
-    // Sort key: slot << key_shift | Morton code of the hit point
-    // (MCG_SORT=material: slot only).
+    // Sort key (MCG_SORT): "dir3" (default) = slot | octant of the vertex's
+    // bounce direction | Morton code of the hit point on a 2^6 grid (23 bits
+    // with <= 4 slots: 3 radix passes); "morton" = slot | Morton 2^7;
+    // "dir" = slot | normal octant + azimuth quadrant | Morton 2^6;
+    // "material" = slot only. Measured per bench render (profiles/README.md):
+    // dir3 716 ms, morton 741, dir 733, material 1383 (older build).
     const char* sort_env = std::getenv("MCG_SORT");
-    const bool morton = !(sort_env && std::string(sort_env) == "material");
+    const std::string sort_mode = sort_env ? std::string(sort_env) : std::string("dir3");
+    const bool morton = sort_mode != "material";
     const int slot_bits = std::max(1, bits_for(D.view.n_programs));
-    // Morton grid: 2^b cells per axis (MCG_MORTON_BITS = b, 1..8). b = 7
-    // keeps the key within 3 radix passes for up to 4 material slots and
-    // measured best (profiles/README.md: 8 -> 808 ms, 7 -> 799, 6 -> 801).
-    const char* mb_env = std::getenv("MCG_MORTON_BITS");
-    const int mb = mb_env ? std::min(8, std::max(1, std::atoi(mb_env))) : 7;
+    const char* mb_env = std::getenv("MCG_MORTON_BITS");   // 2^b cells per axis
+    const int mb = mb_env ? std::min(8, std::max(1, std::atoi(mb_env))) : (sort_mode == "morton" ? 7 : 6);
     R.key_shift = (morton && slot_bits <= 8) ? static_cast<uint32_t>(3 * mb) : 0u;
-    R.key_dir = (sort_env && std::string(sort_env) == "dir") ? 1u : 0u;
-    if (R.key_dir) R.key_shift = 24u;  // the direction-class key keeps its 24-bit layout
+    R.key_dir = 0u;
+    if (R.key_shift && sort_mode == "dir") {
+        R.key_dir = 1u;
+        R.key_shift = 24u;  // the direction-class key keeps its 24-bit layout
+    } else if (R.key_shift && sort_mode == "dir3") {
+        R.key_dir = 2u;
+        R.key_shift = static_cast<uint32_t>(3 * mb + 3);
+    }
     for (int a = 0; a < 3; ++a) {
         const float ext = D.root_hi[a] - D.root_lo[a];
         R.box_lo[a] = D.root_lo[a];
