@@ -165,7 +165,9 @@ mcg_status mcg_cache_counters_get(mcg_cache* cache, mcg_cache_counters* out);
 mcg_status mcg_cache_counters_reset(mcg_cache* cache);
 /* dump (cache.cpp:159-173): u64 n_cells, u64 n_entries, then every slot word, LE. */
 mcg_status mcg_cache_dump(mcg_cache* cache, const char* path);
-/* Device pointer of the slot array (n_cells*n_entries u64), for tooling. */
+/* Device pointer of the slot array, for tooling: cell c's n_entries words
+ * start at word c * n_entries (builds with MCG_CELL_PITCH_SECTORS pad cells to
+ * whole 32-byte sectors; slot indices in this API stay c * n_entries + e). */
 uint64_t* mcg_cache_device_slots(mcg_cache* cache);
 
 /* Striped shared table (one logical Nc x Ne table over `world`

@@ -17,10 +17,11 @@ constexpr unsigned kFull = 0xffffffffu;
 // Table view
 // ---------------------------------------------------------------------------
 struct CacheView {
-    uint64_t* slots;          // n_cells * n_entries words, cell-major (cache.cpp:159 dump order)
+    uint64_t* slots;          // cell-major, `stride` words per cell (n_entries used, the rest zero)
     uint64_t n_cells;
     uint64_t magic;           // floor((2^64-1) / n_cells) for fast_mod
     uint32_t n_entries;
+    uint32_t stride;          // words per cell in memory: n_entries rounded so cells start on 32-byte sectors
     uint32_t world;           // > 1: one logical table striped by cell over `world` devices
     uint64_t* const* stripes; // device pointers of every stripe (peer memory over NVLink)
     uint32_t* trace;          // optional descriptor log: 5 words per lookup (mcg_descriptor)
@@ -28,13 +29,14 @@ struct CacheView {
     uint64_t trace_cap;
 };
 
-// Words of the cell starting at logical slot `base` (= cell * n_entries). A
-// striped table keeps cell c on stripe c % world at local cell c / world, so
+// The words of cell `cell`. Cells are laid out `stride` words apart (80-byte
+// cells at 96-byte pitch: a cell is exactly three 32-byte DRAM sectors instead
+// of three or four); slot indices stay the logical cell * n_entries + entry.
+// A striped table keeps cell c on stripe c % world at local cell c / world, so
 // every device sees the same logical table.
-__device__ __forceinline__ uint64_t* cell_words(const CacheView& c, uint64_t base) {
-    if (c.world <= 1u) return c.slots + base;
-    const uint64_t cell = base / c.n_entries;
-    return c.stripes[cell % c.world] + (cell / c.world) * c.n_entries;
+__device__ __forceinline__ uint64_t* cell_words(const CacheView& c, uint64_t cell) {
+    if (c.world <= 1u) return c.slots + cell * c.stride;
+    return c.stripes[cell % c.world] + (cell / c.world) * c.stride;
 }
 
 // Result of scanning one cell as lookup() does (cache.cpp:121-136): a match,
@@ -70,12 +72,12 @@ __device__ __forceinline__ bool scan_word(uint64_t w, int32_t idx, uint32_t chec
 // (ld.global.cg) so concurrent inserts from other SMs are seen as soon as L2
 // sees them.
 template <int kFirstPairs>
-__device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t base, uint32_t check) {
+__device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t cell_index, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
-    const uint64_t* cell = cell_words(c, base);
+    const uint64_t* cell = cell_words(c, cell_index);
     uint32_t i = 0;
-    if ((base & 1ull) == 0ull && ne >= 2 && ne <= 10) {
+    if ((reinterpret_cast<uintptr_t>(cell) & 15u) == 0u && ne >= 2 && ne <= 10) {
         const uint32_t npairs = ne >> 1;
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
         ulonglong2 w[5];
@@ -102,8 +104,8 @@ __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t base,
     return r;  // full, no match
 }
 
-__device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, uint32_t check) {
-    return probe_cell_t<1>(c, base, check);
+__device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t cell, uint32_t check) {
+    return probe_cell_t<1>(c, cell, check);
 }
 
 // Two-round scan aligned to 64-byte DRAM blocks: round one reads from the
@@ -111,11 +113,11 @@ __device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t base, u
 // round two the rest of the cell (at most one more block for Ne <= 10). A
 // scan that ends in round one costs one block; a full scan two -- never the
 // three blocks an 80-byte cell can straddle.
-__device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t base, uint32_t check) {
+__device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t cell_index, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
-    const uint64_t* cell = cell_words(c, base);
-    if ((base & 1ull) != 0ull || ne > 10) return probe_cell_t<1>(c, base, check);
+    const uint64_t* cell = cell_words(c, cell_index);
+    if ((reinterpret_cast<uintptr_t>(cell) & 15u) != 0u || ne > 10) return probe_cell_t<1>(c, cell_index, check);
     const uint32_t npairs = ne >> 1;
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
     // pairs in the first 64-byte block: (64 - (addr % 64)) / 16
@@ -152,7 +154,7 @@ __device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t bas
 // before any decision; per cell, ballots over its lanes give the first empty
 // slot and the first matching check-hash, i.e. the reference scan.
 template <int kNe>
-__device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, uint32_t check,
+__device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t cell, uint32_t check,
                                             bool valid) {
     constexpr int kPer = 32 / kNe;
     constexpr int kRounds = (32 + kPer - 1) / kPer;
@@ -162,9 +164,9 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, u
 #pragma unroll
     for (int rd = 0; rd < kRounds; ++rd) {
         const int owner = rd * kPer + g;
-        const uint64_t ob = __shfl_sync(kFull, base, owner & 31);
+        const uint64_t oc = __shfl_sync(kFull, cell, owner & 31);
         const bool ov = __shfl_sync(kFull, valid, owner & 31);
-        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(cell_words(c, ob) + word) : ~0ull;
+        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(cell_words(c, oc) + word) : ~0ull;
     }
     Probe mine{0u, -1, false};
 #pragma unroll
@@ -204,7 +206,7 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t base, u
 // 16-byte pair that ends the reference's linear scan (an empty slot or the
 // matching check hash, cache.cpp:127-134), and the descriptor's lane reads the
 // outcome from the deciding lane. Every lane of the warp must call it.
-__device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base, uint32_t check,
+__device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell, uint32_t check,
                                               bool valid) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lpc = c.n_entries >> 1;   // lanes (pairs) per cell
@@ -219,11 +221,11 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base,
         chk[r] = 0u;
         if (static_cast<uint32_t>(r) < rounds) {
             const uint32_t owner = static_cast<uint32_t>(r) * cpr + g;
-            const uint64_t ob = __shfl_sync(kFull, base, owner & 31u);
+            const uint64_t oc = __shfl_sync(kFull, cell, owner & 31u);
             const bool ov = __shfl_sync(kFull, valid, owner & 31u);
             chk[r] = __shfl_sync(kFull, check, owner & 31u);
             if (g < cpr && owner < 32u && ov) {
-                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, ob)) + k);
+                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, oc)) + k);
             }
         }
     }
@@ -267,7 +269,7 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t base,
 // the first decision, as in probe_warp16. Falls back to per-lane scans by the
 // leaders when the group is too small or has too many cells. Every lane of
 // `grp` must call it; only leaders' results are meaningful.
-__device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base, uint32_t check,
+__device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell, uint32_t check,
                                               bool leader, unsigned grp) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned L = __ballot_sync(grp, leader);
@@ -276,7 +278,7 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base
     const uint32_t cpr = lpc ? nW / lpc : 0u;
     const uint32_t rounds = cpr ? (nL + cpr - 1u) / cpr : 99u;
     if ((c.n_entries & 1u) != 0u || c.n_entries > 10u || cpr == 0u || rounds > 6u) {
-        return leader ? probe_cell(c, base, check) : Probe{0u, -1, false};
+        return leader ? probe_cell(c, cell, check) : Probe{0u, -1, false};
     }
     const unsigned below = (1u << lane) - 1u;
     const uint32_t rank = __popc(grp & below);
@@ -289,8 +291,8 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base
             const uint32_t j = static_cast<uint32_t>(r) * cpr + g;
             const bool work = g < cpr && j < nL;
             const uint32_t owner = work ? __fns(L, 0u, static_cast<int>(j) + 1) : lane;
-            const uint64_t ob = __shfl_sync(grp, base, owner);
-            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, ob)) + k);
+            const uint64_t oc = __shfl_sync(grp, cell, owner);
+            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, oc)) + k);
         }
     }
     Probe mine{0u, -1, false};
@@ -342,20 +344,20 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t base
 // The warp's probes: the cooperative one-round-trip scan where the cell
 // shape allows it (Ne even, <= 10), else the per-lane scan. Warp-collective:
 // every lane of the warp calls it (invalid lanes with valid = false).
-__device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t base, uint32_t check,
+__device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t cell, uint32_t check,
                                              bool valid) {
-    if ((c.n_entries & 1u) == 0u && c.n_entries <= 10u) return probe_warp16(c, base, check, valid);
-    return valid ? probe_cell(c, base, check) : Probe{0u, -1, false};
+    if ((c.n_entries & 1u) == 0u && c.n_entries <= 10u) return probe_warp16(c, cell, check, valid);
+    return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
 }
 
 // One CAS from zero on the slot the scan found empty (cache.cpp:108-114).
 // Returns MCG_INSERT_WON / LOST_RACE / CELL_FULL.
-__device__ __forceinline__ int insert_at(const CacheView& c, uint64_t base, int32_t where,
+__device__ __forceinline__ int insert_at(const CacheView& c, uint64_t cell, int32_t where,
                                          uint32_t check, uint32_t payload) {
     if (where < 0) return MCG_INSERT_CELL_FULL;
     const unsigned long long packed = (static_cast<unsigned long long>(check) << 32) | payload;
     const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long*>(cell_words(c, base) + where), 0ull, packed);
+        atomicCAS(reinterpret_cast<unsigned long long*>(cell_words(c, cell) + where), 0ull, packed);
     return prev == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
 }
 
@@ -476,7 +478,6 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
     const unsigned lane = threadIdx.x & 31u;
     bool parked = false;
     int resume = -1;
-    uint64_t p_base = 0;
     uint32_t p_check = 0;
     int32_t p_where = -1;
     unsigned long long p_cell = 0;
@@ -633,7 +634,6 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 uint64_t h;
                 hash_desc(desc, h, p_check);
                 const uint64_t cell = fast_mod(h, C.n_cells, C.magic);
-                p_base = cell * C.n_entries;
                 p_cell = cell;
                 // Lanes asking for the same (cell, check) share one probe.
                 const unsigned long long key = (cell << 32) ^ p_check;
@@ -643,10 +643,10 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 // cooperative scan by the group (measured slower in the VM:
                 // 115 vs 96 registers, and few leaders per warp after the
                 // Morton sort -- profiles/README.md)
-                Probe pr = probe_group16(C, p_base, p_check, static_cast<int>(lane) == leader, grp);
+                Probe pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, grp);
 #else
                 Probe pr{0u, -1, false};
-                if (static_cast<int>(lane) == leader) pr = probe_cell(C, p_base, p_check);
+                if (static_cast<int>(lane) == leader) pr = probe_cell(C, p_cell, p_check);
 #endif
                 pr.payload = __shfl_sync(grp, pr.payload, leader);
                 pr.where = __shfl_sync(grp, pr.where, leader);
@@ -712,7 +712,7 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                         const int leader = __ffs(peers) - 1;
                         int res = MCG_INSERT_ALREADY_PRESENT;
                         if (static_cast<int>(lane) == leader) {
-                            res = insert_at(C, p_base, p_where, p_check, payload);
+                            res = insert_at(C, p_cell, p_where, p_check, payload);
                         } else if (p_where < 0) {
                             res = MCG_INSERT_CELL_FULL;
                         }

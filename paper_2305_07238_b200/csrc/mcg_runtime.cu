@@ -140,7 +140,7 @@ __global__ void k_lookup(CacheView c, const mcg_descriptor* d, size_t n, uint8_t
     uint32_t chk = 0;
     if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
     const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
-    const mcgd::Probe p = mcgd::probe_lanes(c, cell * c.n_entries, chk, valid);
+    const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
     uint32_t hits = 0, looks = 0;
     if (valid) {
         looks = 1;
@@ -166,8 +166,9 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
     uint64_t h = 0;
     uint32_t chk = 0;
     if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
-    const uint64_t base = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries : 0;
-    const mcgd::Probe p = mcgd::probe_lanes(c, base, chk, valid);
+    const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
+    const uint64_t base = cell * c.n_entries;   // logical slot index of the cell
+    const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
     uint32_t won = 0, full = 0, lost = 0;
     if (valid) {
         int res;
@@ -178,7 +179,7 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
             packed = (static_cast<uint64_t>(chk) << 32) | p.payload;
         } else {
             const uint32_t payload = mcgd::encode_rgbe(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
-            res = mcgd::insert_at(c, base, p.where, chk, payload);
+            res = mcgd::insert_at(c, cell, p.where, chk, payload);
             if (res != MCG_INSERT_CELL_FULL) {
                 slot = base + p.where;
                 packed = (static_cast<uint64_t>(chk) << 32) | payload;
@@ -221,7 +222,7 @@ __global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
     if (i < n) {
         const uint64_t cell = keys[i] >> ob;
         if (i == 0 || (keys[i - 1] >> ob) != cell) {
-            uint64_t* words = mcgd::cell_words(c, cell * c.n_entries);
+            uint64_t* words = mcgd::cell_words(c, cell);
             const unsigned long long omask = ob >= 64 ? ~0ull : ((1ull << ob) - 1ull);
             for (size_t j = i; j < n && (keys[j] >> ob) == cell; ++j) {
                 const uint32_t chk = static_cast<uint32_t>(vals[j] >> 32);
@@ -291,13 +292,13 @@ __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, ui
         uint64_t h;
         uint32_t chk;
         mcgd::hash_desc(bench_desc(seed, i), h, chk);
-        const uint64_t base = mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries;
+        const uint64_t cell = mcgd::fast_mod(h, c.n_cells, c.magic);
         mcgd::Probe p;
-        if (kVariant == 4) p = mcgd::probe_warp16(c, base, chk, valid);
-        else if (kVariant == 2) p = mcgd::probe_warp<10>(c, base, chk, valid);
-        else if (kVariant == 1) p = valid ? mcgd::probe_cell_t<5>(c, base, chk) : mcgd::Probe{0u, -1, false};
-        else if (kVariant == 3) p = valid ? mcgd::probe_cell_blk(c, base, chk) : mcgd::Probe{0u, -1, false};
-        else p = valid ? mcgd::probe_cell_t<1>(c, base, chk) : mcgd::Probe{0u, -1, false};
+        if (kVariant == 4) p = mcgd::probe_warp16(c, cell, chk, valid);
+        else if (kVariant == 2) p = mcgd::probe_warp<10>(c, cell, chk, valid);
+        else if (kVariant == 1) p = valid ? mcgd::probe_cell_t<5>(c, cell, chk) : mcgd::Probe{0u, -1, false};
+        else if (kVariant == 3) p = valid ? mcgd::probe_cell_blk(c, cell, chk) : mcgd::Probe{0u, -1, false};
+        else p = valid ? mcgd::probe_cell_t<1>(c, cell, chk) : mcgd::Probe{0u, -1, false};
         if (!valid) continue;
         const bool insert = phase == 0 || (phase == 2 && (i & 1u));
         if (!insert) {
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, ui
         } else {
             ++inserts;
             if (!p.hit) {
-                const int r = mcgd::insert_at(c, base, p.where, chk,
+                const int r = mcgd::insert_at(c, cell, p.where, chk,
                                               static_cast<uint32_t>(h) | 0x80000000u);
                 won += r == MCG_INSERT_WON;
                 full += r == MCG_INSERT_CELL_FULL;
@@ -334,13 +335,13 @@ __global__ void __launch_bounds__(256) k_probe_replay(CacheView c, const mcg_des
         uint64_t h = 0;
         uint32_t chk = 0;
         if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
-        const uint64_t base = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) * c.n_entries : 0;
-        const mcgd::Probe p = mcgd::probe_lanes(c, base, chk, valid);
+        const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
+        const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
         if (!valid) continue;
         ++looks;
         hits += p.hit;
         if (!p.hit) {
-            const int r = mcgd::insert_at(c, base, p.where, chk, static_cast<uint32_t>(h) | 0x80000000u);
+            const int r = mcgd::insert_at(c, cell, p.where, chk, static_cast<uint32_t>(h) | 0x80000000u);
             won += r == MCG_INSERT_WON;
             full += r == MCG_INSERT_CELL_FULL;
         }
@@ -788,8 +789,10 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
         c->ctx = ctx;
         c->n_cells = n_cells;
         c->n_entries = n_entries;
+        c->stride = cell_pitch(n_entries);
         c->magic = mod_magic(n_cells);
         c->local_cells = n_cells;
+        bytes = c->local_phys_words() * 8;
         cudaError_t e = cudaMalloc(&c->slots, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -802,6 +805,24 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
         sync(ctx);
         *out = c;
     });
+}
+
+// Logical slots [first, first + n) of this object's cells (cell-major,
+// n_entries per cell: the reference's dump order) from the padded layout.
+static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* out) {
+    mcg_ctx* ctx = cache->ctx;
+    const uint32_t ne = cache->n_entries, pitch = cache->stride;
+    if (pitch == ne) {
+        dev_download(ctx, out, cache->slots + first, n);
+        sync(ctx);
+        return;
+    }
+    const uint64_t c0 = first / ne, c1 = (first + n + ne - 1) / ne;
+    std::vector<uint64_t> tmp((c1 - c0) * ne);
+    cuda_check(cudaMemcpy2DAsync(tmp.data(), ne * 8ull, cache->slots + c0 * pitch, pitch * 8ull, ne * 8ull,
+                                 c1 - c0, cudaMemcpyDeviceToHost, ctx->stream), "D2H cells");
+    sync(ctx);
+    std::memcpy(out, tmp.data() + (first - c0 * ne), n * 8);
 }
 
 mcg_status mcg_cache_destroy(mcg_cache* cache) {
@@ -836,8 +857,9 @@ mcg_status mcg_cache_create_stripe(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_en
         c->magic = mod_magic(n_cells);
         c->world = world;
         c->rank = rank;
+        c->stride = cell_pitch(n_entries);
         c->local_cells = n_cells > rank ? (n_cells - rank + world - 1) / world : 0;
-        const size_t local_bytes = std::max<uint64_t>(8, c->local_words() * 8);
+        const size_t local_bytes = std::max<uint64_t>(8, c->local_phys_words() * 8);
         cudaError_t e = cudaMalloc(&c->slots, local_bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -920,7 +942,7 @@ mcg_status mcg_cache_stripe_info(const mcg_cache* cache, uint32_t* rank, uint32_
 mcg_status mcg_cache_clear(mcg_cache* cache) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_words() * 8,
+        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_phys_words() * 8,
                                    cache->ctx->stream), "memset cache");
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
                                    cache->ctx->stream), "memset counters");
@@ -1039,8 +1061,7 @@ mcg_status mcg_cache_read_slots(mcg_cache* cache, uint64_t first, size_t n, uint
         need(cache && words, "null argument");
         need(first + n <= cache->local_words(), "slot range out of bounds (this stripe's words)");
         if (!n) return;
-        dev_download(cache->ctx, words, cache->slots + first, n);
-        sync(cache->ctx);
+        read_logical(cache, first, n, words);
     });
 }
 
@@ -1049,7 +1070,7 @@ mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
         need(cache && occupied, "null argument");
         mcg_ctx* ctx = cache->ctx;
         cuda_check(cudaMemsetAsync(cache->counters + 7, 0, 8, ctx->stream), "memset");
-        const uint64_t n = cache->local_words();
+        const uint64_t n = cache->local_phys_words();   // padding words are always zero
         LaunchScope ls(ctx, "occupied", n * 8.0);
         k_occupied<<<148 * 8, 256, 0, ctx->stream>>>(cache->slots, n, cache->counters + 7);
         ls.done();
@@ -1095,8 +1116,7 @@ mcg_status mcg_cache_dump(mcg_cache* cache, const char* path) {
         std::vector<uint64_t> buf(std::min<uint64_t>(total, chunk));
         for (uint64_t off = 0; off < total; off += chunk) {
             const size_t n = static_cast<size_t>(std::min<uint64_t>(chunk, total - off));
-            dev_download(cache->ctx, buf.data(), cache->slots + off, n);
-            sync(cache->ctx);
+            read_logical(cache, off, n, buf.data());
             out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(n * 8));
         }
         if (!out) fail(MCG_ERR_IO, std::string("short write on cache dump: ") + path);
@@ -1391,7 +1411,7 @@ mcg_status mcg_execute_batch(mcg_ctx* ctx, uint32_t slot, const float* sp, size_
         const int max_stack = static_cast<int>(ctx->scene.max_stack);
         const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
         if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
-        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, nullptr, nullptr, nullptr, 0};
+        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
         unsigned long long* counters = cache ? cache->counters : ctx->stats_mem.as<unsigned long long>();
         mcgd::StoreQueue q{nullptr, nullptr, nullptr, 0};
         const uint64_t cap = deferred ? n * std::max<uint32_t>(1, ctx->scene.max_cache_points) : 0;
