@@ -75,9 +75,9 @@ struct DeviceScene {
 }  // namespace mcg
 
 // Words per cell in memory. Padding cells to whole 32-byte sectors (80-byte
-// cells at a 96-byte pitch; MCG_CELL_PITCH_SECTORS) was measured slower on
-// the 1e7 x 10 table -- 31.1 vs 34.3 G lookups/s, 23.0 vs 24.0 G inserts/s
-// (profiles/README.md) -- so cells stay packed by default.
+// cells at a 96-byte pitch; MCG_CELL_PITCH_SECTORS) measured the same as
+// packed cells on the 1e7 x 10 table (profiles/README.md), so cells stay
+// packed: the table keeps the reference's 8 * Nc * Ne bytes.
 inline uint32_t cell_pitch(uint32_t n_entries) {
 #ifdef MCG_CELL_PITCH_SECTORS
     if (n_entries <= 2u || n_entries % 4u == 0u) return n_entries;
