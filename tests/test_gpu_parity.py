@@ -303,3 +303,54 @@ def test_striped_table_equals_one_table(ctx, scene_dir):
     lone = MaterialCache.stripe(nc, ne, 0, 2, ctx)
     with pytest.raises(ValueError, match="attach"):
         lone.lookup_batch(d[:4])
+
+
+def _edit_scene(path, **changes):
+    import json
+    with open(path) as f:
+        doc = json.load(f)
+    doc.update(changes)
+    with open(path, "w") as f:
+        json.dump(doc, f)
+    return path
+
+
+@pytest.mark.parametrize("case", [
+    # (name, kind, w, h, spp, n_cells, n_entries, max_bounces, mip_offset, samples_per_pass, edit)
+    ("one_pixel_one_slot", "junkshop", 1, 1, 3, 1, 1, 4, 0, 1, None),
+    ("ragged_odd_entries", "classroom", 17, 5, 2, 1, 3, 4, 0, 2, None),
+    ("wide_cells", "italianflat", 33, 20, 3, 997, 12, 4, 0, 1, None),
+    ("primary_only_mip2", "monster", 40, 24, 4, 4099, 4, 0, 2, 4, None),
+    ("zero_cache_points", "hostile", 24, 16, 2, 997, 4, 4, 0, 1, None),
+    ("no_lights", "cornell", 24, 16, 2, 997, 4, 4, 0, 1, {"lights": []}),
+    ("no_geometry", "cornell", 24, 16, 2, 997, 4, 4, 0, 1, {"meshes": []}),
+])
+def test_render_edge_cases_match_oracle(ctx, oracle, scene_dir, case):
+    """Degenerate inputs, deterministic mode, bit for bit against the oracle:
+    a one-slot table (every insert after the first is CellFull), odd and
+    > 10 entries per cell (the scalar scan paths), ragged tiles, no bounce,
+    a mip offset, no cache points, no lights, no geometry."""
+    name, kind, w, h, spp, nc, ne, mb, mip, k, edit = case
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=4, libm_ops=False),
+                              f"{scene_dir}/edge_{name}")
+    if edit:
+        _edit_scene(path, **edit)
+    s = load_scene(path)
+    cache = MaterialCache(nc, ne, ctx)
+    cfg = RenderConfig(width=w, height=h, spp=spp, max_bounces=mb, cache_enabled=True, deterministic=True,
+                       n_cells=nc, n_entries=ne, mip_offset=mip, samples_per_pass=k)
+    res = render(s, cfg, external_cache=cache, ctx=ctx)
+    P = _params(w, h, spp, 3, k, nc, ne, mip)
+    P.max_bounces = mb
+    oc = oracle.cache_new(nc, ne)
+    rad, nodes, samples, hps, st = oracle.render(s.flat, P, cache=oc)
+    np.testing.assert_array_equal(bits(res.frame.radiance), bits(rad))
+    np.testing.assert_array_equal(res.frame.nodes_found, nodes)
+    np.testing.assert_array_equal(res.frame.samples, samples)
+    np.testing.assert_array_equal(cache.slot_words(), oracle.cache_slots(oc, nc, ne))
+    assert res.stats.lookups == st.lookups and res.stats.hits == st.hits
+    if name == "zero_cache_points":
+        assert st.lookups == 0
+    if name == "no_geometry":
+        assert st.lookups == 0 and (res.frame.radiance > 0).all()
+    oracle.cache_free(oc)
