@@ -104,6 +104,9 @@ __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t cell_
     return r;  // full, no match
 }
 
+#ifndef MCG_VM_FIRST_PAIRS
+#define MCG_VM_FIRST_PAIRS 1   // 16-byte pairs the VM's probe reads before its first decision
+#endif
 __device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t cell, uint32_t check) {
     return probe_cell_t<1>(c, cell, check);
 }
@@ -646,7 +649,7 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 Probe pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, grp);
 #else
                 Probe pr{0u, -1, false};
-                if (static_cast<int>(lane) == leader) pr = probe_cell(C, p_cell, p_check);
+                if (static_cast<int>(lane) == leader) pr = probe_cell_t<MCG_VM_FIRST_PAIRS>(C, p_cell, p_check);
 #endif
                 pr.payload = __shfl_sync(grp, pr.payload, leader);
                 pr.where = __shfl_sync(grp, pr.where, leader);
