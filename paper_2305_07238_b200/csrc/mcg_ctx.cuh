@@ -125,6 +125,10 @@ struct mcg_ctx {
     std::vector<cudaEvent_t> event_pool;
     mcg::DeviceScene scene;
     mcg_cache* own_cache = nullptr;
+    // second stream for work that overlaps the main one (shadow rays while
+    // the continuation rays are traced), joined through the two events
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // scratch
     mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
     mcg::DevMem path_mem, queue_mem, stats_mem;
@@ -139,10 +143,11 @@ void resolve_events(mcg_ctx* ctx);  // synchronizes on the pending events
 // events on the context stream around it.
 class LaunchScope {
 public:
-    LaunchScope(mcg_ctx* ctx, const char* name, double bytes) : ctx_(ctx), name_(name), bytes_(bytes) {
+    LaunchScope(mcg_ctx* ctx, const char* name, double bytes, cudaStream_t stream = nullptr)
+        : ctx_(ctx), name_(name), bytes_(bytes), stream_(stream ? stream : ctx->stream) {
         if (ctx_->profile) {
             a_ = take_event(ctx_);
-            cudaEventRecord(a_, ctx_->stream);
+            cudaEventRecord(a_, stream_);
         }
     }
     void done() {
@@ -150,7 +155,7 @@ public:
         ++ctx_->launches;
         if (ctx_->profile) {
             cudaEvent_t b = take_event(ctx_);
-            cudaEventRecord(b, ctx_->stream);
+            cudaEventRecord(b, stream_);
             ctx_->pending.push_back({name_, a_, b, bytes_});
         }
     }
@@ -159,6 +164,7 @@ private:
     mcg_ctx* ctx_;
     const char* name_;
     double bytes_;
+    cudaStream_t stream_;
     cudaEvent_t a_ = nullptr;
 };
 

@@ -1622,7 +1622,9 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(Render
                              b1, b2, vtx);
             R.ro[q] = ro;
         } else {
-            key = hit_record(R, q, pid, ro, rd, R.thr[q], R.L[q], false, prim, t, b1, b2, vtx);
+            // the path ends; k_resolve_lights (which runs after this kernel
+            // and the shadow rays) adds throughput * env to its final radiance
+            key = no_hit_key(R);
         }
         R.keys[q] = key;
         R.vals[q] = q;
@@ -1632,10 +1634,11 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(Render
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
-// Finishes vertex b at sorted position i: adds the visible light
-// contributions in light order (the oracle's summation order); at the last
-// vertex the path ends (fin[pid]). Writes "no hit" sort keys for the slots
-// past the live list.
+// Finishes vertex b at sorted position i, after the shadow rays and the
+// continuation rays of the vertex: adds the visible light contributions in
+// light order (the oracle's summation order); the path ends (fin[pid]) at the
+// last vertex, or with the environment term when its continuation ray missed.
+// Writes "no hit" sort keys for the slots past the live list.
 __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R.n_paths) return;
@@ -1653,8 +1656,16 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
                 L.z = L.z + c.z;
             }
         }
-        if (b >= R.max_bounces) R.fin[R.pid[i]] = make_float4(L.x, L.y, L.z, R.thr[i].w);
-        else R.L[i] = L;
+        if (b >= R.max_bounces) {
+            R.fin[R.pid[i]] = make_float4(L.x, L.y, L.z, R.thr[i].w);
+        } else if (R.keys[i] == no_hit_key(R)) {
+            // the continuation ray missed (k_trace_closest_ww): env term, path ends
+            const float4 thr = R.thr[i];
+            R.fin[R.pid[i]] = make_float4(L.x + thr.x * R.S.env[0], L.y + thr.y * R.S.env[1],
+                                          L.z + thr.z * R.S.env[2], thr.w);
+        } else {
+            R.L[i] = L;
+        }
     } else {
         R.keys[i] = no_hit_key(R);
         R.vals[i] = i;
@@ -1944,6 +1955,14 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     // any-hit); MCG_SHADOW_TREE=ref keeps the reference's own tree.
     const char* stree_env = std::getenv("MCG_SHADOW_TREE");
     const bool sah_shadow = !(stree_env && std::string(stree_env) == "ref");
+    // MCG_OVERLAP=0: shadow rays on the main stream (no concurrency)
+    const char* ov_env = std::getenv("MCG_OVERLAP");
+    const bool overlap = !(ov_env && std::string(ov_env) == "0");
+    if (overlap && !ctx->aux) {
+        cuda_check(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "aux stream");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
+    }
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
@@ -2012,20 +2031,30 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                     apply_ordered(ctx, cache, k1, v1, count, 32, nullptr, nullptr, nullptr, R.stats);
                 }
             }
+            // Shadow rays (aux stream) and continuation rays (main stream)
+            // of vertex b are independent; k_resolve_lights waits for both.
+            const bool fork = overlap && n_lights && b < P.max_bounces;
+            if (fork) {
+                cuda_check(cudaEventRecord(ctx->ev_fork, ctx->stream), "event");
+                cuda_check(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0), "wait");
+            }
             if (n_lights) {
-                LaunchScope ls(ctx, "trace_shadow", 0.0);
-                if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
-                else k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, ctx->stream>>>(R);
+                cudaStream_t st = fork ? ctx->aux : ctx->stream;
+                LaunchScope ls(ctx, "trace_shadow", 0.0, st);
+                if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, st>>>(R);
+                else k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, st>>>(R);
                 ls.done();
             }
-            {
-                LaunchScope ls(ctx, "resolve_lights", 0.0);
-                k_resolve_lights<<<grid, 256, 0, ctx->stream>>>(R, b);
-                ls.done();
-            }
+            if (fork) cuda_check(cudaEventRecord(ctx->ev_join, ctx->aux), "event");
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
                 k_trace_closest_ww<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                ls.done();
+            }
+            if (fork) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0), "wait");
+            {
+                LaunchScope ls(ctx, "resolve_lights", 0.0);
+                k_resolve_lights<<<grid, 256, 0, ctx->stream>>>(R, b);
                 ls.done();
             }
         }

@@ -659,6 +659,9 @@ mcg_status mcg_destroy(mcg_ctx* ctx) {
         cudaEventDestroy(r.b);
     }
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MCG_OK;
