@@ -1461,7 +1461,10 @@ __device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& cod
 
 // Pass start: primary rays of every path of the pass, traced to vertex 0,
 // state written at layout position = path id.
-__global__ void __launch_bounds__(256) k_primary(RenderView R) {
+#ifndef MCG_PRIMARY_BLOCK
+#define MCG_PRIMARY_BLOCK 128
+#endif
+__global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = i < R.n_paths;
@@ -1576,7 +1579,10 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
 #define MCG_TRACE_MINB 1
 #endif
 template <bool kSah>
-__global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R) {
+#ifndef MCG_SHADOW_BLOCK
+#define MCG_SHADOW_BLOCK 128
+#endif
+__global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_TRACE_MINB) k_shadow_ww(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *R.shadow_count;
@@ -1600,7 +1606,10 @@ __global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_shadow_ww(RenderView R)
 
 // Closest hits of the continuation rays, one per thread at its own layout
 // position, speculative 4-wide traversal in the reference's order.
-__global__ void __launch_bounds__(256, MCG_TRACE_MINB) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
+#ifndef MCG_TRACE_BLOCK
+#define MCG_TRACE_BLOCK 128
+#endif
+__global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *count;
@@ -1986,7 +1995,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0);
-            k_primary<<<grid, 256, 0, ctx->stream>>>(R);
+            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, ctx->stream>>>(R);
             ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
@@ -2041,14 +2050,15 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             if (n_lights) {
                 cudaStream_t st = fork ? ctx->aux : ctx->stream;
                 LaunchScope ls(ctx, "trace_shadow", 0.0, st);
-                if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, 256), 256, 0, st>>>(R);
-                else k_shadow_ww<false><<<grid_for(n_shadow, 256), 256, 0, st>>>(R);
+                if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, MCG_SHADOW_BLOCK), MCG_SHADOW_BLOCK, 0, st>>>(R);
+                else k_shadow_ww<false><<<grid_for(n_shadow, MCG_SHADOW_BLOCK), MCG_SHADOW_BLOCK, 0, st>>>(R);
                 ls.done();
             }
             if (fork) cuda_check(cudaEventRecord(ctx->ev_join, ctx->aux), "event");
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0);
-                k_trace_closest_ww<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2, b + 1);
+                k_trace_closest_ww<<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, ctx->stream>>>(
+                    R, R.shadow_count + 2, b + 1);
                 ls.done();
             }
             if (fork) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0), "wait");
