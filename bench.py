@@ -126,7 +126,10 @@ def make_scene(tmp: str):
 # reference arm: the reference's own CPU path on the host cores
 # --------------------------------------------------------------------------
 
-def cpu_reference_sample(scene_path: str, spp: int = 1, threads: int = 0, cache: bool = True):
+CPU_SPP = 4   # the CPU is timed on the same frame at 4 spp (full spp takes hours)
+
+
+def cpu_reference_sample(scene_path: str, spp: int = CPU_SPP, threads: int = 0, cache: bool = True):
     """Times oracle/_ref's render (reference sources + restated tracer, tile
     queue over worker threads, shared MaterialCache) on a bounded sample:
     the full 1920x1080 frame at `spp` samples per pixel."""
@@ -170,9 +173,9 @@ def run_reference_arm(args) -> None:
             times.append(info["seconds"])
     t = sum(times) / len(times)
     v = info["samples"] / t
-    sample = (f"{W}x{H}x1spp frame per step (of the {W}x{H}x{SPP} workload), cache "
-              f"{N_CELLS:.0e}x{N_ENTRIES}, tile queue over {info['cores']} threads"
-              if info["kind"] == "reference" else "480x270x1spp crop, 1 thread (C port)")
+    sample = (f"{W}x{H}x{CPU_SPP}spp frame per step (of the {W}x{H}x{SPP} workload), fresh cache "
+              f"{N_CELLS:.0e}x{N_ENTRIES} per step, tile queue over {info['cores']} threads"
+              if info["kind"] == "reference" else f"480x270x{CPU_SPP}spp crop, 1 thread (C port)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -486,12 +489,14 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            info = cpu_reference_sample(scene_path)
+            # median of 3 runs, a fresh table each
+            runs = [cpu_reference_sample(scene_path) for _ in range(3)]
+            info = sorted(runs, key=lambda r: r["seconds"])[1]
             cpu = {"value": info["samples"] / info["seconds"], "unit": "samples/s",
                    "cores": info["cores"], "kind": info["kind"],
-                   "sample": (f"{W}x{H}x1spp frame, cache {N_CELLS:.0e}x{N_ENTRIES}, tile queue over "
-                              f"{info['cores']} threads" if info["kind"] == "reference"
-                              else "480x270x1spp crop, 1 thread")}
+                   "sample": (f"{W}x{H}x{CPU_SPP}spp frame, median of 3 runs with a fresh cache "
+                              f"{N_CELLS:.0e}x{N_ENTRIES}, tile queue over {info['cores']} threads"
+                              if info["kind"] == "reference" else f"480x270x{CPU_SPP}spp crop, 1 thread")}
         except Exception as e:  # the checker must never break the bench line
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
