@@ -74,24 +74,15 @@ struct DeviceScene {
 
 }  // namespace mcg
 
-// Words per cell in memory. Padding cells to whole 32-byte sectors (80-byte
-// cells at a 96-byte pitch; MCG_CELL_PITCH_SECTORS) measured the same as
-// packed cells on the 1e7 x 10 table (profiles/README.md), so cells stay
-// packed: the table keeps the reference's 8 * Nc * Ne bytes.
-inline uint32_t cell_pitch(uint32_t n_entries) {
-#ifdef MCG_CELL_PITCH_SECTORS
-    if (n_entries <= 2u || n_entries % 4u == 0u) return n_entries;
-    return (n_entries + 3u) & ~3u;
-#else
-    return n_entries;
-#endif
-}
+// Slots of a cell kept in the head array: one 64-byte DRAM block
+// (mcg_device.cuh head_words); the rest go to the tail array.
+inline uint32_t head_slots(uint32_t n_entries) { return n_entries > 8u ? 8u : n_entries; }
 
 struct mcg_cache {
     mcg_ctx* ctx = nullptr;
     uint64_t n_cells = 0;         // logical cells (all stripes)
     uint32_t n_entries = 0;
-    uint32_t stride = 0;          // words per cell in memory (cell_pitch(n_entries))
+    uint32_t head_n = 0;          // slots per cell in the head array (head_slots(n_entries))
     uint64_t magic = 0;
     uint64_t* slots = nullptr;    // this device's cells (all of them when world == 1)
     unsigned long long* counters = nullptr;  // lookups, hits, won, lost_full, lost_race
@@ -106,10 +97,10 @@ struct mcg_cache {
     uint32_t* trace = nullptr;
     unsigned long long* trace_count = nullptr;
     uint64_t trace_cap = 0;
-    uint64_t local_words() const { return local_cells * n_entries; }    // logical slots held here
-    uint64_t local_phys_words() const { return local_cells * stride; } // words allocated
+    uint64_t local_words() const { return local_cells * n_entries; }   // slots held here (head + tail)
+    uint64_t* tail() const { return n_entries > head_n ? slots + local_cells * head_n : nullptr; }
     mcgd::CacheView view() const {
-        return {slots, n_cells, magic, n_entries, stride, world, stripes, trace, trace_count, trace_cap};
+        return {slots, tail(), n_cells, magic, n_entries, head_n, world, stripes, trace, trace_count, trace_cap};
     }
 };
 

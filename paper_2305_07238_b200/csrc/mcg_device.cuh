@@ -17,28 +17,39 @@ constexpr unsigned kFull = 0xffffffffu;
 // Table view
 // ---------------------------------------------------------------------------
 struct CacheView {
-    uint64_t* slots;          // cell-major, `stride` words per cell (n_entries used, the rest zero)
+    uint64_t* slots;          // head words: n_cells x head_n, cell-major
+    uint64_t* tail;           // tail words: n_cells x (n_entries - head_n), or null
     uint64_t n_cells;
     uint64_t magic;           // floor((2^64-1) / n_cells) for fast_mod
     uint32_t n_entries;
-    uint32_t stride;          // words per cell in memory: n_entries rounded so cells start on 32-byte sectors
+    uint32_t head_n;          // a cell's first min(n_entries, 8) slots: one 64-byte DRAM block
     uint32_t world;           // > 1: one logical table striped by cell over `world` devices
-    uint64_t* const* stripes; // device pointers of every stripe (peer memory over NVLink)
+    uint64_t* const* stripes; // (head, tail) device pointers of every stripe (peer memory over NVLink)
     uint32_t* trace;          // optional descriptor log: 5 words per lookup (mcg_descriptor)
     unsigned long long* trace_count;
     uint64_t trace_cap;
 };
 
-// The words of cell `cell`. Cells are laid out `stride` words apart (80-byte
-// cells at 96-byte pitch: a cell is exactly three 32-byte DRAM sectors instead
-// of three or four); slot indices stay the logical cell * n_entries + entry.
-// A striped table keeps cell c on stripe c % world at local cell c / world, so
-// every device sees the same logical table.
-__device__ __forceinline__ uint64_t* cell_words(const CacheView& c, uint64_t cell) {
-    if (c.world <= 1u) return c.slots + cell * c.stride;
-    return c.stripes[cell % c.world] + (cell / c.world) * c.stride;
+// Where a cell's slots live. DRAM serves random reads in 64-byte blocks, and
+// an 80-byte cell always straddles two of them (ncu: 142 B of DRAM per
+// lookup); so a cell of more than 8 slots keeps its first 8 in a 64-byte
+// aligned head array and the rest in a tail array. The scan reads the head
+// (one block) and touches the tail only when the head neither matched nor
+// held an empty slot. Slot indices stay the logical cell * n_entries + e.
+// A striped table keeps cell c on stripe c % world at local cell c / world,
+// so every device sees the same logical table.
+__device__ __forceinline__ uint64_t* head_words(const CacheView& c, uint64_t cell) {
+    if (c.world <= 1u) return c.slots + cell * c.head_n;
+    return c.stripes[2 * (cell % c.world)] + (cell / c.world) * c.head_n;
 }
-
+__device__ __forceinline__ uint64_t* tail_words(const CacheView& c, uint64_t cell) {
+    const uint32_t tn = c.n_entries - c.head_n;
+    if (c.world <= 1u) return c.tail + cell * tn;
+    return c.stripes[2 * (cell % c.world) + 1] + (cell / c.world) * tn;
+}
+__device__ __forceinline__ uint64_t* slot_ptr(const CacheView& c, uint64_t cell, uint32_t e) {
+    return e < c.head_n ? head_words(c, cell) + e : tail_words(c, cell) + (e - c.head_n);
+}
 // Result of scanning one cell as lookup() does (cache.cpp:121-136): a match,
 // or the first empty slot (where update() would CAS, cache.cpp:108), or a
 // full cell (update() -> CellFull).
@@ -74,11 +85,11 @@ __device__ __forceinline__ bool scan_word(uint64_t w, int32_t idx, uint32_t chec
 template <int kFirstPairs>
 __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t cell_index, uint32_t check) {
     Probe r{0u, -1, false};
-    const uint32_t ne = c.n_entries;
-    const uint64_t* cell = cell_words(c, cell_index);
+    const uint32_t ne = c.n_entries, hn = c.head_n;
+    const uint64_t* cell = head_words(c, cell_index);
     uint32_t i = 0;
-    if ((reinterpret_cast<uintptr_t>(cell) & 15u) == 0u && ne >= 2 && ne <= 10) {
-        const uint32_t npairs = ne >> 1;
+    if ((reinterpret_cast<uintptr_t>(cell) & 15u) == 0u && hn >= 2 && hn <= 10) {
+        const uint32_t npairs = hn >> 1;
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
         ulonglong2 w[5];
 #pragma unroll
@@ -98,8 +109,14 @@ __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t cell_
         }
         i = 2 * npairs;
     }
-    for (; i < ne; ++i) {
+    for (; i < hn; ++i) {
         if (scan_word(__ldcg(cell + i), static_cast<int32_t>(i), check, r)) return r;
+    }
+    if (ne > hn) {
+        const uint64_t* t = tail_words(c, cell_index);
+        for (uint32_t j = 0; j < ne - hn; ++j) {
+            if (scan_word(__ldcg(t + j), static_cast<int32_t>(hn + j), check, r)) return r;
+        }
     }
     return r;  // full, no match
 }
@@ -119,8 +136,10 @@ __device__ __forceinline__ Probe probe_cell(const CacheView& c, uint64_t cell, u
 __device__ __forceinline__ Probe probe_cell_blk(const CacheView& c, uint64_t cell_index, uint32_t check) {
     Probe r{0u, -1, false};
     const uint32_t ne = c.n_entries;
-    const uint64_t* cell = cell_words(c, cell_index);
-    if ((reinterpret_cast<uintptr_t>(cell) & 15u) != 0u || ne > 10) return probe_cell_t<1>(c, cell_index, check);
+    const uint64_t* cell = head_words(c, cell_index);
+    if ((reinterpret_cast<uintptr_t>(cell) & 15u) != 0u || ne > 10 || c.head_n != ne) {
+        return probe_cell_t<1>(c, cell_index, check);
+    }
     const uint32_t npairs = ne >> 1;
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
     // pairs in the first 64-byte block: (64 - (addr % 64)) / 16
@@ -169,7 +188,7 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t cell, u
         const int owner = rd * kPer + g;
         const uint64_t oc = __shfl_sync(kFull, cell, owner & 31);
         const bool ov = __shfl_sync(kFull, valid, owner & 31);
-        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(cell_words(c, oc) + word) : ~0ull;
+        w[rd] = (g < kPer && owner < 32 && ov) ? __ldcg(slot_ptr(c, oc, static_cast<uint32_t>(word))) : ~0ull;
     }
     Probe mine{0u, -1, false};
 #pragma unroll
@@ -200,26 +219,28 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t cell, u
     return mine;
 }
 
-// Warp-cooperative probe with one 16-byte load per lane: the cell of each
-// lane's descriptor (Ne even, <= 10) is read by Ne/2 adjacent lanes as one
-// coalesced access, and every round's load is issued before the first
-// decision, so a probe costs one DRAM round trip (the per-lane scans need
-// two, and a random access that comes back to a row after it closed pays the
-// row activation again). Per round one ballot finds, for each cell, the first
-// 16-byte pair that ends the reference's linear scan (an empty slot or the
-// matching check hash, cache.cpp:127-134), and the descriptor's lane reads the
-// outcome from the deciding lane. Every lane of the warp must call it.
+// Warp-cooperative probe with one 16-byte load per lane: the head of each
+// lane's cell (head_n even, <= 8 slots: one 64-byte DRAM block) is read by
+// head_n/2 adjacent lanes as one coalesced access, and every round's load is
+// issued before the first decision, so a probe costs one DRAM round trip (the
+// per-lane scans need two, and a random access that comes back to a row after
+// it closed pays the row activation again). Per round one ballot finds, for
+// each cell, the first 16-byte pair that ends the reference's linear scan (an
+// empty slot or the matching check hash, cache.cpp:127-134), and the
+// descriptor's lane reads the outcome from the deciding lane. A scan the head
+// does not end continues in the cell's tail, lane by lane. Every lane of the
+// warp must call it.
 __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell, uint32_t check,
                                               bool valid) {
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t lpc = c.n_entries >> 1;   // lanes (pairs) per cell
+    const uint32_t lpc = c.head_n >> 1;      // lanes (pairs) per cell head
     const uint32_t cpr = 32u / lpc;          // cells per round
-    const uint32_t rounds = (32u + cpr - 1u) / cpr;
+    const uint32_t rounds = (32u + cpr - 1u) / cpr;   // <= 4 for head_n <= 8
     const uint32_t g = lane / lpc, k = lane - g * lpc;
-    ulonglong2 w[6];
-    uint32_t chk[6];
+    ulonglong2 w[4];
+    uint32_t chk[4];
 #pragma unroll
-    for (int r = 0; r < 6; ++r) {
+    for (int r = 0; r < 4; ++r) {
         w[r] = make_ulonglong2(~0ull, ~0ull);
         chk[r] = 0u;
         if (static_cast<uint32_t>(r) < rounds) {
@@ -228,14 +249,15 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell,
             const bool ov = __shfl_sync(kFull, valid, owner & 31u);
             chk[r] = __shfl_sync(kFull, check, owner & 31u);
             if (g < cpr && owner < 32u && ov) {
-                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, oc)) + k);
+                w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(head_words(c, oc)) + k);
             }
         }
     }
     Probe mine{0u, -1, false};
+    bool ended = false;
     const uint32_t my_round = lane / cpr, my_g = lane - my_round * cpr;
 #pragma unroll
-    for (int r = 0; r < 6; ++r) {
+    for (int r = 0; r < 4; ++r) {
         if (static_cast<uint32_t>(r) >= rounds) break;
         const bool e0 = w[r].x == 0ull, m0 = static_cast<uint32_t>(w[r].x >> 32) == chk[r];
         const bool e1 = w[r].y == 0ull, m1 = static_cast<uint32_t>(w[r].y >> 32) == chk[r];
@@ -253,14 +275,17 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell,
         }
         const uint32_t m = __shfl_sync(kFull, meta, src);
         const uint32_t pl = __shfl_sync(kFull, pay, src);
-        if (my_round == static_cast<uint32_t>(r)) {
-            if (found) {
-                mine.where = static_cast<int32_t>(m >> 1);
-                mine.hit = (m & 1u) != 0u;
-                if (mine.hit) mine.payload = pl;
-            } else {
-                mine.where = -1;
-            }
+        if (my_round == static_cast<uint32_t>(r) && found) {
+            ended = true;
+            mine.where = static_cast<int32_t>(m >> 1);
+            mine.hit = (m & 1u) != 0u;
+            if (mine.hit) mine.payload = pl;
+        }
+    }
+    if (valid && !ended && c.n_entries > c.head_n) {
+        const uint64_t* t = tail_words(c, cell);
+        for (uint32_t j = 0; j < c.n_entries - c.head_n; ++j) {
+            if (scan_word(__ldcg(t + j), static_cast<int32_t>(c.head_n + j), check, mine)) break;
         }
     }
     return mine;
@@ -280,7 +305,7 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell
     const uint32_t lpc = c.n_entries >> 1;
     const uint32_t cpr = lpc ? nW / lpc : 0u;
     const uint32_t rounds = cpr ? (nL + cpr - 1u) / cpr : 99u;
-    if ((c.n_entries & 1u) != 0u || c.n_entries > 10u || cpr == 0u || rounds > 6u) {
+    if ((c.n_entries & 1u) != 0u || c.n_entries > c.head_n || cpr == 0u || rounds > 6u) {
         return leader ? probe_cell(c, cell, check) : Probe{0u, -1, false};
     }
     const unsigned below = (1u << lane) - 1u;
@@ -295,7 +320,7 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell
             const bool work = g < cpr && j < nL;
             const uint32_t owner = work ? __fns(L, 0u, static_cast<int>(j) + 1) : lane;
             const uint64_t oc = __shfl_sync(grp, cell, owner);
-            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(cell_words(c, oc)) + k);
+            if (work) w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(head_words(c, oc)) + k);
         }
     }
     Probe mine{0u, -1, false};
@@ -349,7 +374,7 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell
 // every lane of the warp calls it (invalid lanes with valid = false).
 __device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t cell, uint32_t check,
                                              bool valid) {
-    if ((c.n_entries & 1u) == 0u && c.n_entries <= 10u) return probe_warp16(c, cell, check, valid);
+    if ((c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u) return probe_warp16(c, cell, check, valid);
     return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
 }
 
@@ -360,7 +385,7 @@ __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t cell, int3
     if (where < 0) return MCG_INSERT_CELL_FULL;
     const unsigned long long packed = (static_cast<unsigned long long>(check) << 32) | payload;
     const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long*>(cell_words(c, cell) + where), 0ull, packed);
+        atomicCAS(reinterpret_cast<unsigned long long*>(slot_ptr(c, cell, static_cast<uint32_t>(where))), 0ull, packed);
     return prev == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
 }
 

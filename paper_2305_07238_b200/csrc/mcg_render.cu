@@ -1874,7 +1874,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     RenderView R{};
     R.S = D.view;
     if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
-    R.C = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
+    R.C = cache ? cache->view() : mcgd::CacheView{nullptr, nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
     R.cache_on = cache_on ? 1 : 0;
     R.mip_offset = P.mip_offset;
     camera_setup(D.cam, W, H, R.cam);

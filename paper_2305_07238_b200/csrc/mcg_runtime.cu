@@ -222,7 +222,6 @@ __global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
     if (i < n) {
         const uint64_t cell = keys[i] >> ob;
         if (i == 0 || (keys[i - 1] >> ob) != cell) {
-            uint64_t* words = mcgd::cell_words(c, cell);
             const unsigned long long omask = ob >= 64 ? ~0ull : ((1ull << ob) - 1ull);
             for (size_t j = i; j < n && (keys[j] >> ob) == cell; ++j) {
                 const uint32_t chk = static_cast<uint32_t>(vals[j] >> 32);
@@ -230,7 +229,8 @@ __global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
                 int res = MCG_INSERT_CELL_FULL;
                 uint64_t slot = ~0ull, pk = 0;
                 for (uint32_t s = 0; s < c.n_entries; ++s) {
-                    const uint64_t cur = words[s];
+                    uint64_t* word = mcgd::slot_ptr(c, cell, s);
+                    const uint64_t cur = *word;
                     if (static_cast<uint32_t>(cur >> 32) == chk) {
                         res = MCG_INSERT_ALREADY_PRESENT;
                         slot = cell * c.n_entries + s;
@@ -238,7 +238,7 @@ __global__ void k_apply_ordered(CacheView c, const unsigned long long* keys,
                         break;
                     }
                     if (cur == 0ull) {
-                        words[s] = packed;
+                        *word = packed;
                         res = MCG_INSERT_WON;
                         slot = cell * c.n_entries + s;
                         pk = packed;
@@ -792,10 +792,9 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
         c->ctx = ctx;
         c->n_cells = n_cells;
         c->n_entries = n_entries;
-        c->stride = cell_pitch(n_entries);
+        c->head_n = head_slots(n_entries);
         c->magic = mod_magic(n_cells);
         c->local_cells = n_cells;
-        bytes = c->local_phys_words() * 8;
         cudaError_t e = cudaMalloc(&c->slots, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -811,19 +810,22 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
 }
 
 // Logical slots [first, first + n) of this object's cells (cell-major,
-// n_entries per cell: the reference's dump order) from the padded layout.
+// n_entries per cell: the reference's dump order) from the head/tail arrays.
 static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* out) {
     mcg_ctx* ctx = cache->ctx;
-    const uint32_t ne = cache->n_entries, pitch = cache->stride;
-    if (pitch == ne) {
+    const uint32_t ne = cache->n_entries, hn = cache->head_n, tn = ne - hn;
+    if (tn == 0) {
         dev_download(ctx, out, cache->slots + first, n);
         sync(ctx);
         return;
     }
     const uint64_t c0 = first / ne, c1 = (first + n + ne - 1) / ne;
     std::vector<uint64_t> tmp((c1 - c0) * ne);
-    cuda_check(cudaMemcpy2DAsync(tmp.data(), ne * 8ull, cache->slots + c0 * pitch, pitch * 8ull, ne * 8ull,
-                                 c1 - c0, cudaMemcpyDeviceToHost, ctx->stream), "D2H cells");
+    // heads into columns [0, hn), tails into [hn, ne) of each logical cell
+    cuda_check(cudaMemcpy2DAsync(tmp.data(), ne * 8ull, cache->slots + c0 * hn, hn * 8ull, hn * 8ull, c1 - c0,
+                                 cudaMemcpyDeviceToHost, ctx->stream), "D2H heads");
+    cuda_check(cudaMemcpy2DAsync(tmp.data() + hn, ne * 8ull, cache->tail() + c0 * tn, tn * 8ull, tn * 8ull,
+                                 c1 - c0, cudaMemcpyDeviceToHost, ctx->stream), "D2H tails");
     sync(ctx);
     std::memcpy(out, tmp.data() + (first - c0 * ne), n * 8);
 }
@@ -860,9 +862,9 @@ mcg_status mcg_cache_create_stripe(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_en
         c->magic = mod_magic(n_cells);
         c->world = world;
         c->rank = rank;
-        c->stride = cell_pitch(n_entries);
+        c->head_n = head_slots(n_entries);
         c->local_cells = n_cells > rank ? (n_cells - rank + world - 1) / world : 0;
-        const size_t local_bytes = std::max<uint64_t>(8, c->local_phys_words() * 8);
+        const size_t local_bytes = std::max<uint64_t>(8, c->local_words() * 8);
         cudaError_t e = cudaMalloc(&c->slots, local_bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -888,12 +890,13 @@ mcg_status mcg_cache_attach_local(mcg_cache* cache, mcg_cache* const* stripes, u
     return guarded([&] {
         need(cache && stripes, "null argument");
         need(world == cache->world, "world does not match the stripe's");
-        std::vector<uint64_t*> ptrs(world);
+        std::vector<uint64_t*> ptrs(2 * world);
         for (uint32_t r = 0; r < world; ++r) {
             need(stripes[r] && stripes[r]->world == world && stripes[r]->rank == r &&
                      stripes[r]->n_cells == cache->n_cells && stripes[r]->n_entries == cache->n_entries,
                  "stripe r must be rank r of the same logical table");
-            ptrs[r] = stripes[r]->slots;
+            ptrs[2 * r] = stripes[r]->slots;
+            ptrs[2 * r + 1] = stripes[r]->tail();
         }
         upload_stripes(cache, ptrs);
     });
@@ -914,11 +917,14 @@ mcg_status mcg_cache_attach_ipc(mcg_cache* cache, const void* handles, uint32_t 
         need(cache && handles, "null argument");
         need(world == cache->world, "world does not match the stripe's");
         need(cache->ipc_opened.empty(), "stripes already attached");
-        std::vector<uint64_t*> ptrs(world);
+        std::vector<uint64_t*> ptrs(2 * world);
         const auto* hb = static_cast<const unsigned char*>(handles);
         for (uint32_t r = 0; r < world; ++r) {
+            // stripe r's cells and the offset of its tail array
+            const uint64_t cells_r = cache->n_cells > r ? (cache->n_cells - r + world - 1) / world : 0;
             if (r == cache->rank) {
-                ptrs[r] = cache->slots;
+                ptrs[2 * r] = cache->slots;
+                ptrs[2 * r + 1] = cache->tail();
                 continue;
             }
             cudaIpcMemHandle_t h;
@@ -926,7 +932,8 @@ mcg_status mcg_cache_attach_ipc(mcg_cache* cache, const void* handles, uint32_t 
             void* p = nullptr;
             cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
             cache->ipc_opened.push_back(p);
-            ptrs[r] = static_cast<uint64_t*>(p);
+            ptrs[2 * r] = static_cast<uint64_t*>(p);
+            ptrs[2 * r + 1] = cache->n_entries > cache->head_n ? ptrs[2 * r] + cells_r * cache->head_n : nullptr;
         }
         upload_stripes(cache, ptrs);
     });
@@ -945,7 +952,7 @@ mcg_status mcg_cache_stripe_info(const mcg_cache* cache, uint32_t* rank, uint32_
 mcg_status mcg_cache_clear(mcg_cache* cache) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_phys_words() * 8,
+        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_words() * 8,
                                    cache->ctx->stream), "memset cache");
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
                                    cache->ctx->stream), "memset counters");
@@ -1073,7 +1080,7 @@ mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
         need(cache && occupied, "null argument");
         mcg_ctx* ctx = cache->ctx;
         cuda_check(cudaMemsetAsync(cache->counters + 7, 0, 8, ctx->stream), "memset");
-        const uint64_t n = cache->local_phys_words();   // padding words are always zero
+        const uint64_t n = cache->local_words();   // head and tail arrays
         LaunchScope ls(ctx, "occupied", n * 8.0);
         k_occupied<<<148 * 8, 256, 0, ctx->stream>>>(cache->slots, n, cache->counters + 7);
         ls.done();
@@ -1414,7 +1421,7 @@ mcg_status mcg_execute_batch(mcg_ctx* ctx, uint32_t slot, const float* sp, size_
         const int max_stack = static_cast<int>(ctx->scene.max_stack);
         const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
         if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
-        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
+        mcgd::CacheView cv = cache ? cache->view() : mcgd::CacheView{nullptr, nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
         unsigned long long* counters = cache ? cache->counters : ctx->stats_mem.as<unsigned long long>();
         mcgd::StoreQueue q{nullptr, nullptr, nullptr, 0};
         const uint64_t cap = deferred ? n * std::max<uint32_t>(1, ctx->scene.max_cache_points) : 0;
