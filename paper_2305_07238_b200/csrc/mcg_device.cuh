@@ -85,36 +85,43 @@ __device__ __forceinline__ bool scan_word(uint64_t w, int32_t idx, uint32_t chec
 template <int kFirstPairs>
 __device__ __forceinline__ Probe probe_cell_t(const CacheView& c, uint64_t cell_index, uint32_t check) {
     Probe r{0u, -1, false};
-    const uint32_t ne = c.n_entries, hn = c.head_n;
+    const uint32_t ne = c.n_entries, hn = c.head_n, tn = ne - hn;
     const uint64_t* cell = head_words(c, cell_index);
     uint32_t i = 0;
-    if ((reinterpret_cast<uintptr_t>(cell) & 15u) == 0u && hn >= 2 && hn <= 10) {
+    if ((reinterpret_cast<uintptr_t>(cell) & 15u) == 0u && hn >= 2 && hn <= 8 && (hn & 1u) == 0u) {
         const uint32_t npairs = hn >> 1;
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(cell);
+        // the tail's first pair joins the head's second round trip
+        // (16-byte aligned when the tail holds an even number of slots)
+        const ulonglong2* tp = (tn >= 2 && (tn & 1u) == 0u)
+                                   ? reinterpret_cast<const ulonglong2*>(tail_words(c, cell_index))
+                                   : nullptr;
         ulonglong2 w[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < 4; ++k) {
             if (k < kFirstPairs && k < static_cast<int>(npairs)) w[k] = __ldcg(p + k);
         }
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            if (k >= static_cast<int>(npairs)) break;
+            if (k >= static_cast<int>(npairs) + (tp ? 1 : 0)) break;
             if (k == kFirstPairs) {
 #pragma unroll
                 for (int j = kFirstPairs; j < 5; ++j) {
                     if (j < static_cast<int>(npairs)) w[j] = __ldcg(p + j);
+                    else if (j == static_cast<int>(npairs) && tp) w[j] = __ldcg(tp);
                 }
             }
+            if (k == static_cast<int>(npairs) && k < kFirstPairs) w[k] = __ldcg(tp);
             if (scan_word(w[k].x, 2 * k, check, r) || scan_word(w[k].y, 2 * k + 1, check, r)) return r;
         }
-        i = 2 * npairs;
+        i = tp ? hn + 2 : hn;
     }
     for (; i < hn; ++i) {
         if (scan_word(__ldcg(cell + i), static_cast<int32_t>(i), check, r)) return r;
     }
     if (ne > hn) {
         const uint64_t* t = tail_words(c, cell_index);
-        for (uint32_t j = 0; j < ne - hn; ++j) {
+        for (uint32_t j = (i > hn ? i - hn : 0u); j < tn; ++j) {
             if (scan_word(__ldcg(t + j), static_cast<int32_t>(hn + j), check, r)) return r;
         }
     }

@@ -320,6 +320,8 @@ def _edit_scene(path, **changes):
     ("one_pixel_one_slot", "junkshop", 1, 1, 3, 1, 1, 4, 0, 1, None),
     ("ragged_odd_entries", "classroom", 17, 5, 2, 1, 3, 4, 0, 2, None),
     ("wide_cells", "italianflat", 33, 20, 3, 997, 12, 4, 0, 1, None),
+    ("odd_tail", "junkshop", 20, 12, 3, 61, 11, 4, 0, 1, None),
+    ("nine_entries", "classroom", 20, 12, 3, 61, 9, 4, 0, 1, None),
     ("primary_only_mip2", "monster", 40, 24, 4, 4099, 4, 0, 2, 4, None),
     ("zero_cache_points", "hostile", 24, 16, 2, 997, 4, 4, 0, 1, None),
     ("no_lights", "cornell", 24, 16, 2, 997, 4, 4, 0, 1, {"lights": []}),
