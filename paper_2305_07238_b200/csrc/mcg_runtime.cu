@@ -279,8 +279,11 @@ __device__ __forceinline__ Desc bench_desc(uint64_t seed, uint64_t i) {
                 static_cast<uint32_t>(h2) & mask, static_cast<uint32_t>(h2 >> 32) & mask, mip};
 }
 
+#ifndef MCG_PROBE_MINB
+#define MCG_PROBE_MINB 1
+#endif
 template <int kVariant>
-__global__ void __launch_bounds__(256) k_probe_bench(CacheView c, uint64_t n, uint64_t seed,
+__global__ void __launch_bounds__(256, MCG_PROBE_MINB) k_probe_bench(CacheView c, uint64_t n, uint64_t seed,
                                                      int phase, unsigned long long* counters) {
     uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
