@@ -403,6 +403,10 @@ __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t cell, int3
 #define MCG_SHADOW_WIDTH 4
 #endif
 constexpr int kShadowWidth = MCG_SHADOW_WIDTH;   // entries per node of the shadow tree
+#ifndef MCG_CLOSEST_WIDTH
+#define MCG_CLOSEST_WIDTH 4
+#endif
+constexpr int kClosestWidth = MCG_CLOSEST_WIDTH; // entries per node of the collapsed reference tree
 
 struct SceneView {
     const float4* prim_geom;      // 3 float4 per prim
@@ -410,7 +414,7 @@ struct SceneView {
     const uint32_t* prim_info;
     const float4* nodes;          // 2 float4 per BVH node (the reference tree, own boxes)
     const float4* pairs;          // 4 float4 per internal node: both children's records
-    const float4* quads;          // 8 float4 per 4-wide node (collapsed reference tree)
+    const float4* quads;          // 2 * kClosestWidth float4 per node (collapsed reference tree)
     int32_t root_a, root_b;       // root entry into `quads`: (0, -1) or a leaf (~first, count)
     const float4* squads;         // kShadowWidth-wide SAH tree over the reference's leaves (any-hit only)
     int32_t sroot_a, sroot_b;     // root entry into `squads`

@@ -770,9 +770,9 @@ __device__ __forceinline__ bool closest_ww4(const mcgd::SceneView& S, bool activ
                             la = a;
                             lb = b;
                         } else {
-                            const float4* p = S.quads + 8 * a;
+                            const float4* p = S.quads + 2 * mcgd::kClosestWidth * a;
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
+                            for (int k = 0; k < mcgd::kClosestWidth; ++k) {
                                 const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
                                 const int32_t eb = __float_as_int(hi.w);
                                 if (eb == 0) continue;  // empty entry
@@ -845,41 +845,21 @@ __device__ __forceinline__ bool any_ww4(const mcgd::SceneView& S, bool active, V
                         la = a;
                         lb = b;
                     } else {
-                        // Surviving entries, pushed far-to-near so the nearest pops first.
-                        const float4* p = S.quads + 8 * a;
-                        float ke[4];
-                        int32_t ka[4], kb[4];
-                        int n = 0;
+                        // surviving entries in entry order (any order is exact for any-hit)
+                        const float4* p = S.quads + 2 * mcgd::kClosestWidth * a;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
+                        for (int k = 0; k < mcgd::kClosestWidth; ++k) {
                             const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
                             const int32_t eb = __float_as_int(hi.w);
+                            if (eb == 0) break;
                             float E, T1;
                             slab(o, inv, lo, hi, tmin, E, T1);
-                            const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
-                            ke[k] = ok ? E : __int_as_float(0x7f800000);
-                            ka[k] = __float_as_int(lo.w);
-                            kb[k] = ok ? eb : 0;
-                            n += ok;
-                        }
-                        // sort 4 (E descending) with a fixed network
-#define MCG_CSWAP(i, j)                                                              \
-    if (ke[i] < ke[j]) {                                                             \
-        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
-        const int32_t ta = ka[i]; ka[i] = ka[j]; ka[j] = ta;                         \
-        const int32_t tb = kb[i]; kb[i] = kb[j]; kb[j] = tb;                         \
-    }
-                        MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
-#undef MCG_CSWAP
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (kb[k] != 0) {
-                                sa[top] = ka[k];
-                                sb[top] = kb[k];
+                            if (!(fminf(tmax, T1) < E)) {
+                                sa[top] = __float_as_int(lo.w);
+                                sb[top] = eb;
                                 ++top;
                             }
                         }
-                        (void)n;
                     }
                 }
             }
@@ -997,9 +977,9 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                 } else {
                     ++nodes_visited;
                     has_n = false;
-                    const float4* p = S.quads + 8 * nc;
+                    const float4* p = S.quads + 2 * mcgd::kClosestWidth * nc;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < mcgd::kClosestWidth; ++k) {
                         const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
                         const int32_t eb = __float_as_int(hi.w);
                         if (eb == 0) continue;  // empty entry
@@ -1066,97 +1046,9 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
     return found;
 }
 
-// Any-hit with the same entries and speculation; children pushed far to
-// near so the nearest pops first (any order is exact for a boolean query).
-__device__ __forceinline__ bool any_ww4s(const mcgd::SceneView& S, const float4* Q, int32_t root_a,
-                                         int32_t root_b, bool active, V3 o, V3 d, float tmin, float tmax,
-                                         uint32_t& nodes_visited, uint32_t& prims_tested) {
-    const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
-    int32_t st[64];
-    int top = 0;
-    int32_t nc = 0;
-    bool has_n = false;
-    if (active && S.n_nodes) {
-        const float4 lo = __ldg(S.nodes), hi = __ldg(S.nodes + 1);
-        float E, T1;
-        slab(o, inv, lo, hi, tmin, E, T1);
-        if (!(fminf(tmax, T1) < E)) {
-            nc = entry_code(root_a, root_b);
-            has_n = true;
-        }
-    }
-    bool hit = false;
-    int32_t lc = 0;
-    bool leaf = false;
-    while (__any_sync(mcgd::kFull, has_n || leaf)) {
-        for (;;) {
-            if (has_n) {
-                if (nc < 0) {
-                    if (!leaf) {
-                        ++nodes_visited;
-                        leaf = true;
-                        lc = nc;
-                        has_n = false;
-                    }
-                } else {
-                    ++nodes_visited;
-                    has_n = false;
-                    const float4* p = Q + 8 * nc;
-                    float ke[4];
-                    int32_t kc[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
-                        const int32_t eb = __float_as_int(hi.w);
-                        float E, T1;
-                        slab(o, inv, lo, hi, tmin, E, T1);
-                        const bool ok = eb != 0 && !(fminf(tmax, T1) < E);
-                        ke[k] = ok ? E : __int_as_float(0x7f800000);
-                        kc[k] = ok ? entry_code(__float_as_int(lo.w), eb) : 0x7fffffff;
-                    }
-#define MCG_CSWAP(i, j)                                                              \
-    if (ke[i] < ke[j]) {                                                             \
-        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
-        const int32_t tc = kc[i]; kc[i] = kc[j]; kc[j] = tc;                         \
-    }
-                    MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
-#undef MCG_CSWAP
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (kc[k] != 0x7fffffff) {
-                            if (has_n) st[top++] = nc;
-                            nc = kc[k];
-                            has_n = true;
-                        }
-                    }
-                }
-            }
-            if (!has_n && top > 0) {
-                nc = st[--top];
-                has_n = true;
-            }
-            if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
-        }
-        if (leaf) {
-            const uint32_t v = static_cast<uint32_t>(~lc);
-            const uint32_t first = v >> 3, cnt = v & 7u;
-            prims_tested += cnt;
-            for (uint32_t i = first; i < first + cnt; ++i) {
-                float t, b1, b2;
-                if (hit_prim(S, i, o, d, tmin, tmax, t, b1, b2)) {
-                    hit = true;
-                    break;
-                }
-            }
-            leaf = false;
-            if (hit) has_n = false, top = 0;
-        }
-    }
-    return hit;
-}
 
 // Any hit over a kW-wide tree (the SAH shadow tree over the reference's
-// leaves): speculative while-while like any_ww4s; of the entries a node
+// leaves): speculative while-while like closest_ww4s; of the entries a node
 // passes, the nearest stays in registers (popped next), the rest go to the
 // stack in entry order -- any order is exact for a boolean query.
 #ifndef MCG_SHADOW_LEAVES
@@ -1331,9 +1223,9 @@ __device__ __forceinline__ bool closest_pk(const mcgd::SceneView& S, bool active
                 }
             }
         } else {
-            const float4* p = S.quads + 8 * code;
+            const float4* p = S.quads + 2 * mcgd::kClosestWidth * code;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < mcgd::kClosestWidth; ++k) {
                 const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
                 const int32_t eb = __float_as_int(hi.w);
                 if (eb == 0) continue;  // empty entry (uniform)
@@ -1404,43 +1296,24 @@ __device__ __forceinline__ bool any_pk(const mcgd::SceneView& S, bool active, V3
             }
             if (__all_sync(mcgd::kFull, hit || !active)) break;
         } else {
-            const float4* p = S.quads + 8 * code;
-            const int leader = __ffs(m) - 1;
-            float ke[4];
-            uint32_t km[4];
-            int32_t kc[4];
+            const float4* p = S.quads + 2 * mcgd::kClosestWidth * code;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < mcgd::kClosestWidth; ++k) {
                 const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
                 const int32_t eb = __float_as_int(hi.w);
+                if (eb == 0) break;  // uniform
                 float E, T1;
                 slab(o, inv, lo, hi, tmin, E, T1);
-                const bool ok = me && eb != 0 && !(fminf(tmax, T1) < E);
-                km[k] = __ballot_sync(mcgd::kFull, ok);
-                // order entries by the leader lane's entry distance (any
-                // order is exact for a boolean query; near first exits early)
-                ke[k] = __shfl_sync(mcgd::kFull, ok ? E : __int_as_float(0x7f800000), leader);
-                kc[k] = entry_code(__float_as_int(lo.w), eb);
-            }
-#define MCG_CSWAP(i, j)                                                              \
-    if (ke[i] < ke[j]) {                                                             \
-        const float te = ke[i]; ke[i] = ke[j]; ke[j] = te;                           \
-        const int32_t tc = kc[i]; kc[i] = kc[j]; kc[j] = tc;                         \
-        const uint32_t tm = km[i]; km[i] = km[j]; km[j] = tm;                        \
-    }
-            MCG_CSWAP(0, 1) MCG_CSWAP(2, 3) MCG_CSWAP(0, 2) MCG_CSWAP(1, 3) MCG_CSWAP(1, 2)
-#undef MCG_CSWAP
-            if (lane == 0) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (km[k]) {
-                        s_code[top] = kc[k];
-                        s_mask[top] = km[k];
-                        ++top;
+                const uint32_t mk = __ballot_sync(mcgd::kFull, me && !(fminf(tmax, T1) < E));
+                if (mk) {  // uniform; entry order (any order is exact for a boolean query)
+                    if (lane == 0) {
+                        s_code[top] = entry_code(__float_as_int(lo.w), eb);
+                        s_mask[top] = mk;
                     }
+                    ++top;
                 }
             }
-            top = __shfl_sync(mcgd::kFull, top, 0);
+
         }
         __syncwarp();
     }
@@ -1560,7 +1433,7 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
     if (kVar == 0) occ = active && traverse_any(S, o, d, tmin, tm, nv, nt);
     else if (kVar == 1) occ = any_ww(S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 2) occ = any_ww4(S, active, o, d, tmin, tm, nv, nt);
-    else if (kVar == 3) occ = any_ww4s(S, S.quads, S.root_a, S.root_b, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 3) occ = any_wws<mcgd::kClosestWidth>(S.quads, S.root_a, S.root_b, S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 5) occ = any_wws<mcgd::kShadowWidth>(S.squads, S.sroot_a, S.sroot_b, S, active, o, d, tmin, tm, nv, nt);
     else {
         int32_t* pc;
@@ -1597,7 +1470,7 @@ __global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_TRACE_MINB) k_shadow_ww(
         tmax = so.w;
     }
     const bool occ = kSah ? any_wws<mcgd::kShadowWidth>(R.S.squads, R.S.sroot_a, R.S.sroot_b, R.S, active, o, d, kTMin, tmax, nvis, ntest)
-                          : any_ww4s(R.S, R.S.quads, R.S.root_a, R.S.root_b, active, o, d, kTMin, tmax, nvis, ntest);
+                          : any_wws<mcgd::kClosestWidth>(R.S.quads, R.S.root_a, R.S.root_b, R.S, active, o, d, kTMin, tmax, nvis, ntest);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodesShadow, nvis);

@@ -1304,33 +1304,40 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             }
         }
         v.pairs = static_cast<const float4*>(up(14, pairs.data(), f.n_nodes * 2 * sizeof(mcg_bvh_node)));
-        // 4-wide nodes: each holds the grandchildren of a reference node (a
-        // child that is a leaf stands for itself), left part before right
-        // part, so a LIFO stack still visits in the reference's order; the
-        // skipped child boxes contain their children's boxes, so their
-        // culling is implied.
+        // W-wide nodes (W = mcgd::kClosestWidth, 4 or 8): each holds the
+        // descendants log2(W) levels below a reference node (a leaf above
+        // that depth stands for itself), in left-to-right order, so a LIFO
+        // stack still visits in the reference's order; the skipped boxes
+        // contain their children's boxes, so their culling is implied
+        // (DESIGN.md §5).
+        const int W = mcgd::kClosestWidth;
+        int depth_levels = 0;
+        while ((1 << depth_levels) < W) ++depth_levels;
         std::vector<mcg_bvh_node> quads;
         std::function<int32_t(int32_t)> collapse = [&](int32_t x) -> int32_t {
-            const int32_t q = static_cast<int32_t>(quads.size() / 4);
-            quads.resize(quads.size() + 4, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
-            int k = 0;
-            const int32_t kids[2] = {f.nodes[x].a, f.nodes[x].b};
-            std::vector<int32_t> entries;
-            for (int32_t c : kids) {
-                if (f.nodes[c].a < 0) {
-                    entries.push_back(c);
-                } else {
-                    entries.push_back(f.nodes[c].a);
-                    entries.push_back(f.nodes[c].b);
+            const int32_t q = static_cast<int32_t>(quads.size() / W);
+            quads.resize(quads.size() + W, mcg_bvh_node{{0, 0, 0}, 0, {0, 0, 0}, 0});
+            std::vector<int32_t> entries{f.nodes[x].a, f.nodes[x].b};
+            for (int level = 1; level < depth_levels; ++level) {
+                std::vector<int32_t> next;
+                for (int32_t e : entries) {
+                    if (f.nodes[e].a < 0) {
+                        next.push_back(e);
+                    } else {
+                        next.push_back(f.nodes[e].a);
+                        next.push_back(f.nodes[e].b);
+                    }
                 }
+                entries.swap(next);
             }
+            int k = 0;
             for (int32_t e : entries) {
                 mcg_bvh_node rec = f.nodes[e];
                 if (rec.a >= 0) {
                     rec.a = collapse(e);
                     rec.b = -1;
                 }
-                quads[4 * static_cast<size_t>(q) + k++] = rec;
+                quads[static_cast<size_t>(W) * q + k++] = rec;
             }
             return q;
         };
@@ -1366,7 +1373,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             }
             return nq ? std::max<uint32_t>(1, need[0]) : 1;
         };
-        D.max_stack4 = stack_need(quads, 4);
+        D.max_stack4 = stack_need(quads, W);
         if (D.max_stack4 > 63) fail(MCG_ERR_INVALID_ARGUMENT, "BVH too deep for the traversal stack");
         // Shadow tree: the reference's leaves (their exact boxes and
         // primitive ranges) regrouped by a binned SAH build. Any-hit is a
