@@ -1653,11 +1653,6 @@ __global__ void __launch_bounds__(256) k_accumulate(RenderView R, uint32_t k) {
     }
 }
 
-__global__ void k_iota(uint32_t* v, uint32_t n) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = i;
-}
-
 bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
     if (p.shard_count <= 1) return true;
     if (p.shard_mode == MCG_SHARD_INTERLEAVED) return tile % p.shard_count == p.shard_rank;
