@@ -417,6 +417,8 @@ struct SceneView {
     const float4* quads;          // 2 * kClosestWidth float4 per node (collapsed reference tree)
     int32_t root_a, root_b;       // root entry into `quads`: (0, -1) or a leaf (~first, count)
     const float4* squads;         // kShadowWidth-wide SAH tree over the reference's leaves (any-hit only)
+    const float4* quads_soa;      // the 4-wide trees transposed: 8 float4 rows per node
+    const float4* squads_soa;
     int32_t sroot_a, sroot_b;     // root entry into `squads`
     uint32_t n_nodes;
     const mcg_point_light* plights;

@@ -882,6 +882,91 @@ __device__ __forceinline__ bool any_ww4(const mcgd::SceneView& S, bool active, V
     return hit;
 }
 
+
+// ---------------------------------------------------------------------------
+// Four boxes at a time with packed f32x2 arithmetic (Blackwell FADD2/FMUL2,
+// round-to-nearest per element: bit for bit the scalar operations) over the
+// transposed 4-wide nodes (SceneView::quads_soa / squads_soa). The near and
+// far plane of each axis are picked by address from the ray's direction
+// signs -- the reference's swap of (lo - o) * inv and (hi - o) * inv when
+// inv < 0 -- so a node costs 12 packed sub/mul pairs instead of 48 scalar
+// operations and 24 selects.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2splat(float f) {
+    const unsigned long long u = __float_as_uint(f);
+    return (u << 32) | u;
+}
+__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+
+struct RayQ {
+    unsigned long long ox, oy, oz;  // origin, splatted
+    unsigned long long ix, iy, iz;  // 1 / direction, splatted
+    int nx, ny, nz;                 // rows of the near planes (lo: 0-2, hi: 3-5)
+};
+__device__ __forceinline__ RayQ make_rayq(V3 o, V3 inv) {
+    RayQ r;
+    r.ox = f2splat(o.x);
+    r.oy = f2splat(o.y);
+    r.oz = f2splat(o.z);
+    r.ix = f2splat(inv.x);
+    r.iy = f2splat(inv.y);
+    r.iz = f2splat(inv.z);
+    r.nx = inv.x < 0.0f ? 3 : 0;
+    r.ny = inv.y < 0.0f ? 4 : 1;
+    r.nz = inv.z < 0.0f ? 5 : 2;
+    return r;
+}
+// Entry distance E = max(tmin, near planes) and exit T1 = min(far planes)
+// of the four boxes of a transposed node (the slab() split, per box), axis
+// by axis so few packed values are live at once.
+__device__ __forceinline__ void box4_axis(const ulonglong2* q, int near_row, unsigned long long o2,
+                                          unsigned long long i2, float N[4], float F[4]) {
+    const ulonglong2 n = __ldg(q + near_row), f = __ldg(q + (near_row >= 3 ? near_row - 3 : near_row + 3));
+    const unsigned long long n01 = f2mul(f2sub(n.x, o2), i2), n23 = f2mul(f2sub(n.y, o2), i2);
+    const unsigned long long f01 = f2mul(f2sub(f.x, o2), i2), f23 = f2mul(f2sub(f.y, o2), i2);
+    N[0] = f2lo(n01);
+    N[1] = f2hi(n01);
+    N[2] = f2lo(n23);
+    N[3] = f2hi(n23);
+    F[0] = f2lo(f01);
+    F[1] = f2hi(f01);
+    F[2] = f2lo(f23);
+    F[3] = f2hi(f23);
+}
+__device__ __forceinline__ void box4(const float4* node, const RayQ& r, float tmin, float E[4], float T1[4]) {
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(node);
+    float N[4], F[4];
+    box4_axis(q, r.nx, r.ox, r.ix, N, F);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        E[k] = fmaxf(tmin, N[k]);
+        T1[k] = F[k];
+    }
+    box4_axis(q, r.ny, r.oy, r.iy, N, F);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        E[k] = fmaxf(E[k], N[k]);
+        T1[k] = fminf(T1[k], F[k]);
+    }
+    box4_axis(q, r.nz, r.oz, r.iz, N, F);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        E[k] = fmaxf(E[k], N[k]);
+        T1[k] = fminf(T1[k], F[k]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 4-wide traversal with speculative expansion and one-word stack entries.
 // An entry is (code, E): code >= 0 a 4-wide node, code < 0 a leaf
@@ -916,6 +1001,7 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                                              float& b1_out, float& b2_out, uint32_t& nodes_visited,
                                              uint32_t& prims_tested) {
     const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    const RayQ rq = make_rayq(o, inv);
     int2 st[64];
     int top = 0;
     int32_t nc = 0;  // register-held next entry
@@ -977,19 +1063,37 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                 } else {
                     ++nodes_visited;
                     has_n = false;
-                    const float4* p = S.quads + 2 * mcgd::kClosestWidth * nc;
+                    if constexpr (mcgd::kClosestWidth == 4) {
+                        const float4* p = S.quads_soa + 8 * nc;
+                        float E[4], T1[4];
+                        box4(p, rq, tmin, E, T1);
+                        const int4 ea = __ldg(reinterpret_cast<const int4*>(p + 6));
+                        const int4 eb = __ldg(reinterpret_cast<const int4*>(p + 7));
+                        const int32_t A[4] = {ea.x, ea.y, ea.z, ea.w}, B[4] = {eb.x, eb.y, eb.z, eb.w};
 #pragma unroll
-                    for (int k = 0; k < mcgd::kClosestWidth; ++k) {
-                        const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
-                        const int32_t eb = __float_as_int(hi.w);
-                        if (eb == 0) continue;  // empty entry
-                        float E, T1;
-                        slab(o, inv, lo, hi, tmin, E, T1);
-                        if (!(T1 < E)) {
-                            if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
-                            nc = entry_code(__float_as_int(lo.w), eb);
-                            ne = E;
-                            has_n = true;
+                        for (int k = 0; k < 4; ++k) {
+                            if (B[k] != 0 && !(T1[k] < E[k])) {
+                                if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
+                                nc = entry_code(A[k], B[k]);
+                                ne = E[k];
+                                has_n = true;
+                            }
+                        }
+                    } else {
+                        const float4* p = S.quads + 2 * mcgd::kClosestWidth * nc;
+#pragma unroll
+                        for (int k = 0; k < mcgd::kClosestWidth; ++k) {
+                            const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
+                            const int32_t eb = __float_as_int(hi.w);
+                            if (eb == 0) continue;  // empty entry
+                            float E, T1;
+                            slab(o, inv, lo, hi, tmin, E, T1);
+                            if (!(T1 < E)) {
+                                if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
+                                nc = entry_code(__float_as_int(lo.w), eb);
+                                ne = E;
+                                has_n = true;
+                            }
                         }
                     }
                 }
@@ -1057,8 +1161,10 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
 template <int kW, int kLeaves = MCG_SHADOW_LEAVES>
 __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t root_b, const mcgd::SceneView& S,
                                         bool active, V3 o, V3 d, float tmin, float tmax,
-                                        uint32_t& nodes_visited, uint32_t& prims_tested) {
+                                        uint32_t& nodes_visited, uint32_t& prims_tested,
+                                        const float4* Qs = nullptr) {
     const V3 inv{1.0f / d.x, 1.0f / d.y, 1.0f / d.z};
+    const RayQ rq = make_rayq(o, inv);
     int32_t st[64];
     int top = 0;
     int32_t nc = 0;
@@ -1093,8 +1199,34 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
                 } else {
                     ++nodes_visited;
                     has_n = false;
-                    const float4* p = Q + 2 * kW * nc;
                     float best = __int_as_float(0x7f800000);
+                    if (kW == 4 && Qs != nullptr) {
+                        // transposed node: four boxes with packed arithmetic
+                        const float4* p = Qs + 8 * nc;
+                        float E[4], T1[4];
+                        box4(p, rq, tmin, E, T1);
+                        const int4 ea = __ldg(reinterpret_cast<const int4*>(p + 6));
+                        const int4 eb = __ldg(reinterpret_cast<const int4*>(p + 7));
+                        const int32_t A[4] = {ea.x, ea.y, ea.z, ea.w}, B[4] = {eb.x, eb.y, eb.z, eb.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (B[k] != 0 && !(fminf(tmax, T1[k]) < E[k])) {
+                                const int32_t code = entry_code(A[k], B[k]);
+                                if (!has_n) {
+                                    nc = code;
+                                    best = E[k];
+                                    has_n = true;
+                                } else if (E[k] < best) {
+                                    st[top++] = nc;
+                                    nc = code;
+                                    best = E[k];
+                                } else {
+                                    st[top++] = code;
+                                }
+                            }
+                        }
+                    } else {
+                    const float4* p = Q + 2 * kW * nc;
 #pragma unroll
                     for (int k = 0; k < kW; ++k) {
                         const float4 lo = __ldg(p + 2 * k), hi = __ldg(p + 2 * k + 1);
@@ -1116,6 +1248,7 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
                                 st[top++] = code;
                             }
                         }
+                    }
                     }
                 }
             }
@@ -1433,8 +1566,8 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
     if (kVar == 0) occ = active && traverse_any(S, o, d, tmin, tm, nv, nt);
     else if (kVar == 1) occ = any_ww(S, active, o, d, tmin, tm, nv, nt);
     else if (kVar == 2) occ = any_ww4(S, active, o, d, tmin, tm, nv, nt);
-    else if (kVar == 3) occ = any_wws<mcgd::kClosestWidth>(S.quads, S.root_a, S.root_b, S, active, o, d, tmin, tm, nv, nt);
-    else if (kVar == 5) occ = any_wws<mcgd::kShadowWidth>(S.squads, S.sroot_a, S.sroot_b, S, active, o, d, tmin, tm, nv, nt);
+    else if (kVar == 3) occ = any_wws<mcgd::kClosestWidth>(S.quads, S.root_a, S.root_b, S, active, o, d, tmin, tm, nv, nt, S.quads_soa);
+    else if (kVar == 5) occ = any_wws<mcgd::kShadowWidth>(S.squads, S.sroot_a, S.sroot_b, S, active, o, d, tmin, tm, nv, nt, S.squads_soa);
     else {
         int32_t* pc;
         uint32_t* pm;
@@ -1449,7 +1582,7 @@ __global__ void __launch_bounds__(256) k_occluded_batch(mcgd::SceneView S, const
 // of the SAH tree over the reference's leaves (kSah) or of the reference's
 // own tree.
 #ifndef MCG_TRACE_MINB
-#define MCG_TRACE_MINB 1
+#define MCG_TRACE_MINB 8
 #endif
 template <bool kSah>
 #ifndef MCG_SHADOW_BLOCK
@@ -1469,8 +1602,8 @@ __global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_TRACE_MINB) k_shadow_ww(
         d = V3{sd.x, sd.y, sd.z};
         tmax = so.w;
     }
-    const bool occ = kSah ? any_wws<mcgd::kShadowWidth>(R.S.squads, R.S.sroot_a, R.S.sroot_b, R.S, active, o, d, kTMin, tmax, nvis, ntest)
-                          : any_wws<mcgd::kClosestWidth>(R.S.quads, R.S.root_a, R.S.root_b, R.S, active, o, d, kTMin, tmax, nvis, ntest);
+    const bool occ = kSah ? any_wws<mcgd::kShadowWidth>(R.S.squads, R.S.sroot_a, R.S.sroot_b, R.S, active, o, d, kTMin, tmax, nvis, ntest, R.S.squads_soa)
+                          : any_wws<mcgd::kClosestWidth>(R.S.quads, R.S.root_a, R.S.root_b, R.S, active, o, d, kTMin, tmax, nvis, ntest, R.S.quads_soa);
     if (active) R.vis[s] = occ ? 0 : 1;
     mcgd::warp_add(R.stats + kStatShadow, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodesShadow, nvis);

@@ -1272,7 +1272,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         if (s != MCG_OK) fail(s, mcg_last_error());
         DeviceScene& D = ctx->scene;
         D.clear();
-        D.bufs.resize(17);
+        D.bufs.resize(19);
         auto up = [&](int k, const void* p, size_t bytes) -> const void* {
             D.bufs[k].ensure(std::max<size_t>(bytes, 16));
             if (bytes) cuda_check(cudaMemcpyAsync(D.bufs[k].p, p, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D scene");
@@ -1386,6 +1386,36 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         D.max_stack_s = stack_need(squads, mcgd::kShadowWidth);
         if (D.max_stack_s > 63) fail(MCG_ERR_INVALID_ARGUMENT, "shadow BVH too deep for the traversal stack");
         v.squads = static_cast<const float4*>(up(16, squads.data(), squads.size() * sizeof(mcg_bvh_node)));
+        // The same 4-wide nodes transposed (mcg_device.cuh, closest_q4): eight
+        // float4 rows -- lo.x, lo.y, lo.z, hi.x, hi.y, hi.z of the four entries,
+        // then their a and b words -- so the traversal tests four boxes with
+        // packed f32x2 arithmetic and picks near/far planes by address.
+        auto transpose4 = [](const std::vector<mcg_bvh_node>& aos) {
+            std::vector<float> soa(aos.size() / 4 * 32, 0.0f);
+            for (size_t q = 0; q < aos.size() / 4; ++q) {
+                float* row = soa.data() + 32 * q;
+                for (int e = 0; e < 4; ++e) {
+                    const mcg_bvh_node& r = aos[4 * q + e];
+                    row[0 + e] = r.lo[0];
+                    row[4 + e] = r.lo[1];
+                    row[8 + e] = r.lo[2];
+                    row[12 + e] = r.hi[0];
+                    row[16 + e] = r.hi[1];
+                    row[20 + e] = r.hi[2];
+                    std::memcpy(row + 24 + e, &r.a, 4);
+                    std::memcpy(row + 28 + e, &r.b, 4);
+                }
+            }
+            return soa;
+        };
+        if (mcgd::kClosestWidth == 4) {
+            const std::vector<float> qs = transpose4(quads);
+            v.quads_soa = static_cast<const float4*>(up(17, qs.data(), qs.size() * sizeof(float)));
+        }
+        if (mcgd::kShadowWidth == 4) {
+            const std::vector<float> ss = transpose4(squads);
+            v.squads_soa = static_cast<const float4*>(up(18, ss.data(), ss.size() * sizeof(float)));
+        }
         v.plights = static_cast<const mcg_point_light*>(up(4, f.point_lights, f.n_point_lights * sizeof(mcg_point_light)));
         v.n_plights = f.n_point_lights;
         v.rlights = static_cast<const mcg_rect_light*>(up(5, f.rect_lights, f.n_rect_lights * sizeof(mcg_rect_light)));
