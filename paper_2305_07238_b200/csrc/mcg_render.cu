@@ -1588,7 +1588,10 @@ template <bool kSah>
 #ifndef MCG_SHADOW_BLOCK
 #define MCG_SHADOW_BLOCK 128
 #endif
-__global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_TRACE_MINB) k_shadow_ww(RenderView R) {
+#ifndef MCG_SHADOW_MINB
+#define MCG_SHADOW_MINB 10
+#endif
+__global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_SHADOW_MINB) k_shadow_ww(RenderView R) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = q < *R.shadow_count;
