@@ -1105,6 +1105,12 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                 ne = __int_as_float(e.y);
                 has_n = true;
             }
+#ifdef MCG_PREFETCH_NODES
+            // the next node's 128-byte line on its way while the warp syncs
+            if (mcgd::kClosestWidth == 4 && has_n && nc >= 0) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(S.quads_soa + 8 * nc));
+            }
+#endif
             if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
         }
         // Phase 2: every lane holding a leaf tests it (the reference's order).
