@@ -70,6 +70,12 @@ struct DeviceScene {
         view = mcgd::SceneView{};
         loaded = false;
     }
+    // A new upload reuses the device buffers (grown when too small):
+    // cudaFree/cudaMalloc per upload cost tens to hundreds of ms.
+    void reset() {
+        view = mcgd::SceneView{};
+        loaded = false;
+    }
 };
 
 }  // namespace mcg

@@ -1271,8 +1271,8 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         const mcg_status s = mcg_scene_flat(scene, &f);
         if (s != MCG_OK) fail(s, mcg_last_error());
         DeviceScene& D = ctx->scene;
-        D.clear();
-        D.bufs.resize(19);
+        D.reset();
+        if (D.bufs.size() < 19) D.bufs.resize(19);
         auto up = [&](int k, const void* p, size_t bytes) -> const void* {
             D.bufs[k].ensure(std::max<size_t>(bytes, 16));
             if (bytes) cuda_check(cudaMemcpyAsync(D.bufs[k].p, p, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D scene");
