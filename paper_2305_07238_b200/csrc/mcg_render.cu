@@ -465,7 +465,7 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
 // contribution computed now, applied in light order by k_resolve once
 // visibility is known -- and the continuation ray.
 __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, int b, float4 s0,
-                                           float4 s1, float3 bc, float4 thr, float4 ro, float4 rd) {
+                                           float4 s1, float3 bc, float4 thr, float width, float spread) {
     const uint32_t slot_j = pid / R.n_pix;
     const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
@@ -549,8 +549,8 @@ __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint
         thr.x = thr.x * alb.x;
         thr.y = thr.y * alb.y;
         thr.z = thr.z * alb.z;
-        R.ro2[i] = make_float4(o.x, o.y, o.z, ro.w);
-        R.rd2[i] = make_float4(nd.x, nd.y, nd.z, rd.w + R.diffuse_spread);  // widen
+        R.ro2[i] = make_float4(o.x, o.y, o.z, width);
+        R.rd2[i] = make_float4(nd.x, nd.y, nd.z, spread + R.diffuse_spread);  // widen
     }
     R.thr2[i] = thr;
 }
@@ -1711,7 +1711,7 @@ __global__ void k_count_live(RenderView R, uint32_t* live) {
 // order, then NEE and the bounce; the path's state moves from its old layout
 // position q = order[i] to i in the next layout.
 #ifndef MCG_SHADE_MINB
-#define MCG_SHADE_MINB 1
+#define MCG_SHADE_MINB 5
 #endif
 template <bool kDeferred>
 __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
@@ -1731,9 +1731,12 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
     const uint32_t pid = R.pid[q];
     // the rest of the path's state is loaded now, in the same round trip as
-    // the shading record, not after the VM
+    // the shading record, not after the VM; what the VM does not change is
+    // written to the next layout right away, so little of it stays live
     float4 thr = R.thr[q];
-    const float4 Lq = R.L[q], ro = R.ro[q];
+    const float width = R.ro[q].w;
+    R.L2[i] = R.L[q];
+    R.pid2[i] = pid;
     const mcgd::ShadeIn in{s0.x, s0.y, s0.z, s1.x, s1.y, s1.z, rd.x, rd.y, rd.z,
                            s0.w, s1.w, s2.x, s2.y, s2.z, s2.w};
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
@@ -1745,9 +1748,7 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
-    R.L2[i] = Lq;
-    R.pid2[i] = pid;
-    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, ro, rd);
+    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, width, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
     mcgd::warp_add(R.stats + kStatWon, cnt.won);
