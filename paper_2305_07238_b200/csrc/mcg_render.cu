@@ -1696,16 +1696,6 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
     }
 }
 
-// Number of live paths after a sort (hits sort first): the first index whose
-// key is "no hit", found by the warp that straddles the boundary.
-__global__ void k_count_live(RenderView R, uint32_t* live) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R.n_paths) return;
-    const bool v = key_slot(R, R.skey[i]) < R.S.n_programs;
-    const bool prev = i == 0 ? true : key_slot(R, R.skey[i - 1]) < R.S.n_programs;
-    if (!v && prev) *live = i;
-    if (v && i + 1 == R.n_paths) *live = R.n_paths;
-}
 
 // Material evaluation of every live hit, in sorted (material, Morton)
 // order, then NEE and the bounce; the path's state moves from its old layout
@@ -1726,6 +1716,8 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     const bool valid = slot < R.S.n_programs;
     const unsigned live = __ballot_sync(mcgd::kFull, valid);
     if (!valid) return;
+    // live-path count (hits sort first): the last live position writes it
+    if (i + 1 == R.n_paths || key_slot(R, skey[i + 1]) >= R.S.n_programs) R.shadow_count[2] = i + 1;
     const uint32_t q = order[i];
     const unsigned grp = __match_any_sync(live, slot);
     const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
@@ -2015,11 +2007,6 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             sort_pairs_u32(ctx, R.keys, skey, R.vals, order, R.n_paths, key_bits);
             // counters: [0] shadow rays queued, [1] shadow cursor, [2] live paths, [3] trace cursor
             cuda_check(cudaMemsetAsync(R.shadow_count, 0, 16, ctx->stream), "memset");
-            {
-                LaunchScope ls(ctx, "count_live", 0.0);
-                k_count_live<<<grid, 256, 0, ctx->stream>>>(R, R.shadow_count + 2);
-                ls.done();
-            }
             if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, ctx->stream), "memset");
             {
                 LaunchScope ls(ctx, "shade", 0.0);
