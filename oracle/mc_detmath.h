@@ -8,7 +8,8 @@
  * Why: the reference calls glibc sinf/powf (include/matcache/value.hpp:125-137),
  * which CUDA's sinf/powf do not reproduce bit-for-bit. Both implementations
  * of the hot path therefore evaluate sin and pow with these double-precision
- * routines: the result is the float nearest the double-precision value,
+ * routines (and the sphere parameterization's atan2f/acosf, scene.cpp:234-235,
+ * likewise): the result is the float nearest the double-precision value,
  * i.e. correctly rounded except in astronomically rare ties. Against glibc
  * they agree except where glibc itself is not correctly rounded (measured
  * in tests/test_oracle_vs_ref.py; "parity vs glibc unpinned at <= 1 ulp").
@@ -161,6 +162,54 @@ static inline float mc_powf_nonneg(float xf, float yf) {
         return yf > 0.0f ? INFINITY : 0.0f;
     }
     return (float)mc_exp2(y * mc_log2_pos(x));
+}
+
+/* atan of t in [0, 1], ~1e-16 relative: reflect above tan(pi/8) around
+ * pi/4, halve the angle once (atan t = 2 atan(t / (1 + sqrt(1 + t^2))),
+ * |h| <= 0.199), then 12 terms of the Taylor series. */
+static inline double mc_atan_unit(double t) {
+    double base = 0.0;
+    if (t > 0.41421356237309504880) {
+        t = (t - 1.0) / (t + 1.0);
+        base = 0.78539816339744830962;
+    }
+    const double h = t / (1.0 + sqrt(1.0 + t * t));
+    const double z = h * h;
+    double p = -1.0 / 23.0;
+    p = p * z + 1.0 / 21.0;
+    p = p * z - 1.0 / 19.0;
+    p = p * z + 1.0 / 17.0;
+    p = p * z - 1.0 / 15.0;
+    p = p * z + 1.0 / 13.0;
+    p = p * z - 1.0 / 11.0;
+    p = p * z + 1.0 / 9.0;
+    p = p * z - 1.0 / 7.0;
+    p = p * z + 1.0 / 5.0;
+    p = p * z - 1.0 / 3.0;
+    return base + 2.0 * (h + (h * z) * p);
+}
+
+/* atan2 in double with C99 special cases (zeros, infinities, nan). */
+static inline double mc_atan2_d(double y, double x) {
+    if (x != x || y != y) return x + y;
+    const double ax = fabs(x), ay = fabs(y);
+    double a;
+    if (ay == 0.0) a = 0.0;
+    else if (isinf(ax) && isinf(ay)) a = 0.78539816339744830962;
+    else if (ay <= ax) a = mc_atan_unit(ay / ax);
+    else a = 1.57079632679489661923 - mc_atan_unit(ax / ay);
+    if (signbit(x)) a = 3.14159265358979323846 - a;
+    return copysign(a, y);
+}
+
+/* atan2f / acosf of the sphere parameterization (scene.cpp:234-235), each
+ * rounded once from double. */
+static inline float mc_atan2f(float y, float x) { return (float)mc_atan2_d((double)y, (double)x); }
+
+static inline float mc_acosf(float a) {
+    const double x = (double)a;
+    if (x != x || fabs(x) > 1.0) return (float)((x - x) / (x - x));
+    return (float)mc_atan2_d(sqrt((1.0 - x) * (1.0 + x)), x);
 }
 
 #ifdef __cplusplus

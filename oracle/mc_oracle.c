@@ -820,7 +820,7 @@ static void surface(const mcg_flat_scene* s, const Ray* r, const Hit* h, Surface
         o->duv2.y = uv[5] - uv[1];
         return;
     }
-    /* sphere: scene.cpp:227-246, libm atan2f/acosf as the reference */
+    /* sphere: scene.cpp:227-246; atan2f/acosf via mc_detmath.h (as the device) */
     const float kPi = 3.14159265358979323846f;
     const V3 c = v3_load(g);
     const float radius = g[3];
@@ -828,8 +828,8 @@ static void surface(const mcg_flat_scene* s, const Ray* r, const Hit* h, Surface
     V3 n = m;
     if (v3_dot(n, r->dir) > 0.0f) { n.x = -n.x; n.y = -n.y; n.z = -n.z; }
     o->normal = n;
-    o->uv.x = 0.5f + atan2f(m.z, m.x) / (2.0f * kPi);
-    o->uv.y = acosf(fminf(fmaxf(m.y, -1.0f), 1.0f)) / kPi;
+    o->uv.x = 0.5f + mc_atan2f(m.z, m.x) / (2.0f * kPi);
+    o->uv.y = mc_acosf(fminf(fmaxf(m.y, -1.0f), 1.0f)) / kPi;
     const float sin_t = sqrtf(fmaxf(0.0f, 1.0f - m.y * m.y));
     V3 du, dv;
     if (sin_t > 1e-6f) {
@@ -1167,6 +1167,13 @@ void mco_fbm_batch(const int32_t* octaves, const float* fp, const float* uv, siz
 }
 void mco_sin_wave_batch(const float* x, size_t n, float* out) {
     for (size_t i = 0; i < n; ++i) out[i] = mco_sin_wave(x[i]);
+}
+/* sphere uv's atan2f / acosf (mc_detmath.h) */
+void mco_atan2f_batch(const float* y, const float* x, size_t n, float* out) {
+    for (size_t i = 0; i < n; ++i) out[i] = mc_atan2f(y[i], x[i]);
+}
+void mco_acosf_batch(const float* x, size_t n, float* out) {
+    for (size_t i = 0; i < n; ++i) out[i] = mc_acosf(x[i]);
 }
 void mco_power_batch(const float* x, const float* y, size_t n, float* out) {
     for (size_t i = 0; i < n; ++i) out[i] = mco_power(x[i], y[i]);

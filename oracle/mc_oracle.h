@@ -50,6 +50,8 @@ void mco_footprint_batch(const float* in, size_t n, float* out);
 void mco_fbm_batch(const int32_t* octaves, const float* fp, const float* uv, size_t n, float* out);
 void mco_sin_wave_batch(const float* x, size_t n, float* out);
 void mco_power_batch(const float* x, const float* y, size_t n, float* out);
+void mco_atan2f_batch(const float* y, const float* x, size_t n, float* out);
+void mco_acosf_batch(const float* x, size_t n, float* out);
 
 /* The table (cache.cpp semantics; single-threaded). */
 typedef struct mco_cache mco_cache;

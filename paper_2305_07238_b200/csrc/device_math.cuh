@@ -408,6 +408,50 @@ __device__ __forceinline__ float det_powf_nonneg(float xf, float yf) {
     return static_cast<float>(exp2_det(static_cast<double>(yf) * log2_pos(static_cast<double>(xf))));
 }
 
+// atan2f / acosf of the sphere parameterization (scene.cpp:234-235): the
+// same double-precision sequence as oracle/mc_detmath.h (mc_atan_unit,
+// mc_atan2_d, mc_acosf), rounded once to float.
+__device__ __forceinline__ double atan_unit(double t) {
+    double base = 0.0;
+    if (t > 0.41421356237309504880) {
+        t = (t - 1.0) / (t + 1.0);
+        base = 0.78539816339744830962;
+    }
+    const double h = t / (1.0 + sqrt(1.0 + t * t));
+    const double z = h * h;
+    double p = -1.0 / 23.0;
+    p = p * z + 1.0 / 21.0;
+    p = p * z - 1.0 / 19.0;
+    p = p * z + 1.0 / 17.0;
+    p = p * z - 1.0 / 15.0;
+    p = p * z + 1.0 / 13.0;
+    p = p * z - 1.0 / 11.0;
+    p = p * z + 1.0 / 9.0;
+    p = p * z - 1.0 / 7.0;
+    p = p * z + 1.0 / 5.0;
+    p = p * z - 1.0 / 3.0;
+    return base + 2.0 * (h + (h * z) * p);
+}
+__device__ __forceinline__ double atan2_det(double y, double x) {
+    if (x != x || y != y) return x + y;
+    const double ax = fabs(x), ay = fabs(y);
+    double a;
+    if (ay == 0.0) a = 0.0;
+    else if (isinf(ax) && isinf(ay)) a = 0.78539816339744830962;
+    else if (ay <= ax) a = atan_unit(ay / ax);
+    else a = 1.57079632679489661923 - atan_unit(ax / ay);
+    if (signbit(x)) a = 3.14159265358979323846 - a;
+    return copysign(a, y);
+}
+__device__ __forceinline__ float det_atan2f(float y, float x) {
+    return static_cast<float>(atan2_det(static_cast<double>(y), static_cast<double>(x)));
+}
+__device__ __forceinline__ float det_acosf(float a) {
+    const double x = static_cast<double>(a);
+    if (x != x || fabs(x) > 1.0) return static_cast<float>((x - x) / (x - x));
+    return static_cast<float>(atan2_det(sqrt((1.0 - x) * (1.0 + x)), x));
+}
+
 // sin_wave / power node kernels (value.hpp:125-137)
 __device__ __forceinline__ float sin_wave(float x) { return 0.5f + 0.5f * det_sinf(x * kTwoPi); }
 __device__ __forceinline__ float power(float x, float y) {

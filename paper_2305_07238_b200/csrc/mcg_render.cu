@@ -393,15 +393,15 @@ __device__ Surface surface(const mcgd::SceneView& S, V3 o, V3 d, uint32_t prim, 
         s.d2 = make_float2(uv2.x - uv0.x, uv2.y - uv0.y);
         return s;
     }
-    // Sphere (scene.cpp:227-246). atan2f/acosf are CUDA's: sphere uv is the
-    // one quantity not bit-pinned to glibc.
+    // Sphere (scene.cpp:227-246). atan2f/acosf: the deterministic routines
+    // the oracle uses (device_math.cuh), within 1 ulp of glibc's.
     const float kPi = 3.14159265358979323846f;
     const V3 m = mcgd::normalize(s.p - V3{g0.x, g0.y, g0.z});
     V3 n = m;
     if (mcgd::dot(n, d) > 0.0f) n = V3{-n.x, -n.y, -n.z};
     s.n = n;
-    s.u = 0.5f + atan2f(m.z, m.x) / (2.0f * kPi);
-    s.v = acosf(fminf(fmaxf(m.y, -1.0f), 1.0f)) / kPi;
+    s.u = 0.5f + mcgd::det_atan2f(m.z, m.x) / (2.0f * kPi);
+    s.v = mcgd::det_acosf(fminf(fmaxf(m.y, -1.0f), 1.0f)) / kPi;
     const float sin_t = sqrtf(fmaxf(0.0f, 1.0f - m.y * m.y));
     const float r = g0.w;
     if (sin_t > 1e-6f) {

@@ -300,6 +300,7 @@ class SceneSpec:
     seed: int = 0
     libm_ops: bool = True
     tris_per_side: int = 10
+    spheres: int = 0           # analytic spheres (scene.cpp:80-97, 222-249) inside the room
 
 
 def _room(materials: list[int], rng: random.Random, uv_scale: float, n: int,
@@ -385,6 +386,12 @@ def build_scene(spec: SceneSpec, out_dir: str) -> str:
         ],
         "env": [0.05, 0.06, 0.08],
     }
+    if spec.spheres:
+        srng = random.Random(f"{BASE_SEED}:{spec.kind}:{spec.seed}:spheres")
+        scene["spheres"] = [
+            {"center": [_f(srng.uniform(-6.5, 6.5)), _f(srng.uniform(0.6, 4.0)), _f(srng.uniform(-8.0, 6.0))],
+             "radius": _f(srng.uniform(0.25, 0.9)), "material": ids[k % len(ids)]}
+            for k in range(spec.spheres)]
     path = os.path.join(out_dir, "scene.json")
     with open(path, "w") as f:
         json.dump(scene, f)

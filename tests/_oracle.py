@@ -74,6 +74,8 @@ class Oracle:
         L.mco_fbm_batch.argtypes = [vp, vp, vp, C.c_size_t, vp]
         L.mco_sin_wave_batch.argtypes = [vp, C.c_size_t, vp]
         L.mco_power_batch.argtypes = [vp, vp, C.c_size_t, vp]
+        L.mco_atan2f_batch.argtypes = [vp, vp, C.c_size_t, vp]
+        L.mco_acosf_batch.argtypes = [vp, C.c_size_t, vp]
         L.mco_rng.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32]
         L.mco_rng.restype = C.c_float
         L.mco_cache_new.argtypes = [C.c_uint64, C.c_uint32]
@@ -137,6 +139,18 @@ class Oracle:
         x = np.ascontiguousarray(x, np.float32)
         out = np.zeros_like(x)
         self.L.mco_sin_wave_batch(ptr(x), x.shape[0], ptr(out))
+        return out
+
+    def atan2f(self, y, x):
+        y, x = np.ascontiguousarray(y, np.float32), np.ascontiguousarray(x, np.float32)
+        out = np.zeros_like(x)
+        self.L.mco_atan2f_batch(ptr(y), ptr(x), x.shape[0], ptr(out))
+        return out
+
+    def acosf(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros_like(x)
+        self.L.mco_acosf_batch(ptr(x), x.shape[0], ptr(out))
         return out
 
     def power(self, x, y):

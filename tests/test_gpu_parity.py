@@ -156,11 +156,12 @@ def _params(w, h, spp, mode, spp_pass, nc=997, ne=4, mip=0):
     return _oracle.RenderParamsC(w, h, spp, 4, mode, mip, nc, ne, 0, 1, 0.2, 16, 0, 1, 0, 0, spp_pass)
 
 
-@pytest.mark.parametrize("kind,libm", [("cornell", False), ("classroom", True), ("monster", True)])
-def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm):
+@pytest.mark.parametrize("kind,libm,spheres", [("cornell", False, 0), ("classroom", True, 0), ("monster", True, 0),
+                                               ("junkshop", True, 16)])
+def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm, spheres):
     w, h, spp = 64, 48, 4
-    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=libm),
-                              f"{scene_dir}/r_{kind}")
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=libm, spheres=spheres),
+                              f"{scene_dir}/r_{kind}_{spheres}")
     s = load_scene(path)
     res = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=False), ctx=ctx)
     rad, nodes, samples, hps, st = oracle.render(s.flat, _params(w, h, spp, 0, 1))
@@ -170,11 +171,12 @@ def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm):
     assert res.stats.shading_points == st.shading_points
 
 
-@pytest.mark.parametrize("kind,k", [("cornell", 1), ("junkshop", 2), ("italianflat", 3)])
-def test_render_deterministic_matches_oracle(ctx, oracle, scene_dir, kind, k):
+@pytest.mark.parametrize("kind,k,spheres", [("cornell", 1, 0), ("junkshop", 2, 0), ("italianflat", 3, 0),
+                                            ("classroom", 2, 16)])
+def test_render_deterministic_matches_oracle(ctx, oracle, scene_dir, kind, k, spheres):
     w, h, spp, nc, ne = 64, 48, 6, 4099, 4
-    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=True),
-                              f"{scene_dir}/d_{kind}")
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=True, spheres=spheres),
+                              f"{scene_dir}/d_{kind}_{spheres}")
     s = load_scene(path)
     cache = MaterialCache(nc, ne, ctx)
     cfg = RenderConfig(width=w, height=h, spp=spp, cache_enabled=True, deterministic=True,
@@ -228,12 +230,13 @@ def _edge_rays(s, r, n):
     return np.concatenate([o, d], 1).astype(np.float32)
 
 
-@pytest.mark.parametrize("kind,tps", [("cornell", 8), ("classroom", 24)])
-def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, kind, tps):
+@pytest.mark.parametrize("kind,tps,spheres", [("cornell", 8, 0), ("classroom", 24, 0), ("cornell", 8, 24)])
+def test_scene_queries_every_traversal_matches_oracle(ctx, oracle, scene_dir, kind, tps, spheres):
     """Closest hit and any hit through each traversal variant (per-thread DFS,
     child pairs, 4-wide, speculative 4-wide, packet) == the oracle's reference DFS,
     bit for bit, on random rays and on rays aimed at vertices and edges."""
-    path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=tps), f"{scene_dir}/q_{kind}")
+    path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=tps, spheres=spheres),
+                              f"{scene_dir}/q_{kind}_{spheres}")
     s = load_scene(path)
     ctx.upload(s)
     r = np.random.default_rng(11)

@@ -155,9 +155,13 @@ def test_vm_with_cache_matches_reference(oracle, ref, scene_dir):
         ref.cache_free(rc)
 
 
-@pytest.mark.parametrize("kind", ["cornell", "classroom"])
-def test_bvh_queries_bit_exact(oracle, ref, scene_dir, kind):
-    path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=8), f"{scene_dir}/bvh_{kind}")
+@pytest.mark.parametrize("kind,spheres", [("cornell", 0), ("classroom", 0), ("cornell", 24)])
+def test_bvh_queries_bit_exact(oracle, ref, scene_dir, kind, spheres):
+    """Closest / any hit vs Scene::intersect / occluded: bit-exact, except a
+    sphere hit's uv (atan2f/acosf, scene.cpp:234-235), which the oracle and
+    the device take from the deterministic routines: within 1 ulp of glibc's."""
+    path = scenes.build_scene(scenes.SceneSpec(kind, 16, 16, tris_per_side=8, spheres=spheres),
+                              f"{scene_dir}/bvh_{kind}_{spheres}")
     s = load_scene(path)
     rs = ref.scene_load(path)
     r = np.random.default_rng(4)
@@ -168,7 +172,15 @@ def test_bvh_queries_bit_exact(oracle, ref, scene_dir, kind):
     d[:200] = [0, -1, 0]   # axis-aligned rays (infinite reciprocals)
     d[200:400] = [1, 0, 0]
     rays = np.concatenate([o, d], 1).astype(np.float32)
-    np.testing.assert_array_equal(bits(oracle.intersect(s.flat, rays)), bits(ref.intersect(rs, rays)))
+    A, B = oracle.intersect(s.flat, rays), ref.intersect(rs, rays)
+    if spheres:
+        # u = 0.5 + atan2f/(2 pi), v = acosf/pi: one ulp of atan2f/acosf
+        # (<= 2^-22 on [0, pi]) moves u or v by at most 2^-23 + a rounding.
+        du = np.abs(A[:, 8:10].astype(np.float64) - B[:, 8:10])
+        assert du.max() <= 2.0 ** -22
+        assert 0 < (du.sum(1) > 0).mean() < 0.05
+        A, B = np.delete(A, [8, 9], 1), np.delete(B, [8, 9], 1)
+    np.testing.assert_array_equal(bits(A), bits(B))
     tm = r.uniform(0.01, 20, n).astype(np.float32)
     np.testing.assert_array_equal(oracle.occluded(s.flat, rays, 1e-4, tm), ref.occluded(rs, rays, 1e-4, tm))
     ref.L.ref_scene_free(rs)
@@ -204,6 +216,25 @@ def test_render_matches_reference_backed_render(oracle, ref, scene_dir, kind, li
     else:
         np.testing.assert_array_equal(bits(A[0]), bits(B[0]))
     for f in ("lookups", "hits", "inserts_won", "inserts_lost_full", "instructions_executed", "shading_points"):
+        assert getattr(A[4], f) == getattr(B[4], f), f
+    ref.L.ref_scene_free(rs)
+
+
+def test_render_with_spheres_matches_reference_backed_render(oracle, ref, scene_dir):
+    """Cache off, a scene with analytic spheres: sphere uv differs from
+    glibc's by <= 1 ulp of atan2f/acosf, so radiance is compared at the
+    north-star 1e-5 relative bound; everything else exactly."""
+    w, h, spp = 40, 28, 4
+    path = scenes.build_scene(scenes.SceneSpec("junkshop", w, h, tris_per_side=5, spheres=16),
+                              f"{scene_dir}/rr_spheres")
+    s = load_scene(path)
+    rs = ref.scene_load(path)
+    P = RenderParamsC(w, h, spp, 4, 0, 0, 1021, 4, 0, 1, 0.2, 16, 0, 1, 0, 0, 1)
+    A = oracle.render(s.flat, P)
+    B = ref.render(rs, P, w, h)
+    np.testing.assert_array_equal(A[2], B[2])
+    assert np.abs(A[0] - B[0]).max() <= 1e-5 * np.abs(B[0]).max()
+    for f in ("instructions_executed", "shading_points"):
         assert getattr(A[4], f) == getattr(B[4], f), f
     ref.L.ref_scene_free(rs)
 
