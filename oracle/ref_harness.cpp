@@ -36,6 +36,20 @@
 
 using namespace matcache;
 
+// Read access to Scene's private BVH (scene.hpp:114-118) without touching the
+// reference: explicit template instantiation may name private members.
+namespace {
+struct BvhTag {
+    using type = std::vector<detail::BvhNode> Scene::*;
+    friend type bvh_member(BvhTag);
+};
+template <typename Tag, typename Tag::type M>
+struct Expose {
+    friend typename Tag::type bvh_member(Tag) { return M; }
+};
+template struct Expose<BvhTag, &Scene::bvh_>;
+}  // namespace
+
 namespace {
 
 thread_local std::string g_err;
@@ -307,6 +321,24 @@ void ref_scene_intersect(void* s, const float* rays, size_t n, float t_min, floa
                                 0.0f, 0.0f};
         std::memcpy(o, vals, sizeof(vals));
     }
+}
+// The reference's BVH nodes (scene.cpp:154-194), 10 words each: bounds_min,
+// bounds_max (float bits), left, right, first, count. Returns the node count;
+// writes min(count, cap) nodes.
+size_t ref_scene_bvh(void* s, uint32_t* out, size_t cap) {
+    const Scene& scene = *static_cast<Scene*>(s);
+    const std::vector<detail::BvhNode>& nodes = scene.*bvh_member(BvhTag{});
+    for (size_t i = 0; i < nodes.size() && i < cap; ++i) {
+        const detail::BvhNode& n = nodes[i];
+        const float b[6] = {n.bounds_min.x, n.bounds_min.y, n.bounds_min.z,
+                            n.bounds_max.x, n.bounds_max.y, n.bounds_max.z};
+        std::memcpy(out + 10 * i, b, sizeof(b));
+        std::memcpy(out + 10 * i + 6, &n.left, 4);
+        std::memcpy(out + 10 * i + 7, &n.right, 4);
+        out[10 * i + 8] = n.first;
+        out[10 * i + 9] = n.count;
+    }
+    return nodes.size();
 }
 void ref_scene_occluded(void* s, const float* rays, size_t n, float t_min, const float* t_max,
                         uint8_t* out) {

@@ -13,12 +13,16 @@
 // equal t resolve by visit order. It is rebuilt with the same median split
 // and the same std::nth_element call over the same primitive order.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cctype>
 #include <cmath>
 #include <cstring>
 #include <fstream>
 #include <map>
 #include <sstream>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 
@@ -169,69 +173,108 @@ struct Prim {
     uint32_t sphere;
 };
 
+// The reference's recursive median split (scene.cpp:154-194), producing the
+// identical tree faster: primitive boxes and centroids are computed once
+// (the reference recomputes them inside every comparison; the values, hence
+// every comparison and std::nth_element's permutation, are the same), and
+// the top levels build their two subtrees on two threads into private node
+// arrays that are then appended in the reference's preorder (node, left
+// subtree, right subtree) with child indices rebased.
 class BvhBuilder {
 public:
-    BvhBuilder(const SceneData& s, const std::vector<Prim>& prims, std::vector<uint32_t>& order,
-               std::vector<mcg_bvh_node>& nodes)
-        : s_(s), prims_(prims), order_(order), nodes_(nodes) {}
-
-    Box bounds(uint32_t prim) const {
-        Box b;
-        const Prim& p = prims_[prim];
-        if (p.mesh != ~0u) {
-            const MeshData& m = s_.meshes[p.mesh];
-            for (int k = 0; k < 3; ++k) b.grow(load3(&m.positions[3 * m.indices[p.first + k]]));
-        } else {
-            const mcg_sphere_in& sp = s_.spheres[p.sphere];
-            const V3 c = load3(sp.center);
-            const V3 r{sp.radius, sp.radius, sp.radius};
-            b.grow(sub(c, r));
-            b.grow(add(c, r));
+    BvhBuilder(const SceneData& s, const std::vector<Prim>& prims, std::vector<uint32_t>& order)
+        : order_(order), boxes_(prims.size()), key_{std::vector<float>(prims.size()),
+                                                   std::vector<float>(prims.size()),
+                                                   std::vector<float>(prims.size())} {
+        for (size_t i = 0; i < prims.size(); ++i) {
+            Box b;
+            const Prim& p = prims[i];
+            if (p.mesh != ~0u) {
+                const MeshData& m = s.meshes[p.mesh];
+                for (int k = 0; k < 3; ++k) b.grow(load3(&m.positions[3 * m.indices[p.first + k]]));
+            } else {
+                const mcg_sphere_in& sp = s.spheres[p.sphere];
+                const V3 c = load3(sp.center);
+                const V3 r{sp.radius, sp.radius, sp.radius};
+                b.grow(sub(c, r));
+                b.grow(add(c, r));
+            }
+            boxes_[i] = b;
+            const V3 c = b.center();
+            key_[0][i] = c.x;
+            key_[1][i] = c.y;
+            key_[2][i] = c.z;
         }
-        return b;
     }
 
-    // Recursive median split, node index assigned before the children
-    // (scene.cpp:154-194).
-    int32_t build(uint32_t first, uint32_t count) {
+    void run(std::vector<mcg_bvh_node>& nodes) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        int depth = 0;
+        while ((2u << depth) <= hw && depth < 6) ++depth;  // 2^depth parallel subtrees
+        build(0, static_cast<uint32_t>(order_.size()), nodes, order_.size() >= 65536 ? depth : 0);
+    }
+
+private:
+    // Appends the subtree over order_[first, first+count) to `out`; returns
+    // its root's index in `out`.
+    int32_t build(uint32_t first, uint32_t count, std::vector<mcg_bvh_node>& out, int par) {
         Box all, centers;
         for (uint32_t i = first; i < first + count; ++i) {
-            const Box b = bounds(order_[i]);
+            const Box& b = boxes_[order_[i]];
             all.grow(b);
             centers.grow(b.center());
         }
-        const int32_t index = static_cast<int32_t>(nodes_.size());
-        nodes_.push_back(mcg_bvh_node{{all.lo.x, all.lo.y, all.lo.z}, 0,
-                                      {all.hi.x, all.hi.y, all.hi.z}, 0});
+        const int32_t index = static_cast<int32_t>(out.size());
+        out.push_back(mcg_bvh_node{{all.lo.x, all.lo.y, all.lo.z}, 0,
+                                   {all.hi.x, all.hi.y, all.hi.z}, 0});
         if (count <= 4) {
-            nodes_[index].a = ~static_cast<int32_t>(first);
-            nodes_[index].b = static_cast<int32_t>(count);
+            out[index].a = ~static_cast<int32_t>(first);
+            out[index].b = static_cast<int32_t>(count);
             return index;
         }
         const V3 ext = sub(centers.hi, centers.lo);
         int axis = 0;
         if (ext.y > ext.x) axis = 1;
         if (ext.z > (axis == 0 ? ext.x : ext.y)) axis = 2;
-        auto key = [&](uint32_t prim) {
-            const V3 c = bounds(prim).center();
-            return axis == 0 ? c.x : (axis == 1 ? c.y : c.z);
-        };
+        const float* key = key_[axis].data();
         const uint32_t mid = first + count / 2;
         std::nth_element(order_.begin() + first, order_.begin() + mid,
                          order_.begin() + first + count,
-                         [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
-        const int32_t left = build(first, mid - first);
-        const int32_t right = build(mid, first + count - mid);
-        nodes_[index].a = left;
-        nodes_[index].b = right;
+                         [key](uint32_t a, uint32_t b) { return key[a] < key[b]; });
+        if (par <= 0) {
+            const int32_t left = build(first, mid - first, out, 0);
+            const int32_t right = build(mid, first + count - mid, out, 0);
+            out[index].a = left;
+            out[index].b = right;
+            return index;
+        }
+        std::vector<mcg_bvh_node> lo, hi;
+        std::thread t([&] { build(first, mid - first, lo, par - 1); });
+        build(mid, first + count - mid, hi, par - 1);
+        t.join();
+        const int32_t base_lo = static_cast<int32_t>(out.size());
+        append(out, lo, base_lo);
+        const int32_t base_hi = static_cast<int32_t>(out.size());
+        append(out, hi, base_hi);
+        out[index].a = base_lo;
+        out[index].b = base_hi;
         return index;
     }
 
-private:
-    const SceneData& s_;
-    const std::vector<Prim>& prims_;
+    static void append(std::vector<mcg_bvh_node>& out, const std::vector<mcg_bvh_node>& part,
+                       int32_t base) {
+        for (mcg_bvh_node n : part) {
+            if (n.a >= 0) {  // inner node: a, b are child indices in `part`
+                n.a += base;
+                n.b += base;
+            }
+            out.push_back(n);
+        }
+    }
+
     std::vector<uint32_t>& order_;
-    std::vector<mcg_bvh_node>& nodes_;
+    std::vector<Box> boxes_;
+    std::vector<float> key_[3];
 };
 
 }  // namespace
@@ -277,7 +320,7 @@ void prepare_scene(SceneData& s) {
     for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
     s.nodes.clear();
     if (!prims.empty()) {
-        BvhBuilder(s, prims, order, s.nodes).build(0, static_cast<uint32_t>(prims.size()));
+        BvhBuilder(s, prims, order).run(s.nodes);
     }
 
     // Leaf-ordered primitive arrays.
@@ -385,11 +428,27 @@ void fill_flat(const SceneData& s, mcg_flat_scene* f) {
     f->texels = s.texels.data();
 }
 
+// MCG_LOAD_TIMING=1: per-phase wall times of a scene load on stderr.
+struct LoadTimer {
+    bool on = std::getenv("MCG_LOAD_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void phase(const char* name) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mcg load] %-20s %8.3f s\n", name,
+                     std::chrono::duration<double>(now - t).count());
+        t = now;
+    }
+};
+
 SceneData load_scene_file(const std::string& path, int min_subtree_size) {
+    LoadTimer timer;
     const std::string text = slurp(path, MCG_ERR_SCENE, "scene file");
+    timer.phase("read");
     json doc;
     try {
         doc = json::parse(text);
+        timer.phase("json parse");
     } catch (const json::parse_error& e) {
         scene_error(std::string("scene JSON parse error: ") + e.what());
     }
@@ -467,8 +526,10 @@ SceneData load_scene_file(const std::string& path, int min_subtree_size) {
     } catch (const json::exception& e) {
         scene_error(std::string("scene JSON schema error: ") + e.what());
     }
+    timer.phase("materials + meshes");
     flatten_programs(s);
     prepare_scene(s);
+    timer.phase("bvh + flat layout");
     return s;
 }
 

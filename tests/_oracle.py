@@ -267,6 +267,8 @@ class Ref:
         L.ref_scene_eval_reference.argtypes = [vp, C.c_int, vp, C.c_size_t, vp]
         L.ref_scene_intersect.argtypes = [vp, vp, C.c_size_t, C.c_float, C.c_float, vp]
         L.ref_scene_occluded.argtypes = [vp, vp, C.c_size_t, C.c_float, vp, vp]
+        L.ref_scene_bvh.argtypes = [vp, vp, C.c_size_t]
+        L.ref_scene_bvh.restype = C.c_size_t
         L.ref_render.argtypes = [vp, C.POINTER(RenderParamsC), vp, vp, vp, vp, vp,
                                  C.POINTER(RenderStatsC)]
 
@@ -406,6 +408,14 @@ class Ref:
         rays = np.ascontiguousarray(rays, np.float32)
         out = np.zeros((rays.shape[0], 24), np.float32)
         self.L.ref_scene_intersect(s, ptr(rays), rays.shape[0], tmin, tmax, ptr(out))
+        return out
+
+    def bvh(self, s):
+        """The reference Scene's BVH nodes as (n, 10) uint32: min, max (float
+        bits), left, right, first, count."""
+        n = self.L.ref_scene_bvh(s, None, 0)
+        out = np.zeros((n, 10), np.uint32)
+        self.L.ref_scene_bvh(s, ptr(out), n)
         return out
 
     def occluded(self, s, rays, tmin, tmax):

@@ -2,6 +2,8 @@
 (oracle/_ref/libmcref.so): every stage of the path, bit for bit."""
 import os
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -184,6 +186,35 @@ def test_bvh_queries_bit_exact(oracle, ref, scene_dir, kind, spheres):
     tm = r.uniform(0.01, 20, n).astype(np.float32)
     np.testing.assert_array_equal(oracle.occluded(s.flat, rays, 1e-4, tm), ref.occluded(rs, rays, 1e-4, tm))
     ref.L.ref_scene_free(rs)
+
+
+@pytest.mark.parametrize("tps,spheres", [(6, 8), (80, 40)])
+def test_bvh_nodes_identical_to_reference(ref, scene_dir, tps, spheres):
+    """libmcg's BVH build (precomputed centroids; subtrees on parallel threads
+    above 65 536 primitives) == Scene::prepare's tree node for node: bounds,
+    children, leaf ranges (scene.cpp:154-194)."""
+    path = scenes.build_scene(scenes.SceneSpec("classroom", 16, 16, tris_per_side=tps, spheres=spheres),
+                              f"{scene_dir}/bvhn_{tps}")
+    s = load_scene(path)
+    rs = ref.scene_load(path)
+    want = ref.bvh(rs)
+    ref.L.ref_scene_free(rs)
+    f = s.flat
+    got = np.ctypeslib.as_array(ctypes.cast(f.nodes, ctypes.POINTER(ctypes.c_uint32)), (f.n_nodes * 8,))
+    got = got.reshape(-1, 8)
+    assert got.shape[0] == want.shape[0]
+    if tps == 80:
+        assert f.n_prims >= 65536
+    np.testing.assert_array_equal(got[:, 0:3], want[:, 0:3])
+    np.testing.assert_array_equal(got[:, 4:7], want[:, 3:6])
+    a, b = got[:, 3].view(np.int32), got[:, 7].view(np.int32)
+    left, right = want[:, 6].view(np.int32), want[:, 7].view(np.int32)
+    leaf = left < 0
+    np.testing.assert_array_equal(a < 0, leaf)
+    np.testing.assert_array_equal(a[~leaf], left[~leaf])
+    np.testing.assert_array_equal(b[~leaf], right[~leaf])
+    np.testing.assert_array_equal(~a[leaf], want[leaf, 8].view(np.int32))
+    np.testing.assert_array_equal(b[leaf], want[leaf, 9].view(np.int32))
 
 
 def test_camera_setup_matches(oracle, scene_dir):
