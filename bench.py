@@ -45,7 +45,7 @@ W, H, SPP = 1920, 1080, 128
 N_CELLS, N_ENTRIES = 10_000_000, 10
 SCENE_KIND = "classroom"
 TRIS_PER_SIDE = 24
-PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 4, 8          # HBM table: warp-cooperative, one round trip
+PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 7, 8          # HBM table: warp-cooperative, one round trip, software-pipelined
 PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM = 0, 8    # L2-resident table: per-lane scan (issue-bound)
 METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
 
@@ -362,7 +362,14 @@ def main() -> None:
 
             table = MaterialCache(N_CELLS, N_ENTRIES, ctx)
             pr = {"bound": "hbm", "unit": "GB/s", "peak": peak, "table": "1e7x10 (800 MB)",
-                  "kernel": "k_probe_bench", "random_access_ceiling_gbs": 2900.0, "descriptors": n}
+                  "kernel": "k_probe_bench", "descriptors": n,
+                  # profiles/scripts/rand_read2.cu (B200, 800 MB buffer): random 64-byte
+                  # reads by 4 lanes x 16 B top out at 43.9 G accesses/s (each costs a
+                  # 128-byte DRAM fetch); one 64-byte head read per lookup at that rate
+                  # is 3512 GB/s in 80-byte-cell algorithmic bytes.
+                  "random_access_ceiling": {"g_accesses_per_s": 43.9, "bytes_per_access": 64,
+                                            "algorithmic_gbs_80B_cells": 3512.0,
+                                            "source": "profiles/scripts/rand_read2.cu"}}
             pr.update(legs(table, PROBE_VARIANT, PROBE_BLOCKS_PER_SM))
             table.close()
             # replay of the bench render's own lookups (first 2^26 of them)
@@ -382,6 +389,8 @@ def main() -> None:
             fresh.close()
             pr["trace_replay"] = {"descriptors": int(n_tr), "source": "the bench render's first lookups",
                                   "achieved": b_r / ms_r / 1e6, "frac": b_r / ms_r / 1e6 / peak,
+                                  # + the 20-byte descriptor records the kernel streams in
+                                  "achieved_incl_descriptors": (b_r + 20.0 * n_tr) / ms_r / 1e6,
                                   "mprobes_per_s": n_tr / ms_r / 1e3,
                                   "hit_rate": c_r["hits"] / max(1, c_r["lookups"])}
             small = MaterialCache(100_000, N_ENTRIES, ctx)

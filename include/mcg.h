@@ -205,7 +205,9 @@ mcg_status mcg_audit_dump(const char* path, mcg_audit_report* out);
  * (warp-aggregated), up to `capacity` records; stop returns the count kept.
  * mcg_probe_replay runs a descriptor list (host) through the table as the VM
  * would -- lookup, insert on a miss -- with the warp-cooperative probe, and
- * returns the device time, the algorithmic bytes and the outcome counts. */
+ * returns the device time, the algorithmic bytes and the outcome counts
+ * (blocks_per_sm < 0: |blocks_per_sm| blocks per SM, software-pipelined,
+ * for A/B runs). */
 mcg_status mcg_cache_trace_start(mcg_cache* cache, uint64_t capacity);
 mcg_status mcg_cache_trace_stop(mcg_cache* cache, uint64_t* recorded);
 mcg_status mcg_cache_trace_read(mcg_cache* cache, uint64_t first, size_t n, mcg_descriptor* out);
@@ -218,7 +220,10 @@ mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t 
  * selects the probe variant v: 0 two-round per-lane scan (first 16 B, then
  * the rest), 1 one-round per-lane scan (whole cell), 2 warp-cooperative
  * (coalesced whole cells + ballots; Ne = 10 only), 4 warp-cooperative with
- * 16-byte lanes (one round trip per probe; Ne even <= 10). Returns the kernel's
+ * 16-byte lanes (one round trip per probe; Ne even <= 10); 5 / 6 / 7 the same
+ * probe software-pipelined over 2 / 4 / 1 batches of 32 descriptors per warp
+ * (all head loads of the step in flight while the next step is hashed);
+ * + 256*b runs b blocks of 256 threads per SM (default 8). Returns the kernel's
  * device milliseconds and the algorithmic bytes it moved. */
 mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t phase,
                            int32_t iters, double* ms_out, double* algorithmic_bytes_out);

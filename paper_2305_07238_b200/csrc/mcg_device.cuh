@@ -237,37 +237,51 @@ __device__ __forceinline__ Probe probe_warp(const CacheView& c, uint64_t cell, u
 // descriptor's lane reads the outcome from the deciding lane. A scan the head
 // does not end continues in the cell's tail, lane by lane. Every lane of the
 // warp must call it.
-__device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell, uint32_t check,
-                                              bool valid) {
+// Issue half of probe_warp16: every round's 16-byte head load for the warp's
+// 32 cells (w[] holds them; lanes without a cell read ~0, which never ends a
+// scan). Split from the resolve half so a kernel can keep several batches of
+// loads in flight and do independent work (the next batch's hashes) while
+// they are outstanding.
+__device__ __forceinline__ void probe_warp16_issue(const CacheView& c, uint64_t cell, bool valid,
+                                                   ulonglong2 (&w)[4]) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lpc = c.head_n >> 1;      // lanes (pairs) per cell head
     const uint32_t cpr = 32u / lpc;          // cells per round
     const uint32_t rounds = (32u + cpr - 1u) / cpr;   // <= 4 for head_n <= 8
     const uint32_t g = lane / lpc, k = lane - g * lpc;
-    ulonglong2 w[4];
-    uint32_t chk[4];
+    // n_cells < 2^32 (mcg_cache_create), so a cell index fits one shuffle and
+    // 0xffffffff can mark a lane without a cell.
+    const uint32_t c32 = valid ? static_cast<uint32_t>(cell) : 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         w[r] = make_ulonglong2(~0ull, ~0ull);
-        chk[r] = 0u;
         if (static_cast<uint32_t>(r) < rounds) {
             const uint32_t owner = static_cast<uint32_t>(r) * cpr + g;
-            const uint64_t oc = __shfl_sync(kFull, cell, owner & 31u);
-            const bool ov = __shfl_sync(kFull, valid, owner & 31u);
-            chk[r] = __shfl_sync(kFull, check, owner & 31u);
-            if (g < cpr && owner < 32u && ov) {
+            const uint32_t oc = __shfl_sync(kFull, c32, owner & 31u);
+            if (g < cpr && owner < 32u && oc != 0xffffffffu) {
                 w[r] = __ldcg(reinterpret_cast<const ulonglong2*>(head_words(c, oc)) + k);
             }
         }
     }
+}
+
+// Resolve half of probe_warp16 over the words probe_warp16_issue loaded.
+__device__ __forceinline__ Probe probe_warp16_resolve(const CacheView& c, uint64_t cell, uint32_t check,
+                                                      bool valid, const ulonglong2 (&w)[4]) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lpc = c.head_n >> 1;
+    const uint32_t cpr = 32u / lpc;
+    const uint32_t rounds = (32u + cpr - 1u) / cpr;
+    const uint32_t g = lane / lpc, k = lane - g * lpc;
     Probe mine{0u, -1, false};
     bool ended = false;
     const uint32_t my_round = lane / cpr, my_g = lane - my_round * cpr;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         if (static_cast<uint32_t>(r) >= rounds) break;
-        const bool e0 = w[r].x == 0ull, m0 = static_cast<uint32_t>(w[r].x >> 32) == chk[r];
-        const bool e1 = w[r].y == 0ull, m1 = static_cast<uint32_t>(w[r].y >> 32) == chk[r];
+        const uint32_t chk = __shfl_sync(kFull, check, (static_cast<uint32_t>(r) * cpr + g) & 31u);
+        const bool e0 = w[r].x == 0ull, m0 = static_cast<uint32_t>(w[r].x >> 32) == chk;
+        const bool e1 = w[r].y == 0ull, m1 = static_cast<uint32_t>(w[r].y >> 32) == chk;
         const bool first0 = e0 || m0;
         const unsigned bal = __ballot_sync(kFull, (first0 || e1 || m1) && g < cpr);
         const bool hit = first0 ? (m0 && !e0) : (m1 && !e1);
@@ -296,6 +310,13 @@ __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell,
         }
     }
     return mine;
+}
+
+__device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell, uint32_t check,
+                                              bool valid) {
+    ulonglong2 w[4];
+    probe_warp16_issue(c, cell, valid, w);
+    return probe_warp16_resolve(c, cell, check, valid, w);
 }
 
 // Cooperative probe inside a lane group `grp` (the VM's material group,

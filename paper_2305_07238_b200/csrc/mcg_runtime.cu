@@ -270,13 +270,15 @@ __global__ void k_occupied(const uint64_t* slots, uint64_t n, unsigned long long
 // Probe microbenchmark: descriptors are generated in registers
 // (mat < 8, node < 256, mip <= 16, texels uniform in 2^mip) so the kernel's
 // DRAM traffic is the table's alone.
+// One splitmix64 output feeds every field (bits 0-2 mat, 3-10 node, 11-31 ->
+// mip mod 17, 32-47 texel x, 48-63 texel y; mip <= 16 so 16 texel bits
+// suffice), so the generator costs one mix64 next to the probe's six.
 __device__ __forceinline__ Desc bench_desc(uint64_t seed, uint64_t i) {
     const uint64_t h = mcgd::mix64(seed + 0x9e3779b97f4a7c15ull * (i + 1));
-    const uint64_t h2 = mcgd::mix64(h ^ 0x5851f42d4c957f2dull);
-    const uint32_t mip = static_cast<uint32_t>((h >> 11) % 17u);
+    const uint32_t lo = static_cast<uint32_t>(h), hi = static_cast<uint32_t>(h >> 32);
+    const uint32_t mip = (lo >> 11) % 17u;
     const uint32_t mask = (1u << mip) - 1u;
-    return Desc{static_cast<uint32_t>(h & 7u), static_cast<uint32_t>((h >> 3) & 255u),
-                static_cast<uint32_t>(h2) & mask, static_cast<uint32_t>(h2 >> 32) & mask, mip};
+    return Desc{lo & 7u, (lo >> 3) & 255u, hi & mask, (hi >> 16) & mask, mip};
 }
 
 #ifndef MCG_PROBE_MINB
@@ -324,29 +326,127 @@ __global__ void __launch_bounds__(256, MCG_PROBE_MINB) k_probe_bench(CacheView c
     mcgd::warp_add(counters + 5, inserts);
 }
 
+// Software-pipelined cooperative probe (variants 5/6): a warp takes U batches
+// of 32 descriptors per step, issues every head load of all U batches (4U
+// 16-byte loads per lane in flight), then hashes the next step's descriptors
+// while the loads are outstanding, and only then resolves the scans. Same
+// scan, same outcomes as variant 4; more DRAM requests in flight per warp
+// and the hashing off the critical path.
+// Register budgets: 64 (U = 1, 4 blocks of 256 per SM), 80 (U = 2, 3 blocks),
+// 128 (U = 4, 2 blocks): more loads in flight per SM as U grows.
+// kNoHash (diagnostic only, variants 8/9): the cell and check come from one
+// multiply-high of a counter hash instead of the reference's descriptor hash,
+// to measure what the hashing costs the probe.
+template <int U, bool kNoHash = false>
+__global__ void __launch_bounds__(256, U == 1 ? 4 : (U == 2 ? 3 : 2)) k_probe_bench_pipe(CacheView c, uint64_t n, uint64_t seed,
+                                                          int phase, unsigned long long* counters) {
+    uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x * U;
+    uint64_t i0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u)) * U;
+    uint64_t cell[U], h[U];
+    uint32_t chk[U];
+    auto gen = [&](uint64_t i, uint64_t& hh, uint32_t& ck, uint64_t& cl) {
+        if (kNoHash) {
+            hh = (seed + i) * 0x9e3779b97f4a7c15ull;
+            ck = static_cast<uint32_t>(hh) | 1u;
+            cl = ((hh >> 32) * c.n_cells) >> 32;
+        } else {
+            mcgd::hash_desc(bench_desc(seed, i), hh, ck);
+            cl = mcgd::fast_mod(hh, c.n_cells, c.magic);
+        }
+    };
+#pragma unroll
+    for (int u = 0; u < U; ++u) gen(i0 + 32u * u + lane, h[u], chk[u], cell[u]);
+    for (; i0 < n; i0 += step) {
+        ulonglong2 w[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) mcgd::probe_warp16_issue(c, cell[u], i0 + 32u * u + lane < n, w[u]);
+        uint64_t ncell[U], nh[U];
+        uint32_t nchk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) gen(i0 + step + 32u * u + lane, nh[u], nchk[u], ncell[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + 32u * u + lane;
+            const bool valid = i < n;
+            const mcgd::Probe p = mcgd::probe_warp16_resolve(c, cell[u], chk[u], valid, w[u]);
+            if (valid) {
+                const bool insert = phase == 0 || (phase == 2 && (i & 1u));
+                if (!insert) {
+                    ++looks;
+                    hits += p.hit;
+                } else {
+                    ++inserts;
+                    if (!p.hit) {
+                        const int r = mcgd::insert_at(c, cell[u], p.where, chk[u],
+                                                      static_cast<uint32_t>(h[u]) | 0x80000000u);
+                        won += r == MCG_INSERT_WON;
+                        full += r == MCG_INSERT_CELL_FULL;
+                    }
+                }
+            }
+            cell[u] = ncell[u];
+            h[u] = nh[u];
+            chk[u] = nchk[u];
+        }
+    }
+    mcgd::warp_add(counters + 0, looks);
+    mcgd::warp_add(counters + 1, hits);
+    mcgd::warp_add(counters + 2, won);
+    mcgd::warp_add(counters + 3, full);
+    mcgd::warp_add(counters + 5, inserts);
+}
+
 // Replay of a recorded descriptor trace: in trace order, each
 // warp takes 32 consecutive lookups, probes them cooperatively and inserts
 // the misses (payload from the hash), as the VM's lookup + store would.
-__global__ void __launch_bounds__(256) k_probe_replay(CacheView c, const mcg_descriptor* d, uint64_t n,
-                                                      unsigned long long* counters) {
+template <bool kPipe>
+__global__ void __launch_bounds__(256, 4) k_probe_replay(CacheView c, const mcg_descriptor* d, uint64_t n,
+                                                         unsigned long long* counters) {
+    // kPipe: software-pipelined like k_probe_bench_pipe -- the step's head
+    // loads are issued, then the next step's descriptors are read and hashed
+    // while they are outstanding (one round trip for both). Off by default:
+    // a render's trace is coherent and mostly hits L2, where it measured slower.
     uint32_t looks = 0, hits = 0, won = 0, full = 0;
+    const uint32_t lane = threadIdx.x & 31u;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); i0 < n;
-         i0 += stride) {
-        const uint64_t i = i0 + (threadIdx.x & 31u);
+    uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u);
+    auto gen = [&](uint64_t i, uint64_t& h, uint32_t& chk, uint64_t& cell) {
+        h = 0;
+        chk = 0;
+        if (i < n) mcgd::hash_desc(load_desc(d, i), h, chk);
+        cell = i < n ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
+    };
+    uint64_t h, cell;
+    uint32_t chk;
+    gen(i0 + lane, h, chk, cell);
+    for (; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + lane;
         const bool valid = i < n;
-        uint64_t h = 0;
-        uint32_t chk = 0;
-        if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
-        const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
-        const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
-        if (!valid) continue;
-        ++looks;
-        hits += p.hit;
-        if (!p.hit) {
-            const int r = mcgd::insert_at(c, cell, p.where, chk, static_cast<uint32_t>(h) | 0x80000000u);
-            won += r == MCG_INSERT_WON;
-            full += r == MCG_INSERT_CELL_FULL;
+        ulonglong2 w[4];
+        const bool coop = (c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u;
+        if (coop) mcgd::probe_warp16_issue(c, cell, valid, w);
+        uint64_t nh = 0, ncell = 0;
+        uint32_t nchk = 0;
+        if (kPipe) gen(i + stride, nh, nchk, ncell);
+        const mcgd::Probe p = coop ? mcgd::probe_warp16_resolve(c, cell, chk, valid, w)
+                                   : (valid ? mcgd::probe_cell(c, cell, chk) : mcgd::Probe{0u, -1, false});
+        if (valid) {
+            ++looks;
+            hits += p.hit;
+            if (!p.hit) {
+                const int r = mcgd::insert_at(c, cell, p.where, chk, static_cast<uint32_t>(h) | 0x80000000u);
+                won += r == MCG_INSERT_WON;
+                full += r == MCG_INSERT_CELL_FULL;
+            }
+        }
+        if (kPipe) {
+            h = nh;
+            chk = nchk;
+            cell = ncell;
+        } else {
+            gen(i + stride, h, chk, cell);
         }
     }
     mcgd::warp_add(counters + 0, looks);
@@ -1191,8 +1291,14 @@ mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t 
         cudaEventRecord(a, ctx->stream);
         {
             LaunchScope ls(ctx, "probe_replay", 0.0);
-            const unsigned grid = 148u * static_cast<unsigned>(blocks_per_sm > 0 ? blocks_per_sm : 8);
-            k_probe_replay<<<grid, 256, 0, ctx->stream>>>(cache->view(), dd, n, cache->counters);
+            // blocks_per_sm < 0: the software-pipelined kernel (measured slower on
+            // a render's trace, whose coherent lookups mostly hit L2: 34.4 vs
+            // 37.3 G probes/s, profiles/README.md)
+            const bool pipe = blocks_per_sm < 0;
+            const int bps = blocks_per_sm < 0 ? -blocks_per_sm : blocks_per_sm;
+            const unsigned grid = 148u * static_cast<unsigned>(bps > 0 ? bps : 8);
+            if (pipe) k_probe_replay<true><<<grid, 256, 0, ctx->stream>>>(cache->view(), dd, n, cache->counters);
+            else k_probe_replay<false><<<grid, 256, 0, ctx->stream>>>(cache->view(), dd, n, cache->counters);
             ls.done();
         }
         cudaEventRecord(b, ctx->stream);
@@ -1220,7 +1326,7 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 4,
+        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 9,
              "phase must be 0, 1 or 2 (+16 * variant, +256 * blocks per SM)");
         mcg_ctx* ctx = cache->ctx;
         cudaEvent_t a = take_event(ctx), b = take_event(ctx);
@@ -1232,7 +1338,18 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
             const int variant = (phase >> 4) & 15, ph = phase & 15;
             const int per_sm = (phase >> 8) ? (phase >> 8) : 8;   // blocks per SM
             const unsigned grid = 148u * static_cast<unsigned>(per_sm);
-            if (variant == 4 && cache->n_entries % 2 == 0 && cache->n_entries <= 10) {
+            const bool coop = cache->n_entries % 2 == 0 && cache->n_entries <= 10;
+            if (variant == 5 && coop) {
+                k_probe_bench_pipe<2><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 6 && coop) {
+                k_probe_bench_pipe<4><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 8 && coop) {
+                k_probe_bench_pipe<1, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 9 && coop) {
+                k_probe_bench_pipe<2, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 7 && coop) {
+                k_probe_bench_pipe<1><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 4 && coop) {
                 k_probe_bench<4><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 2 && cache->n_entries == 10) {
                 k_probe_bench<2><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);

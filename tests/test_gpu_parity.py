@@ -95,6 +95,42 @@ def test_ordered_updates_match_oracle_table(ctx, oracle, nc, ne):
     oracle.cache_free(oc)
 
 
+@pytest.mark.parametrize("nc,ne", [(100_003, 10), (65_537, 8), (70_001, 4)])
+def test_probe_bench_variants_agree(ctx, nc, ne, tmp_path):
+    """Every probe variant of the microbenchmark (per-lane, cooperative,
+    software-pipelined) makes the same hit/miss decisions on the same table:
+    lookup-all after an insert-all gives identical hit counts and leaves the
+    table word for word unchanged; an insert-all through a pipelined variant
+    leaves a table that passes the reference's audit (occupied prefix, no
+    duplicate check-hash in a cell)."""
+    n = (1 << 20) + 77     # ragged: the last warp step is partial
+    t = MaterialCache(nc, ne, ctx)
+    t.probe_bench(n, 7, 0, 1)
+    words = t.slot_words()
+    variants = (0, 1, 3, 4, 5, 6, 7) if ne % 2 == 0 else (0, 1, 3)
+    hits = {}
+    for v in variants:
+        t.reset_counters()
+        t.probe_bench(n, 7, 1 + 16 * v, 1)
+        c = t.counters()
+        assert c["lookups"] == n, v
+        hits[v] = c["hits"]
+    assert len(set(hits.values())) == 1, hits
+    assert 0 < hits[0] < n
+    np.testing.assert_array_equal(t.slot_words(), words)
+    for v in (5, 6):
+        f = MaterialCache(nc, ne, ctx)
+        f.probe_bench(n, 7, 0 + 16 * v, 1)
+        w = f.slot_words().reshape(nc, ne)
+        occ = w != 0
+        assert (occ[:, 1:] <= occ[:, :-1]).all()
+        path = str(tmp_path / f"d{v}.bin")
+        f.dump(path)
+        rep = audit_dump(path)
+        assert rep.clean, rep.problem
+        assert int(occ.sum()) == f.occupied_slots() > 0
+
+
 def test_concurrent_updates_keep_table_invariants(ctx, tmp_path):
     """First-insert-wins under contention: single CAS
     from zero, no duplicate check-hash in a cell, occupied slots form a prefix,
