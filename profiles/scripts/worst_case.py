@@ -1,0 +1,46 @@
+"""Worst case for the cache (BASELINE.json config 4): the Bmw-like analogue at
+1920x1080x128, cache 1e7x10, with the texel grid made finer than the ray-cone
+footprint by RenderConfig.mip_offset (2^k x 2^k texels per footprint), so
+samples stop sharing texels: hit rate -> 0, every miss attempts an insert and
+the table fills (then CellFull). Reports time relative to the no-cache render
+of the same scene (north_star: >= 90% of no-cache throughput)."""
+import json
+import os
+import statistics
+import sys
+import tempfile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2305_07238_b200 import Context, RenderConfig, load_scene, render, scenes  # noqa: E402
+
+W, H, SPP = 1920, 1080, 128
+ctx = Context(0)
+tmp = tempfile.mkdtemp()
+out = {}
+for kind in ("bmw", "classroom"):
+    s = load_scene(scenes.build_scene(scenes.SceneSpec(kind, W, H, tris_per_side=24), os.path.join(tmp, kind)))
+    base = RenderConfig(width=W, height=H, spp=SPP, n_cells=10_000_000, n_entries=10)
+    render(s, base, ctx=ctx)
+
+    def med(cfg, reps=3):
+        ts, last = [], None
+        for _ in range(reps):
+            last = render(s, cfg, ctx=ctx)
+            ts.append(last.stats.device_ms)
+        return statistics.median(ts), last
+
+    t_off, _ = med(base)
+    rows = {"ms_no_cache": t_off}
+    for mo in (0, 2, 4, 8, 12):
+        t_on, r = med(RenderConfig(**{**base.__dict__, "cache_enabled": True, "mip_offset": mo}))
+        st = r.stats
+        rows[f"mip_offset_{mo}"] = {
+            "ms_cache": t_on, "relative_time_pct": 100 * t_on / t_off,
+            "throughput_vs_no_cache_pct": 100 * t_off / t_on,
+            "hit_rate": st.hit_rate, "lookups": st.lookups, "inserts_won": st.inserts_won,
+            "inserts_lost_full": st.inserts_lost_full}
+        print(kind, mo, json.dumps(rows[f"mip_offset_{mo}"]), flush=True)
+    out[kind] = rows
+os.makedirs("gpurun_out", exist_ok=True)
+with open("gpurun_out/worst_case.json", "w") as f:
+    json.dump(out, f, indent=1)
