@@ -1718,7 +1718,11 @@ __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, con
     if (!valid) return;
     // live-path count (hits sort first): the last live position writes it
     if (i + 1 == R.n_paths || key_slot(R, skey[i + 1]) >= R.S.n_programs) R.shadow_count[2] = i + 1;
+#ifdef MCG_EXP_SHADE_NOGATHER
+    const uint32_t q = i;   // timing experiment only: no permutation (wrong images)
+#else
     const uint32_t q = order[i];
+#endif
     const unsigned grp = __match_any_sync(live, slot);
     const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
     const uint32_t pid = R.pid[q];

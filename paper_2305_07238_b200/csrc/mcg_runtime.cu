@@ -338,7 +338,13 @@ __global__ void __launch_bounds__(256, MCG_PROBE_MINB) k_probe_bench(CacheView c
 // multiply-high of a counter hash instead of the reference's descriptor hash,
 // to measure what the hashing costs the probe.
 template <int U, bool kNoHash = false>
-__global__ void __launch_bounds__(256, U == 1 ? 4 : (U == 2 ? 3 : 2)) k_probe_bench_pipe(CacheView c, uint64_t n, uint64_t seed,
+#ifndef MCG_PIPE1_MINB
+#define MCG_PIPE1_MINB 4
+#endif
+#ifndef MCG_PIPE2_MINB
+#define MCG_PIPE2_MINB 3
+#endif
+__global__ void __launch_bounds__(256, U == 1 ? MCG_PIPE1_MINB : (U == 2 ? MCG_PIPE2_MINB : 2)) k_probe_bench_pipe(CacheView c, uint64_t n, uint64_t seed,
                                                           int phase, unsigned long long* counters) {
     uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
     const uint32_t lane = threadIdx.x & 31u;
