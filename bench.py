@@ -481,9 +481,11 @@ def main() -> None:
     shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ktimes.values())), 4)
               for k, v in ktimes.items()}
     roof["kernel_share"] = shares
-    roof["kernel_share_note"] = ("shares of summed per-launch CUDA-event times; trace_shadow runs on a "
-                                 "second stream concurrently with trace_closest (MCG_OVERLAP), so its "
-                                 "event time includes the overlap")
+    roof["kernel_share_note"] = ("shares of summed per-launch CUDA-event times over the timed region; "
+                                 "trace_shadow runs on a second stream concurrently with trace_closest "
+                                 "(MCG_OVERLAP), and two passes are in flight on two stream pairs "
+                                 "(MCG_LANES=2), so event times include the overlap; the serialized "
+                                 "shares are in the ncu launch list (profiles/)")
     # The north-star kernel (material VM + cache probes) beside it.
     roof_shade = kernel_roofline("shade")
     if "shade" in eff:

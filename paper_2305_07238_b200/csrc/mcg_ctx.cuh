@@ -126,6 +126,12 @@ struct mcg_ctx {
     // the continuation rays are traced), joined through the two events
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // second pass lane (render passes in flight on two stream pairs): its
+    // main and aux streams, fork/join events, pass-order events, scratch
+    cudaStream_t lane2 = nullptr, aux2 = nullptr;
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    cudaEvent_t ev_lane[3] = {nullptr, nullptr, nullptr};
+    mcg::DevMem cub_temp2, path_mem2;
     // scratch
     mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
     mcg::DevMem path_mem, queue_mem, stats_mem;
@@ -181,7 +187,8 @@ void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* keys_in, unsigned lo
                     const unsigned long long* vals_in, unsigned long long* vals_out, size_t n,
                     int end_bit);
 void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* keys_in, uint32_t* keys_out,
-                    const uint32_t* vals_in, uint32_t* vals_out, size_t n, int end_bit);
+                    const uint32_t* vals_in, uint32_t* vals_out, size_t n, int end_bit,
+                    cudaStream_t stream = nullptr, DevMem* temp = nullptr);
 
 // Applies sorted (cell << order_bits | order) -> (check << 32 | payload)
 // records cell by cell in order (the deterministic-insert rule). Outcomes are

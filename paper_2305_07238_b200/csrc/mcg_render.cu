@@ -1807,6 +1807,11 @@ void pk_smem_attr(size_t bytes) {
     cudaFuncSetAttribute(k_occluded_batch<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
+#ifndef MCG_DEFAULT_LANES
+#define MCG_DEFAULT_LANES 2
+#endif
+constexpr int kDefaultLanes = MCG_DEFAULT_LANES;
+
 void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external,
                    double* d_rad, double* d_nodes, uint32_t* d_samples, mcg_render_stats* stats) {
     const DeviceScene& D = ctx->scene;
@@ -1836,12 +1841,22 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 pix.push_back(static_cast<uint32_t>(y * W + x));
     const uint32_t n_pix = static_cast<uint32_t>(pix.size());
 
+    // Pass lanes: with 2, consecutive passes alternate between two stream
+    // pairs with their own path state, so one pass's latency-bound shading
+    // overlaps the other's issue-bound traversal (MCG_LANES=1: one pass at a
+    // time). Deterministic mode keeps one lane: its epochs are (pass, bounce).
+    const char* lanes_env = std::getenv("MCG_LANES");
+    int lanes = lanes_env ? std::max(1, std::min(2, std::atoi(lanes_env))) : kDefaultLanes;
+    if (deferred) lanes = 1;
     uint32_t k = P.samples_per_pass > 0 ? static_cast<uint32_t>(P.samples_per_pass) : 0;
     if (k == 0) {
-        // ~4M paths in flight (measured: 1M 866 ms, 2M 773, 4M 751, 8M 769 per
-        // bench render); MCG_PASS_PATHS overrides (experiments)
+        // paths in flight per pass: ~4M with one lane (measured 1M 866 ms,
+        // 2M 773, 4M 751, 8M 769 per bench render), ~2M per lane with two
+        // (1080p, same call: one lane 6.2M 658 ms; two lanes 2.1M 657, 4.1M
+        // 648); MCG_PASS_PATHS overrides (experiments)
         const char* pp_env = std::getenv("MCG_PASS_PATHS");
-        const uint64_t target = pp_env ? std::max<uint64_t>(1, std::strtoull(pp_env, nullptr, 10)) : (1u << 22);
+        const uint64_t target = pp_env ? std::max<uint64_t>(1, std::strtoull(pp_env, nullptr, 10))
+                                       : (lanes > 1 ? (1u << 21) : (1u << 22));
         k = static_cast<uint32_t>(std::max<uint64_t>(1, (target + n_pix - 1) / std::max<uint32_t>(n_pix, 1)));
     }
     k = std::min<uint32_t>(std::min<uint32_t>(k, 32u), static_cast<uint32_t>(P.spp));
@@ -1876,8 +1891,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint32_t n_lights = D.view.n_plights + D.view.n_rlights;
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
-    ctx->path_mem.ensure(f4 * 12 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024);
-    char* base = ctx->path_mem.as<char>();
+    if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
+    const size_t lane_bytes = f4 * 12 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
+    ctx->path_mem.ensure(lane_bytes);
+    if (lanes > 1) ctx->path_mem2.ensure(lane_bytes);
     RenderView R{};
     R.S = D.view;
     if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
@@ -1892,36 +1909,38 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.seed = P.rng_seed;
     R.diffuse_spread = P.diffuse_spread;
     R.n_pix = n_pix;
-    R.ro = reinterpret_cast<float4*>(base);
-    R.rd = R.ro + max_paths;
-    R.thr = R.rd + max_paths;
-    R.L = R.thr + max_paths;
-    R.ro2 = R.L + max_paths;
-    R.rd2 = R.ro2 + max_paths;
-    R.thr2 = R.rd2 + max_paths;
-    R.L2 = R.thr2 + max_paths;
-    R.sh0 = R.L2 + max_paths;
-    R.sh1 = R.sh0 + max_paths;
-    R.sh2 = R.sh1 + max_paths;
-    R.fin = R.sh2 + max_paths;
-    R.sro = R.fin + max_paths;
-    R.srd = R.sro + n_shadow;
-    R.scon = R.srd + n_shadow;
-    uint32_t* u32 = reinterpret_cast<uint32_t*>(R.scon + n_shadow);
-    R.keys = u32;
-    R.vals = u32 + max_paths;
-    uint32_t* skey = u32 + 2 * max_paths;
-    uint32_t* order = u32 + 3 * max_paths;
-    R.pid = u32 + 4 * max_paths;
-    R.pid2 = u32 + 5 * max_paths;
-    R.skey = skey;
-    R.order = order;
-    R.squeue = u32 + 6 * max_paths;
-    uint32_t* d_pix = R.squeue + n_shadow;
-    R.pix = d_pix;
-    R.shadow_count = reinterpret_cast<unsigned int*>(d_pix + n_pix);
-    R.vis = reinterpret_cast<uint8_t*>(R.shadow_count + 64);
-    cuda_check(cudaMemcpyAsync(d_pix, pix.data(), n_pix * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D pixels");
+    auto layout = [&](RenderView& V, char* base) {
+        V.ro = reinterpret_cast<float4*>(base);
+        V.rd = V.ro + max_paths;
+        V.thr = V.rd + max_paths;
+        V.L = V.thr + max_paths;
+        V.ro2 = V.L + max_paths;
+        V.rd2 = V.ro2 + max_paths;
+        V.thr2 = V.rd2 + max_paths;
+        V.L2 = V.thr2 + max_paths;
+        V.sh0 = V.L2 + max_paths;
+        V.sh1 = V.sh0 + max_paths;
+        V.sh2 = V.sh1 + max_paths;
+        V.fin = V.sh2 + max_paths;
+        V.sro = V.fin + max_paths;
+        V.srd = V.sro + n_shadow;
+        V.scon = V.srd + n_shadow;
+        uint32_t* u32 = reinterpret_cast<uint32_t*>(V.scon + n_shadow);
+        V.keys = u32;
+        V.vals = u32 + max_paths;
+        uint32_t* skey_ = u32 + 2 * max_paths;
+        uint32_t* order_ = u32 + 3 * max_paths;
+        V.pid = u32 + 4 * max_paths;
+        V.pid2 = u32 + 5 * max_paths;
+        V.skey = skey_;
+        V.order = order_;
+        V.squeue = u32 + 6 * max_paths;
+        uint32_t* d_pix = V.squeue + n_shadow;
+        V.pix = d_pix;
+        V.shadow_count = reinterpret_cast<unsigned int*>(d_pix + n_pix);
+        V.vis = reinterpret_cast<uint8_t*>(V.shadow_count + 64);
+        cuda_check(cudaMemcpyAsync(d_pix, pix.data(), n_pix * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D pixels");
+    };
     R.radiance = d_rad;
     R.nodes_found = d_nodes;
     R.samples = d_samples;
@@ -1979,47 +1998,69 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     }
+    if (lanes > 1 && !ctx->lane2) {
+        cuda_check(cudaStreamCreateWithFlags(&ctx->lane2, cudaStreamNonBlocking), "lane stream");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->aux2, cudaStreamNonBlocking), "aux stream");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming), "event");
+        for (cudaEvent_t& e : ctx->ev_lane) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    RenderView RL[2] = {R, R};
+    layout(RL[0], ctx->path_mem.as<char>());
+    if (lanes > 1) layout(RL[1], ctx->path_mem2.as<char>());
+    const cudaStream_t lane_main[2] = {ctx->stream, ctx->lane2};
+    const cudaStream_t lane_aux[2] = {ctx->aux, ctx->aux2};
+    const cudaEvent_t lane_fork[2] = {ctx->ev_fork, ctx->ev_fork2};
+    const cudaEvent_t lane_join[2] = {ctx->ev_join, ctx->ev_join2};
+    mcg::DevMem* lane_tmp[2] = {&ctx->cub_temp, &ctx->cub_temp2};
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
     if (smem > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "material stack too deep for shared memory");
     cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const RenderView R0 = R;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cuda_check(cudaEventCreate(&ev0), "event");
     cuda_check(cudaEventCreate(&ev1), "event");
     cuda_check(cudaEventRecord(ev0, ctx->stream), "event record");
+    if (lanes > 1) {
+        // lane 2 starts after the setup (stats reset, pixel lists) on the main stream
+        cuda_check(cudaEventRecord(ctx->ev_lane[2], ctx->stream), "event record");
+        cuda_check(cudaStreamWaitEvent(ctx->lane2, ctx->ev_lane[2], 0), "wait");
+    }
 
-    for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k) {
+    int prev_lane = -1;
+    uint32_t pass = 0;
+    for (uint32_t start = 0; start < static_cast<uint32_t>(P.spp); start += k, ++pass) {
+        const int l = static_cast<int>(pass % static_cast<uint32_t>(lanes));
+        const cudaStream_t sm = lane_main[l], sa = lane_aux[l];
+        RenderView R = RL[l];   // the pass starts on the lane's first layout
         const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(P.spp) - start);
-        // the pass starts on the first layout
-        R.ro = R0.ro; R.rd = R0.rd; R.thr = R0.thr; R.L = R0.L; R.pid = R0.pid;
-        R.ro2 = R0.ro2; R.rd2 = R0.rd2; R.thr2 = R0.thr2; R.L2 = R0.L2; R.pid2 = R0.pid2;
         R.n_paths = n_pix * kk;
         R.sample0 = P.first_sample + start;
         R.hps_base = start;
         const unsigned grid = grid_for(R.n_paths, 256);
         {
-            LaunchScope ls(ctx, "primary", 0.0);
-            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, ctx->stream>>>(R);
+            LaunchScope ls(ctx, "primary", 0.0, sm);
+            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
             ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
             // Stable radix sort of (key -> layout position): hits in
             // material order first, paths without a hit (key n_programs) last.
-            sort_pairs_u32(ctx, R.keys, skey, R.vals, order, R.n_paths, key_bits);
+            sort_pairs_u32(ctx, R.keys, const_cast<uint32_t*>(R.skey), R.vals, const_cast<uint32_t*>(R.order), R.n_paths,
+                           key_bits, sm, lane_tmp[l]);
             // counters: [0] shadow rays queued, [1] shadow cursor, [2] live paths, [3] trace cursor
-            cuda_check(cudaMemsetAsync(R.shadow_count, 0, 16, ctx->stream), "memset");
-            if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, ctx->stream), "memset");
+            cuda_check(cudaMemsetAsync(R.shadow_count, 0, 16, sm), "memset");
+            if (deferred) cuda_check(cudaMemsetAsync(R.q.count, 0, 4, sm), "memset");
             {
-                LaunchScope ls(ctx, "shade", 0.0);
+                LaunchScope ls(ctx, "shade", 0.0, sm);
                 const unsigned sg = grid_for(R.n_paths, block);
                 const uint32_t wh32 = static_cast<uint32_t>(wh);
                 // deterministic mode: stores are queued and applied after the
                 // shade (NEE and the bounce need none of them)
-                if (deferred) k_shade<true><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
-                else k_shade<false><<<sg, block, smem, ctx->stream>>>(R, skey, order, max_stack, wh32, b);
+                if (deferred) k_shade<true><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                else k_shade<false><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
                 ls.done();
             }
             // the path state now lives at the sorted positions
@@ -2028,10 +2069,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             std::swap(R.thr, R.thr2);
             std::swap(R.L, R.L2);
             std::swap(R.pid, R.pid2);
-            if (deferred) {
+            if (deferred) {   // one lane: sm == ctx->stream
                 unsigned int count = 0;
-                cuda_check(cudaMemcpyAsync(&count, R.q.count, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-                cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+                cuda_check(cudaMemcpyAsync(&count, R.q.count, 4, cudaMemcpyDeviceToHost, sm), "D2H");
+                cuda_check(cudaStreamSynchronize(sm), "sync");
                 if (count > R.q.capacity) fail(MCG_ERR_CUDA, "store queue overflow");
                 if (count) {
                     const uint64_t cap = R.q.capacity;
@@ -2046,35 +2087,45 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             // of vertex b are independent; k_resolve_lights waits for both.
             const bool fork = overlap && n_lights && b < P.max_bounces;
             if (fork) {
-                cuda_check(cudaEventRecord(ctx->ev_fork, ctx->stream), "event");
-                cuda_check(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0), "wait");
+                cuda_check(cudaEventRecord(lane_fork[l], sm), "event");
+                cuda_check(cudaStreamWaitEvent(sa, lane_fork[l], 0), "wait");
             }
             if (n_lights) {
-                cudaStream_t st = fork ? ctx->aux : ctx->stream;
+                cudaStream_t st = fork ? sa : sm;
                 LaunchScope ls(ctx, "trace_shadow", 0.0, st);
                 if (sah_shadow) k_shadow_ww<true><<<grid_for(n_shadow, MCG_SHADOW_BLOCK), MCG_SHADOW_BLOCK, 0, st>>>(R);
                 else k_shadow_ww<false><<<grid_for(n_shadow, MCG_SHADOW_BLOCK), MCG_SHADOW_BLOCK, 0, st>>>(R);
                 ls.done();
             }
-            if (fork) cuda_check(cudaEventRecord(ctx->ev_join, ctx->aux), "event");
+            if (fork) cuda_check(cudaEventRecord(lane_join[l], sa), "event");
             if (b < P.max_bounces) {
-                LaunchScope ls(ctx, "trace_closest", 0.0);
-                k_trace_closest_ww<<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, ctx->stream>>>(
+                LaunchScope ls(ctx, "trace_closest", 0.0, sm);
+                k_trace_closest_ww<<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, sm>>>(
                     R, R.shadow_count + 2, b + 1);
                 ls.done();
             }
-            if (fork) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0), "wait");
+            if (fork) cuda_check(cudaStreamWaitEvent(sm, lane_join[l], 0), "wait");
             {
-                LaunchScope ls(ctx, "resolve_lights", 0.0);
-                k_resolve_lights<<<grid, 256, 0, ctx->stream>>>(R, b);
+                LaunchScope ls(ctx, "resolve_lights", 0.0, sm);
+                k_resolve_lights<<<grid, 256, 0, sm>>>(R, b);
                 ls.done();
             }
         }
+        // passes reach the framebuffers in sample order (the double
+        // accumulators' summation order): wait for the previous pass's
+        // accumulate when it ran on the other lane
+        if (prev_lane >= 0 && prev_lane != l) cuda_check(cudaStreamWaitEvent(sm, ctx->ev_lane[prev_lane], 0), "wait");
         {
-            LaunchScope ls(ctx, "accumulate", n_pix * (40.0 + 40.0 * kk));
-            k_accumulate<<<grid_for(n_pix, 256), 256, 0, ctx->stream>>>(R, kk);
+            LaunchScope ls(ctx, "accumulate", n_pix * (40.0 + 40.0 * kk), sm);
+            k_accumulate<<<grid_for(n_pix, 256), 256, 0, sm>>>(R, kk);
             ls.done();
         }
+        if (lanes > 1) cuda_check(cudaEventRecord(ctx->ev_lane[l], sm), "event record");
+        prev_lane = l;
+    }
+    if (lanes > 1) {
+        cuda_check(cudaEventRecord(ctx->ev_lane[2], ctx->lane2), "event record");
+        cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_lane[2], 0), "wait");
     }
     cuda_check(cudaEventRecord(ev1, ctx->stream), "event record");
     unsigned long long st[kStatCount];

@@ -59,23 +59,25 @@ void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* ki, unsigned long lo
 }
 
 void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* ki, uint32_t* ko, const uint32_t* vi,
-                    uint32_t* vo, size_t n, int end_bit) {
+                    uint32_t* vo, size_t n, int end_bit, cudaStream_t stream, DevMem* temp) {
+    const cudaStream_t st = stream ? stream : ctx->stream;
+    DevMem& tmp = temp ? *temp : ctx->cub_temp;
     size_t bytes = 0;
     cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ki, ko, vi, vo, static_cast<int>(n), 0,
-                                               end_bit, ctx->stream),
+                                               end_bit, st),
                "cub sort (size)");
-    ctx->cub_temp.ensure(std::max<size_t>(bytes, 256));
+    tmp.ensure(std::max<size_t>(bytes, 256));
     cudaEvent_t a = nullptr;
     if (ctx->profile) {
         a = take_event(ctx);
-        cudaEventRecord(a, ctx->stream);
+        cudaEventRecord(a, st);
     }
-    cuda_check(cub::DeviceRadixSort::SortPairs(ctx->cub_temp.p, bytes, ki, ko, vi, vo,
-                                               static_cast<int>(n), 0, end_bit, ctx->stream),
+    cuda_check(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, ki, ko, vi, vo,
+                                               static_cast<int>(n), 0, end_bit, st),
                "cub sort");
     if (ctx->profile) {  // timed with the kernels, but CUB's launches are not counted as ours
         cudaEvent_t b = take_event(ctx);
-        cudaEventRecord(b, ctx->stream);
+        cudaEventRecord(b, st);
         ctx->pending.push_back({"sort (cub)", a, b, static_cast<double>(n) * 16.0 * ((end_bit + 7) / 8)});
     }
     ++ctx->library_sorts;
@@ -771,6 +773,11 @@ mcg_status mcg_destroy(mcg_ctx* ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->ev_fork2) cudaEventDestroy(ctx->ev_fork2);
+    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
+    for (cudaEvent_t e : ctx->ev_lane) if (e) cudaEventDestroy(e);
+    if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
+    if (ctx->lane2) cudaStreamDestroy(ctx->lane2);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MCG_OK;
