@@ -440,6 +440,7 @@ typedef struct mcg_render_stats {    /* RenderStats, tracer.hpp:45-55 */
     uint64_t bvh_nodes, prims_tested, tex_samples;   /* work counters (roofline bytes) */
     uint64_t bvh_nodes_shadow, prims_tested_shadow;  /* of which any-hit (shadow) rays */
     uint64_t closest_rays;                           /* continuation rays traced (after the primary) */
+    uint64_t shadow_occluded;                        /* shadow rays that found an occluder */
     uint64_t launches;               /* this library's kernel launches in the call */
     uint64_t* hits_per_sample;       /* optional, caller array of spp entries */
 } mcg_render_stats;

@@ -569,6 +569,7 @@ class RenderStats:
     shadow_rays: int = 0
     paths: int = 0
     device_ms: float = 0.0       # CUDA-event time of the render on the context's stream
+    shadow_occluded: int = 0     # shadow rays that found an occluder
 
 
 @dataclass
@@ -602,7 +603,7 @@ def render(scene: Scene, config: RenderConfig, external_cache: Optional[Material
                         (st.hits / st.lookups) if st.lookups else 0.0, st.inserts_won,
                         st.inserts_lost_full, st.stores_attempted, st.instructions_executed,
                         [int(x) for x in hps], st.shading_points, st.shadow_rays, st.paths,
-                        st.device_ms)
+                        st.device_ms, st.shadow_occluded)
     return RenderResult(fb, stats)
 
 

@@ -85,7 +85,7 @@ class RenderStats(C.Structure):
                 ("paths", u64), ("shading_points", u64), ("shadow_rays", u64),
                 ("bvh_nodes", u64), ("prims_tested", u64), ("tex_samples", u64),
                 ("bvh_nodes_shadow", u64), ("prims_tested_shadow", u64), ("closest_rays", u64),
-                ("launches", u64), ("hits_per_sample", P(u64))]
+                ("shadow_occluded", u64), ("launches", u64), ("hits_per_sample", P(u64))]
 
 
 # (name, restype, argtypes)
