@@ -192,14 +192,19 @@ def _params(w, h, spp, mode, spp_pass, nc=997, ne=4, mip=0):
     return _oracle.RenderParamsC(w, h, spp, 4, mode, mip, nc, ne, 0, 1, 0.2, 16, 0, 1, 0, 0, spp_pass)
 
 
-@pytest.mark.parametrize("kind,libm,spheres", [("cornell", False, 0), ("classroom", True, 0), ("monster", True, 0),
-                                               ("junkshop", True, 16)])
-def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm, spheres):
-    w, h, spp = 64, 48, 4
+@pytest.mark.parametrize("kind,libm,spheres,spp_pass", [("cornell", False, 0, 0), ("classroom", True, 0, 0),
+                                                        ("monster", True, 0, 0), ("junkshop", True, 16, 0),
+                                                        ("classroom", True, 0, 1), ("junkshop", True, 16, 3)])
+def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm, spheres, spp_pass):
+    """spp_pass > 0 splits the render into several passes, which run two at a
+    time on two stream pairs (MCG_LANES): the framebuffers still receive
+    the samples in order, so the image is the oracle's bit for bit."""
+    w, h, spp = 64, 48, 4 if spp_pass == 0 else 7
     path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=libm, spheres=spheres),
                               f"{scene_dir}/r_{kind}_{spheres}")
     s = load_scene(path)
-    res = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=False), ctx=ctx)
+    res = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=False, samples_per_pass=spp_pass),
+                 ctx=ctx)
     rad, nodes, samples, hps, st = oracle.render(s.flat, _params(w, h, spp, 0, 1))
     np.testing.assert_array_equal(bits(res.frame.radiance), bits(rad))
     np.testing.assert_array_equal(res.frame.samples, samples)
@@ -231,16 +236,18 @@ def test_render_deterministic_matches_oracle(ctx, oracle, scene_dir, kind, k, sp
     oracle.cache_free(oc)
 
 
-def test_render_concurrent_rmse_bound(ctx, oracle, scene_dir):
+@pytest.mark.parametrize("spp_pass", [0, 1])
+def test_render_concurrent_rmse_bound(ctx, oracle, scene_dir, spp_pass):
     """Concurrent mode: RMSE vs the no-cache image within the reference's own
-    cached-vs-uncached RMSE + 1e-4 (north star)."""
+    cached-vs-uncached RMSE + 1e-4 (north star); spp_pass = 1: one sample per
+    pass, two passes in flight sharing the table."""
     w, h, spp, nc, ne = 96, 64, 8, 20011, 8
     path = scenes.build_scene(scenes.SceneSpec("classroom", w, h, tris_per_side=6, libm_ops=True),
                               f"{scene_dir}/c_classroom")
     s = load_scene(path)
     off = render(s, RenderConfig(width=w, height=h, spp=spp), ctx=ctx).frame.radiance_image()
     conc = render(s, RenderConfig(width=w, height=h, spp=spp, cache_enabled=True, n_cells=nc,
-                                  n_entries=ne), ctx=ctx)
+                                  n_entries=ne, samples_per_pass=spp_pass), ctx=ctx)
     oc = oracle.cache_new(nc, ne)
     rad, *_ = oracle.render(s.flat, _params(w, h, spp, 1, 1, nc, ne), cache=oc)
     ref_cached = (rad / spp).astype(np.float32)
