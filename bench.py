@@ -45,7 +45,7 @@ W, H, SPP = 1920, 1080, 128
 N_CELLS, N_ENTRIES = 10_000_000, 10
 SCENE_KIND = "classroom"
 TRIS_PER_SIDE = 24
-PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 7, 8          # HBM table: warp-cooperative, one round trip, software-pipelined
+PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 10, 8         # HBM table: warp-cooperative one-round-trip loads, software-pipelined, scan through shared memory
 PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM = 0, 8    # L2-resident table: per-lane scan (issue-bound)
 METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
 

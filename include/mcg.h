@@ -223,6 +223,8 @@ mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t 
  * 16-byte lanes (one round trip per probe; Ne even <= 10); 5 / 6 / 7 the same
  * probe software-pipelined over 2 / 4 / 1 batches of 32 descriptors per warp
  * (all head loads of the step in flight while the next step is hashed);
+ * 10 / 11 as 7 / 5 with each lane scanning its own cell after a shared-memory
+ * transpose of the warp's loads (fewer instructions than per-round ballots);
  * + 256*b runs b blocks of 256 threads per SM (default 8). Returns the kernel's
  * device milliseconds and the algorithmic bytes it moved. */
 mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t phase,

@@ -312,6 +312,63 @@ __device__ __forceinline__ Probe probe_warp16_resolve(const CacheView& c, uint64
     return mine;
 }
 
+// Resolve half through shared memory: the warp's loaded pairs are transposed
+// through `tile` (4 rounds x 32 lanes x 16 B, this warp's slice) so that
+// each lane then holds its own cell's head (head_n words) and scans it
+// alone, branch-free: the first word that is empty or carries the check hash
+// decides (cache.cpp:127-134). Same outcome as probe_warp16_resolve, with
+// four shared-memory stores and head_n/2 loads instead of per-round ballots
+// and shuffles. Every lane of the warp must call it.
+__device__ __forceinline__ Probe probe_warp16_resolve_smem(const CacheView& c, uint64_t cell, uint32_t check,
+                                                           bool valid, const ulonglong2 (&w)[4],
+                                                           ulonglong2* tile) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lpc = c.head_n >> 1;
+    const uint32_t cpr = 32u / lpc;
+    const uint32_t rounds = (32u + cpr - 1u) / cpr;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if (static_cast<uint32_t>(r) < rounds) tile[r * 32 + lane] = w[r];
+    }
+    __syncwarp();
+    const uint32_t my_round = lane / cpr, my_g = lane - my_round * cpr;
+    const ulonglong2* mine_p = tile + my_round * 32u + my_g * lpc;
+    uint32_t decisive = 0u, hitm = 0u;
+    uint32_t pay[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        ulonglong2 q = make_ulonglong2(~0ull, ~0ull);
+        if (static_cast<uint32_t>(k) < lpc) q = mine_p[k];
+        const uint64_t x[2] = {q.x, q.y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool in = static_cast<uint32_t>(k) < lpc;   // a slot of this cell's head
+            const bool e = in && x[h] == 0ull;
+            const bool m = in && static_cast<uint32_t>(x[h] >> 32) == check;
+            decisive |= (e || m) ? (1u << (2 * k + h)) : 0u;
+            hitm |= (m && !e) ? (1u << (2 * k + h)) : 0u;
+            pay[2 * k + h] = static_cast<uint32_t>(x[h]);
+        }
+    }
+    __syncwarp();   // the tile is reused by the next call
+    Probe mine{0u, -1, false};
+    if (decisive) {
+        const int f = __ffs(decisive) - 1;
+        mine.where = f;
+        mine.hit = ((hitm >> f) & 1u) != 0u;
+        uint32_t p = pay[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) p = (f == i) ? pay[i] : p;
+        if (mine.hit) mine.payload = p;
+    } else if (valid && c.n_entries > c.head_n) {
+        const uint64_t* t = tail_words(c, cell);
+        for (uint32_t j = 0; j < c.n_entries - c.head_n; ++j) {
+            if (scan_word(__ldcg(t + j), static_cast<int32_t>(c.head_n + j), check, mine)) break;
+        }
+    }
+    return mine;
+}
+
 __device__ __forceinline__ Probe probe_warp16(const CacheView& c, uint64_t cell, uint32_t check,
                                               bool valid) {
     ulonglong2 w[4];
@@ -403,6 +460,18 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell
 __device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t cell, uint32_t check,
                                              bool valid) {
     if ((c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u) return probe_warp16(c, cell, check, valid);
+    return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
+}
+
+// probe_lanes with the shared-memory resolve; `tile` is this warp's 128
+// ulonglong2 of shared memory. Warp-collective.
+__device__ __forceinline__ Probe probe_lanes_smem(const CacheView& c, uint64_t cell, uint32_t check,
+                                                  bool valid, ulonglong2* tile) {
+    if ((c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u) {
+        ulonglong2 w[4];
+        probe_warp16_issue(c, cell, valid, w);
+        return probe_warp16_resolve_smem(c, cell, check, valid, w, tile);
+    }
     return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
 }
 

@@ -142,7 +142,8 @@ __global__ void k_lookup(CacheView c, const mcg_descriptor* d, size_t n, uint8_t
     uint32_t chk = 0;
     if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
     const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
-    const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
+    __shared__ ulonglong2 s_tile[8 * 4 * 32];   // blockDim 256: 4 rounds x 32 lanes per warp
+    const mcgd::Probe p = mcgd::probe_lanes_smem(c, cell, chk, valid, s_tile + (threadIdx.x >> 5) * 128u);
     uint32_t hits = 0, looks = 0;
     if (valid) {
         looks = 1;
@@ -170,7 +171,8 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
     if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
     const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
     const uint64_t base = cell * c.n_entries;   // logical slot index of the cell
-    const mcgd::Probe p = mcgd::probe_lanes(c, cell, chk, valid);
+    __shared__ ulonglong2 s_tile[8 * 4 * 32];   // blockDim 256: 4 rounds x 32 lanes per warp
+    const mcgd::Probe p = mcgd::probe_lanes_smem(c, cell, chk, valid, s_tile + (threadIdx.x >> 5) * 128u);
     uint32_t won = 0, full = 0, lost = 0;
     if (valid) {
         int res;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(256, MCG_PROBE_MINB) k_probe_bench(CacheView c
 // kNoHash (diagnostic only, variants 8/9): the cell and check come from one
 // multiply-high of a counter hash instead of the reference's descriptor hash,
 // to measure what the hashing costs the probe.
-template <int U, bool kNoHash = false>
+template <int U, bool kNoHash = false, bool kSmem = false>
 #ifndef MCG_PIPE1_MINB
 #define MCG_PIPE1_MINB 4
 #endif
@@ -351,6 +353,8 @@ __global__ void __launch_bounds__(256, U == 1 ? MCG_PIPE1_MINB : (U == 2 ? MCG_P
     uint32_t looks = 0, hits = 0, won = 0, full = 0, inserts = 0;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x * U;
+    __shared__ ulonglong2 s_tile[kSmem ? 8 * 4 * 32 : 1];   // per warp: 4 rounds x 32 lanes
+    ulonglong2* tile = s_tile + (kSmem ? (threadIdx.x >> 5) * 128u : 0u);
     uint64_t i0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u)) * U;
     uint64_t cell[U], h[U];
     uint32_t chk[U];
@@ -378,7 +382,8 @@ __global__ void __launch_bounds__(256, U == 1 ? MCG_PIPE1_MINB : (U == 2 ? MCG_P
         for (int u = 0; u < U; ++u) {
             const uint64_t i = i0 + 32u * u + lane;
             const bool valid = i < n;
-            const mcgd::Probe p = mcgd::probe_warp16_resolve(c, cell[u], chk[u], valid, w[u]);
+            const mcgd::Probe p = kSmem ? mcgd::probe_warp16_resolve_smem(c, cell[u], chk[u], valid, w[u], tile)
+                                        : mcgd::probe_warp16_resolve(c, cell[u], chk[u], valid, w[u]);
             if (valid) {
                 const bool insert = phase == 0 || (phase == 2 && (i & 1u));
                 if (!insert) {
@@ -419,6 +424,8 @@ __global__ void __launch_bounds__(256, 4) k_probe_replay(CacheView c, const mcg_
     uint32_t looks = 0, hits = 0, won = 0, full = 0;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    __shared__ ulonglong2 s_tile[8 * 4 * 32];   // per warp: 4 rounds x 32 lanes (probe_warp16_resolve_smem)
+    ulonglong2* tile = s_tile + (threadIdx.x >> 5) * 128u;
     uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u);
     auto gen = [&](uint64_t i, uint64_t& h, uint32_t& chk, uint64_t& cell) {
         h = 0;
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(256, 4) k_probe_replay(CacheView c, const mcg_
         uint64_t nh = 0, ncell = 0;
         uint32_t nchk = 0;
         if (kPipe) gen(i + stride, nh, nchk, ncell);
-        const mcgd::Probe p = coop ? mcgd::probe_warp16_resolve(c, cell, chk, valid, w)
+        const mcgd::Probe p = coop ? mcgd::probe_warp16_resolve_smem(c, cell, chk, valid, w, tile)
                                    : (valid ? mcgd::probe_cell(c, cell, chk) : mcgd::Probe{0u, -1, false});
         if (valid) {
             ++looks;
@@ -1339,7 +1346,7 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                            int32_t iters, double* ms_out, double* bytes_out) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 9,
+        need((phase & 15) <= 2 && ((phase >> 4) & 15) <= 11,
              "phase must be 0, 1 or 2 (+16 * variant, +256 * blocks per SM)");
         mcg_ctx* ctx = cache->ctx;
         cudaEvent_t a = take_event(ctx), b = take_event(ctx);
@@ -1360,6 +1367,10 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
                 k_probe_bench_pipe<1, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 9 && coop) {
                 k_probe_bench_pipe<2, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 10 && coop) {
+                k_probe_bench_pipe<1, false, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
+            } else if (variant == 11 && coop) {
+                k_probe_bench_pipe<2, false, true><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 7 && coop) {
                 k_probe_bench_pipe<1><<<grid, 256, 0, ctx->stream>>>(cache->view(), n, seed, ph, cache->counters);
             } else if (variant == 4 && coop) {
