@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MCG_ABI_VERSION 1
+#define MCG_ABI_VERSION 2   /* 2: mcg_render_stats.shadow_occluded */
 
 typedef enum mcg_status {
     MCG_OK = 0,

@@ -154,6 +154,9 @@ EXPORTED = [s[0] for s in _SIGS]
 _lib = None
 
 
+ABI_VERSION = 2   # include/mcg.h MCG_ABI_VERSION (the struct layouts below)
+
+
 def lib():
     """The loaded libmcg (raises ImportError when the build is missing)."""
     global _lib
@@ -166,6 +169,9 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.mcg_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH}: ABI version {L.mcg_abi_version()}, this binding expects "
+                              f"{ABI_VERSION}; rebuild with __graft_entry__.build()")
         _lib = L
     return _lib
 
