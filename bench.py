@@ -113,7 +113,23 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # control-flow check of the N > 1 path on a one-GPU box (never a
+    # measurement): every rank on cuda:0, gloo instead of NCCL
+    if os.environ.get("MCG_BENCH_SAME_DEVICE") == "1":
+        local = 0
     return rank, world, local
+
+
+def frame_reduce(dist, tensors):
+    """Framebuffer gather to rank 0: reduce(sum) over NCCL (exact: each pixel
+    belongs to one rank, the others contribute zeros). With the gloo
+    control-flow backend (CUDA tensors support all_reduce only) an
+    all_reduce stands in."""
+    for t in tensors:
+        if dist.get_backend() == "gloo":
+            dist.all_reduce(t)
+        else:
+            dist.reduce(t, 0)
 
 
 def make_scene(tmp: str):
@@ -216,7 +232,11 @@ def main() -> None:
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MCG_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2305_07238_b200 import (Context, RenderConfig, load_scene)
     from paper_2305_07238_b200 import _native as N
 
@@ -263,9 +283,7 @@ def main() -> None:
         N.check(L.mcg_render_device(ctx.handle, C.byref(p), ext, C.byref(dframe), C.byref(st)))
         if world > 1:
             with torch.cuda.stream(stream):
-                dist.reduce(rad, 0)
-                dist.reduce(nodes, 0)
-                dist.reduce(samples, 0)
+                frame_reduce(dist, [rad, nodes, samples])
         return st
 
     def timed(fn, steps, warmup):
@@ -311,10 +329,25 @@ def main() -> None:
     frame_bytes = H * W * (24 + 8 + 4)
 
     def e2e_step():
-        host_rad.zero_(); host_nodes.zero_(); host_samples.zero_()
+        # the user's call sequence: scene to HBM, render, image back to host
         N.check(L.mcg_upload_scene(ctx.handle, scene.handle))
         s = N.RenderStats()
-        N.check(L.mcg_render(ctx.handle, C.byref(params), None, C.byref(hframe), C.byref(s)))
+        if world == 1:
+            host_rad.zero_(); host_nodes.zero_(); host_samples.zero_()
+            N.check(L.mcg_render(ctx.handle, C.byref(params), None, C.byref(hframe), C.byref(s)))
+            return s
+        # N > 1: each rank renders its tiles into device frames, the frames
+        # are reduced to rank 0 over NCCL, rank 0 copies the image to host
+        with torch.cuda.stream(stream):
+            rad.zero_(); nodes.zero_(); samples.zero_()
+        N.check(L.mcg_render_device(ctx.handle, C.byref(params), None, C.byref(dframe), C.byref(s)))
+        with torch.cuda.stream(stream):
+            frame_reduce(dist, [rad, nodes, samples])
+            if rank == 0:
+                host_rad.copy_(rad, non_blocking=True)
+                host_nodes.copy_(nodes, non_blocking=True)
+                host_samples.copy_(samples, non_blocking=True)
+        stream.synchronize()
         return s
 
     e2e_steps = max(1, min(args.steps, 2))
@@ -526,7 +559,10 @@ def main() -> None:
                              f"{(W * H * 10 * 16) >> 20} MB path state)"},
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": "samples/s",
-                    "h2d_bytes_per_step": int(scene_bytes + frame_bytes),
+                    # N = 1: scene + framebuffers in (mcg_render accumulates into
+                    # the caller's frame), image out; N > 1: scene in on every
+                    # rank, frames reduced to rank 0 over NCCL, image out on rank 0
+                    "h2d_bytes_per_step": int(scene_bytes * world + (frame_bytes if world == 1 else 0)),
                     "d2h_bytes_per_step": int(frame_bytes)},
             "gpu_launches": int(launches),
             "roofline": roof,
