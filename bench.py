@@ -544,6 +544,26 @@ def main() -> None:
         except Exception as e:  # the checker must never break the bench line
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
+        try:
+            # the reference's MaterialCache on the 1e7x10 table,
+            # 1 thread and every host thread, same descriptor generator as the
+            # device probe (2^22 descriptors: insert-all, then lookup-all)
+            import _oracle
+            if _oracle.Ref.available():
+                ref = _oracle.Ref()
+                n_cpu = 1 << 22
+                pcpu = {"table": "1e7x10 (800 MB)", "descriptors": n_cpu, "kind": "reference"}
+                for th in (1, os.cpu_count() or 1):
+                    c = ref.cache_new(N_CELLS, N_ENTRIES)
+                    ref.probe_bench(c, n_cpu, 11, 1, th)          # first touch of the table
+                    t_ins = ref.probe_bench(c, n_cpu, 7, 0, th)
+                    t_look = ref.probe_bench(c, n_cpu, 7, 1, th)
+                    ref.cache_free(c)
+                    pcpu[f"threads_{th}"] = {"insert_mprobes_per_s": n_cpu / t_ins / 1e6,
+                                             "lookup_mprobes_per_s": n_cpu / t_look / 1e6}
+                extras.setdefault("probe_roofline", {})["cpu_reference"] = pcpu
+        except Exception as e:
+            extras.setdefault("probe_roofline", {})["cpu_reference"] = {"unavailable": str(e)[:200]}
 
     if rank == 0:
         line = {

@@ -207,6 +207,45 @@ void ref_cache_lookup(void* c, const CacheDescriptor* d, size_t n, uint8_t* hit,
         rgb[3 * i + 2] = v.b;
     }
 }
+// CPU leg of the probe microbenchmark: the reference's own
+// MaterialCache::update (phase 0, insert-all) or ::lookup (phase 1) over n
+// descriptors from the device benchmark's generator (one splitmix64 per
+// descriptor: mat < 8, node < 256, mip <= 16, texels uniform in 2^mip),
+// split into contiguous ranges over `threads` std::threads. Returns the wall
+// seconds; the payload of an insert is a constant colour.
+double ref_probe_bench(void* c, uint64_t n, uint64_t seed, int phase, int threads) {
+    auto* cache = static_cast<MaterialCache*>(c);
+    const int nt = threads > 0 ? threads : 1;
+    auto work = [&](uint64_t lo, uint64_t hi) {
+        uint64_t found = 0;
+        for (uint64_t i = lo; i < hi; ++i) {
+            const uint64_t h = mix64(seed + 0x9e3779b97f4a7c15ull * (i + 1));
+            const uint32_t w0 = static_cast<uint32_t>(h), w1 = static_cast<uint32_t>(h >> 32);
+            const uint32_t mip = (w0 >> 11) % 17u, mask = (1u << mip) - 1u;
+            CacheDescriptor d;
+            d.mat_idx = w0 & 7u;
+            d.node_idx = (w0 >> 3) & 255u;
+            d.mip_level = static_cast<uint8_t>(mip);
+            d.texel_x = w1 & mask;
+            d.texel_y = (w1 >> 16) & mask;
+            if (phase == 0) {
+                cache->update(d, Color3{0.25f, 0.5f, 0.75f});
+            } else {
+                found += cache->lookup(d).has_value();
+            }
+        }
+        return found;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) {
+        const uint64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+        pool.emplace_back([&, lo, hi] { work(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void ref_cache_slots(void* c, uint64_t first, size_t n, uint64_t* out) {
     auto* cache = static_cast<MaterialCache*>(c);
     for (size_t i = 0; i < n; ++i) out[i] = cache->slot_word(first + i);

@@ -256,6 +256,8 @@ class Ref:
         L.ref_cache_lookup.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.ref_cache_slots.argtypes = [vp, C.c_uint64, C.c_size_t, vp]
         L.ref_cache_counters.argtypes = [vp, vp]
+        L.ref_probe_bench.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int]
+        L.ref_probe_bench.restype = C.c_double
         L.ref_cache_dump.argtypes = [vp, C.c_char_p]
         L.ref_audit.argtypes = [C.c_char_p, vp, C.c_char_p, C.c_size_t]
         L.ref_scene_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
@@ -336,6 +338,11 @@ class Ref:
         out = np.zeros_like(x)
         self.L.ref_power(ptr(x), ptr(y), x.shape[0], ptr(out))
         return out
+
+    def probe_bench(self, c, n, seed, phase, threads):
+        """Seconds for n reference update() (phase 0) / lookup() (phase 1)
+        calls over `threads` host threads (ref_probe_bench)."""
+        return float(self.L.ref_probe_bench(c, n, seed, phase, threads))
 
     def cache_new(self, nc, ne):
         h = vp()

@@ -288,3 +288,20 @@ def test_sharded_oracle_renders_partition_the_image(oracle, scene_dir):
                 cnt += part[2]
             np.testing.assert_array_equal(bits(acc), bits(full[0]))
             np.testing.assert_array_equal(cnt, full[2])
+
+
+def test_reference_probe_bench_threads_agree(ref):
+    """The CPU leg of the probe microbenchmark (ref_probe_bench): lookups are
+    read-only, so 1 and 4 threads find the same hits after one insert-all."""
+    nc, ne, n = 20011, 4, 1 << 16
+    c = ref.cache_new(nc, ne)
+    ref.probe_bench(c, n, 7, 0, 1)
+    words = ref.cache_slots(c, nc * ne)
+    base = ref.cache_counters(c)
+    ref.probe_bench(c, n, 7, 1, 1)
+    one = ref.cache_counters(c) - base
+    ref.probe_bench(c, n, 7, 1, 4)
+    four = ref.cache_counters(c) - base - one
+    assert one[0] == four[0] == n and one[1] == four[1] > 0
+    np.testing.assert_array_equal(ref.cache_slots(c, nc * ne), words)
+    ref.cache_free(c)
