@@ -169,6 +169,19 @@ __device__ __forceinline__ uint32_t no_hit_key(const RenderView& R) {
     return R.S.n_programs << R.key_shift;
 }
 
+// A primitive's geometry as the tests read it: 3 float4 (p0, e1, e2 or
+// centre + radius) and the info word (sphere flag).
+struct PrimG {
+    float4 g0, g1, g2;
+    uint32_t info;
+};
+__device__ __forceinline__ PrimG load_prim(const mcgd::SceneView& S, uint32_t i) {
+    return PrimG{__ldg(S.prim_geom + 3 * i), __ldg(S.prim_geom + 3 * i + 1), __ldg(S.prim_geom + 3 * i + 2),
+                 __ldg(S.prim_info + i)};
+}
+__device__ __forceinline__ bool hit_prim_g(const PrimG& P, V3 o, V3 d, float tmin, float tmax, float& t,
+                                           float& b1, float& b2);
+
 // ray_triangle (scene.cpp:58-78) / ray_sphere (scene.cpp:80-94)
 __device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V3 o, V3 d,
                                          float tmin, float tmax, float& t, float& b1, float& b2) {
@@ -190,6 +203,61 @@ __device__ __forceinline__ bool hit_prim(const mcgd::SceneView& S, uint32_t i, V
         return true;
     }
     const float4 g1 = __ldg(S.prim_geom + 3 * i + 1), g2 = __ldg(S.prim_geom + 3 * i + 2);
+    const V3 p0{g0.x, g0.y, g0.z}, e1{g1.x, g1.y, g1.z}, e2{g2.x, g2.y, g2.z};
+    const V3 pvec = mcgd::cross(d, e2);
+    const float det = mcgd::dot(e1, pvec);
+    if (fabsf(det) < 1e-12f) return false;
+    const V3 tvec = o - p0;
+    const float du = mcgd::dot(tvec, pvec);
+#ifdef MCG_U_PRECHECK
+    // (experiment, off: 653 vs 648 ms per bench render -- the early return
+    // diverges inside the leaf loop) Early-out before the IEEE division, taken only where the reference's
+    // u = fl(du * fl(1/det)) is certainly out of [0, 1]: the quotient
+    // du/det is negative and at least 2^-60 in magnitude (so the rounded
+    // product cannot underflow to -0), or it exceeds 1 + 2^-21 (two roundings
+    // move it by < 2^-22 relative). Every other case takes the exact path.
+    {
+        const float adet = fabsf(det), adu = fabsf(du);
+        const bool neg = (du < 0.0f) != (det < 0.0f) && du != 0.0f;
+        if (neg && adu >= adet * 0x1p-60f) return false;
+        if (!neg && adu > adet * 1.000000953674316f) return false;   // 1 + 2^-20
+    }
+#endif
+    const float inv_det = 1.0f / det;
+    const float u = du * inv_det;
+    if (u < 0.0f || u > 1.0f) return false;
+    const V3 qvec = mcgd::cross(tvec, e1);
+    const float v = mcgd::dot(d, qvec) * inv_det;
+    if (v < 0.0f || u + v > 1.0f) return false;
+    const float ht = mcgd::dot(e2, qvec) * inv_det;
+    if (ht <= tmin || ht >= tmax) return false;
+    t = ht;
+    b1 = u;
+    b2 = v;
+    return true;
+}
+
+// hit_prim over preloaded geometry (the same arithmetic)
+__device__ __forceinline__ bool hit_prim_g(const PrimG& P, V3 o, V3 d, float tmin, float tmax, float& t,
+                                           float& b1, float& b2) {
+    const float4 g0 = P.g0;
+    if (P.info & MCG_PRIM_SPHERE) {
+        const V3 oc = o - V3{g0.x, g0.y, g0.z};
+        const float b = mcgd::dot(oc, d);
+        const float c = mcgd::dot(oc, oc) - g0.w * g0.w;
+        const float disc = b * b - c;
+        if (disc < 0.0f) return false;
+        const float sq = sqrtf(disc);
+        float root = -b - sq;
+        if (root <= tmin || root >= tmax) {
+            root = -b + sq;
+            if (root <= tmin || root >= tmax) return false;
+        }
+        t = root;
+        b1 = b2 = 0.0f;
+        return true;
+    }
+    const float4 g1 = P.g1, g2 = P.g2;
     const V3 p0{g0.x, g0.y, g0.z}, e1{g1.x, g1.y, g1.z}, e2{g2.x, g2.y, g2.z};
     const V3 pvec = mcgd::cross(d, e2);
     const float det = mcgd::dot(e1, pvec);
@@ -1011,6 +1079,49 @@ __device__ __forceinline__ int32_t entry_code(int32_t a, int32_t b) {
     return b > 0 ? static_cast<int32_t>(~((static_cast<uint32_t>(~a) << 3) | static_cast<uint32_t>(b))) : a;
 }
 
+// A leaf's primitives in the reference's order (closest hit, strict <).
+// MCG_TRI_PREFETCH=1 (experiment, off): the next primitive's geometry is
+// loaded before the current one is tested (same arithmetic, same order);
+// measured 652.5 vs 646.8 ms per bench render -- the extra live registers
+// spill at the kernel's 64-register budget.
+#ifndef MCG_TRI_PREFETCH
+#define MCG_TRI_PREFETCH 0
+#endif
+__device__ __forceinline__ void leaf_test(const mcgd::SceneView& S, uint32_t first, uint32_t cnt, V3 o, V3 d,
+                                          float tmin, float& closest, uint32_t& prim, float& t_out,
+                                          float& b1_out, float& b2_out, bool& found) {
+#if MCG_TRI_PREFETCH
+    if (cnt == 0) return;
+    PrimG cur = load_prim(S, first);
+    for (uint32_t i = first; i < first + cnt; ++i) {
+        PrimG nxt = cur;
+        if (i + 1 < first + cnt) nxt = load_prim(S, i + 1);
+        float t, b1, b2;
+        if (hit_prim_g(cur, o, d, tmin, closest, t, b1, b2)) {
+            closest = t;
+            prim = i;
+            t_out = t;
+            b1_out = b1;
+            b2_out = b2;
+            found = true;
+        }
+        cur = nxt;
+    }
+#else
+    for (uint32_t i = first; i < first + cnt; ++i) {
+        float t, b1, b2;
+        if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
+            closest = t;
+            prim = i;
+            t_out = t;
+            b1_out = b1;
+            b2_out = b2;
+            found = true;
+        }
+    }
+#endif
+}
+
 __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool active, V3 o, V3 d,
                                              float tmin, float tmax, uint32_t& prim, float& t_out,
                                              float& b1_out, float& b2_out, uint32_t& nodes_visited,
@@ -1133,17 +1244,7 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
             const uint32_t v = static_cast<uint32_t>(~lc);
             const uint32_t first = v >> 3, cnt = v & 7u;
             prims_tested += cnt;
-            for (uint32_t i = first; i < first + cnt; ++i) {
-                float t, b1, b2;
-                if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
-                    closest = t;
-                    prim = i;
-                    t_out = t;
-                    b1_out = b1;
-                    b2_out = b2;
-                    found = true;
-                }
-            }
+            leaf_test(S, first, cnt, o, d, tmin, closest, prim, t_out, b1_out, b2_out, found);
             leaf = false;
 #if MCG_CLOSEST_LEAVES > 1
             if (leaf2) {
@@ -1152,17 +1253,7 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                     const uint32_t v2 = static_cast<uint32_t>(~lc2);
                     const uint32_t first2 = v2 >> 3, cnt2 = v2 & 7u;
                     prims_tested += cnt2;
-                    for (uint32_t i = first2; i < first2 + cnt2; ++i) {
-                        float t, b1, b2;
-                        if (hit_prim(S, i, o, d, tmin, closest, t, b1, b2)) {
-                            closest = t;
-                            prim = i;
-                            t_out = t;
-                            b1_out = b1;
-                            b2_out = b2;
-                            found = true;
-                        }
-                    }
+                    leaf_test(S, first2, cnt2, o, d, tmin, closest, prim, t_out, b1_out, b2_out, found);
                 }
             }
 #endif
