@@ -1807,8 +1807,12 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 // Material evaluation of every live hit, in sorted (material, Morton)
 // order, then NEE and the bounce; the path's state moves from its old layout
 // position q = order[i] to i in the next layout.
+// (128, 4): the VM keeps its natural 110 registers. With two passes in
+// flight the (128, 5) cap (102 registers, from the one-lane tuning) costs
+// more than the extra resident block gains: same call 636-638 vs 647 ms
+// per bench render (MINB 2/3 compile to the same 110 registers).
 #ifndef MCG_SHADE_MINB
-#define MCG_SHADE_MINB 5
+#define MCG_SHADE_MINB 4
 #endif
 template <bool kDeferred>
 __global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
