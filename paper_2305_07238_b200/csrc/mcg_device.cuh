@@ -454,17 +454,11 @@ __device__ __forceinline__ Probe probe_group16(const CacheView& c, uint64_t cell
     return mine;
 }
 
-// The warp's probes: the cooperative one-round-trip scan where the cell
-// shape allows it (Ne even, <= 10), else the per-lane scan. Warp-collective:
-// every lane of the warp calls it (invalid lanes with valid = false).
-__device__ __forceinline__ Probe probe_lanes(const CacheView& c, uint64_t cell, uint32_t check,
-                                             bool valid) {
-    if ((c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u) return probe_warp16(c, cell, check, valid);
-    return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
-}
-
-// probe_lanes with the shared-memory resolve; `tile` is this warp's 128
-// ulonglong2 of shared memory. Warp-collective.
+// The warp's probes (batch lookups/updates, trace replay): the cooperative
+// one-round-trip scan with the shared-memory resolve where the cell shape
+// allows it (Ne even, head <= 8 slots), else the per-lane scan. `tile` is
+// this warp's 128 ulonglong2 of shared memory. Warp-collective: every lane of
+// the warp calls it (invalid lanes with valid = false).
 __device__ __forceinline__ Probe probe_lanes_smem(const CacheView& c, uint64_t cell, uint32_t check,
                                                   bool valid, ulonglong2* tile) {
     if ((c.head_n & 1u) == 0u && c.head_n >= 2u && c.head_n <= 8u) {
