@@ -126,12 +126,16 @@ struct mcg_ctx {
     // the continuation rays are traced), joined through the two events
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    // second pass lane (render passes in flight on two stream pairs): its
-    // main and aux streams, fork/join events, pass-order events, scratch
-    cudaStream_t lane2 = nullptr, aux2 = nullptr;
-    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
-    cudaEvent_t ev_lane[3] = {nullptr, nullptr, nullptr};
-    mcg::DevMem cub_temp2, path_mem2;
+    // further pass lanes (render passes in flight on several stream pairs):
+    // their main and aux streams, fork/join events, path state and sort
+    // scratch ([0] unused: lane 0 is stream/aux/ev_fork/ev_join/path_mem);
+    // ev_lane[l] marks lane l's last accumulate, ev_lane[kMaxLanes] the
+    // render's start and end
+    static constexpr int kMaxLanes = 4;
+    cudaStream_t lane_stream[kMaxLanes] = {}, lane_aux[kMaxLanes] = {};
+    cudaEvent_t lane_fork[kMaxLanes] = {}, lane_join[kMaxLanes] = {};
+    cudaEvent_t ev_lane[kMaxLanes + 1] = {};
+    mcg::DevMem lane_cub[kMaxLanes], lane_path[kMaxLanes];
     // scratch
     mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
     mcg::DevMem path_mem, queue_mem, stats_mem;

@@ -1957,7 +1957,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     // overlaps the other's issue-bound traversal (MCG_LANES=1: one pass at a
     // time). Deterministic mode keeps one lane: its epochs are (pass, bounce).
     const char* lanes_env = std::getenv("MCG_LANES");
-    int lanes = lanes_env ? std::max(1, std::min(2, std::atoi(lanes_env))) : kDefaultLanes;
+    int lanes = lanes_env ? std::max(1, std::min(mcg_ctx::kMaxLanes, std::atoi(lanes_env))) : kDefaultLanes;
     if (deferred) lanes = 1;
     uint32_t k = P.samples_per_pass > 0 ? static_cast<uint32_t>(P.samples_per_pass) : 0;
     if (k == 0) {
@@ -2005,7 +2005,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
     const size_t lane_bytes = f4 * 12 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
     ctx->path_mem.ensure(lane_bytes);
-    if (lanes > 1) ctx->path_mem2.ensure(lane_bytes);
+    for (int l = 1; l < lanes; ++l) ctx->lane_path[l].ensure(lane_bytes);
     RenderView R{};
     R.S = D.view;
     if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
@@ -2109,21 +2109,30 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
     }
-    if (lanes > 1 && !ctx->lane2) {
-        cuda_check(cudaStreamCreateWithFlags(&ctx->lane2, cudaStreamNonBlocking), "lane stream");
-        cuda_check(cudaStreamCreateWithFlags(&ctx->aux2, cudaStreamNonBlocking), "aux stream");
-        cuda_check(cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming), "event");
+    if (lanes > 1 && !ctx->ev_lane[0]) {
         for (cudaEvent_t& e : ctx->ev_lane) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
-    RenderView RL[2] = {R, R};
-    layout(RL[0], ctx->path_mem.as<char>());
-    if (lanes > 1) layout(RL[1], ctx->path_mem2.as<char>());
-    const cudaStream_t lane_main[2] = {ctx->stream, ctx->lane2};
-    const cudaStream_t lane_aux[2] = {ctx->aux, ctx->aux2};
-    const cudaEvent_t lane_fork[2] = {ctx->ev_fork, ctx->ev_fork2};
-    const cudaEvent_t lane_join[2] = {ctx->ev_join, ctx->ev_join2};
-    mcg::DevMem* lane_tmp[2] = {&ctx->cub_temp, &ctx->cub_temp2};
+    for (int l = 1; l < lanes; ++l) {
+        if (ctx->lane_stream[l]) continue;
+        cuda_check(cudaStreamCreateWithFlags(&ctx->lane_stream[l], cudaStreamNonBlocking), "lane stream");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->lane_aux[l], cudaStreamNonBlocking), "aux stream");
+        cuda_check(cudaEventCreateWithFlags(&ctx->lane_fork[l], cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&ctx->lane_join[l], cudaEventDisableTiming), "event");
+    }
+    constexpr int kML = mcg_ctx::kMaxLanes;
+    RenderView RL[kML];
+    cudaStream_t lane_main[kML], lane_aux[kML];
+    cudaEvent_t lane_fork[kML], lane_join[kML];
+    mcg::DevMem* lane_tmp[kML];
+    for (int l = 0; l < lanes; ++l) {
+        RL[l] = R;
+        layout(RL[l], (l == 0 ? ctx->path_mem : ctx->lane_path[l]).as<char>());
+        lane_main[l] = l == 0 ? ctx->stream : ctx->lane_stream[l];
+        lane_aux[l] = l == 0 ? ctx->aux : ctx->lane_aux[l];
+        lane_fork[l] = l == 0 ? ctx->ev_fork : ctx->lane_fork[l];
+        lane_join[l] = l == 0 ? ctx->ev_join : ctx->lane_join[l];
+        lane_tmp[l] = l == 0 ? &ctx->cub_temp : &ctx->lane_cub[l];
+    }
     const int block = 128;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
@@ -2144,9 +2153,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     cuda_check(cudaEventCreate(&ev1), "event");
     cuda_check(cudaEventRecord(ev0, ctx->stream), "event record");
     if (lanes > 1) {
-        // lane 2 starts after the setup (stats reset, pixel lists) on the main stream
-        cuda_check(cudaEventRecord(ctx->ev_lane[2], ctx->stream), "event record");
-        cuda_check(cudaStreamWaitEvent(ctx->lane2, ctx->ev_lane[2], 0), "wait");
+        // the other lanes start after the setup (stats reset, pixel lists) on the main stream
+        cuda_check(cudaEventRecord(ctx->ev_lane[kML], ctx->stream), "event record");
+        for (int l = 1; l < lanes; ++l) cuda_check(cudaStreamWaitEvent(lane_main[l], ctx->ev_lane[kML], 0), "wait");
     }
 
     int prev_lane = -1;
@@ -2243,9 +2252,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         if (lanes > 1) cuda_check(cudaEventRecord(ctx->ev_lane[l], sm), "event record");
         prev_lane = l;
     }
-    if (lanes > 1) {
-        cuda_check(cudaEventRecord(ctx->ev_lane[2], ctx->lane2), "event record");
-        cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_lane[2], 0), "wait");
+    for (int l = 1; l < lanes; ++l) {   // the render ends when every lane is done
+        cuda_check(cudaEventRecord(ctx->ev_lane[l], lane_main[l]), "event record");
+        cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_lane[l], 0), "wait");
     }
     cuda_check(cudaEventRecord(ev1, ctx->stream), "event record");
     unsigned long long st[kStatCount];

@@ -780,11 +780,13 @@ mcg_status mcg_destroy(mcg_ctx* ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
-    if (ctx->ev_fork2) cudaEventDestroy(ctx->ev_fork2);
-    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
+    for (int l = 0; l < mcg_ctx::kMaxLanes; ++l) {
+        if (ctx->lane_fork[l]) cudaEventDestroy(ctx->lane_fork[l]);
+        if (ctx->lane_join[l]) cudaEventDestroy(ctx->lane_join[l]);
+        if (ctx->lane_aux[l]) cudaStreamDestroy(ctx->lane_aux[l]);
+        if (ctx->lane_stream[l]) cudaStreamDestroy(ctx->lane_stream[l]);
+    }
     for (cudaEvent_t e : ctx->ev_lane) if (e) cudaEventDestroy(e);
-    if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
-    if (ctx->lane2) cudaStreamDestroy(ctx->lane2);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MCG_OK;
