@@ -136,6 +136,11 @@ struct mcg_ctx {
     cudaEvent_t lane_fork[kMaxLanes] = {}, lane_join[kMaxLanes] = {};
     cudaEvent_t ev_lane[kMaxLanes + 1] = {};
     mcg::DevMem lane_cub[kMaxLanes], lane_path[kMaxLanes];
+    // the shard's pixel list, device-resident across render calls with the
+    // same (width, height, tile size, shard rank, count, mode)
+    mcg::DevMem pix_mem;
+    int64_t pix_key[6] = {-1, -1, -1, -1, -1, -1};
+    uint32_t pix_n = 0;
     // scratch
     mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
     mcg::DevMem path_mem, queue_mem, stats_mem;

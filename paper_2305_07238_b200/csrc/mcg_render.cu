@@ -1941,16 +1941,29 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const bool cache_on = P.cache_mode != MCG_CACHE_OFF;
     const bool deferred = P.cache_mode == MCG_CACHE_DETERMINISTIC;
 
-    // Shard pixel list (16x16 tiles, tracer.hpp:19).
+    // Shard pixel list (16x16 tiles, tracer.hpp:19), built on the host and
+    // uploaded once per (size, tiling, shard): a render call otherwise left
+    // the GPU idle for the few ms this loop and copy take.
     const int ts = P.tile_size > 0 ? P.tile_size : 16;
-    const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
-    std::vector<uint32_t> pix;
-    pix.reserve(static_cast<size_t>(W) * H);
-    for (int y = 0; y < H; ++y)
-        for (int x = 0; x < W; ++x)
-            if (tile_mine(P, (y / ts) * tiles_x + x / ts, tiles_x * tiles_y))
-                pix.push_back(static_cast<uint32_t>(y * W + x));
-    const uint32_t n_pix = static_cast<uint32_t>(pix.size());
+    const int64_t pkey[6] = {W, H, ts, P.shard_count > 1 ? P.shard_rank : 0, std::max(1, P.shard_count),
+                             P.shard_count > 1 ? P.shard_mode : 0};
+    if (std::memcmp(pkey, ctx->pix_key, sizeof(pkey)) != 0) {
+        const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
+        std::vector<uint32_t> pix;
+        pix.reserve(static_cast<size_t>(W) * H);
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                if (tile_mine(P, (y / ts) * tiles_x + x / ts, tiles_x * tiles_y))
+                    pix.push_back(static_cast<uint32_t>(y * W + x));
+        ctx->pix_mem.ensure(std::max<size_t>(pix.size(), 1) * 4);
+        cuda_check(cudaMemcpyAsync(ctx->pix_mem.p, pix.data(), pix.size() * 4ull, cudaMemcpyHostToDevice,
+                                   ctx->stream), "H2D pixels");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "H2D pixels");
+        ctx->pix_n = static_cast<uint32_t>(pix.size());
+        std::memcpy(ctx->pix_key, pkey, sizeof(pkey));
+    }
+    const uint32_t n_pix = ctx->pix_n;
+    const uint32_t* d_pix_all = ctx->pix_mem.as<uint32_t>();
 
     // Pass lanes: with 2, consecutive passes alternate between two stream
     // pairs with their own path state, so one pass's latency-bound shading
@@ -2046,11 +2059,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         V.skey = skey_;
         V.order = order_;
         V.squeue = u32 + 6 * max_paths;
-        uint32_t* d_pix = V.squeue + n_shadow;
-        V.pix = d_pix;
-        V.shadow_count = reinterpret_cast<unsigned int*>(d_pix + n_pix);
+        V.pix = d_pix_all;
+        V.shadow_count = reinterpret_cast<unsigned int*>(V.squeue + n_shadow + n_pix);
         V.vis = reinterpret_cast<uint8_t*>(V.shadow_count + 64);
-        cuda_check(cudaMemcpyAsync(d_pix, pix.data(), n_pix * 4ull, cudaMemcpyHostToDevice, ctx->stream), "H2D pixels");
     };
     R.radiance = d_rad;
     R.nodes_found = d_nodes;

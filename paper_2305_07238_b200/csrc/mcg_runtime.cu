@@ -769,8 +769,12 @@ mcg_status mcg_destroy(mcg_ctx* ctx) {
     ctx->scene.clear();
     for (DevMem* m : {&ctx->cub_temp, &ctx->scratch_a, &ctx->scratch_b, &ctx->scratch_c,
                       &ctx->scratch_d, &ctx->scratch_e, &ctx->path_mem, &ctx->queue_mem,
-                      &ctx->stats_mem}) {
+                      &ctx->stats_mem, &ctx->pix_mem}) {
         m->release();
+    }
+    for (int l = 0; l < mcg_ctx::kMaxLanes; ++l) {
+        ctx->lane_cub[l].release();
+        ctx->lane_path[l].release();
     }
     for (auto& r : ctx->pending) {
         cudaEventDestroy(r.a);
