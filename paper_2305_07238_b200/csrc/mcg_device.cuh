@@ -593,6 +593,12 @@ struct VmResult {
 // stores are queued with an order key (applied later, lowest key first);
 // otherwise stores CAS immediately (concurrent mode).
 template <bool kDeferred>
+// MCG_VM_PREFETCH=1 (experiment, off): fetch the next instruction word
+// while the current one executes; neutral (636.6-637.7 vs 636.4-638.3 ms per
+// bench render): the 16-byte words are L1 hits and not the VM's bound.
+#ifndef MCG_VM_PREFETCH
+#define MCG_VM_PREFETCH 0
+#endif
 __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheView& C,
                                                 bool cache_on, int mip_offset, uint32_t slot,
                                                 const ShadeIn& sp, unsigned grp, const Stack& st,
@@ -607,12 +613,23 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
     int32_t p_where = -1;
     unsigned long long p_cell = 0;
     VmResult out{make_float3(0.0f, 0.0f, 0.0f), true};
+#if MCG_VM_PREFETCH
+    // the next word is fetched while this one executes (the upload pads the
+    // code buffer by one word, so pc + 1 is always readable); a group skip
+    // refetches at its target
+    uint4 w_next = __ldg(code);
+#endif
     for (int pc = 0;; ++pc) {
         if (pc == resume) {
             parked = false;
             resume = -1;
         }
+#if MCG_VM_PREFETCH
+        const uint4 w = w_next;
+        w_next = __ldg(code + pc + 1);
+#else
         const uint4 w = __ldg(code + pc);
+#endif
         const uint8_t op = static_cast<uint8_t>(w.x & 0xffu);
         const uint8_t flags = static_cast<uint8_t>((w.x >> 8) & 0xffu);
         const int d = static_cast<int>((w.x >> 16) & 0xffu);
@@ -804,6 +821,9 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 if (__all_sync(grp, pr.hit)) {
                     parked = false;
                     pc += skip;  // the whole group skips the subtree
+#if MCG_VM_PREFETCH
+                    w_next = __ldg(code + pc + 1);
+#endif
                 } else {
                     resume = pc + 1 + skip;
                 }

@@ -1569,6 +1569,8 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         v.n_rlights = f.n_rect_lights;
         v.programs = static_cast<const mcg_program*>(up(6, f.programs, f.n_programs * sizeof(mcg_program)));
         v.n_programs = f.n_programs;
+        // one spare word past the last program: the VM fetches pc + 1 ahead
+        D.bufs[7].ensure((f.n_code + 1) * sizeof(mcg_insn));
         v.code = static_cast<const mcg_insn*>(up(7, f.code, f.n_code * sizeof(mcg_insn)));
         v.consts = static_cast<const mcg_const*>(up(8, f.consts, f.n_consts * sizeof(mcg_const)));
         v.noise = static_cast<const mcg_noise*>(up(9, f.noise, f.n_noise * sizeof(mcg_noise)));
