@@ -16,12 +16,35 @@ constexpr int kMaxMip = 24;                       // raycone.hpp:18
 constexpr float kTwoPi = 6.28318530717958647692f; // value.hpp:126
 
 // ---------------------------------------------------------------- rng.hpp
+#ifndef MCG_MIX_IMAD
+#define MCG_MIX_IMAD 0
+#endif
+#if MCG_MIX_IMAD
+// (experiment, off: probe lookups 40.4 vs 43.3 G/s -- more instructions in
+// total) x ^ (x >> s) on 32-bit halves with the right shifts done as multiply-highs
+// (IMAD.HI on the FMA pipe instead of SHF on the ALU pipe, which the hashing
+// kernels saturate); integer arithmetic, so the result is the same word.
+__device__ __forceinline__ uint64_t xorshr(uint64_t x, uint32_t s) {
+    const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+    uint32_t m;   // 2^(32 - s), opaque to the compiler so it stays a multiply
+    asm("mov.b32 %0, %1;" : "=r"(m) : "r"(1u << (32 - s)));
+    const uint32_t lo_s = __umulhi(lo, m) | (hi * m), hi_s = __umulhi(hi, m);
+    return (static_cast<uint64_t>(hi ^ hi_s) << 32) | (lo ^ lo_s);
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:8-13
+    x += 0x9e3779b97f4a7c15ull;
+    x = xorshr(x, 30) * 0xbf58476d1ce4e5b9ull;
+    x = xorshr(x, 27) * 0x94d049bb133111ebull;
+    return xorshr(x, 31);
+}
+#else
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:8-13
     x += 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
     return x ^ (x >> 31);
 }
+#endif
 
 __device__ __forceinline__ uint64_t path_key(uint64_t seed, uint64_t pixel, uint64_t sample) {
     return mix64(seed ^ mix64(pixel ^ mix64(sample)));   // rng.hpp:20-21
