@@ -1815,7 +1815,10 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 #define MCG_SHADE_MINB 4
 #endif
 template <bool kDeferred>
-__global__ void __launch_bounds__(128, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
+#ifndef MCG_SHADE_BLOCK
+#define MCG_SHADE_BLOCK 128
+#endif
+__global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
                                                const uint32_t* __restrict__ order, int max_stack,
                                                uint32_t wh, int b) {
     extern __shared__ float smem[];
@@ -2144,7 +2147,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         lane_join[l] = l == 0 ? ctx->ev_join : ctx->lane_join[l];
         lane_tmp[l] = l == 0 ? &ctx->cub_temp : &ctx->lane_cub[l];
     }
-    const int block = 128;
+    const int block = MCG_SHADE_BLOCK;
     const int max_stack = static_cast<int>(D.max_stack);
     const size_t smem = static_cast<size_t>(max_stack) * block * 3 * sizeof(float);
     if (smem > 200 * 1024) fail(MCG_ERR_INVALID_ARGUMENT, "material stack too deep for shared memory");
