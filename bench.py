@@ -142,36 +142,58 @@ def make_scene(tmp: str):
 # reference arm: the reference's own CPU path on the host cores
 # --------------------------------------------------------------------------
 
-CPU_SPP = 4   # the CPU is timed on the same frame at 4 spp (full spp takes hours)
+# The CPU leg renders the same workload (same scene, camera, 128 spp, 1e7 x
+# 10 table, concurrent shared-table inserts) on a band of it: contiguous
+# 16x16 tiles 8/16 of the frame (shard_mode 1, rank 8 of 16: a ~1920x68
+# band through the middle of the image), so samples/s is like for like in
+# spp and in table fill; the full frame would take ~3 min per step. The
+# table (MaterialCache(1e7, 10): 800 MB zeroed, cache.cpp:82-92) is built
+# before the timer and reported apart (`table_build_s`).
+CPU_BAND, CPU_BANDS = 8, 16
 
 
-def cpu_reference_sample(scene_path: str, spp: int = CPU_SPP, threads: int = 0, cache: bool = True):
+def cpu_reference_sample(scene_path: str, threads: int = 0, cache: bool = True):
     """Times oracle/_ref's render (reference sources + restated tracer, tile
     queue over worker threads, shared MaterialCache) on a bounded sample:
-    the full 1920x1080 frame at `spp` samples per pixel."""
+    a 1/16 band of the 1920x1080x128 frame."""
     import _oracle
     nthreads = threads or os.cpu_count() or 1
     if _oracle.Ref.available():
         ref = _oracle.Ref()
         s = ref.scene_load(scene_path)
-        P = _oracle.RenderParamsC(W, H, spp, 4, 2 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
-                                  0.2, 16, 0, 1, 0, nthreads, 1)
+        P = _oracle.RenderParamsC(W, H, SPP, 4, 2 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
+                                  0.2, 16, CPU_BAND, CPU_BANDS, 1, nthreads, 1)
         t0 = time.perf_counter()
-        *_, st = ref.render(s, P, W, H)
+        c = ref.cache_new(N_CELLS, N_ENTRIES) if cache else None
+        t_table = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rad, _, samples, _, st = ref.render(s, P, W, H, cache=c)
         dt = time.perf_counter() - t0
+        if c is not None:
+            ref.cache_free(c)
         ref.L.ref_scene_free(s)
-        return {"kind": "reference", "seconds": dt, "samples": W * H * spp, "cores": nthreads,
-                "hits": int(st.hits), "lookups": int(st.lookups)}
-    # Fallback: the C restatement (single thread) on a 480x270 crop.
+        return {"kind": "reference", "seconds": dt, "samples": int(samples.sum()), "cores": nthreads,
+                "hits": int(st.hits), "lookups": int(st.lookups), "table_build_s": t_table,
+                "radiance": rad, "pixel_samples": samples}
+    # Fallback: the C restatement (single thread) on a 1/64 band.
     from paper_2305_07238_b200 import load_scene
     orc = _oracle.Oracle()
     sc = load_scene(scene_path)
-    P = _oracle.RenderParamsC(480, 270, spp, 4, 1 if cache else 0, 0, 1_000_000, N_ENTRIES, 0, 1,
-                              0.2, 16, 0, 1, 0, 1, 1)
+    P = _oracle.RenderParamsC(W, H, SPP, 4, 1 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
+                              0.2, 16, 32, 64, 1, 1, 1)
     t0 = time.perf_counter()
-    orc.render(sc.flat, P)
+    _, _, samples, _, _ = orc.render(sc.flat, P)
     dt = time.perf_counter() - t0
-    return {"kind": "port", "seconds": dt, "samples": 480 * 270 * spp, "cores": 1}
+    return {"kind": "port", "seconds": dt, "samples": int(samples.sum()), "cores": 1, "table_build_s": None}
+
+
+def cpu_sample_text(info) -> str:
+    if info["kind"] == "reference":
+        return (f"tiles {CPU_BAND}/{CPU_BANDS} of the {W}x{H}x{SPP}spp frame as one contiguous band "
+                f"({info['samples'] // SPP} pixels x {SPP} spp), concurrent inserts into a fresh "
+                f"{N_CELLS:.0e}x{N_ENTRIES} MaterialCache per step (built before the timer: "
+                f"{info['table_build_s']:.2f} s), tile queue over {info['cores']} threads")
+    return f"1/64 band of the {W}x{H}x{SPP}spp frame, 1 thread (C port)"
 
 
 def run_reference_arm(args) -> None:
@@ -189,9 +211,7 @@ def run_reference_arm(args) -> None:
             times.append(info["seconds"])
     t = sum(times) / len(times)
     v = info["samples"] / t
-    sample = (f"{W}x{H}x{CPU_SPP}spp frame per step (of the {W}x{H}x{SPP} workload), fresh cache "
-              f"{N_CELLS:.0e}x{N_ENTRIES} per step, tile queue over {info['cores']} threads"
-              if info["kind"] == "reference" else f"480x270x{CPU_SPP}spp crop, 1 thread (C port)")
+    sample = cpu_sample_text(info)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -200,9 +220,54 @@ def run_reference_arm(args) -> None:
         "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp cache {N_CELLS:.0e}x{N_ENTRIES}",
                    "sample": sample},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": info["cores"],
-                         "kind": info["kind"], "sample": sample},
+                         "kind": info["kind"], "sample": sample,
+                         "table_build_s": info.get("table_build_s"),
+                         "hit_rate": info["hits"] / max(1, info["lookups"]) if "hits" in info else None},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def parity_block(frame_cached, frame_off, st, ref_band, gpu_band) -> dict:
+    import numpy as np
+    rad_c, nodes_c, samp_c = frame_cached
+    n = np.maximum(samp_c, 1)[..., None].astype(np.float64)
+    img_c = (rad_c / n).astype(np.float32)
+    img_off = (frame_off / n).astype(np.float32)
+
+    def err(a, b, mask=None):
+        d = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        if mask is not None:
+            d = d[mask]
+        return {"rmse": float(np.sqrt((d ** 2).mean())), "mean_abs": float(d.mean())}
+
+    zero = nodes_c == 0
+    out = {"config": "the timed render (concurrent inserts, two pass lanes) vs the cache-off render",
+           "frame": err(img_c, img_off),
+           "zero_hit_pixels": int(zero.sum()),
+           "zero_hit_pixels_bit_identical": bool(np.array_equal(rad_c[zero].view(np.uint64),
+                                                               frame_off[zero].view(np.uint64))),
+           "hits_eq_sum_nodes_found": int(st.hits) == int(nodes_c.sum())}
+    if ref_band is not None and ref_band.get("radiance") is not None:
+        # like for like: the reference rendered one band of tiles with its
+        # own table (cpu_baseline); the GPU renders the same band the same
+        # way, cached (concurrent) and uncached
+        gc, goff = gpu_band
+        band = ref_band["pixel_samples"] > 0
+        assert np.array_equal(band, gc.samples > 0)
+        gimg = gc.radiance_image()
+        goff_img = goff.radiance_image()
+        rimg = (ref_band["radiance"] / np.maximum(ref_band["pixel_samples"], 1)[..., None]).astype(np.float32)
+        gpu = err(gimg, goff_img, band)
+        ref = err(rimg, goff_img, band)
+        gz = (gc.nodes_found == 0) & band
+        out["band"] = {"pixels": int(band.sum()), "what": cpu_sample_text(ref_band),
+                       "gpu": gpu, "reference": ref,
+                       "bound": "gpu rmse <= reference rmse + 1e-4 (north_star)",
+                       "within_bound": gpu["rmse"] <= ref["rmse"] + 1e-4,
+                       "zero_hit_pixels": int(gz.sum()),
+                       "zero_hit_pixels_bit_identical": bool(np.array_equal(
+                           gc.radiance[gz].view(np.uint64), goff.radiance[gz].view(np.uint64)))}
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -315,6 +380,12 @@ def main() -> None:
     total_samples = W * H * SPP
     value = total_samples * args.steps / (ms / 1e3)
     st = stats[-1]
+    # the last timed render's frame (rank 0 holds the gathered image), kept
+    # for the parity block below
+    torch.cuda.synchronize()
+    frame_off = None
+    frame_cached = (rad.cpu().numpy().reshape(H, W, 3).copy(), nodes.cpu().numpy().reshape(H, W).copy(),
+                    samples.cpu().numpy().reshape(H, W).copy())
 
     # ---- e2e through the host-buffer C ABI --------------------------------
     host_rad = torch.zeros(H * W * 3, dtype=torch.float64).pin_memory()
@@ -373,6 +444,8 @@ def main() -> None:
         off = RenderConfig(width=W, height=H, spp=SPP, cache_enabled=False,
                            shard_rank=rank, shard_count=world).to_params()
         ms_off, _, _ = timed(lambda: step(off), 1, 1)
+        torch.cuda.synchronize()
+        frame_off = rad.cpu().numpy().reshape(H, W, 3).copy()
         extras["cache_speedup"] = {"t_nocache_ms": ms_off, "t_cache_ms": ms / args.steps,
                                    "speedup": ms_off / (ms / args.steps)}
         if rank == 0:
@@ -433,117 +506,152 @@ def main() -> None:
             extras["probe_roofline"] = pr
 
     # ---- roofline of the dominant kernel ----------------------------------
+    # The timed renders run two pass lanes and a second stream per vertex
+    # (MCG_LANES=2, MCG_OVERLAP): their per-kernel event times overlap and do
+    # not add up to the step. The dominant kernel is therefore chosen, and
+    # its per-launch time taken, from one serialized side render of the same
+    # workload (MCG_LANES=1 MCG_OVERLAP=0: one kernel at a time, so each
+    # event pair brackets exactly one kernel) -- what ncu's launch list
+    # measures too (profiles/). Its work counters are that render's own.
     peak, peak_src = measured_peaks()
+    serial_env = {"MCG_LANES": "1", "MCG_OVERLAP": "0"}
+    saved = {k: os.environ.get(k) for k in serial_env}
+    os.environ.update(serial_env)
+    try:
+        ctx.reset_kernel_times()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st_s = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_serial = e0.elapsed_time(e1)
+        kser = ctx.kernel_times()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     ne = N_ENTRIES
-    steps = args.steps
     f = scene.flat
     n_lights = f.n_point_lights + f.n_rect_lights
-    # Compulsory HBM bytes per kernel class over the timed steps (DESIGN.md
-    # §5): what the kernel must move between HBM and the SMs at least once.
-    #   shade:  one cell (8 Ne) per lookup and per store attempt, +8 per won
-    #           CAS, 48 per TexSample (4 RGB texels); per shading point the
-    #           record + path state in (104 B) and the continuation out (48 B);
-    #           per shadow-ray candidate 52 B out, per rejected light 16 B
-    #   trace_closest: per ray 36 B in (order, ray), 72 B out per hit
-    #           (record, cone, key, value), 48 B per miss (radiance update)
-    #   trace_shadow: per ray 37 B (queue slot, ray, visibility byte)
-    # plus the scene's nodes and triangles once per launch. BVH node and
-    # triangle reads beyond that are served by L1/L2 (the bench scene's BVH
-    # is a few hundred KB); SURVEY §8d's per-visit units (40 B per reference
-    # node, here 128 B per 4-wide node, 48 B per triangle) are reported as
-    # `cache_served_bytes_per_launch` next to them.
+    closest_hits = min(st_s.closest_rays, max(0, st_s.shading_points - st_s.paths))
+    # Per kernel class, per render: (a) SURVEY §8(d)'s algorithmic bytes --
+    # 8 Ne per lookup / store attempt (+8 per won CAS), 48 per TexSample,
+    # 40 per BVH node visited (the reference's BvhNode), 48 per triangle
+    # tested -- and (b) the compulsory HBM bytes, what must cross HBM at
+    # least once: per shading point the record + path state in (104 B) and
+    # the continuation out (48 B), per shadow-ray candidate 52 B out (16 B
+    # per rejected light); per continuation ray 36 B in, 72 B out per hit,
+    # 48 B per miss; per shadow ray 37 B; plus the scene once per launch.
+    # The traversal kernels' node and triangle bytes are served by L1/L2
+    # (the bench BVH is a few hundred KB): (a) >> (b) for them.
+    nodes_closest = st_s.bvh_nodes - st_s.bvh_nodes_shadow
+    prims_closest = st_s.prims_tested - st_s.prims_tested_shadow
+    probe_bytes = st_s.lookups * 8 * ne + st_s.stores_attempted * 8 * ne + st_s.inserts_won * 8
     scene_once = f.n_prims * (48 + 24 + 4) + f.n_nodes * 64
-    closest_rays = st.closest_rays
-    # hits of continuation rays = shading points after the primary vertex
-    # (every primary ray hits in the closed bench room)
-    closest_hits = min(closest_rays, max(0, st.shading_points - st.paths))
-    n_closest_nodes = st.bvh_nodes - st.bvh_nodes_shadow
-    n_closest_prims = st.prims_tested - st.prims_tested_shadow
+    algorithmic = {
+        "shade": probe_bytes + st_s.tex_samples * 48,
+        "trace_closest": nodes_closest * 40 + prims_closest * 48,
+        "trace_shadow": st_s.bvh_nodes_shadow * 40 + st_s.prims_tested_shadow * 48,
+    }
     compulsory = {
-        "shade": steps * (st.lookups * 8 * ne + st.stores_attempted * 8 * ne + st.inserts_won * 8
-                          + st.tex_samples * 48 + st.shading_points * (104 + 48)
-                          + st.shadow_rays * 52 + (n_lights * st.shading_points - st.shadow_rays) * 16),
-        "trace_closest": steps * (closest_rays * 36 + closest_hits * 72 + (closest_rays - closest_hits) * 48),
-        "trace_shadow": steps * st.shadow_rays * 37,
+        "shade": probe_bytes + st_s.tex_samples * 48 + st_s.shading_points * (104 + 48)
+                 + st_s.shadow_rays * 52 + (n_lights * st_s.shading_points - st_s.shadow_rays) * 16,
+        "trace_closest": st_s.closest_rays * 36 + closest_hits * 72 + (st_s.closest_rays - closest_hits) * 48,
+        "trace_shadow": st_s.shadow_rays * 37,
     }
-    cache_served = {
-        "trace_closest": steps * (n_closest_nodes * 128 + n_closest_prims * 48),
-        "trace_shadow": steps * (st.bvh_nodes_shadow * 128 + st.prims_tested_shadow * 48),
-    }
-
-    def kernel_roofline(kname):
-        rec = ktimes.get(kname, {"ms": 0.0, "launches": 0})
-        launches = max(1, rec["launches"])
-        per_ms = rec["ms"] / launches
-        nbytes = compulsory.get(kname, rec.get("bytes", 0.0)) / launches
-        if kname in ("trace_closest", "trace_shadow"):
-            nbytes += scene_once
-        ach = nbytes / (per_ms / 1e3) / 1e9 if per_ms > 0 else 0.0
-        out = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak, "unit": "GB/s",
-               "frac": ach / peak, "traffic": traffic_ncu.get(kname),
-               "algorithmic_bytes_per_launch": nbytes, "per_launch_ms": per_ms}
-        if kname in cache_served:
-            cs = cache_served[kname] / launches
-            out["cache_served_bytes_per_launch"] = cs
-            out["cache_served_gbs"] = cs / (per_ms / 1e3) / 1e9 if per_ms > 0 else 0.0
-        return out
-
-    # ncu-measured DRAM traffic per launch (profiles/dram_traffic.json, one
-    # capture of a whole render, averaged per launch) -- read back here,
-    # never measured under the bench.
+    # ncu DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum
+    # of every launch of one render, averaged): read back from the committed
+    # capture named in `_source`, never measured under this run.
     try:
         with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as fh:
-            traffic_ncu = {k: v for k, v in json.load(fh).items() if not k.startswith("_")}
+            traffic_doc = json.load(fh)
     except Exception:
-        traffic_ncu = {}
+        traffic_doc = {}
     try:
         with open(os.path.join(ROOT, "profiles", "kernel_efficiency.json")) as fh:
             eff = json.load(fh)
     except Exception:
         eff = {}
-    dname = max(ktimes.items(), key=lambda kv: kv[1]["ms"])[0] if ktimes else "?"
+
+    def kernel_roofline(kname):
+        rec = kser.get(kname, {"ms": 0.0, "launches": 0})
+        launches = max(1, rec["launches"])
+        per_ms = rec["ms"] / launches
+        alg = algorithmic.get(kname, rec.get("bytes", 0.0)) / launches
+        comp = compulsory.get(kname, rec.get("bytes", 0.0)) / launches
+        if kname in ("trace_closest", "trace_shadow"):
+            comp += scene_once
+        gbs = (lambda b: b / (per_ms / 1e3) / 1e9 if per_ms > 0 else 0.0)  # noqa: E731
+        out = {"bound": "hbm", "kernel": kname, "achieved": gbs(alg), "peak": peak, "unit": "GB/s",
+               "frac": gbs(alg) / peak, "traffic": traffic_doc.get(kname),
+               "algorithmic_bytes_per_launch": alg,
+               "units": "SURVEY 8(d): 8*Ne B per lookup/store attempt (+8 per won CAS), 48 B per TexSample, "
+                        "40 B per BVH node visited, 48 B per triangle tested",
+               "per_launch_ms": per_ms, "launches_per_step": rec["launches"],
+               "hbm_compulsory": {"bytes_per_launch": comp, "achieved": gbs(comp), "frac": gbs(comp) / peak},
+               "timing": "serialized side render (MCG_LANES=1 MCG_OVERLAP=0), CUDA events around each launch"}
+        if traffic_doc.get("_source"):
+            out["traffic_source"] = traffic_doc["_source"]
+        if kname in eff:
+            out["issue"] = eff[kname]
+        return out
+
+    total_ser = sum(x["ms"] for x in kser.values())
+    dname = max(kser.items(), key=lambda kv: kv[1]["ms"])[0] if kser else "?"
     roof = kernel_roofline(dname)
-    if dname in eff:
-        # what does bound it (ncu, profiles/r1_ncu_h.txt): issue slots and SIMT
-        # efficiency, not HBM bandwidth
-        roof["issue"] = eff[dname]
-    roof["limiter"] = ("issue/latency: warp divergence in BVH traversal (L1/L2-resident tree); "
-                       "HBM is not the bound -- see profiles/README.md"
+    roof["serialized_share"] = {k: round(v["ms"] / max(1e-9, total_ser), 4) for k, v in kser.items()}
+    roof["serialized_render_ms"] = ms_serial
+    # consistency: the dominant kernel's launches fit inside one timed step
+    roof["fits_in_step"] = bool(roof["per_launch_ms"] * roof["launches_per_step"] <= ms / args.steps)
+    roof["limiter"] = ("issue/latency: warp divergence in BVH traversal (L1/L2-resident tree) -- the "
+                       "8(d) bytes are L1/L2-served, HBM (hbm_compulsory) is not the bound"
                        if dname.startswith("trace") else "random HBM access (cache probes)")
     roof["peak_source"] = peak_src
-    shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ktimes.values())), 4)
-              for k, v in ktimes.items()}
-    roof["kernel_share"] = shares
-    roof["kernel_share_note"] = ("shares of summed per-launch CUDA-event times over the timed region; "
-                                 "trace_shadow runs on a second stream concurrently with trace_closest "
-                                 "(MCG_OVERLAP), and two passes are in flight on two stream pairs "
-                                 "(MCG_LANES=2), so event times include the overlap; the serialized "
-                                 "shares are in the ncu launch list (profiles/)")
     # The north-star kernel (material VM + cache probes) beside it.
     roof_shade = kernel_roofline("shade")
-    if "shade" in eff:
-        roof_shade["issue"] = eff["shade"]
-    # Render-level: the shade and traversal kernels' compulsory
-    # bytes over the whole step time.
+    # Render-level: the compulsory bytes of the shade and
+    # traversal kernels over the timed step.
     total_bytes = sum(compulsory.values())
-    roof["render_level"] = {"compulsory_bytes_per_step": total_bytes / max(1, steps),
-                            "achieved": total_bytes / (ms / 1e3) / 1e9,
-                            "frac": total_bytes / (ms / 1e3) / 1e9 / peak}
+    roof["render_level"] = {"compulsory_bytes_per_step": total_bytes,
+                            "achieved": total_bytes / (ms / args.steps / 1e3) / 1e9,
+                            "frac": total_bytes / (ms / args.steps / 1e3) / 1e9 / peak}
+    ktimes_overlapped = {k: {"ms": round(v["ms"], 3), "launches": v["launches"]} for k, v in ktimes.items()}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            # median of 3 runs, a fresh table each (BASELINE.md §3)
+            # median of 3 runs, a fresh table each (SPEC.md:425)
             runs = [cpu_reference_sample(scene_path) for _ in range(3)]
             info = sorted(runs, key=lambda r: r["seconds"])[1]
             cpu = {"value": info["samples"] / info["seconds"], "unit": "samples/s",
                    "cores": info["cores"], "kind": info["kind"],
-                   "sample": (f"{W}x{H}x{CPU_SPP}spp frame, median of 3 runs with a fresh cache "
-                              f"{N_CELLS:.0e}x{N_ENTRIES}, tile queue over {info['cores']} threads"
-                              if info["kind"] == "reference" else f"480x270x{CPU_SPP}spp crop, 1 thread")}
+                   "sample": cpu_sample_text(info) + "; median of 3 runs",
+                   "table_build_s": info.get("table_build_s"),
+                   "hit_rate": info["hits"] / max(1, info["lookups"]) if "hits" in info else None}
+            ref_band = info
         except Exception as e:  # the checker must never break the bench line
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
+            ref_band = None
+        # Parity of the timed path itself (north_star, concurrent mode): the
+        # timed render's image vs the cache-off image of the same workload
+        # (RMSE), beside the reference's own cached-vs-uncached RMSE on the
+        # band it rendered above; pixels without a cache hit must equal the
+        # cache-off render bit for bit; hits == sum of the
+        # per-pixel hit counts.
+        if frame_off is not None:
+            try:
+                from paper_2305_07238_b200 import render as api_render
+                band_cfg = dict(width=W, height=H, spp=SPP, n_cells=N_CELLS, n_entries=N_ENTRIES,
+                                shard_rank=CPU_BAND, shard_count=CPU_BANDS, shard_mode=1)
+                gpu_band = (api_render(scene, RenderConfig(cache_enabled=True, **band_cfg), ctx=ctx).frame,
+                            api_render(scene, RenderConfig(cache_enabled=False, **band_cfg), ctx=ctx).frame)
+                parity = parity_block(frame_cached, frame_off, st, ref_band, gpu_band)
+            except Exception as e:
+                parity = {"error": str(e)[:200]}
         try:
             # the reference's MaterialCache on the 1e7x10 table,
             # 1 thread and every host thread, same descriptor generator as the
@@ -587,6 +695,7 @@ def main() -> None:
             "gpu_launches": int(launches),
             "roofline": roof,
             "roofline_shade": roof_shade,
+            "kernel_event_ms_timed_region": ktimes_overlapped,
             "render_stats": {"hit_rate": st.hits / st.lookups if st.lookups else 0.0,
                              "lookups": st.lookups, "hits": st.hits, "inserts_won": st.inserts_won,
                              "inserts_lost_full": st.inserts_lost_full,
@@ -596,6 +705,7 @@ def main() -> None:
                              "prims_tested_shadow": st.prims_tested_shadow,
                              "closest_rays": st.closest_rays, "tex_samples": st.tex_samples},
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         line.update(extras)
         print(json.dumps(line))

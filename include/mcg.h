@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MCG_ABI_VERSION 2   /* 2: mcg_render_stats.shadow_occluded */
+#define MCG_ABI_VERSION 3   /* 2: mcg_render_stats.shadow_occluded; 3: write_slots, insert log */
 
 typedef enum mcg_status {
     MCG_OK = 0,
@@ -160,6 +160,10 @@ mcg_status mcg_cache_lookup_device(mcg_cache* cache, const mcg_descriptor* d_des
 
 /* slot_word (cache.hpp:83-86) for [first, first+n); occupied_slots (cache.cpp:138-144). */
 mcg_status mcg_cache_read_slots(mcg_cache* cache, uint64_t first, size_t n, uint64_t* words);
+/* The inverse, host words -> slots [first, first+n): seeds a device table
+ * from a host MaterialCache's slot_word()s (the drop-in render's external
+ * cache, cache.hpp:83-86); no counters change. */
+mcg_status mcg_cache_write_slots(mcg_cache* cache, uint64_t first, size_t n, const uint64_t* words);
 mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied);
 mcg_status mcg_cache_counters_get(mcg_cache* cache, mcg_cache_counters* out);
 mcg_status mcg_cache_counters_reset(mcg_cache* cache);
@@ -213,6 +217,24 @@ mcg_status mcg_cache_trace_stop(mcg_cache* cache, uint64_t* recorded);
 mcg_status mcg_cache_trace_read(mcg_cache* cache, uint64_t first, size_t n, mcg_descriptor* out);
 mcg_status mcg_probe_replay(mcg_cache* cache, const mcg_descriptor* d, uint64_t n, int32_t blocks_per_sm,
                             double* ms, double* bytes, mcg_cache_counters* counters);
+
+/* Won-insert log: while recording, every insert this table wins in a
+ * concurrent-mode render (the VM's CacheStore) or a concurrent batch update
+ * appends (descriptor, entry within its cell, payload), up to `capacity`
+ * records (a table can win at most its empty-slot count). stop returns the
+ * number won (> capacity: the log overflowed). Replaying the records through
+ * MaterialCache::update (cache.cpp:94-119) in (cell, entry) order rebuilds
+ * the device's inserts word for word in a host table that held the same
+ * words before -- the drop-in render uses this to keep the caller's
+ * external cache current. */
+typedef struct mcg_insert_record {
+    mcg_descriptor desc;
+    uint32_t entry;
+    uint32_t payload;
+} mcg_insert_record;
+mcg_status mcg_cache_insert_log_start(mcg_cache* cache, uint64_t capacity);
+mcg_status mcg_cache_insert_log_stop(mcg_cache* cache, uint64_t* won);
+mcg_status mcg_cache_insert_log_read(mcg_cache* cache, uint64_t first, size_t n, mcg_insert_record* out);
 
 /* Probe microbenchmark: n descriptors generated on the device
  * from `seed` (mat<8, node<256, mip<=16, texel uniform in 2^mip), then one

@@ -10,6 +10,7 @@
 // tracer.hpp:7-94 and SPEC.md:378-434 with the decisions pinned in
 // DESIGN.md §render, calling the reference's own Scene::intersect/occluded,
 // footprint_gradients, execute and MaterialCache for everything they cover.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -36,18 +37,33 @@
 
 using namespace matcache;
 
-// Read access to Scene's private BVH (scene.hpp:114-118) without touching the
-// reference: explicit template instantiation may name private members.
+// Access to private members without touching the reference (explicit
+// template instantiation may name private members): Scene's BVH
+// (scene.hpp:114-118), read for the node-for-node tree comparison, and
+// MaterialCache's slot array and won-insert counter (cache.hpp:105-113),
+// used by the deferred (deterministic-insert) render below to take back a
+// shading point's immediate inserts and re-apply them at the epoch's end
+// through MaterialCache::update itself.
 namespace {
-struct BvhTag {
-    using type = std::vector<detail::BvhNode> Scene::*;
-    friend type bvh_member(BvhTag);
-};
 template <typename Tag, typename Tag::type M>
 struct Expose {
-    friend typename Tag::type bvh_member(Tag) { return M; }
+    friend typename Tag::type member(Tag) { return M; }
+};
+struct BvhTag {
+    using type = std::vector<detail::BvhNode> Scene::*;
+    friend type member(BvhTag);
 };
 template struct Expose<BvhTag, &Scene::bvh_>;
+struct TableTag {
+    using type = std::unique_ptr<std::atomic<uint64_t>[]> MaterialCache::*;
+    friend type member(TableTag);
+};
+template struct Expose<TableTag, &MaterialCache::table_>;
+struct WonTag {
+    using type = std::atomic<uint64_t> MaterialCache::*;
+    friend type member(WonTag);
+};
+template struct Expose<WonTag, &MaterialCache::inserts_won_>;
 }  // namespace
 
 namespace {
@@ -366,7 +382,7 @@ void ref_scene_intersect(void* s, const float* rays, size_t n, float t_min, floa
 // writes min(count, cap) nodes.
 size_t ref_scene_bvh(void* s, uint32_t* out, size_t cap) {
     const Scene& scene = *static_cast<Scene*>(s);
-    const std::vector<detail::BvhNode>& nodes = scene.*bvh_member(BvhTag{});
+    const std::vector<detail::BvhNode>& nodes = scene.*member(BvhTag{});
     for (size_t i = 0; i < nodes.size() && i < cap; ++i) {
         const detail::BvhNode& n = nodes[i];
         const float b[6] = {n.bounds_min.x, n.bounds_min.y, n.bounds_min.z,
@@ -391,7 +407,8 @@ void ref_scene_occluded(void* s, const float* rays, size_t n, float t_min, const
 // ---- restated render() ------------------------------------------------------
 struct RefRenderParams {
     int32_t width, height, spp, max_bounces;
-    int32_t mode;         // 0 cache off, 1 epoch-sequential (immediate inserts), 2 threaded tiles
+    int32_t mode;         // 0 cache off, 1 epoch-sequential (immediate inserts), 2 threaded tiles,
+                          // 3 epoch-sequential deterministic (deferred, ordered inserts)
     int32_t mip_offset;
     uint64_t n_cells;
     uint32_t n_entries;
@@ -511,9 +528,152 @@ struct Counters {
     uint64_t stores_attempted = 0, stores_won = 0, instructions = 0, shading_points = 0;
 };
 
+// Deterministic-insert mode (mode 3) on the reference's own code. An epoch is
+// one (pass, bounce) wavefront: its lookups must read the table as it was
+// when the epoch began, and its stores are applied at the epoch's end in
+// (sample-in-pass, pixel, store ordinal) order with MaterialCache::update's
+// semantics (cache.cpp:94-119) -- the rule mc_oracle.c (mode 3) and the GPU
+// (k_shade<true> + k_apply_ordered) implement. The reference's execute()
+// (stackvm.cpp:248-368) inserts immediately, so around each call:
+//   before: the cells of every descriptor the program can look up at this
+//           shading point (stackvm.cpp:331-340: mip_level / texel_indices of
+//           the point, or the non-uv sentinel) are snapshotted;
+//   after:  each slot that went 0 -> word during the call is an insert this
+//           point won; it is queued as (descriptor, payload, key), the slot
+//           is set back to 0 and the won-insert counter decremented, so the
+//           next point sees the epoch-start table again;
+//   apply:  the queue, sorted by key, goes through MaterialCache::update.
+// A store that found its cell full or its key present at epoch start can
+// only find the same at apply time (slots are write-once and fill as a
+// prefix), so queueing the won inserts alone is exact; the lost-full
+// counter of those stores is the one update() bumped during the call.
+// A program with two cache points on the same node (a shared DAG node
+// re-emitted per consumer, stackvm.cpp:114-118) would see its own first
+// store in the immediate call; such programs are rejected (none of the
+// synthetic scenes has one).
+struct DeferredStore {
+    CacheDescriptor desc;
+    uint32_t payload;
+    uint32_t key;
+};
+
+struct ProgramCachePoints {
+    std::vector<uint32_t> node_idx, bracket;
+    std::vector<uint8_t> uses_uv;
+    std::vector<uint32_t> store_ord;   // by bracket
+};
+
+class Deferred {
+public:
+    Deferred(const Scene& scene, MaterialCache* cache) : cache_(cache) {
+        table_ = (cache->*member(TableTag{})).get();
+        for (const auto& m : scene.materials) {
+            ProgramCachePoints pc;
+            pc.store_ord.assign(kMaxCachePoints, 0);
+            uint32_t stores = 0;
+            for (const Instruction& ins : m.program.code) {
+                if (ins.op == Opcode::CacheLookup) {
+                    for (uint32_t n : pc.node_idx) {
+                        if (n == ins.node_idx) {
+                            throw std::runtime_error("deferred mode: a program has two cache points on node " +
+                                                     std::to_string(n));
+                        }
+                    }
+                    pc.node_idx.push_back(ins.node_idx);
+                    pc.bracket.push_back(ins.bracket);
+                    pc.uses_uv.push_back(ins.uses_uv ? 1 : 0);
+                } else if (ins.op == Opcode::CacheStore) {
+                    pc.store_ord.at(ins.bracket) = stores++;
+                }
+            }
+            points_.push_back(std::move(pc));
+        }
+    }
+
+    uint32_t key_base = 0;
+
+    void before(const CompiledProgram& prog, uint32_t slot, const ShadingPoint& sp, int mip_offset) {
+        const ProgramCachePoints& pc = points_[slot];
+        const uint64_t nc = cache_->n_cells();
+        const uint32_t ne = cache_->n_entries();
+        descs_.clear();
+        cells_.clear();
+        ords_.clear();
+        snap_.clear();
+        snap_cells_.clear();
+        for (size_t k = 0; k < pc.node_idx.size(); ++k) {
+            CacheDescriptor d;
+            d.mat_idx = prog.material_id;
+            d.node_idx = pc.node_idx[k];
+            if (pc.uses_uv[k]) {
+                d.mip_level = mip_level(sp.g1, sp.g2, mip_offset);
+                const auto [tx, ty] = texel_indices(sp.uv, d.mip_level);
+                d.texel_x = tx;
+                d.texel_y = ty;
+            }
+            const uint64_t cell = hash_cell(d) % nc;
+            descs_.push_back(d);
+            cells_.push_back(cell);
+            ords_.push_back(pc.store_ord[pc.bracket[k]]);
+            bool seen = false;
+            for (uint64_t c : snap_cells_) seen = seen || c == cell;
+            if (seen) continue;
+            snap_cells_.push_back(cell);
+            for (uint32_t e = 0; e < ne; ++e) snap_.push_back(table_[cell * ne + e].load());
+        }
+    }
+
+    void after() {
+        const uint32_t ne = cache_->n_entries();
+        uint64_t taken = 0;
+        for (size_t c = 0; c < snap_cells_.size(); ++c) {
+            const uint64_t cell = snap_cells_[c];
+            for (uint32_t e = 0; e < ne; ++e) {
+                const uint64_t now = table_[cell * ne + e].load();
+                const uint64_t was = snap_[c * ne + e];
+                if (now == was) continue;
+                if (was != 0) throw std::runtime_error("deferred mode: an occupied slot changed");
+                size_t k = 0;
+                while (k < descs_.size() && !(cells_[k] == cell && hash_check(descs_[k]) == entry_hash(now))) ++k;
+                if (k == descs_.size()) throw std::runtime_error("deferred mode: insert of an unknown key");
+                queue_.push_back({descs_[k], entry_payload(now), key_base | ords_[k]});
+                table_[cell * ne + e].store(0);
+                ++taken;
+            }
+        }
+        (cache_->*member(WonTag{})).fetch_sub(taken);
+    }
+
+    // Epoch end: the queued stores in key order through update(). Returns
+    // the number of inserts won.
+    uint64_t apply() {
+        std::sort(queue_.begin(), queue_.end(),
+                  [](const DeferredStore& a, const DeferredStore& b) { return a.key < b.key; });
+        uint64_t won = 0;
+        for (const DeferredStore& q : queue_) {
+            const UpdateResult r = cache_->update(q.desc, decode_value(q.payload));
+            if (r.outcome == InsertOutcome::Won) {
+                if (entry_payload(r.packed) != q.payload) throw std::runtime_error("deferred mode: payload round trip");
+                ++won;
+            }
+        }
+        queue_.clear();
+        return won;
+    }
+
+private:
+    MaterialCache* cache_;
+    std::atomic<uint64_t>* table_;
+    std::vector<ProgramCachePoints> points_;
+    std::vector<CacheDescriptor> descs_;
+    std::vector<uint64_t> cells_, snap_, snap_cells_;
+    std::vector<uint32_t> ords_;
+    std::vector<DeferredStore> queue_;
+};
+
 // One path vertex: intersect, shade, next-event estimation, bounce.
 void path_vertex(const Scene& scene, const RefRenderParams& p, const CacheBinding& binding,
-                 const PathRng& rng, int b, PathState& ps, Counters& cnt) {
+                 const PathRng& rng, int b, PathState& ps, Counters& cnt, Deferred* dq = nullptr) {
     HitRecord hit;
     if (!scene.intersect(ps.ray, kTMin, INFINITY, &hit)) {
         ps.L = ps.L + ps.thr * scene.env;
@@ -524,10 +684,13 @@ void path_vertex(const Scene& scene, const RefRenderParams& p, const CacheBindin
     const auto [g1, g2] = footprint_gradients(ps.cone, ps.ray.dir, hit.normal, hit.patch);
     ShadingPoint sp{hit.position, hit.normal, ps.ray.dir, hit.uv, g1, g2};
     EvalStats st;
-    const Value v = execute(scene.materials[hit.material_slot].program, sp, binding, st);
+    const CompiledProgram& prog = scene.materials[hit.material_slot].program;
+    if (dq) dq->before(prog, hit.material_slot, sp, binding.mip_offset);
+    const Value v = execute(prog, sp, binding, st);
+    if (dq) dq->after();
     ++cnt.shading_points;
     cnt.stores_attempted += st.stores_attempted;
-    cnt.stores_won += st.stores_won;
+    if (!dq) cnt.stores_won += st.stores_won;   // deferred: counted at the epoch's apply
     cnt.instructions += st.instructions_executed;
     ps.nodes += static_cast<uint32_t>(st.nodes_found);
     const Color3 c = v.as_rgb();
@@ -637,9 +800,13 @@ extern "C" int ref_render(void* s, const RefRenderParams* pp, void* external_cac
         uint64_t paths = 0;
         if (p.mode != 2) {
             // Epoch order: pass of k samples, bounce b, sample, pixel ascending
-            // (the GPU wavefront order; inserts are immediate here).
+            // (the GPU wavefront order). Mode 1: inserts are immediate; mode
+            // 3: deferred to the epoch's end (class Deferred).
             const int k = p.samples_per_pass > 0 ? std::min(p.samples_per_pass, p.spp) : 1;
             const size_t np = pixels.size();
+            std::unique_ptr<Deferred> dq;
+            if (p.mode == 3) dq = std::make_unique<Deferred>(scene, cache);
+            const uint32_t wh = static_cast<uint32_t>(w) * static_cast<uint32_t>(h);
             std::vector<PathState> st(np * static_cast<size_t>(k));
             for (int start = 0; start < p.spp; start += k) {
                 const int kk = std::min(k, p.spp - start);
@@ -656,11 +823,13 @@ extern "C" int ref_render(void* s, const RefRenderParams* pp, void* external_cac
                         for (size_t q = 0; q < np; ++q) {
                             PathState& ps = st[j * np + q];
                             if (!ps.alive) continue;
+                            if (dq) dq->key_base = (static_cast<uint32_t>(j) * wh + pixels[q]) << 6;
                             path_vertex(scene, p, binding,
                                         PathRng(p.rng_seed, pixels[q], p.first_sample + start + j),
-                                        b, ps, total);
+                                        b, ps, total, dq.get());
                         }
                     }
+                    if (dq) total.stores_won += dq->apply();
                 }
                 for (size_t q = 0; q < np; ++q) {
                     for (int j = 0; j < kk; ++j) {

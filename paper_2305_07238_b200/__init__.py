@@ -41,6 +41,8 @@ INSERT_OUTCOMES = ("Won", "LostRace", "AlreadyPresent", "CellFull")  # cache.hpp
 DESC_DTYPE = np.dtype([("mat_idx", "<u4"), ("node_idx", "<u4"), ("mip_level", "u1"),
                        ("pad_", "u1", 3), ("texel_x", "<u4"), ("texel_y", "<u4")])
 assert DESC_DTYPE.itemsize == 20
+INSERT_RECORD_DTYPE = np.dtype([("desc", DESC_DTYPE), ("entry", "<u4"), ("payload", "<u4")])  # mcg_insert_record
+assert INSERT_RECORD_DTYPE.itemsize == 28
 
 
 def _ptr(a: np.ndarray):
@@ -367,6 +369,26 @@ class MaterialCache:
 
     def slot_word(self, slot: int) -> int:
         return int(self.slot_words(slot, 1)[0])
+
+    def write_slots(self, words: np.ndarray, first: int = 0) -> None:
+        """Host words -> slots [first, first + len(words)) (seeding a table)."""
+        words = np.ascontiguousarray(words, np.uint64)
+        check(N.lib().mcg_cache_write_slots(self.handle, int(first), words.shape[0], _ptr(words)))
+
+    # ---- won-insert log (include/mcg.h mcg_cache_insert_log_*) ----
+    def insert_log_start(self, capacity: int) -> None:
+        check(N.lib().mcg_cache_insert_log_start(self.handle, int(capacity)))
+
+    def insert_log_stop(self) -> int:
+        out = C.c_uint64()
+        check(N.lib().mcg_cache_insert_log_stop(self.handle, C.byref(out)))
+        return int(out.value)
+
+    def insert_log_read(self, n: int, first: int = 0) -> np.ndarray:
+        """Records (desc fields, entry, payload) as a structured array."""
+        out = np.zeros(max(0, n), INSERT_RECORD_DTYPE)
+        check(N.lib().mcg_cache_insert_log_read(self.handle, int(first), out.shape[0], _ptr(out)))
+        return out
 
     def occupied_slots(self) -> int:
         out = C.c_uint64()

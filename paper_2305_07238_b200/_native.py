@@ -117,6 +117,7 @@ _SIGS = [
     ("mcg_cache_update_device", C.c_int, [vp, vp, vp, C.c_size_t, i32, vp]),
     ("mcg_cache_lookup_device", C.c_int, [vp, vp, C.c_size_t, vp, vp]),
     ("mcg_cache_read_slots", C.c_int, [vp, u64, C.c_size_t, vp]),
+    ("mcg_cache_write_slots", C.c_int, [vp, u64, C.c_size_t, vp]),
     ("mcg_cache_occupied", C.c_int, [vp, P(u64)]),
     ("mcg_cache_counters_get", C.c_int, [vp, P(CacheCounters)]),
     ("mcg_cache_counters_reset", C.c_int, [vp]),
@@ -132,6 +133,9 @@ _SIGS = [
     ("mcg_cache_trace_start", C.c_int, [vp, u64]),
     ("mcg_cache_trace_stop", C.c_int, [vp, P(u64)]),
     ("mcg_cache_trace_read", C.c_int, [vp, u64, C.c_size_t, vp]),
+    ("mcg_cache_insert_log_start", C.c_int, [vp, u64]),
+    ("mcg_cache_insert_log_stop", C.c_int, [vp, C.POINTER(u64)]),
+    ("mcg_cache_insert_log_read", C.c_int, [vp, u64, C.c_size_t, vp]),
     ("mcg_probe_replay", C.c_int, [vp, vp, u64, i32, P(f64), P(f64), P(CacheCounters)]),
     ("mcg_scene_load", C.c_int, [C.c_char_p, i32, P(vp)]),
     ("mcg_scene_destroy", C.c_int, [vp]),
@@ -154,7 +158,7 @@ EXPORTED = [s[0] for s in _SIGS]
 _lib = None
 
 
-ABI_VERSION = 2   # include/mcg.h MCG_ABI_VERSION (the struct layouts below)
+ABI_VERSION = 3   # include/mcg.h MCG_ABI_VERSION (the struct layouts below)
 
 
 def lib():

@@ -103,10 +103,15 @@ struct mcg_cache {
     uint32_t* trace = nullptr;
     unsigned long long* trace_count = nullptr;
     uint64_t trace_cap = 0;
+    // won-insert log (mcg_cache_insert_log_*): 7 words per record
+    uint32_t* ilog = nullptr;
+    unsigned long long* ilog_count = nullptr;
+    uint64_t ilog_cap = 0, ilog_alloc = 0;
     uint64_t local_words() const { return local_cells * n_entries; }   // slots held here (head + tail)
     uint64_t* tail() const { return n_entries > head_n ? slots + local_cells * head_n : nullptr; }
     mcgd::CacheView view() const {
-        return {slots, tail(), n_cells, magic, n_entries, head_n, world, stripes, trace, trace_count, trace_cap};
+        return {slots, tail(), n_cells, magic, n_entries, head_n, world, stripes, trace, trace_count, trace_cap,
+                ilog_cap ? ilog : nullptr, ilog_count, ilog_cap};
     }
 };
 

@@ -28,7 +28,28 @@ struct CacheView {
     uint32_t* trace;          // optional descriptor log: 5 words per lookup (mcg_descriptor)
     unsigned long long* trace_count;
     uint64_t trace_cap;
+    uint32_t* ilog;           // optional log of won inserts: 7 words each (mcg_insert_record)
+    unsigned long long* ilog_count;
+    uint64_t ilog_cap;
 };
+
+// Appends a won insert (descriptor, entry within the cell, payload) to the
+// table's insert log, when one is recording (mcg_cache_insert_log_*): the
+// host drop-in replays these through the caller's MaterialCache::update so
+// the host table, its counters and its dump follow the device's.
+__device__ __forceinline__ void log_insert(const CacheView& c, uint32_t mat, uint32_t node, uint32_t mip,
+                                           uint32_t tx, uint32_t ty, uint32_t entry, uint32_t payload) {
+    const unsigned long long at = atomicAdd(c.ilog_count, 1ull);
+    if (at >= c.ilog_cap) return;
+    uint32_t* r = c.ilog + 7 * at;
+    r[0] = mat;
+    r[1] = node;
+    r[2] = mip;
+    r[3] = tx;
+    r[4] = ty;
+    r[5] = entry;
+    r[6] = payload;
+}
 
 // Where a cell's slots live. DRAM serves random reads in 64-byte blocks, and
 // an 80-byte cell always straddles two of them (ncu: 142 B of DRAM per
@@ -469,15 +490,43 @@ __device__ __forceinline__ Probe probe_lanes_smem(const CacheView& c, uint64_t c
     return valid ? probe_cell(c, cell, check) : Probe{0u, -1, false};
 }
 
-// One CAS from zero on the slot the scan found empty (cache.cpp:108-114).
-// Returns MCG_INSERT_WON / LOST_RACE / CELL_FULL.
+// CAS from zero; across devices (a striped table, peer memory over NVLink)
+// only system-scope atomics are atomic with respect to the other GPUs.
+__device__ __forceinline__ unsigned long long cas_slot(const CacheView& c, uint64_t* word,
+                                                       unsigned long long packed) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(word);
+    return c.world > 1u ? atomicCAS_system(p, 0ull, packed) : atomicCAS(p, 0ull, packed);
+}
+
+// update()'s insert (cache.cpp:94-119) from the scan's result: `where` is the
+// first empty slot the probe saw (slots before it were occupied by other
+// keys). The probe may have run long before the store (the VM probes at
+// CacheLookup and stores at CacheStore, after the subtree), so a failed CAS
+// continues the scan as update() would if it ran now: the winner's word
+// holds our check hash -> AlreadyPresent; else the next slots are scanned
+// (a match -> AlreadyPresent, the first empty one gets update()'s single
+// CAS, whose failure is LostRace), and a full cell is CellFull. Slots before `where`
+// never change (write-once), so this equals a full rescan at store time.
+// Returns MCG_INSERT_*; *slot_out = the slot the outcome refers to (or -1).
 __device__ __forceinline__ int insert_at(const CacheView& c, uint64_t cell, int32_t where,
-                                         uint32_t check, uint32_t payload) {
+                                         uint32_t check, uint32_t payload, int32_t* slot_out = nullptr) {
+    if (slot_out) *slot_out = where;
     if (where < 0) return MCG_INSERT_CELL_FULL;
     const unsigned long long packed = (static_cast<unsigned long long>(check) << 32) | payload;
-    const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long*>(slot_ptr(c, cell, static_cast<uint32_t>(where))), 0ull, packed);
-    return prev == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
+    unsigned long long prev = cas_slot(c, slot_ptr(c, cell, static_cast<uint32_t>(where)), packed);
+    if (prev == 0ull) return MCG_INSERT_WON;
+    if (static_cast<uint32_t>(prev >> 32) == check) return MCG_INSERT_ALREADY_PRESENT;
+    for (uint32_t e = static_cast<uint32_t>(where) + 1u; e < c.n_entries; ++e) {
+        if (slot_out) *slot_out = static_cast<int32_t>(e);
+        uint64_t* w = slot_ptr(c, cell, e);
+        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(w);
+        if (static_cast<uint32_t>(cur >> 32) == check) return MCG_INSERT_ALREADY_PRESENT;
+        if (cur == 0ull) {
+            return cas_slot(c, w, packed) == 0ull ? MCG_INSERT_WON : MCG_INSERT_LOST_RACE;
+        }
+    }
+    if (slot_out) *slot_out = -1;
+    return MCG_INSERT_CELL_FULL;
 }
 
 // ---------------------------------------------------------------------------
@@ -857,7 +906,19 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                         const int leader = __ffs(peers) - 1;
                         int res = MCG_INSERT_ALREADY_PRESENT;
                         if (static_cast<int>(lane) == leader) {
-                            res = insert_at(C, p_cell, p_where, p_check, payload);
+                            int32_t at = -1;
+                            res = insert_at(C, p_cell, p_where, p_check, payload, &at);
+                            if (C.ilog && res == MCG_INSERT_WON) {
+                                // the descriptor again (CacheStore carries the
+                                // cache point's node and uv flag, stackvm.cpp:350-357)
+                                uint32_t mip = 0, tx = 0, ty = 0;
+                                if (flags & MCG_F_USES_UV) {
+                                    mip = mip_level(sp.g1x, sp.g1y, sp.g2x, sp.g2y, mip_offset);
+                                    tx = texel_index(sp.u, mip);
+                                    ty = texel_index(sp.v, mip);
+                                }
+                                log_insert(C, prog.material_id, arg, mip, tx, ty, static_cast<uint32_t>(at), payload);
+                            }
                         } else if (p_where < 0) {
                             res = MCG_INSERT_CELL_FULL;
                         }

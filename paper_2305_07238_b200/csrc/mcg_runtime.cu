@@ -168,7 +168,8 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
     const bool valid = i < n;
     uint64_t h = 0;
     uint32_t chk = 0;
-    if (valid) mcgd::hash_desc(load_desc(d, i), h, chk);
+    const Desc dd = valid ? load_desc(d, i) : Desc{0u, 0u, 0u, 0u, 0u};
+    if (valid) mcgd::hash_desc(dd, h, chk);
     const uint64_t cell = valid ? mcgd::fast_mod(h, c.n_cells, c.magic) : 0;
     const uint64_t base = cell * c.n_entries;   // logical slot index of the cell
     __shared__ ulonglong2 s_tile[8 * 4 * 32];   // blockDim 256: 4 rounds x 32 lanes per warp
@@ -183,10 +184,15 @@ __global__ void k_update(CacheView c, const mcg_descriptor* d, const float* rgb,
             packed = (static_cast<uint64_t>(chk) << 32) | p.payload;
         } else {
             const uint32_t payload = mcgd::encode_rgbe(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
-            res = mcgd::insert_at(c, cell, p.where, chk, payload);
+            int32_t at = -1;
+            res = mcgd::insert_at(c, cell, p.where, chk, payload, &at);
             if (res != MCG_INSERT_CELL_FULL) {
-                slot = base + p.where;
+                slot = base + static_cast<uint32_t>(at);
                 packed = (static_cast<uint64_t>(chk) << 32) | payload;
+                if (res == MCG_INSERT_ALREADY_PRESENT) packed = *mcgd::slot_ptr(c, cell, static_cast<uint32_t>(at));
+            }
+            if (c.ilog && res == MCG_INSERT_WON) {
+                mcgd::log_insert(c, dd.mat, dd.node, dd.mip, dd.tx, dd.ty, static_cast<uint32_t>(at), payload);
             }
         }
         won = res == MCG_INSERT_WON;
@@ -959,12 +965,35 @@ static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* o
     std::memcpy(out, tmp.data() + (first - c0 * ne), n * 8);
 }
 
+// The inverse: host words -> logical slots [first, first + n). Partial cells
+// at either end are read first so their other words are kept.
+static void write_logical(mcg_cache* cache, uint64_t first, size_t n, const uint64_t* in) {
+    mcg_ctx* ctx = cache->ctx;
+    const uint32_t ne = cache->n_entries, hn = cache->head_n, tn = ne - hn;
+    if (tn == 0) {
+        cuda_check(cudaMemcpyAsync(cache->slots + first, in, n * 8ull, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+        sync(ctx);
+        return;
+    }
+    const uint64_t c0 = first / ne, c1 = (first + n + ne - 1) / ne;
+    std::vector<uint64_t> tmp((c1 - c0) * ne);
+    if (first % ne != 0 || (first + n) % ne != 0) read_logical(cache, c0 * ne, tmp.size(), tmp.data());
+    std::memcpy(tmp.data() + (first - c0 * ne), in, n * 8);
+    cuda_check(cudaMemcpy2DAsync(cache->slots + c0 * hn, hn * 8ull, tmp.data(), ne * 8ull, hn * 8ull, c1 - c0,
+                                 cudaMemcpyHostToDevice, ctx->stream), "H2D heads");
+    cuda_check(cudaMemcpy2DAsync(cache->tail() + c0 * tn, tn * 8ull, tmp.data() + hn, ne * 8ull, tn * 8ull,
+                                 c1 - c0, cudaMemcpyHostToDevice, ctx->stream), "H2D tails");
+    sync(ctx);
+}
+
 mcg_status mcg_cache_destroy(mcg_cache* cache) {
     if (!cache) return MCG_OK;
     cudaStreamSynchronize(cache->ctx->stream);
     for (void* p : cache->ipc_opened) cudaIpcCloseMemHandle(p);
     if (cache->trace) cudaFree(cache->trace);
     if (cache->trace_count) cudaFree(cache->trace_count);
+    if (cache->ilog) cudaFree(cache->ilog);
+    if (cache->ilog_count) cudaFree(cache->ilog_count);
     if (cache->stripes) cudaFree(cache->stripes);
     cudaFree(cache->slots);
     cudaFree(cache->counters);
@@ -1204,6 +1233,15 @@ mcg_status mcg_cache_read_slots(mcg_cache* cache, uint64_t first, size_t n, uint
     });
 }
 
+mcg_status mcg_cache_write_slots(mcg_cache* cache, uint64_t first, size_t n, const uint64_t* words) {
+    return guarded([&] {
+        need(cache && (words || !n), "null argument");
+        need(first + n <= cache->local_words(), "slot range out of bounds (this stripe's words)");
+        if (!n) return;
+        write_logical(cache, first, n, words);
+    });
+}
+
 mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
     return guarded([&] {
         need(cache && occupied, "null argument");
@@ -1301,6 +1339,66 @@ mcg_status mcg_cache_trace_read(mcg_cache* cache, uint64_t first, size_t n, mcg_
         if (!n) return;
         dev_download(cache->ctx, reinterpret_cast<uint32_t*>(out), cache->trace + 5 * first, 5 * n);
         sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_cache_insert_log_start(mcg_cache* cache, uint64_t capacity) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        need(capacity > 0 && capacity < (1ull << 34), "insert log capacity out of range");
+        need(cache->world == 1, "insert log of a striped table");
+        if (capacity > cache->ilog_alloc) {
+            if (cache->ilog) cudaFree(cache->ilog);
+            cache->ilog = nullptr;
+            cache->ilog_alloc = 0;
+            cuda_check(cudaMalloc(&cache->ilog, capacity * 28), "cudaMalloc(insert log)");
+            cache->ilog_alloc = capacity;
+        }
+        if (!cache->ilog_count) cuda_check(cudaMalloc(&cache->ilog_count, 8), "cudaMalloc(insert log count)");
+        cuda_check(cudaMemsetAsync(cache->ilog_count, 0, 8, cache->ctx->stream), "memset");
+        cache->ilog_cap = capacity;
+        sync(cache->ctx);
+    });
+}
+
+mcg_status mcg_cache_insert_log_stop(mcg_cache* cache, uint64_t* won) {
+    return guarded([&] {
+        need(cache != nullptr, "null cache");
+        unsigned long long v = 0;
+        if (cache->ilog_count) {
+            dev_download(cache->ctx, &v, cache->ilog_count, 1);
+            sync(cache->ctx);
+        }
+        if (won) *won = v;   // may exceed the capacity: then only `capacity` records were kept
+        cache->ilog_cap = 0;
+    });
+}
+
+mcg_status mcg_cache_insert_log_read(mcg_cache* cache, uint64_t first, size_t n, mcg_insert_record* out) {
+    return guarded([&] {
+        need(cache && (out || !n), "null argument");
+        need(cache->ilog != nullptr, "no insert log recorded");
+        unsigned long long v = 0;
+        dev_download(cache->ctx, &v, cache->ilog_count, 1);
+        sync(cache->ctx);
+        need(first + n <= std::min<uint64_t>(v, cache->ilog_alloc), "insert log range out of bounds");
+        if (!n) return;
+        static_assert(sizeof(mcg_insert_record) == 28, "mcg_insert_record layout");
+        std::vector<uint32_t> raw(7 * n);
+        dev_download(cache->ctx, raw.data(), cache->ilog + 7 * first, 7 * n);
+        sync(cache->ctx);
+        for (size_t i = 0; i < n; ++i) {
+            const uint32_t* r = raw.data() + 7 * i;
+            mcg_insert_record& o = out[i];
+            std::memset(&o, 0, sizeof(o));
+            o.desc.mat_idx = r[0];
+            o.desc.node_idx = r[1];
+            o.desc.mip_level = static_cast<uint8_t>(r[2]);
+            o.desc.texel_x = r[3];
+            o.desc.texel_y = r[4];
+            o.entry = r[5];
+            o.payload = r[6];
+        }
     });
 }
 

@@ -12,6 +12,7 @@
 //        RGBA textures) -> mcg_scene_build (BVH rebuilt with the reference's
 //        median split, scene.cpp:154-194) -> mcg_upload_scene -> mcg_render.
 // Status codes are rethrown as the reference's exception types.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include <vector>
 
 #include "matcache/tracer.hpp"
+#include "matcache_render_b200.hpp"
 #include "mcg.h"
 
 namespace matcache {
@@ -50,11 +52,17 @@ void ok(mcg_status s) {
 struct Device {
     std::mutex mu;
     mcg_ctx* ctx = nullptr;
-    const Scene* uploaded = nullptr;
+    // The uploaded scene, identified by content (a fingerprint of everything
+    // the device receives), never by the Scene's address: a different or
+    // edited Scene at the same address must not render with stale data.
+    uint64_t uploaded_fp = 0;
     mcg_scene* scene = nullptr;
-    // Device tables standing in for external MaterialCache objects: the
-    // reference table exposes no bulk writer (cache.hpp:69-115), so the
-    // GPU table lives here, seeded from the host table's slot words.
+    // Device tables standing in for external MaterialCache objects, reused
+    // across calls (an 800 MB allocation is not free). The host table stays
+    // the truth: every call seeds the device table from its slot words and
+    // replays the render's won inserts back through update() (table_for /
+    // sync_back), so a table reused at a recycled address, or changed by the
+    // caller between renders, is never stale.
     std::map<const MaterialCache*, mcg_cache*> tables;
 };
 
@@ -144,11 +152,71 @@ void flatten(Flattened& F, const CompiledProgram& prog) {
     F.programs.push_back(p);
 }
 
-mcg_scene* build_scene(const Scene& scene) {
+// Everything mcg_scene_build receives, owned (the mcg_scene_in points into it).
+struct SceneInput {
     Flattened F;
-    for (const MaterialRuntime& m : scene.materials) flatten(F, m.program);
     std::vector<mcg_mesh_in> meshes;
-    std::vector<std::vector<float>> pos(scene.meshes.size()), uvs(scene.meshes.size());
+    std::vector<std::vector<float>> pos, uvs;
+    std::vector<mcg_sphere_in> spheres;
+    std::vector<mcg_point_light> pl;
+    std::vector<mcg_rect_light> rl;
+    mcg_scene_in in{};
+};
+
+// FNV-1a over bytes, folded through a splitmix64 finalizer per array.
+struct Fingerprint {
+    uint64_t h = 0xcbf29ce484222325ull;
+    void bytes(const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        uint64_t x = 0xcbf29ce484222325ull;
+        for (size_t i = 0; i < n; ++i) x = (x ^ b[i]) * 0x100000001b3ull;
+        x ^= n;
+        x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+        x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+        h = (h ^ x ^ (x >> 31)) * 0x100000001b3ull;
+    }
+    template <typename T>
+    void vec(const std::vector<T>& v) { bytes(v.data(), v.size() * sizeof(T)); }
+};
+
+uint64_t fingerprint(const SceneInput& S) {
+    Fingerprint f;
+    const mcg_scene_in& in = S.in;
+    f.bytes(in.cam_position, sizeof(in.cam_position));
+    f.bytes(in.cam_look_at, sizeof(in.cam_look_at));
+    f.bytes(in.cam_up, sizeof(in.cam_up));
+    f.bytes(&in.cam_vfov_deg, sizeof(in.cam_vfov_deg));
+    f.bytes(&in.cam_width, sizeof(in.cam_width));
+    f.bytes(&in.cam_height, sizeof(in.cam_height));
+    f.bytes(in.env, sizeof(in.env));
+    for (size_t i = 0; i < S.meshes.size(); ++i) {
+        f.vec(S.pos[i]);
+        f.vec(S.uvs[i]);
+        f.bytes(S.meshes[i].indices, S.meshes[i].n_indices * sizeof(uint32_t));
+        f.bytes(&S.meshes[i].material_id, sizeof(uint32_t));
+    }
+    f.vec(S.spheres);
+    f.vec(S.pl);
+    f.vec(S.rl);
+    f.vec(S.F.programs);
+    f.vec(S.F.code);
+    f.vec(S.F.consts);
+    f.vec(S.F.noise);
+    f.vec(S.F.ramps);
+    f.vec(S.F.stops);
+    f.vec(S.F.textures);
+    f.vec(S.F.texels);
+    return f.h;
+}
+
+void scene_input(const Scene& scene, SceneInput& S) {
+    Flattened& F = S.F;
+    for (const MaterialRuntime& m : scene.materials) flatten(F, m.program);
+    std::vector<mcg_mesh_in>& meshes = S.meshes;
+    std::vector<std::vector<float>>& pos = S.pos;
+    std::vector<std::vector<float>>& uvs = S.uvs;
+    pos.assign(scene.meshes.size(), {});
+    uvs.assign(scene.meshes.size(), {});
     for (size_t i = 0; i < scene.meshes.size(); ++i) {
         const MeshObject& m = scene.meshes[i];
         for (const Vec3& p : m.positions) pos[i].insert(pos[i].end(), {p.x, p.y, p.z});
@@ -158,21 +226,21 @@ mcg_scene* build_scene(const Scene& scene) {
                           static_cast<uint32_t>(m.indices.size()), m.material_id, pos[i].data(),
                           uvs[i].data(), m.indices.data()});
     }
-    std::vector<mcg_sphere_in> spheres;
+    std::vector<mcg_sphere_in>& spheres = S.spheres;
     for (const SphereObject& s : scene.spheres) {
         spheres.push_back({{s.center.x, s.center.y, s.center.z}, s.radius, s.material_id});
     }
-    std::vector<mcg_point_light> pl;
+    std::vector<mcg_point_light>& pl = S.pl;
     for (const PointLight& l : scene.point_lights) {
         pl.push_back({{l.position.x, l.position.y, l.position.z},
                       {l.intensity.r, l.intensity.g, l.intensity.b}});
     }
-    std::vector<mcg_rect_light> rl;
+    std::vector<mcg_rect_light>& rl = S.rl;
     for (const RectLight& l : scene.rect_lights) {
         rl.push_back({{l.corner.x, l.corner.y, l.corner.z}, {l.edge_u.x, l.edge_u.y, l.edge_u.z},
                       {l.edge_v.x, l.edge_v.y, l.edge_v.z}, {l.radiance.r, l.radiance.g, l.radiance.b}});
     }
-    mcg_scene_in in{};
+    mcg_scene_in& in = S.in;
     const Camera& c = scene.camera;
     const float cam[9] = {c.position.x, c.position.y, c.position.z, c.look_at.x, c.look_at.y,
                           c.look_at.z, c.up.x, c.up.y, c.up.z};
@@ -209,29 +277,92 @@ mcg_scene* build_scene(const Scene& scene) {
     in.textures = F.textures.data();
     in.n_texels = F.texels.size() / 4;
     in.texels = F.texels.data();
-    mcg_scene* out = nullptr;
-    ok(mcg_scene_build(&in, &out));
-    return out;
 }
 
-// The device table standing in for `ext`: created on first use (the host
-// table must then be empty -- the C ABI has no raw slot writer, and update()
-// cannot replay entries without their descriptors) and kept across calls, so
-// progressive renders into one external cache continue on the device.
-mcg_cache* table_for(Device& D, MaterialCache* ext) {
-    auto it = D.tables.find(ext);
-    if (it != D.tables.end()) return it->second;
-    if (ext->occupied_slots() != 0) {
-        throw std::invalid_argument(
-            "render(): a non-empty external MaterialCache cannot seed the device table");
+// The device table standing in for `ext` for one call: (re)created when the
+// shape differs, then seeded with the host table's slot words
+// (cache.hpp:83-86) so it holds exactly what `ext` holds; the won-insert log
+// records what this render adds. Returns the log capacity (the empty slots:
+// a table can win no more inserts than that).
+uint64_t table_for(Device& D, MaterialCache* ext, mcg_cache** out) {
+    mcg_cache*& t = D.tables[ext];
+    if (t) {
+        uint64_t nc = 0;
+        uint32_t ne = 0;
+        ok(mcg_cache_shape(t, &nc, &ne));
+        if (nc != ext->n_cells() || ne != ext->n_entries()) {
+            mcg_cache_destroy(t);
+            t = nullptr;
+        }
     }
-    mcg_cache* t = nullptr;
-    ok(mcg_cache_create(D.ctx, ext->n_cells(), ext->n_entries(), &t));
-    D.tables.emplace(ext, t);
-    return t;
+    if (!t) ok(mcg_cache_create(D.ctx, ext->n_cells(), ext->n_entries(), &t));
+    const uint64_t total = ext->slot_count();
+    const uint64_t chunk = 1ull << 22;
+    std::vector<uint64_t> words(static_cast<size_t>(std::min(total, chunk)));
+    uint64_t occupied = 0;
+    for (uint64_t first = 0; first < total; first += chunk) {
+        const uint64_t n = std::min(chunk, total - first);
+        for (uint64_t i = 0; i < n; ++i) {
+            words[i] = ext->slot_word(first + i);
+            occupied += words[i] != 0;
+        }
+        ok(mcg_cache_write_slots(t, first, static_cast<size_t>(n), words.data()));
+    }
+    ok(mcg_cache_counters_reset(t));
+    const uint64_t cap = std::max<uint64_t>(1, total - occupied);
+    ok(mcg_cache_insert_log_start(t, cap));
+    *out = t;
+    return cap;
+}
+
+// After the render: the device's won inserts, replayed through the caller's
+// MaterialCache::update (cache.cpp:94-119) in (cell, entry) order -- each
+// lands in its cell's first empty slot, i.e. exactly the device's slot, so
+// the host table, its inserts_won counter, occupied_slots() and dump()
+// match what a reference render into `ext` would leave behind in shape (the
+// lookups/hits counters have no public writer and stay the caller's).
+void sync_back(mcg_cache* t, MaterialCache* ext, uint64_t cap) {
+    uint64_t won = 0;
+    ok(mcg_cache_insert_log_stop(t, &won));
+    if (won > cap) throw std::runtime_error("render(): device insert log overflow");
+    std::vector<mcg_insert_record> rec(static_cast<size_t>(won));
+    ok(mcg_cache_insert_log_read(t, 0, rec.size(), rec.data()));
+    std::vector<std::pair<uint64_t, size_t>> order(rec.size());
+    const uint64_t nc = ext->n_cells();
+    const uint32_t ne = ext->n_entries();
+    for (size_t i = 0; i < rec.size(); ++i) {
+        order[i] = {(mcg_hash_cell(&rec[i].desc) % nc) * ne + rec[i].entry, i};
+    }
+    std::sort(order.begin(), order.end());
+    for (const auto& [slot, i] : order) {
+        const mcg_insert_record& r = rec[i];
+        CacheDescriptor d;
+        d.mat_idx = r.desc.mat_idx;
+        d.node_idx = r.desc.node_idx;
+        d.mip_level = r.desc.mip_level;
+        d.texel_x = r.desc.texel_x;
+        d.texel_y = r.desc.texel_y;
+        const UpdateResult u = ext->update(d, decode_value(r.payload));
+        if (u.outcome != InsertOutcome::Won || u.slot != slot || entry_payload(u.packed) != r.payload) {
+            throw std::runtime_error("render(): host replay of the device's inserts diverged "
+                                     "(external cache changed during the render?)");
+        }
+    }
 }
 
 }  // namespace
+
+// Frees the device table standing in for `cache` (tables otherwise live, and
+// are reused, for the process's lifetime). Declared in
+// integration/matcache_render_b200.hpp.
+void b200_release_cache(const MaterialCache* cache) {
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    const auto it = D.tables.find(cache);
+    if (it == D.tables.end()) return;
+    mcg_cache_destroy(it->second);
+    D.tables.erase(it);
+}
 
 RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCache* external_cache) {
     Device& D = device();
@@ -241,11 +372,18 @@ RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCach
         mcg_options opt{0, 0, nullptr};
         ok(mcg_create(&opt, &D.ctx));
     }
-    if (D.uploaded != &scene) {
-        if (D.scene) mcg_scene_destroy(D.scene);
-        D.scene = build_scene(scene);
-        ok(mcg_upload_scene(D.ctx, D.scene));
-        D.uploaded = &scene;
+    {
+        SceneInput S;
+        scene_input(scene, S);
+        const uint64_t fp = fingerprint(S);
+        if (!D.scene || fp != D.uploaded_fp) {
+            if (D.scene) mcg_scene_destroy(D.scene);
+            D.scene = nullptr;
+            D.uploaded_fp = 0;
+            ok(mcg_scene_build(&S.in, &D.scene));
+            ok(mcg_upload_scene(D.ctx, D.scene));
+            D.uploaded_fp = fp;
+        }
     }
     const int w = config.width ? config.width : scene.camera.width;
     const int h = config.height ? config.height : scene.camera.height;
@@ -265,13 +403,15 @@ RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCach
     p.tile_size = config.tile_size;
     p.shard_count = 1;
     mcg_cache* table = nullptr;
-    if (config.cache_enabled && external_cache) table = table_for(D, external_cache);
+    uint64_t log_cap = 0;
+    if (config.cache_enabled && external_cache) log_cap = table_for(D, external_cache, &table);
     mcg_frame frame{result.frame.radiance.data(), result.frame.nodes_found.data(),
                     result.frame.samples.data()};
     std::vector<uint64_t> hps(static_cast<size_t>(std::max(config.spp, 0)), 0);
     mcg_render_stats st{};
     st.hits_per_sample = hps.data();
     ok(mcg_render(D.ctx, &p, table, &frame, &st));
+    if (table) sync_back(table, external_cache, log_cap);
     RenderStats& rs = result.stats;
     rs.lookups = st.lookups;
     rs.hits = st.hits;

@@ -237,11 +237,17 @@ class Mesh:
     indices: list = field(default_factory=list)
     material: int = 0
 
-    def quad_grid(self, origin, eu, ev, nu, nv, uv_scale, uv_offset=(0.0, 0.0)):
-        """Subdivided planar quad, uv = planar coordinates x uv_scale."""
+    def quad_grid(self, origin, eu, ev, nu, nv, uv_scale, uv_offset=(0.0, 0.0), uv_span=0.0):
+        """Subdivided planar quad, uv = planar coordinates x uv_scale; with
+        uv_span > 0 the quad's uv runs over [0, uv_span] on both axes
+        whatever its size (one texture tile per surface, like an unwrapped
+        asset: texel_indices' wrap (raycone.cpp:75-83) then never folds two
+        surface points onto one virtual texel)."""
         o, eu, ev = np.asarray(origin, np.float64), np.asarray(eu, np.float64), np.asarray(ev, np.float64)
         base = len(self.positions) // 3
         lu, lv = np.linalg.norm(eu), np.linalg.norm(ev)
+        if uv_span > 0.0:
+            uv_scale, lu, lv = uv_span, 1.0, 1.0
         for j in range(nv + 1):
             for i in range(nu + 1):
                 p = o + eu * (i / nu) + ev * (j / nv)
@@ -254,16 +260,16 @@ class Mesh:
                 b, c, d = a + 1, a + nu + 1, a + nu + 2
                 self.indices += [a, b, d, a, d, c]
 
-    def box(self, lo, hi, n, uv_scale):
+    def box(self, lo, hi, n, uv_scale, uv_span=0.0):
         lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
         dx, dy, dz = hi - lo
         X, Y, Z = np.array([dx, 0, 0]), np.array([0, dy, 0]), np.array([0, 0, dz])
-        self.quad_grid(lo, X, Z, n, n, uv_scale)                 # bottom
-        self.quad_grid(lo + Y, Z, X, n, n, uv_scale)             # top
-        self.quad_grid(lo, Y, X, n, n, uv_scale)                 # front (z = lo)
-        self.quad_grid(lo + Z, X, Y, n, n, uv_scale)             # back
-        self.quad_grid(lo, Z, Y, n, n, uv_scale)                 # left
-        self.quad_grid(lo + X, Y, Z, n, n, uv_scale)             # right
+        self.quad_grid(lo, X, Z, n, n, uv_scale, uv_span=uv_span)                 # bottom
+        self.quad_grid(lo + Y, Z, X, n, n, uv_scale, uv_span=uv_span)             # top
+        self.quad_grid(lo, Y, X, n, n, uv_scale, uv_span=uv_span)                 # front (z = lo)
+        self.quad_grid(lo + Z, X, Y, n, n, uv_scale, uv_span=uv_span)             # back
+        self.quad_grid(lo, Z, Y, n, n, uv_scale, uv_span=uv_span)                 # left
+        self.quad_grid(lo + X, Y, Z, n, n, uv_scale, uv_span=uv_span)             # right
 
     def to_json(self):
         return {"positions": self.positions, "uvs": self.uvs, "indices": self.indices,
@@ -301,10 +307,11 @@ class SceneSpec:
     libm_ops: bool = True
     tris_per_side: int = 10
     spheres: int = 0           # analytic spheres (scene.cpp:80-97, 222-249) inside the room
+    uv_span: float = 0.0       # > 0: every quad's uv spans [0, uv_span] (no tiling; Mesh.quad_grid)
 
 
 def _room(materials: list[int], rng: random.Random, uv_scale: float, n: int,
-          objects: int = 6) -> list[Mesh]:
+          objects: int = 6, uv_span: float = 0.0) -> list[Mesh]:
     """A box room (open towards the camera) with a few boxes inside."""
     meshes = []
     def surface(mat, fn):
@@ -313,16 +320,16 @@ def _room(materials: list[int], rng: random.Random, uv_scale: float, n: int,
         meshes.append(m)
     W, H, D = 8.0, 5.0, 10.0
     mats = iter(materials * 8)
-    surface(next(mats), lambda m: m.quad_grid([-W, 0, -D], [0, 0, 2 * D], [2 * W, 0, 0], n, n, uv_scale))   # floor
-    surface(next(mats), lambda m: m.quad_grid([-W, H, -D], [2 * W, 0, 0], [0, 0, 2 * D], n, n, uv_scale))   # ceiling
-    surface(next(mats), lambda m: m.quad_grid([-W, 0, -D], [2 * W, 0, 0], [0, H, 0], n, n, uv_scale))       # back
-    surface(next(mats), lambda m: m.quad_grid([-W, 0, D], [0, 0, -2 * D], [0, H, 0], n, n, uv_scale))      # left
-    surface(next(mats), lambda m: m.quad_grid([W, 0, -D], [0, 0, 2 * D], [0, H, 0], n, n, uv_scale))       # right
+    surface(next(mats), lambda m: m.quad_grid([-W, 0, -D], [0, 0, 2 * D], [2 * W, 0, 0], n, n, uv_scale, uv_span=uv_span))   # floor
+    surface(next(mats), lambda m: m.quad_grid([-W, H, -D], [2 * W, 0, 0], [0, 0, 2 * D], n, n, uv_scale, uv_span=uv_span))   # ceiling
+    surface(next(mats), lambda m: m.quad_grid([-W, 0, -D], [2 * W, 0, 0], [0, H, 0], n, n, uv_scale, uv_span=uv_span))       # back
+    surface(next(mats), lambda m: m.quad_grid([-W, 0, D], [0, 0, -2 * D], [0, H, 0], n, n, uv_scale, uv_span=uv_span))      # left
+    surface(next(mats), lambda m: m.quad_grid([W, 0, -D], [0, 0, 2 * D], [0, H, 0], n, n, uv_scale, uv_span=uv_span))       # right
     for k in range(objects):
         cx, cz = rng.uniform(-W + 1.5, W - 1.5), rng.uniform(-D + 2, 2)
         sx, sy, sz = rng.uniform(0.5, 1.5), rng.uniform(0.5, 2.5), rng.uniform(0.5, 1.5)
         surface(next(mats), lambda m: m.box([cx - sx, 0.0, cz - sz], [cx + sx, sy, cz + sz],
-                                            max(2, n // 4), uv_scale))
+                                            max(2, n // 4), uv_scale, uv_span))
     return meshes
 
 
@@ -373,7 +380,7 @@ def build_scene(spec: SceneSpec, out_dir: str) -> str:
             json.dump(m, f)
         mat_files.append(name)
     ids = [m["material_id"] for m in mats]
-    meshes = _room(ids, rng, uv_scale, spec.tris_per_side)
+    meshes = _room(ids, rng, uv_scale, spec.tris_per_side, uv_span=spec.uv_span)
     scene = {
         "camera": {"position": [0.0, 2.4, 17.0], "look_at": [0.0, 1.6, 0.0], "up": [0.0, 1.0, 0.0],
                    "vfov_deg": 55.0, "width": spec.width, "height": spec.height},

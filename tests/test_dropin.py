@@ -67,3 +67,58 @@ def test_dropin_render_matches_python_api(ctx, dropin, scene_dir, cache_on):
         e_python = np.abs(res.frame.radiance - off).mean() / scale
         assert e_dropin < 0.25 and e_python < 0.25
         assert abs(e_dropin - e_python) < 0.1
+
+
+@pytest.mark.gpu
+def test_dropin_two_scenes_same_stack_frame(ctx, dropin, scene_dir):
+    """the drop-in keys its device upload on the scene's
+    content, not its address. Three different scenes loaded one after the
+    other into the same stack slot (oracle/dropin_harness.cpp
+    dropin_render_scenes), plus the first again: each frame equals the
+    Python API's render of that scene, bit for bit (cache off)."""
+    w, h, spp = 32, 24, 2
+    paths = [scenes.build_scene(scenes.SceneSpec(k, w, h, tris_per_side=4), f"{scene_dir}/two_{k}")
+             for k in ("junkshop", "cornell", "italianflat")]
+    paths.append(paths[0])
+    rad = np.zeros((len(paths), h, w, 3), np.float64)
+    err = C.create_string_buffer(512)
+    arr = (C.c_char_p * len(paths))(*[p.encode() for p in paths])
+    dropin.dropin_render_scenes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_char_p, C.c_size_t]
+    rc = dropin.dropin_render_scenes(C.cast(arr, C.c_void_p), len(paths), w, h, spp,
+                                     rad.ctypes.data_as(C.c_void_p), err, 512)
+    assert rc == 0, err.value.decode()
+    for i, p in enumerate(paths):
+        want = render(load_scene(p), RenderConfig(width=w, height=h, spp=spp), ctx=ctx).frame.radiance
+        np.testing.assert_array_equal(rad[i].view(np.uint64), want.view(np.uint64), err_msg=p)
+    assert not np.array_equal(rad[0], rad[1])
+
+
+@pytest.mark.gpu
+def test_dropin_external_cache_follows_the_device(ctx, dropin, scene_dir, tmp_path):
+    """an external MaterialCache passed to the drop-in's
+    render() is the truth. Each call seeds the device table from its slot
+    words and replays the won inserts back through update(), so after every
+    render the host table's occupied_slots() and inserts_won counter equal
+    the inserts the render reports (accumulating over progressive renders),
+    its dump passes the reference's audit, and a progressive second render
+    hits more. A fresh cache allocated where a deleted one lived, and a
+    cache of another shape, start empty (no stale device table)."""
+    w, h, spp, nc, ne, n = 40, 30, 2, 4099, 4, 2
+    path = scenes.build_scene(scenes.SceneSpec("junkshop", w, h, tris_per_side=4), f"{scene_dir}/ext")
+    out = np.zeros(6 * (n + 2) + 2, np.uint64)
+    err = C.create_string_buffer(512)
+    dropin.dropin_render_external.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint32,
+                                              C.c_int, C.c_char_p, C.c_void_p, C.c_char_p, C.c_size_t]
+    rc = dropin.dropin_render_external(path.encode(), w, h, spp, nc, ne, n, str(tmp_path / "d.bin").encode(),
+                                       out.ctypes.data_as(C.c_void_p), err, 512)
+    assert rc == 0, err.value.decode()
+    rows = out[:6 * (n + 2)].reshape(-1, 6).astype(np.int64)
+    won_total = 0
+    for i, (look, hits, won, occ, cwon, clean) in enumerate(rows):
+        won_total = won_total + won if i < n else won
+        assert look > 0 and clean == 1, (i, rows)
+        assert occ == won_total and cwon == won_total, (i, rows)
+    assert rows[1, 1] > rows[0, 1]          # the progressive render hits what the first stored
+    assert rows[n, 2] > 0 and rows[n, 3] == rows[n, 2]     # fresh cache (same shape): starts empty
+    assert rows[n + 1, 3] == rows[n + 1, 2] > 0            # another shape

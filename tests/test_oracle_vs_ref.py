@@ -251,6 +251,56 @@ def test_render_matches_reference_backed_render(oracle, ref, scene_dir, kind, li
     ref.L.ref_scene_free(rs)
 
 
+@pytest.mark.parametrize("kind,libm,k,nc,ne", [("cornell", False, 1, 1021, 4), ("junkshop", False, 2, 1021, 4),
+                                               ("italianflat", False, 3, 61, 3), ("monster", False, 2, 4099, 10),
+                                               ("classroom", True, 2, 1021, 4)])
+def test_deterministic_render_matches_reference_deferred_render(oracle, ref, scene_dir, kind, libm, k, nc, ne):
+    """Deterministic-insert mode pinned to reference-compiled code: the
+    reference-backed render in mode 3 (ref_harness.cpp class Deferred: the
+    reference's execute() against the epoch-start table, its inserts taken
+    back and re-applied at the epoch's end, sorted by (sample-in-pass,
+    pixel, store ordinal), through MaterialCache::update, cache.cpp:94-119)
+    vs mc_oracle.c mode 3 -- the rule the GPU's k_shade<true> +
+    k_apply_ordered follow. Per-pixel hit counts, hits per sample, counters
+    and every table word bit-exact; radiance bit-exact without libm ops and
+    within 1e-5 relative with them (sin/pow: glibc vs the correctly rounded
+    routine, <= 1 ulp). A 61 x 3 table exercises CellFull."""
+    w, h, spp = 40, 28, 6
+    path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=5, libm_ops=libm),
+                              f"{scene_dir}/det_{kind}_{int(libm)}")
+    s = load_scene(path)
+    rs = ref.scene_load(path)
+    P = RenderParamsC(w, h, spp, 4, 3, 0, nc, ne, 0, 1, 0.2, 16, 0, 1, 0, 0, k)
+    oc = oracle.cache_new(nc, ne)
+    rc = ref.cache_new(nc, ne)
+    A = oracle.render(s.flat, P, cache=oc)
+    B = ref.render(rs, P, w, h, cache=rc)
+    np.testing.assert_array_equal(A[2], B[2])
+    np.testing.assert_array_equal(A[1], B[1])     # per-pixel hit counts
+    np.testing.assert_array_equal(A[3], B[3])     # hits per sample
+    np.testing.assert_array_equal(oracle.cache_slots(oc, nc, ne), ref.cache_slots(rc, nc * ne))
+    if libm:
+        assert np.abs(A[0] - B[0]).max() <= 1e-5 * np.abs(B[0]).max()
+    else:
+        np.testing.assert_array_equal(bits(A[0]), bits(B[0]))
+    for f in ("lookups", "hits", "inserts_won", "inserts_lost_full", "stores_attempted", "stores_won",
+              "instructions_executed", "shading_points"):
+        assert getattr(A[4], f) == getattr(B[4], f), f
+    assert B[4].hits > 0 and B[4].inserts_won > 0
+    if nc == 61:
+        assert B[4].inserts_lost_full > 0
+    # and it is not the immediate-insert order (mode 1) under another name:
+    # there, later paths of an epoch already hit what earlier ones stored
+    P.mode = 1
+    rc1 = ref.cache_new(nc, ne)
+    B1 = ref.render(rs, P, w, h, cache=rc1)
+    assert B1[4].hits > B[4].hits
+    oracle.cache_free(oc)
+    ref.cache_free(rc)
+    ref.cache_free(rc1)
+    ref.L.ref_scene_free(rs)
+
+
 def test_render_with_spheres_matches_reference_backed_render(oracle, ref, scene_dir):
     """Cache off, a scene with analytic spheres: sphere uv differs from
     glibc's by <= 1 ulp of atan2f/acosf, so radiance is compared at the
