@@ -45,6 +45,14 @@ W, H, SPP = 1920, 1080, 128
 N_CELLS, N_ENTRIES = 10_000_000, 10
 SCENE_KIND = "classroom"
 TRIS_PER_SIDE = 24
+# The tuning SPEC acceptance #5 holds at for the reference
+# itself (profiles/README.md "SPEC #5"): one uv tile per surface (no
+# wrapped texels shared across a wall) and mip_offset 3 (texels 1/8 of the
+# pixel footprint, "offsetting the mipmap level ... a bit more accurate
+# result", PAPER.md). The tiled-uv, offset-0 layout of round 1 is faster
+# (hit rate 0.998) but fails SPEC #5 for the reference as well; bench.py
+# reports it beside (`tunings`).
+UV_SPAN, MIP_OFFSET = 0.999, 3
 PROBE_VARIANT, PROBE_BLOCKS_PER_SM = 10, 8         # HBM table: warp-cooperative one-round-trip loads, software-pipelined, scan through shared memory
 PROBE_L2_VARIANT, PROBE_L2_BLOCKS_PER_SM = 0, 8    # L2-resident table: per-lane scan (issue-bound)
 METRIC = "samples/sec at 1920x1080 128spp (classroom-like, cache 1e7x10)"
@@ -135,7 +143,7 @@ def frame_reduce(dist, tensors):
 def make_scene(tmp: str):
     from paper_2305_07238_b200 import scenes
     return scenes.build_scene(scenes.SceneSpec(SCENE_KIND, W, H, tris_per_side=TRIS_PER_SIDE,
-                                               libm_ops=True), os.path.join(tmp, "scene"))
+                                               libm_ops=True, uv_span=UV_SPAN), os.path.join(tmp, "scene"))
 
 
 # --------------------------------------------------------------------------
@@ -161,7 +169,7 @@ def cpu_reference_sample(scene_path: str, threads: int = 0, cache: bool = True):
     if _oracle.Ref.available():
         ref = _oracle.Ref()
         s = ref.scene_load(scene_path)
-        P = _oracle.RenderParamsC(W, H, SPP, 4, 2 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
+        P = _oracle.RenderParamsC(W, H, SPP, 4, 2 if cache else 0, MIP_OFFSET, N_CELLS, N_ENTRIES, 0, 1,
                                   0.2, 16, CPU_BAND, CPU_BANDS, 1, nthreads, 1)
         t0 = time.perf_counter()
         c = ref.cache_new(N_CELLS, N_ENTRIES) if cache else None
@@ -179,7 +187,7 @@ def cpu_reference_sample(scene_path: str, threads: int = 0, cache: bool = True):
     from paper_2305_07238_b200 import load_scene
     orc = _oracle.Oracle()
     sc = load_scene(scene_path)
-    P = _oracle.RenderParamsC(W, H, SPP, 4, 1 if cache else 0, 0, N_CELLS, N_ENTRIES, 0, 1,
+    P = _oracle.RenderParamsC(W, H, SPP, 4, 1 if cache else 0, MIP_OFFSET, N_CELLS, N_ENTRIES, 0, 1,
                               0.2, 16, 32, 64, 1, 1, 1)
     t0 = time.perf_counter()
     _, _, samples, _, _ = orc.render(sc.flat, P)
@@ -217,8 +225,8 @@ def run_reference_arm(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded classroom-like scene, reference JSON/PPM formats)",
-        "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp cache {N_CELLS:.0e}x{N_ENTRIES}",
-                   "sample": sample},
+        "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp cache {N_CELLS:.0e}x{N_ENTRIES}, "
+                               f"unit uv, mip_offset {MIP_OFFSET}", "sample": sample},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": info["cores"],
                          "kind": info["kind"], "sample": sample,
                          "table_build_s": info.get("table_build_s"),
@@ -320,7 +328,8 @@ def main() -> None:
     ctx.upload(scene)
 
     cfg = RenderConfig(width=W, height=H, spp=SPP, cache_enabled=True, n_cells=N_CELLS,
-                       n_entries=N_ENTRIES, shard_rank=rank, shard_count=world, shard_mode=0)
+                       n_entries=N_ENTRIES, mip_offset=MIP_OFFSET, shard_rank=rank, shard_count=world,
+                       shard_mode=0)
     params = cfg.to_params()
     dev = torch.device("cuda", local)
     rad = torch.zeros(H * W * 3, dtype=torch.float64, device=dev)
@@ -448,6 +457,25 @@ def main() -> None:
         frame_off = rad.cpu().numpy().reshape(H, W, 3).copy()
         extras["cache_speedup"] = {"t_nocache_ms": ms_off, "t_cache_ms": ms / args.steps,
                                    "speedup": ms_off / (ms / args.steps)}
+        if rank == 0 and world == 1:
+            # the same frame at other tunings (one render each after a warm-up,
+            # device time): mip_offset 0 on the bench scene, and round 1's
+            # tiled-uv scene at mip_offset 0 (hit rate ~0.998, but SPEC #5
+            # fails there for the reference too: profiles/README.md)
+            from paper_2305_07238_b200 import render as api_render, scenes as S
+            tun = {}
+            tiled = load_scene(S.build_scene(S.SceneSpec(SCENE_KIND, W, H, tris_per_side=TRIS_PER_SIDE,
+                                                         libm_ops=True), os.path.join(tmp, "tiled")))
+            for name, sc, mip in (("unit_uv_mip0", scene, 0), ("tiled_uv_mip0", tiled, 0)):
+                base = dict(width=W, height=H, spp=SPP, n_cells=N_CELLS, n_entries=N_ENTRIES, mip_offset=mip)
+                api_render(sc, RenderConfig(cache_enabled=True, **base), ctx=ctx)
+                on = api_render(sc, RenderConfig(cache_enabled=True, **base), ctx=ctx).stats
+                t_off = (api_render(sc, RenderConfig(**base), ctx=ctx).stats.device_ms if sc is not scene
+                         else ms_off)
+                tun[name] = {"ms_cache": on.device_ms, "ms_no_cache": t_off, "speedup": t_off / on.device_ms,
+                             "hit_rate": on.hit_rate, "samples_per_s": W * H * SPP / (on.device_ms / 1e3)}
+            ctx.upload(scene)
+            extras["tunings"] = tun
         if rank == 0:
             from paper_2305_07238_b200 import MaterialCache
             peak, _ = measured_peaks()
@@ -518,6 +546,8 @@ def main() -> None:
     saved = {k: os.environ.get(k) for k in serial_env}
     os.environ.update(serial_env)
     try:
+        step()   # warm-up: the one-lane layout's buffers are allocated on first use
+        torch.cuda.synchronize()
         ctx.reset_kernel_times()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -646,7 +676,7 @@ def main() -> None:
             try:
                 from paper_2305_07238_b200 import render as api_render
                 band_cfg = dict(width=W, height=H, spp=SPP, n_cells=N_CELLS, n_entries=N_ENTRIES,
-                                shard_rank=CPU_BAND, shard_count=CPU_BANDS, shard_mode=1)
+                                mip_offset=MIP_OFFSET, shard_rank=CPU_BAND, shard_count=CPU_BANDS, shard_mode=1)
                 gpu_band = (api_render(scene, RenderConfig(cache_enabled=True, **band_cfg), ctx=ctx).frame,
                             api_render(scene, RenderConfig(cache_enabled=False, **band_cfg), ctx=ctx).frame)
                 parity = parity_block(frame_cached, frame_off, st, ref_band, gpu_band)
@@ -680,7 +710,8 @@ def main() -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded classroom-like scene in the reference's JSON/PPM formats)",
             "config": {"workload": f"{SCENE_KIND}-like {W}x{H} {SPP}spp, cache {N_CELLS:.0e}x{N_ENTRIES}, "
-                                   "concurrent inserts", "width": W, "height": H, "spp": SPP,
+                                   f"unit uv, mip_offset {MIP_OFFSET}, concurrent inserts",
+                       "width": W, "height": H, "spp": SPP, "uv_span": UV_SPAN, "mip_offset": MIP_OFFSET,
                        "n_cells": N_CELLS, "n_entries": N_ENTRIES, "parallelism": f"tiles/{world}",
                        "cache": "striped over GPUs" if shared is not None else "per-GPU replica",
                        "l2": "inputs larger than L2 (800 MB table re-zeroed per render + "

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MCG_ABI_VERSION 3   /* 2: mcg_render_stats.shadow_occluded; 3: write_slots, insert log */
+#define MCG_ABI_VERSION 3   /* 2: mcg_render_stats.shadow_occluded; 3: write_slots, insert log, n_devices */
 
 typedef enum mcg_status {
     MCG_OK = 0,
@@ -91,6 +91,19 @@ typedef struct mcg_options {
     int32_t device;       /* CUDA ordinal */
     int32_t profile;      /* 1: time every kernel launch with CUDA events on the ctx stream */
     void* stream;         /* optional cudaStream_t to use; NULL: the context creates its own */
+    /* In-process multi-GPU (render() uses every worker, tracer.hpp:12, 69-70):
+     * n_devices > 1 makes the context span `devices` (NULL: `device`,
+     * device+1, ...; the first is the context's own). mcg_upload_scene
+     * uploads to every device; mcg_render splits the image into 16x16 tiles
+     * dealt round-robin to the devices (shard_mode 0, or contiguous bands
+     * with shard_mode 1), one host thread and stream per device, each with
+     * its own cache replica (the context's table on that device; an
+     * external cache is refused), and gathers the frames on the first
+     * device with ncclReduce(sum) of frames zeroed outside each device's
+     * tiles (exact: x + 0 = x). A device listed twice (tests on one GPU)
+     * gathers by device copies instead of NCCL. 0 or 1: one device. */
+    int32_t n_devices;
+    const int32_t* devices;
 } mcg_options;
 
 mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out);

@@ -130,16 +130,25 @@ def audit_dump(path: str) -> AuditReport:
 
 class Context:
     """One CUDA device + stream (mcg_ctx). ``profile=True`` times every kernel
-    launch with CUDA events on the context's stream."""
+    launch with CUDA events on the context's stream. ``devices=[...]``: one
+    context over several GPUs (include/mcg.h mcg_options.n_devices): render()
+    deals the image's 16x16 tiles to the devices, one host thread and cache
+    replica each, and gathers the frames with NCCL on the first device."""
 
     _defaults: dict[int, "Context"] = {}
 
-    def __init__(self, device: int = 0, profile: bool = False, stream: Optional[int] = None):
-        opt = N.Options(device, 1 if profile else 0, C.c_void_p(stream) if stream else None)
+    def __init__(self, device: int = 0, profile: bool = False, stream: Optional[int] = None,
+                 devices: Optional[Sequence[int]] = None):
+        devs = [int(d) for d in devices] if devices else []
+        arr = (C.c_int32 * len(devs))(*devs) if devs else None
+        opt = N.Options(devs[0] if devs else device, 1 if profile else 0,
+                        C.c_void_p(stream) if stream else None, len(devs),
+                        C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None)
         h = C.c_void_p()
         check(N.lib().mcg_create(C.byref(opt), C.byref(h)))
         self.handle = h
-        self.device = device
+        self.device = devs[0] if devs else device
+        self.devices = devs or [device]
         self._scene = None
 
     @classmethod

@@ -22,7 +22,7 @@ class Descriptor(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("device", i32), ("profile", i32), ("stream", vp)]
+    _fields_ = [("device", i32), ("profile", i32), ("stream", vp), ("n_devices", i32), ("devices", P(i32))]
 
 
 class KernelTime(C.Structure):

@@ -99,7 +99,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = [o for o, _, _ in jobs]
     if force or todo or _stale(LIB, objs):
         _run([nvcc, "-ccbin", CXX, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,
-              "-Xcompiler", "-fPIC", "-lpthread"])
+              "-Xcompiler", "-fPIC", "-lpthread", "-ldl"])
         with open(os.path.join(OUT_DIR, "ptxas.log"), "w") as f:
             for o in sorted(logs):
                 f.write(f"==== {os.path.basename(o)}\n{logs[o]}\n")

@@ -149,12 +149,20 @@ struct mcg_ctx {
     // scratch
     mcg::DevMem cub_temp, scratch_a, scratch_b, scratch_c, scratch_d, scratch_e;
     mcg::DevMem path_mem, queue_mem, stats_mem;
+    // in-process multi-GPU (mcg_options.n_devices > 1): one single-device
+    // context per further device, NCCL communicators over all of them
+    // (created on the first multi-device render; distinct devices only)
+    std::vector<mcg_ctx*> peers;
+    std::vector<void*> nccl_comms;
+    bool devices_distinct = true;
+    mcg::DevMem gather_tmp;   // device-copy gather (a device listed twice)
 };
 
 namespace mcg {
 
 cudaEvent_t take_event(mcg_ctx* ctx);
 void resolve_events(mcg_ctx* ctx);  // synchronizes on the pending events
+void nccl_destroy(mcg_ctx* ctx);    // the multi-device context's communicators (mcg_render.cu)
 
 // Brackets one kernel launch: counts it and, when profiling, records CUDA
 // events on the context stream around it.

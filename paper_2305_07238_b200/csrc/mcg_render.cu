@@ -22,10 +22,16 @@
 // kernel of the vertex reads and writes its own index (coalesced). A path's
 // identity travels in `pid` (pass slot j * n_pix + pixel index); its final
 // radiance lands in `fin[pid]` when it ends.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <exception>
 #include <string>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "host_scene.hpp"
@@ -78,9 +84,8 @@ struct RenderView {
     float4* L2;
     uint32_t* pid2;
     float4* fin;              // by path id: final radiance.rgb, nodes_found (uint bits)
-    float4* sh0;              // position.xyz, u
-    float4* sh1;              // normal.xyz, v
-    float4* sh2;              // g1.xy, g2.xy
+    float4* hrec;             // closest hit: primitive (uint bits), t, b1, b2 -- k_shade rebuilds
+                              // the shading record from it (surface + footprint, same arithmetic)
     uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
     uint32_t* vals;           // unsorted layout positions
     const uint32_t* skey;     // sorted keys: hits first, in material order
@@ -516,10 +521,13 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
     d = mcgd::normalize((fwd + right * a) + up * bq);
 }
 
-// Shading record of a closest hit for the path at layout position q (path
-// id pid): position, normal, uv, footprint gradients at q, the propagated
-// cone width into ro.w, and the sort key; on a miss the path ends: radiance
-// + throughput * env goes to fin[pid] and the key is "no hit".
+// Closest hit of the path at layout position q (path id pid): the hit
+// record (primitive, t, barycentrics: 16 bytes) at q, the propagated cone
+// width into ro.w, and the sort key; on a miss the path ends: radiance +
+// throughput * env goes to fin[pid] and the key is "no hit". k_shade
+// rebuilds the shading record (position, normal, uv, footprint gradients)
+// from the hit record with the same arithmetic (shade_input), so one 16-byte
+// gather replaces three.
 __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, uint32_t pid, float4& ro,
                                                const float4& rd, const float4& thr, const float4& L,
                                                bool found, uint32_t prim, float t, float b1, float b2,
@@ -531,33 +539,41 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
         return no_hit_key(R);
     }
     const Surface s = surface(R.S, o, d, prim, t, b1, b2);
-    const float width = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
-    float2 g1, g2;
-    mcgd::footprint(width, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-    R.sh0[q] = make_float4(s.p.x, s.p.y, s.p.z, s.u);
-    R.sh1[q] = make_float4(s.n.x, s.n.y, s.n.z, s.v);
-    R.sh2[q] = make_float4(g1.x, g1.y, g2.x, g2.y);
-    ro.w = width;
+    ro.w = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
+    R.hrec[q] = make_float4(__uint_as_float(prim), t, b1, b2);
     const uint32_t slot_j = pid / R.n_pix;
     const uint64_t rkey = mcgd::path_key(R.seed, R.pix[pid - slot_j * R.n_pix], R.sample0 + slot_j);
     return sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+}
+
+// The shading point of a hit record (ShadingPoint, geom.hpp:49-56): the
+// surface (scene.cpp:211-247) and the footprint gradients of the cone of
+// width ro.w (raycone.cpp:50-65).
+__device__ __forceinline__ mcgd::ShadeIn shade_input(const mcgd::SceneView& S, const float4& ro, const float4& rd,
+                                                     const float4& hr, uint32_t& slot_out) {
+    const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
+    const Surface s = surface(S, o, d, __float_as_uint(hr.x), hr.y, hr.z, hr.w);
+    float2 g1, g2;
+    mcgd::footprint(ro.w, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+    slot_out = s.slot;
+    return mcgd::ShadeIn{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
+                         s.u, s.v, g1.x, g1.y, g2.x, g2.y};
 }
 
 // Next-event estimation and the cosine bounce of vertex b of path pid, whose
 // state goes to sorted position i: one shadow-ray candidate per light -- its
 // contribution computed now, applied in light order by k_resolve once
 // visibility is known -- and the continuation ray.
-__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, int b, float4 s0,
-                                           float4 s1, float3 bc, float4 thr, float width, float spread) {
+__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, int b, V3 pos,
+                                           V3 n, float3 bc, float4 thr, float width, float spread) {
     const uint32_t slot_j = pid / R.n_pix;
     const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
-    const V3 n{s1.x, s1.y, s1.z};
     const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
                  fminf(fmaxf(bc.z, 0.0f), 1.0f)};
     const V3 f = alb * kInvPi;
     const V3 tf{thr.x * f.x, thr.y * f.y, thr.z * f.z};
-    const V3 o = V3{s0.x, s0.y, s0.z} + n * kEps;
+    const V3 o = pos + n * kEps;
     const uint32_t nl = R.S.n_plights + R.S.n_rlights;
     const unsigned lane = threadIdx.x & 31u;
     for (uint32_t j = 0; j < nl; ++j) {
@@ -1122,6 +1138,89 @@ __device__ __forceinline__ void leaf_test(const mcgd::SceneView& S, uint32_t fir
 #endif
 }
 
+// The leaf phase with the warp's (ray, primitive) pairs redistributed over
+// all 32 lanes (MCG_LEAF_REDIST): only ~1/3 of the lanes hold a leaf when
+// the while-while loop reaches it, and each tests its <= 4 (<= 7) triangles
+// one after the other. Here the warp's pairs are numbered lane by lane
+// (prefix sum of the counts), each lane tests the pairs r*32 + lane against
+// its owner's ray with tmax = the owner's closest before this leaf, and the
+// owner then takes its results in primitive order with the reference's
+// strict update (scene.cpp:252-278: closest = t iff t < closest). This is
+// the sequential decision exactly: a primitive's (t, b1, b2) do not depend
+// on tmax, a triangle is accepted iff t < tmax, and a sphere takes its
+// nearer root below tmax -- so "hit below the old closest, then t < current
+// closest" accepts exactly what "hit below the current closest" accepts,
+// with the same values. Warp-collective: every lane calls it.
+// Off: exact, but slower -- trace_closest 1.76 vs 1.43 ms per launch, 700 vs
+// 629 ms per bench render (gpurun_out r2 ab_c: the ~26 shuffles per round
+// of 32 pairs cost more than the idle lanes of the serial leaf loop).
+#ifndef MCG_LEAF_REDIST
+#define MCG_LEAF_REDIST 0
+#endif
+__device__ __forceinline__ void leaf_redist(const mcgd::SceneView& S, bool has, int32_t code, V3 o, V3 d,
+                                            float tmin, float& closest, uint32_t& prim, float& t_out,
+                                            float& b1_out, float& b2_out, bool& found, uint32_t& prims_tested) {
+    const unsigned lane = threadIdx.x & 31u;
+    uint32_t first = 0, cnt = 0;
+    if (has) {
+        const uint32_t v = static_cast<uint32_t>(~code);
+        first = v >> 3;
+        cnt = v & 7u;
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t x = __shfl_up_sync(mcgd::kFull, incl, off);
+        if (lane >= static_cast<unsigned>(off)) incl += x;
+    }
+    const uint32_t total = __shfl_sync(mcgd::kFull, incl, 31);
+    if (total == 0) return;
+    const uint32_t excl = incl - cnt;
+    const uint32_t maxcnt = __reduce_max_sync(mcgd::kFull, cnt);
+    prims_tested += cnt;
+    const float c0 = closest;
+    for (uint32_t base = 0; base < total; base += 32u) {
+        const uint32_t qi = base + lane;
+        // owner: the first lane whose inclusive count exceeds qi
+        int owner = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            if (__shfl_sync(mcgd::kFull, incl, owner + step - 1) <= qi) owner += step;
+        }
+        const float ox = __shfl_sync(mcgd::kFull, o.x, owner), oy = __shfl_sync(mcgd::kFull, o.y, owner),
+                    oz = __shfl_sync(mcgd::kFull, o.z, owner);
+        const float dx = __shfl_sync(mcgd::kFull, d.x, owner), dy = __shfl_sync(mcgd::kFull, d.y, owner),
+                    dz = __shfl_sync(mcgd::kFull, d.z, owner);
+        const float tmax = __shfl_sync(mcgd::kFull, c0, owner);
+        const uint32_t pi = __shfl_sync(mcgd::kFull, first, owner) + qi - __shfl_sync(mcgd::kFull, excl, owner);
+        float t = __int_as_float(0x7f800000), b1 = 0.0f, b2 = 0.0f;
+        if (qi < total) {
+            float tt, bb1, bb2;
+            if (hit_prim(S, pi, V3{ox, oy, oz}, V3{dx, dy, dz}, tmin, tmax, tt, bb1, bb2)) {
+                t = tt;
+                b1 = bb1;
+                b2 = bb2;
+            }
+        }
+        for (uint32_t k = 0; k < maxcnt; ++k) {
+            const uint32_t g = excl + k;
+            const bool mine = k < cnt && g >= base && g < base + 32u;
+            const int src = mine ? static_cast<int>(g - base) : static_cast<int>(lane);
+            const float kt = __shfl_sync(mcgd::kFull, t, src);
+            const float kb1 = __shfl_sync(mcgd::kFull, b1, src);
+            const float kb2 = __shfl_sync(mcgd::kFull, b2, src);
+            if (mine && kt < closest) {
+                closest = kt;
+                prim = first + k;
+                t_out = kt;
+                b1_out = kb1;
+                b2_out = kb2;
+                found = true;
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool active, V3 o, V3 d,
                                              float tmin, float tmax, uint32_t& prim, float& t_out,
                                              float& b1_out, float& b2_out, uint32_t& nodes_visited,
@@ -1240,7 +1339,21 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
             if (__all_sync(mcgd::kFull, leaf || !has_n)) break;
         }
         // Phase 2: every lane holding a leaf tests it (the reference's order).
+#if MCG_LEAF_REDIST
+        leaf_redist(S, leaf, lc, o, d, tmin, closest, prim, t_out, b1_out, b2_out, found, prims_tested);
+        leaf = false;
+#if MCG_CLOSEST_LEAVES > 1
+        {
+            // the second leaf: its cull test against the closest it would see
+            const bool go2 = leaf2 && !(closest < le2);
+            leaf2 = false;
+            leaf_redist(S, go2, lc2, o, d, tmin, closest, prim, t_out, b1_out, b2_out, found, prims_tested);
+        }
+#endif
+        if (false) {
+#else
         if (leaf) {
+#endif
             const uint32_t v = static_cast<uint32_t>(~lc);
             const uint32_t first = v >> 3, cnt = v & 7u;
             prims_tested += cnt;
@@ -1838,17 +1951,16 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t q = order[i];
 #endif
     const unsigned grp = __match_any_sync(live, slot);
-    const float4 s0 = R.sh0[q], s1 = R.sh1[q], s2 = R.sh2[q], rd = R.rd[q];
+    const float4 hr = R.hrec[q], ro = R.ro[q], rd = R.rd[q];
     const uint32_t pid = R.pid[q];
     // the rest of the path's state is loaded now, in the same round trip as
-    // the shading record, not after the VM; what the VM does not change is
+    // the hit record, not after the VM; what the VM does not change is
     // written to the next layout right away, so little of it stays live
     float4 thr = R.thr[q];
-    const float width = R.ro[q].w;
     R.L2[i] = R.L[q];
     R.pid2[i] = pid;
-    const mcgd::ShadeIn in{s0.x, s0.y, s0.z, s1.x, s1.y, s1.z, rd.x, rd.y, rd.z,
-                           s0.w, s1.w, s2.x, s2.y, s2.z, s2.w};
+    uint32_t slot_hit;
+    const mcgd::ShadeIn in = shade_input(R.S, ro, rd, hr, slot_hit);
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
                    static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
     const uint32_t slot_j = pid / R.n_pix;
@@ -1858,7 +1970,7 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
-    nee_bounce(R, i, pid, b, s0, s1, r.value, thr, width, rd.w);
+    nee_bounce(R, i, pid, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, ro.w, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
     mcgd::warp_add(R.stats + kStatWon, cnt.won);
@@ -2012,14 +2124,14 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         }
     }
 
-    // Path state: 2 layouts x (4 float4 + pid) + 3 float4 shading record +
+    // Path state: 2 layouts x (4 float4 + pid) + the hit record (float4) +
     // 1 float4 final radiance per path; shadow rays: 3 float4 + 1 byte per
     // (path, light); sort keys/values and the shadow queue as u32.
     const uint32_t n_lights = D.view.n_plights + D.view.n_rlights;
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
     if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
-    const size_t lane_bytes = f4 * 12 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
+    const size_t lane_bytes = f4 * 10 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
     ctx->path_mem.ensure(lane_bytes);
     for (int l = 1; l < lanes; ++l) ctx->lane_path[l].ensure(lane_bytes);
     RenderView R{};
@@ -2045,10 +2157,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         V.rd2 = V.ro2 + max_paths;
         V.thr2 = V.rd2 + max_paths;
         V.L2 = V.thr2 + max_paths;
-        V.sh0 = V.L2 + max_paths;
-        V.sh1 = V.sh0 + max_paths;
-        V.sh2 = V.sh1 + max_paths;
-        V.fin = V.sh2 + max_paths;
+        V.hrec = V.L2 + max_paths;
+        V.fin = V.hrec + max_paths;
         V.sro = V.fin + max_paths;
         V.srd = V.sro + n_shadow;
         V.scon = V.srd + n_shadow;
@@ -2319,7 +2429,248 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     }
 }
 
+// ---------------------------------------------------------------------------
+// In-process multi-GPU render (mcg_options.n_devices > 1)
+// ---------------------------------------------------------------------------
+
+// NCCL, loaded at run time (the process may already hold torch's copy of
+// libnccl.so.2; dlopen then returns that one): the five calls the frame
+// gather needs, types from the system nccl.h.
+struct NcclApi {
+    bool loaded = false;
+    std::string error;
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return a;
+        }
+        a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+        a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+        a.reduce = reinterpret_cast<decltype(a.reduce)>(dlsym(h, "ncclReduce"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.loaded = a.comm_init_all && a.comm_destroy && a.group_start && a.group_end && a.reduce && a.error_string;
+        if (!a.loaded) a.error = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(MCG_ERR_CUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+
+// Zeroes the frame outside this device's tiles, so the frames sum exactly.
+__global__ void k_zero_unowned(double* rad, double* nodes, uint32_t* samples, int W, int H, int ts, int rank,
+                               int count, int mode) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= static_cast<uint32_t>(W) * static_cast<uint32_t>(H)) return;
+    const int x = static_cast<int>(i % static_cast<uint32_t>(W)), y = static_cast<int>(i / static_cast<uint32_t>(W));
+    const int tiles_x = (W + ts - 1) / ts, n_tiles = tiles_x * ((H + ts - 1) / ts);
+    const int tile = (y / ts) * tiles_x + x / ts;
+    bool mine;
+    if (mode == MCG_SHARD_INTERLEAVED) {
+        mine = tile % count == rank;
+    } else {
+        const int lo = static_cast<int>(static_cast<int64_t>(n_tiles) * rank / count);
+        const int hi = static_cast<int>(static_cast<int64_t>(n_tiles) * (rank + 1) / count);
+        mine = tile >= lo && tile < hi;
+    }
+    if (mine) return;
+    rad[3ull * i] = 0.0;
+    rad[3ull * i + 1] = 0.0;
+    rad[3ull * i + 2] = 0.0;
+    nodes[i] = 0.0;
+    samples[i] = 0u;
+}
+
+__global__ void k_add_frames(double* rad, double* nodes, uint32_t* samples, const double* rad2,
+                             const double* nodes2, const uint32_t* samples2, size_t np) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= np) return;
+    rad[3 * i] += rad2[3 * i];
+    rad[3 * i + 1] += rad2[3 * i + 1];
+    rad[3 * i + 2] += rad2[3 * i + 2];
+    nodes[i] += nodes2[i];
+    samples[i] += samples2[i];
+}
+
+void multi_render(mcg_ctx* ctx, const mcg_render_params& P, mcg_frame* frame, mcg_render_stats* stats) {
+    const int n = 1 + static_cast<int>(ctx->peers.size());
+    if (P.shard_count > 1) fail(MCG_ERR_INVALID_ARGUMENT, "a multi-device context shards the image itself");
+    const int W = P.width ? P.width : ctx->scene.cam.cam_width;
+    const int H = P.height ? P.height : ctx->scene.cam.cam_height;
+    if (W <= 0 || H <= 0) fail(MCG_ERR_INVALID_ARGUMENT, "image size must be positive");
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t np = static_cast<size_t>(W) * H;
+    std::vector<mcg_ctx*> all{ctx};
+    all.insert(all.end(), ctx->peers.begin(), ctx->peers.end());
+    std::vector<mcg_render_stats> st(n);
+    std::vector<std::vector<uint64_t>> hps(n, std::vector<uint64_t>(static_cast<size_t>(std::max(P.spp, 0)), 0));
+    std::vector<std::exception_ptr> err(n);
+    std::vector<std::string> msg(n);
+    std::vector<mcg_status> code(n, MCG_OK);
+    // one host thread per device: render its tiles into a device frame that
+    // starts as the caller's frame, then zero everything outside its tiles
+    auto work = [&](int r) {
+        mcg_ctx* c = all[r];
+        try {
+            cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+            c->scratch_e.ensure(np * 44 + 64);
+            double* rad = c->scratch_e.as<double>();
+            double* nodes = rad + 3 * np;
+            uint32_t* samples = reinterpret_cast<uint32_t*>(nodes + np);
+            cuda_check(cudaMemcpyAsync(rad, frame->radiance, np * 24, cudaMemcpyHostToDevice, c->stream), "H2D frame");
+            cuda_check(cudaMemcpyAsync(nodes, frame->nodes_found, np * 8, cudaMemcpyHostToDevice, c->stream), "H2D frame");
+            cuda_check(cudaMemcpyAsync(samples, frame->samples, np * 4, cudaMemcpyHostToDevice, c->stream), "H2D frame");
+            mcg_render_params pr = P;
+            pr.shard_rank = r;
+            pr.shard_count = n;
+            st[r].hits_per_sample = hps[r].data();
+            render_device(c, pr, nullptr, rad, nodes, samples, &st[r]);
+            const int ts = P.tile_size > 0 ? P.tile_size : 16;
+            k_zero_unowned<<<grid_for(np, 256), 256, 0, c->stream>>>(rad, nodes, samples, W, H, ts, r, n, P.shard_mode);
+            cuda_check(cudaGetLastError(), "k_zero_unowned");
+            ++c->launches;
+            cuda_check(cudaStreamSynchronize(c->stream), "render");
+        } catch (const mcg::Failure& e) {
+            code[r] = e.code;
+            msg[r] = e.what();
+        } catch (...) {
+            err[r] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> threads;
+    for (int r = 1; r < n; ++r) threads.emplace_back(work, r);
+    work(0);
+    for (auto& t : threads) t.join();
+    for (int r = 0; r < n; ++r) {
+        if (err[r]) std::rethrow_exception(err[r]);
+        if (code[r] != MCG_OK) fail(code[r], "device " + std::to_string(all[r]->device) + ": " + msg[r]);
+    }
+    auto frame_of = [&](mcg_ctx* c, double*& rad, double*& nodes, uint32_t*& samples) {
+        rad = c->scratch_e.as<double>();
+        nodes = rad + 3 * np;
+        samples = reinterpret_cast<uint32_t*>(nodes + np);
+    };
+    double *rad0, *nodes0;
+    uint32_t* samples0;
+    frame_of(ctx, rad0, nodes0, samples0);
+    if (ctx->devices_distinct) {
+        // the framebuffer gather over NVLink: ncclReduce(sum) to the first
+        // device, one group over the three buffers of every device
+        const NcclApi& api = nccl();
+        if (!api.loaded) fail(MCG_ERR_CUDA, api.error);
+        if (ctx->nccl_comms.size() != static_cast<size_t>(n)) {
+            std::vector<int> devs(n);
+            for (int r = 0; r < n; ++r) devs[r] = all[r]->device;
+            std::vector<ncclComm_t> comms(n);
+            nccl_check(api.comm_init_all(comms.data(), n, devs.data()), "ncclCommInitAll");
+            ctx->nccl_comms.assign(comms.begin(), comms.end());
+        }
+        nccl_check(api.group_start(), "ncclGroupStart");
+        for (int r = 0; r < n; ++r) {
+            double *rad, *nodes;
+            uint32_t* samples;
+            frame_of(all[r], rad, nodes, samples);
+            ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl_comms[r]);
+            nccl_check(api.reduce(rad, rad, 3 * np, ncclFloat64, ncclSum, 0, comm, all[r]->stream), "ncclReduce");
+            nccl_check(api.reduce(nodes, nodes, np, ncclFloat64, ncclSum, 0, comm, all[r]->stream), "ncclReduce");
+            nccl_check(api.reduce(samples, samples, np, ncclUint32, ncclSum, 0, comm, all[r]->stream), "ncclReduce");
+        }
+        nccl_check(api.group_end(), "ncclGroupEnd");
+        for (int r = 1; r < n; ++r) {
+            cuda_check(cudaSetDevice(all[r]->device), "cudaSetDevice");
+            cuda_check(cudaStreamSynchronize(all[r]->stream), "ncclReduce");
+        }
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    } else {
+        // a device listed twice (tests on one GPU): copy each frame to the
+        // first device and add it there (same exact sum)
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        ctx->gather_tmp.ensure(np * 44 + 64);
+        double* rad2 = ctx->gather_tmp.as<double>();
+        double* nodes2 = rad2 + 3 * np;
+        uint32_t* samples2 = reinterpret_cast<uint32_t*>(nodes2 + np);
+        for (int r = 1; r < n; ++r) {
+            double *rad, *nodes;
+            uint32_t* samples;
+            frame_of(all[r], rad, nodes, samples);
+            cuda_check(cudaMemcpyPeerAsync(rad2, ctx->device, rad, all[r]->device, np * 36, ctx->stream), "gather");
+            k_add_frames<<<grid_for(np, 256), 256, 0, ctx->stream>>>(rad0, nodes0, samples0, rad2, nodes2, samples2, np);
+            cuda_check(cudaGetLastError(), "k_add_frames");
+            ++ctx->launches;
+        }
+    }
+    cuda_check(cudaMemcpyAsync(frame->radiance, rad0, np * 24, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+    cuda_check(cudaMemcpyAsync(frame->nodes_found, nodes0, np * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+    cuda_check(cudaMemcpyAsync(frame->samples, samples0, np * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H frame");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "render");
+    if (stats) {
+        uint64_t* out_hps = stats->hits_per_sample;
+        mcg_render_stats sum = st[0];
+        for (int r = 1; r < n; ++r) {
+            const mcg_render_stats& x = st[r];
+            sum.lookups += x.lookups;
+            sum.hits += x.hits;
+            sum.inserts_won += x.inserts_won;
+            sum.inserts_lost_full += x.inserts_lost_full;
+            sum.stores_attempted += x.stores_attempted;
+            sum.stores_won += x.stores_won;
+            sum.instructions_executed += x.instructions_executed;
+            sum.paths += x.paths;
+            sum.shading_points += x.shading_points;
+            sum.shadow_rays += x.shadow_rays;
+            sum.bvh_nodes += x.bvh_nodes;
+            sum.prims_tested += x.prims_tested;
+            sum.tex_samples += x.tex_samples;
+            sum.bvh_nodes_shadow += x.bvh_nodes_shadow;
+            sum.prims_tested_shadow += x.prims_tested_shadow;
+            sum.closest_rays += x.closest_rays;
+            sum.shadow_occluded += x.shadow_occluded;
+            sum.launches += x.launches;
+            sum.device_ms = std::max(sum.device_ms, x.device_ms);
+        }
+        sum.launches += static_cast<uint64_t>(n) + (ctx->devices_distinct ? 0u : static_cast<uint64_t>(n - 1));
+        sum.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        sum.hits_per_sample = out_hps;
+        if (out_hps) {
+            for (int sidx = 0; sidx < P.spp; ++sidx) {
+                uint64_t a = 0;
+                for (int r = 0; r < n; ++r) a += hps[r][sidx];
+                out_hps[sidx] = a;
+            }
+        }
+        *stats = sum;
+    }
+}
+
 }  // namespace
+
+namespace mcg {
+void nccl_destroy(mcg_ctx* ctx) {
+    if (ctx->nccl_comms.empty()) return;
+    const NcclApi& api = nccl();
+    if (api.loaded) {
+        for (void* c : ctx->nccl_comms) api.comm_destroy(static_cast<ncclComm_t>(c));
+    }
+    ctx->nccl_comms.clear();
+}
+}  // namespace mcg
 
 extern "C" {
 
@@ -2397,6 +2748,8 @@ mcg_status mcg_render_device(mcg_ctx* ctx, const mcg_render_params* params, mcg_
                              mcg_frame* d_frame, mcg_render_stats* stats) {
     return guarded([&] {
         if (!ctx || !params || !d_frame) fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
+        if (!ctx->peers.empty()) fail(MCG_ERR_INVALID_ARGUMENT, "a multi-device context renders through mcg_render");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         render_device(ctx, *params, cache, d_frame->radiance, d_frame->nodes_found,
                       d_frame->samples, stats);
     });
@@ -2409,6 +2762,13 @@ mcg_status mcg_render(mcg_ctx* ctx, const mcg_render_params* params, mcg_cache* 
             fail(MCG_ERR_INVALID_ARGUMENT, "null argument");
         }
         if (!ctx->scene.loaded) fail(MCG_ERR_INVALID_ARGUMENT, "no scene uploaded");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (!ctx->peers.empty()) {
+            if (cache) fail(MCG_ERR_INVALID_ARGUMENT, "a multi-device context keeps one cache replica per device "
+                                                      "(no external cache)");
+            multi_render(ctx, *params, frame, stats);
+            return;
+        }
         const int W = params->width ? params->width : ctx->scene.cam.cam_width;
         const int H = params->height ? params->height : ctx->scene.cam.cam_height;
         if (W <= 0 || H <= 0) fail(MCG_ERR_INVALID_ARGUMENT, "image size must be positive");

@@ -746,8 +746,14 @@ mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out) {
         int count = 0;
         cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
         if (count == 0) fail(MCG_ERR_NO_DEVICE, "no CUDA device");
-        const int dev = opt ? opt->device : 0;
-        need(dev >= 0 && dev < count, "device ordinal out of range");
+        const int n_dev = opt && opt->n_devices > 1 ? opt->n_devices : 1;
+        std::vector<int> devs(n_dev);
+        for (int k = 0; k < n_dev; ++k) {
+            devs[k] = (opt && opt->devices) ? opt->devices[k] : (opt ? opt->device : 0) + k;
+            need(devs[k] >= 0 && devs[k] < count, "device ordinal out of range");
+        }
+        need(n_dev == 1 || !(opt && opt->stream), "a multi-device context creates its own streams");
+        const int dev = devs[0];
         cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         auto* ctx = new mcg_ctx;
         ctx->device = dev;
@@ -763,12 +769,28 @@ mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out) {
             ctx->own_stream = true;
         }
         ctx->stats_mem.ensure(4096);
+        for (int k = 1; k < n_dev; ++k) {
+            mcg_options po{devs[k], opt->profile, nullptr, 0, nullptr};
+            mcg_ctx* peer = nullptr;
+            const mcg_status st = mcg_create(&po, &peer);
+            if (st != MCG_OK) {
+                const std::string msg = mcg_last_error();
+                mcg_destroy(ctx);
+                fail(st, msg);
+            }
+            ctx->peers.push_back(peer);
+            for (int j = 0; j < k; ++j) ctx->devices_distinct = ctx->devices_distinct && devs[j] != devs[k];
+        }
+        cuda_check(cudaSetDevice(dev), "cudaSetDevice");
         *out = ctx;
     });
 }
 
 mcg_status mcg_destroy(mcg_ctx* ctx) {
     if (!ctx) return MCG_OK;
+    mcg::nccl_destroy(ctx);
+    for (mcg_ctx* p : ctx->peers) mcg_destroy(p);
+    ctx->peers.clear();
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_cache) mcg_cache_destroy(ctx->own_cache);
@@ -1510,8 +1532,16 @@ mcg_status mcg_probe_bench(mcg_cache* cache, uint64_t n, uint64_t seed, int32_t 
 // ---- scene upload & per-point execution -----------------------------------
 
 mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
+    if (ctx && !ctx->peers.empty()) {
+        // every device of a multi-device context holds the scene
+        for (mcg_ctx* p : ctx->peers) {
+            const mcg_status st = mcg_upload_scene(p, scene);
+            if (st != MCG_OK) return st;
+        }
+    }
     return guarded([&] {
         need(ctx && scene, "null argument");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         mcg_flat_scene f;
         const mcg_status s = mcg_scene_flat(scene, &f);
         if (s != MCG_OK) fail(s, mcg_last_error());
