@@ -107,6 +107,8 @@ typedef struct mcg_options {
 } mcg_options;
 
 mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out);
+/* Number of visible CUDA devices (MCG_ERR_NO_DEVICE when there is none). */
+mcg_status mcg_device_count(int32_t* count);
 mcg_status mcg_destroy(mcg_ctx* ctx);
 mcg_status mcg_synchronize(mcg_ctx* ctx);
 /* The cudaStream_t the context launches on (for external event timing). */

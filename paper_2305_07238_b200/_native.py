@@ -98,6 +98,7 @@ _SIGS = [
     ("mcg_decode_value", None, [u32, P(f32)]),
     ("mcg_memory_bytes", C.c_int, [u64, u64, P(u64)]),
     ("mcg_create", C.c_int, [P(Options), P(vp)]),
+    ("mcg_device_count", C.c_int, [P(i32)]),
     ("mcg_destroy", C.c_int, [vp]),
     ("mcg_synchronize", C.c_int, [vp]),
     ("mcg_stream", vp, [vp]),

@@ -740,6 +740,16 @@ static std::vector<mcg_bvh_node> build_shadow_tree(const mcg_flat_scene& f, int 
 
 extern "C" {
 
+mcg_status mcg_device_count(int32_t* count) {
+    return guarded([&] {
+        need(count != nullptr, "null out");
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (n == 0) fail(MCG_ERR_NO_DEVICE, "no CUDA device");
+        *count = n;
+    });
+}
+
 mcg_status mcg_create(const mcg_options* opt, mcg_ctx** out) {
     return guarded([&] {
         need(out != nullptr, "null out");

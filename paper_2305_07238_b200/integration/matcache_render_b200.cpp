@@ -14,6 +14,7 @@
 // Status codes are rethrown as the reference's exception types.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -48,14 +49,22 @@ void ok(mcg_status s) {
     if (s != MCG_OK) rethrow(s);
 }
 
-// One device context per process (the reference render() is synchronous).
+// Device contexts, one set per process (the reference render() is
+// synchronous). `ctx` is device 0 alone (external-cache renders: the caller's
+// table is one table); `multi` spans every GPU the process may use
+// (MATCACHE_B200_DEVICES="0,1,..." or all visible ones): render() without an
+// external cache deals its tiles to all of them with a cache replica each
+// and gathers the frame over NCCL, as the reference's render() uses every
+// worker thread (tracer.hpp:12, 69-70).
 struct Device {
     std::mutex mu;
     mcg_ctx* ctx = nullptr;
-    // The uploaded scene, identified by content (a fingerprint of everything
-    // the device receives), never by the Scene's address: a different or
-    // edited Scene at the same address must not render with stale data.
-    uint64_t uploaded_fp = 0;
+    mcg_ctx* multi = nullptr;
+    // The scene, identified by content (a fingerprint of everything the
+    // devices receive), never by the Scene's address: a different or edited
+    // Scene at the same address must not render with stale data.
+    uint64_t scene_fp = 0;
+    uint64_t uploaded_fp = 0, multi_fp = 0;   // what each context holds
     mcg_scene* scene = nullptr;
     // Device tables standing in for external MaterialCache objects, reused
     // across calls (an 800 MB allocation is not free). The host table stays
@@ -368,21 +377,44 @@ RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCach
     Device& D = device();
     std::lock_guard<std::mutex> lock(D.mu);
     const auto t0 = std::chrono::steady_clock::now();
+    const bool use_multi = !(config.cache_enabled && external_cache);
     if (!D.ctx) {
-        mcg_options opt{0, 0, nullptr};
+        mcg_options opt{0, 0, nullptr, 0, nullptr};
         ok(mcg_create(&opt, &D.ctx));
+        std::vector<int32_t> devs;
+        if (const char* env = std::getenv("MATCACHE_B200_DEVICES")) {
+            std::stringstream ss(env);
+            std::string tok;
+            while (std::getline(ss, tok, ',')) {
+                if (!tok.empty()) devs.push_back(static_cast<int32_t>(std::stoi(tok)));
+            }
+        } else {
+            int32_t n = 1;
+            ok(mcg_device_count(&n));
+            for (int32_t k = 0; k < n; ++k) devs.push_back(k);
+        }
+        if (devs.size() > 1) {
+            mcg_options mo{devs[0], 0, nullptr, static_cast<int32_t>(devs.size()), devs.data()};
+            ok(mcg_create(&mo, &D.multi));
+        }
     }
+    mcg_ctx* ctx = (use_multi && D.multi) ? D.multi : D.ctx;
     {
         SceneInput S;
         scene_input(scene, S);
         const uint64_t fp = fingerprint(S);
-        if (!D.scene || fp != D.uploaded_fp) {
+        if (!D.scene || fp != D.scene_fp) {
             if (D.scene) mcg_scene_destroy(D.scene);
             D.scene = nullptr;
-            D.uploaded_fp = 0;
+            D.scene_fp = D.uploaded_fp = D.multi_fp = 0;
             ok(mcg_scene_build(&S.in, &D.scene));
-            ok(mcg_upload_scene(D.ctx, D.scene));
-            D.uploaded_fp = fp;
+            D.scene_fp = fp;
+        }
+        uint64_t& have = ctx == D.multi ? D.multi_fp : D.uploaded_fp;
+        if (have != fp) {
+            have = 0;
+            ok(mcg_upload_scene(ctx, D.scene));
+            have = fp;
         }
     }
     const int w = config.width ? config.width : scene.camera.width;
@@ -410,7 +442,7 @@ RenderResult render(const Scene& scene, const RenderConfig& config, MaterialCach
     std::vector<uint64_t> hps(static_cast<size_t>(std::max(config.spp, 0)), 0);
     mcg_render_stats st{};
     st.hits_per_sample = hps.data();
-    ok(mcg_render(D.ctx, &p, table, &frame, &st));
+    ok(mcg_render(ctx, &p, table, &frame, &st));
     if (table) sync_back(table, external_cache, log_cap);
     RenderStats& rs = result.stats;
     rs.lookups = st.lookups;

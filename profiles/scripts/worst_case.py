@@ -17,8 +17,14 @@ W, H, SPP = 1920, 1080, 128
 ctx = Context(0)
 tmp = tempfile.mkdtemp()
 out = {}
+# unit uv per surface (the bench's layout); mip_offset 24 puts every lookup on
+# the finest virtual level (2^24 texels per uv unit): no two samples share a
+# texel, hit rate ~0, every miss inserts until the 10^8 slots are full and
+# then every lookup scans a full 80-byte cell (the paper's Bmw case: "no
+# gain"; BASELINE configs[3])
 for kind in ("bmw", "classroom"):
-    s = load_scene(scenes.build_scene(scenes.SceneSpec(kind, W, H, tris_per_side=24), os.path.join(tmp, kind)))
+    s = load_scene(scenes.build_scene(scenes.SceneSpec(kind, W, H, tris_per_side=24, uv_span=0.999),
+                                      os.path.join(tmp, kind)))
     base = RenderConfig(width=W, height=H, spp=SPP, n_cells=10_000_000, n_entries=10)
     render(s, base, ctx=ctx)
 
@@ -31,14 +37,14 @@ for kind in ("bmw", "classroom"):
 
     t_off, _ = med(base)
     rows = {"ms_no_cache": t_off}
-    for mo in (0, 2, 4, 8, 12):
+    for mo in (0, 3, 8, 12, 24):
         t_on, r = med(RenderConfig(**{**base.__dict__, "cache_enabled": True, "mip_offset": mo}))
         st = r.stats
         rows[f"mip_offset_{mo}"] = {
             "ms_cache": t_on, "relative_time_pct": 100 * t_on / t_off,
             "throughput_vs_no_cache_pct": 100 * t_off / t_on,
             "hit_rate": st.hit_rate, "lookups": st.lookups, "inserts_won": st.inserts_won,
-            "inserts_lost_full": st.inserts_lost_full}
+            "inserts_lost_full": st.inserts_lost_full, "device_ms": st.device_ms}
         print(kind, mo, json.dumps(rows[f"mip_offset_{mo}"]), flush=True)
     out[kind] = rows
 os.makedirs("gpurun_out", exist_ok=True)

@@ -122,3 +122,36 @@ def test_dropin_external_cache_follows_the_device(ctx, dropin, scene_dir, tmp_pa
     assert rows[1, 1] > rows[0, 1]          # the progressive render hits what the first stored
     assert rows[n, 2] > 0 and rows[n, 3] == rows[n, 2]     # fresh cache (same shape): starts empty
     assert rows[n + 1, 3] == rows[n + 1, 2] > 0            # another shape
+
+
+_MULTI_SCRIPT = r"""
+import ctypes as C, sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2305_07238_b200 import Context, RenderConfig, load_scene, render
+L = C.CDLL(sys.argv[2])
+L.dropin_render_scenes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_size_t]
+w, h, spp = 40, 30, 3
+rad = np.zeros((1, h, w, 3))
+err = C.create_string_buffer(512)
+arr = (C.c_char_p * 1)(sys.argv[3].encode())
+assert L.dropin_render_scenes(C.cast(arr, C.c_void_p), 1, w, h, spp, rad.ctypes.data_as(C.c_void_p), err, 512) == 0, err.value
+want = render(load_scene(sys.argv[3]), RenderConfig(width=w, height=h, spp=spp), ctx=Context(0)).frame.radiance
+assert np.array_equal(rad[0].view(np.uint64), want.view(np.uint64))
+print("multi ok")
+"""
+
+
+@pytest.mark.gpu
+def test_dropin_render_uses_every_listed_device(ctx, dropin, scene_dir):
+    """The drop-in's render() without an external cache runs on a context
+    over every GPU (MATCACHE_B200_DEVICES, default all visible): tiles dealt
+    to the devices, frames gathered. On this one-GPU box device 0 is listed
+    twice (device-copy gather instead of NCCL); the frame equals the
+    one-device render bit for bit. Own process: the drop-in's contexts are
+    created once per process."""
+    import sys
+    path = scenes.build_scene(scenes.SceneSpec("junkshop", 40, 30, tris_per_side=4), f"{scene_dir}/dropin_multi")
+    env = dict(os.environ, MATCACHE_B200_DEVICES="0,0")
+    r = subprocess.run([sys.executable, "-c", _MULTI_SCRIPT, _oracle.ROOT, DROPIN, path], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "multi ok" in r.stdout, r.stderr[-2000:]
