@@ -568,6 +568,21 @@ struct SceneView {
     const mcg_texture* textures;
     const float4* texels;
     float env[3];
+    // Per program, its first kAhead cache points in bracket order: (node_idx,
+    // flags | kAheadValid) -- what the look-ahead probe needs to build their
+    // descriptors before the material sort (mcg_render.cu, k_lookahead).
+    const uint2* ahead_cp;
+};
+
+// Cache points per material probed ahead of the shade (k_lookahead); their
+// results travel in one uint4 per path: x = hit bits (0..2) and the first
+// empty slot each probe saw (bits 8+8c, 0xff = cell full), y/z/w = payloads.
+constexpr uint32_t kAhead = 3;
+constexpr uint32_t kAheadValid = 0x100u;
+
+struct Ahead {
+    uint4 w;
+    bool on;
 };
 
 // Per-lane shading input (ShadingPoint, geom.hpp:49-56).
@@ -652,7 +667,8 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                                                 bool cache_on, int mip_offset, uint32_t slot,
                                                 const ShadeIn& sp, unsigned grp, const Stack& st,
                                                 const uint8_t* perm, uint32_t order_key,
-                                                const StoreQueue& q, VmCounters& cnt) {
+                                                const StoreQueue& q, VmCounters& cnt,
+                                                const Ahead& ah = Ahead{}) {
     const mcg_program prog = S.programs[slot];
     const uint4* code = reinterpret_cast<const uint4*>(S.code + prog.code_offset);
     const unsigned lane = threadIdx.x & 31u;
@@ -816,48 +832,63 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
             case MCG_OP_CACHE_LOOKUP: {  // stackvm.cpp:328-349
                 if (!cache_on) break;
                 // Brackets never nest, so every lane of the group is active here.
-                Desc desc{prog.material_id, arg, 0u, 0u, 0u};
-                if (flags & MCG_F_USES_UV) {
-                    desc.mip = mip_level(sp.g1x, sp.g1y, sp.g2x, sp.g2y, mip_offset);
-                    desc.tx = texel_index(sp.u, desc.mip);
-                    desc.ty = texel_index(sp.v, desc.mip);
-                }
-                uint64_t h;
-                hash_desc(desc, h, p_check);
-                const uint64_t cell = fast_mod(h, C.n_cells, C.magic);
-                p_cell = cell;
-                // Lanes asking for the same (cell, check) share one probe.
-                const unsigned long long key = (cell << 32) ^ p_check;
-                const unsigned peers = __match_any_sync(grp, key);
-                const int leader = __ffs(peers) - 1;
-#ifdef MCG_VM_GROUP_PROBE
-                // cooperative scan by the group (measured slower in the VM:
-                // 115 vs 96 registers, and few leaders per warp after the
-                // Morton sort -- profiles/README.md)
-                Probe pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, grp);
-#else
+                // Cache points probed ahead of the shade (k_lookahead) take
+                // that probe's result: the descriptor (and its hash, for the
+                // store) is only built when a lane of the group missed.
+                const uint32_t bi = w.z & 0xffffu;
+                const bool ahead = ah.on && bi < kAhead;
                 Probe pr{0u, -1, false};
-                if (static_cast<int>(lane) == leader) pr = probe_cell_t<MCG_VM_FIRST_PAIRS>(C, p_cell, p_check);
+                if (ahead) {
+                    pr.hit = ((ah.w.x >> bi) & 1u) != 0u;
+                    pr.payload = bi == 0u ? ah.w.y : (bi == 1u ? ah.w.z : ah.w.w);
+                    const uint32_t wb = (ah.w.x >> (8u + 8u * bi)) & 0xffu;
+                    pr.where = wb == 0xffu ? -1 : static_cast<int32_t>(wb);
+                }
+                if (!ahead || C.trace || !__all_sync(grp, pr.hit)) {
+                    Desc desc{prog.material_id, arg, 0u, 0u, 0u};
+                    if (flags & MCG_F_USES_UV) {
+                        desc.mip = mip_level(sp.g1x, sp.g1y, sp.g2x, sp.g2y, mip_offset);
+                        desc.tx = texel_index(sp.u, desc.mip);
+                        desc.ty = texel_index(sp.v, desc.mip);
+                    }
+                    uint64_t h;
+                    hash_desc(desc, h, p_check);
+                    const uint64_t cell = fast_mod(h, C.n_cells, C.magic);
+                    p_cell = cell;
+                    if (!ahead) {
+                        // Lanes asking for the same (cell, check) share one probe.
+                        const unsigned long long key = (cell << 32) ^ p_check;
+                        const unsigned peers = __match_any_sync(grp, key);
+                        const int leader = __ffs(peers) - 1;
+#ifdef MCG_VM_GROUP_PROBE
+                        // cooperative scan by the group (measured slower in the VM:
+                        // 115 vs 96 registers, and few leaders per warp after the
+                        // Morton sort -- profiles/README.md)
+                        pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, grp);
+#else
+                        if (static_cast<int>(lane) == leader) pr = probe_cell_t<MCG_VM_FIRST_PAIRS>(C, p_cell, p_check);
 #endif
-                pr.payload = __shfl_sync(grp, pr.payload, leader);
-                pr.where = __shfl_sync(grp, pr.where, leader);
-                pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;
-                ++cnt.lookups;
-                if (C.trace) {
-                    // descriptor log (SURVEY §8d trace replay): warp-aggregated append
-                    const int ldr = __ffs(grp) - 1;
-                    unsigned long long at = 0;
-                    if (static_cast<int>(lane) == ldr) at = atomicAdd(C.trace_count, __popc(grp));
-                    at = __shfl_sync(grp, at, ldr) + __popc(grp & ((1u << lane) - 1u));
-                    if (at < C.trace_cap) {
-                        uint32_t* t = C.trace + 5 * at;
-                        t[0] = desc.mat;
-                        t[1] = desc.node;
-                        t[2] = desc.mip;
-                        t[3] = desc.tx;
-                        t[4] = desc.ty;
+                        pr.payload = __shfl_sync(grp, pr.payload, leader);
+                        pr.where = __shfl_sync(grp, pr.where, leader);
+                        pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;
+                    }
+                    if (C.trace) {
+                        // descriptor log (SURVEY §8d trace replay): warp-aggregated append
+                        const int ldr = __ffs(grp) - 1;
+                        unsigned long long at = 0;
+                        if (static_cast<int>(lane) == ldr) at = atomicAdd(C.trace_count, __popc(grp));
+                        at = __shfl_sync(grp, at, ldr) + __popc(grp & ((1u << lane) - 1u));
+                        if (at < C.trace_cap) {
+                            uint32_t* t = C.trace + 5 * at;
+                            t[0] = desc.mat;
+                            t[1] = desc.node;
+                            t[2] = desc.mip;
+                            t[3] = desc.tx;
+                            t[4] = desc.ty;
+                        }
                     }
                 }
+                ++cnt.lookups;
                 p_where = pr.where;
                 if (pr.hit) {
                     const float3 v = decode_rgbe(pr.payload);

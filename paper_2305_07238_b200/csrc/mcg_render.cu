@@ -89,7 +89,10 @@ struct RenderView {
     uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
     uint32_t* vals;           // unsorted layout positions
     const uint32_t* skey;     // sorted keys: hits first, in material order
-    uint32_t key_shift;       // key = slot << key_shift | Morton code of the hit point
+    uint32_t key_shift;       // key = slot << key_shift | look-ahead hits << key_pat | Morton code
+    uint32_t key_pat;         // bits below the look-ahead hit pattern (the direction/Morton part)
+    uint32_t pat_mask;        // look-ahead hit bits that enter the key (0: none)
+    uint4* ahead;             // per path (at its layout position): look-ahead probe results (mcgd::kAhead)
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
     float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
     const uint32_t* order;    // sorted layout positions
@@ -154,7 +157,7 @@ __device__ __forceinline__ uint32_t sort_key(const RenderView& R, uint32_t slot,
             const V3 dv = (t * lx + bt * ly) + n * lz;
             oct = (dv.x < 0.0f ? 1u : 0u) | (dv.y < 0.0f ? 2u : 0u) | (dv.z < 0.0f ? 4u : 0u);
         }
-        const uint32_t mbits = R.key_shift - 3u;
+        const uint32_t mbits = R.key_pat - 3u;
         return (slot << R.key_shift) | (oct << mbits) | spread8(c[0]) | (spread8(c[1]) << 1) | (spread8(c[2]) << 2);
     }
     // Direction class of the cosine bounce this vertex will take: the
@@ -1878,6 +1881,57 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
 
+// Look-ahead probe of every live hit, before the material sort: the shading
+// point is rebuilt from the hit record exactly as k_shade will (shade_input),
+// the descriptors of the material's first kAhead cache points are built and
+// probed (cache.cpp:121-136), and the hit bits enter the sort key below the
+// material slot -- so the shade sees warps whose lanes all hit (the group
+// skips the subtree, Alg. 2) or all miss (the subtree runs with every lane
+// active), instead of a few misses holding a whole warp in the subtree.
+// Concurrent mode: a lookup observed before the vertex's stores is one of the
+// interleavings the reference's threads allow (slots are write-once, a hit
+// stays valid). Deterministic mode: the probe runs after the previous epoch's
+// ordered apply, so it reads the epoch-start table -- the same rule.
+__global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t* count) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (count ? *count : R.n_paths)) return;
+    const uint32_t key = R.keys[q];
+    const uint32_t slot = key_slot(R, key);
+    if (slot >= R.S.n_programs) return;
+    const mcg_program prog = R.S.programs[slot];
+    const uint32_t ncp = min(prog.cache_point_count, mcgd::kAhead);
+    uint4 out = make_uint4(0xffffff00u, 0u, 0u, 0u);
+    if (ncp) {
+        uint32_t slot_hit;
+        const mcgd::ShadeIn in = shade_input(R.S, R.ro[q], R.rd[q], R.hrec[q], slot_hit);
+        uint32_t pay[mcgd::kAhead] = {0u, 0u, 0u};
+#pragma unroll
+        for (uint32_t c = 0; c < mcgd::kAhead; ++c) {
+            if (c >= ncp) break;
+            const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
+            mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
+            if (cp.y & MCG_F_USES_UV) {
+                desc.mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
+                desc.tx = mcgd::texel_index(in.u, desc.mip);
+                desc.ty = mcgd::texel_index(in.v, desc.mip);
+            }
+            uint64_t h;
+            uint32_t check;
+            mcgd::hash_desc(desc, h, check);
+            const mcgd::Probe pr = mcgd::probe_cell_t<1>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
+            if (pr.hit) out.x |= 1u << c;
+            pay[c] = pr.payload;
+            const uint32_t wb = pr.where < 0 ? 0xffu : static_cast<uint32_t>(pr.where);
+            out.x = (out.x & ~(0xffu << (8u + 8u * c))) | (wb << (8u + 8u * c));
+        }
+        out.y = pay[0];
+        out.z = pay[1];
+        out.w = pay[2];
+    }
+    R.ahead[q] = out;
+    R.keys[q] = key | ((out.x & R.pat_mask) << R.key_pat);
+}
+
 // Finishes vertex b at sorted position i, after the shadow rays and the
 // continuation rays of the vertex: adds the visible light contributions in
 // light order (the oracle's summation order); the path ends (fin[pid]) at the
@@ -1967,8 +2021,10 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
+    mcgd::Ahead ah{make_uint4(0u, 0u, 0u, 0u), R.ahead != nullptr};
+    if (ah.on) ah.w = R.ahead[q];
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
-                                                          slot, in, grp, st, s_perm, okey, R.q, cnt);
+                                                          slot, in, grp, st, s_perm, okey, R.q, cnt, ah);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
     nee_bounce(R, i, pid, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, ro.w, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
@@ -2055,6 +2111,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint64_t launches0 = ctx->launches;
     const bool cache_on = P.cache_mode != MCG_CACHE_OFF;
     const bool deferred = P.cache_mode == MCG_CACHE_DETERMINISTIC;
+    const char* la_env = std::getenv("MCG_LOOKAHEAD");
+    const bool look_ahead_req = cache_on && D.max_cache_points > 0 && D.view.ahead_cp &&
+                                !(la_env && std::string(la_env) == "0");
 
     // Shard pixel list (16x16 tiles, tracer.hpp:19), built on the host and
     // uploaded once per (size, tiling, shard): a render call otherwise left
@@ -2131,13 +2190,16 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
     if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
-    const size_t lane_bytes = f4 * 10 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
+    const size_t lane_bytes = f4 * 11 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
     ctx->path_mem.ensure(lane_bytes);
     for (int l = 1; l < lanes; ++l) ctx->lane_path[l].ensure(lane_bytes);
     RenderView R{};
     R.S = D.view;
     if (cache && cache->world > 1 && !cache->stripes) fail(MCG_ERR_INVALID_ARGUMENT, "striped table: attach the stripes first");
     R.C = cache ? cache->view() : mcgd::CacheView{nullptr, nullptr, 1, ~0ull, 1, 1, 1, nullptr, nullptr, nullptr, 0};
+    // (a descriptor trace records lookups in the VM's order: no look-ahead
+    // then; the where-hint packs into 8 bits)
+    const bool look_ahead = look_ahead_req && R.C.trace == nullptr && R.C.n_entries < 255u;
     R.cache_on = cache_on ? 1 : 0;
     R.mip_offset = P.mip_offset;
     camera_setup(D.cam, W, H, R.cam);
@@ -2159,7 +2221,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         V.L2 = V.thr2 + max_paths;
         V.hrec = V.L2 + max_paths;
         V.fin = V.hrec + max_paths;
-        V.sro = V.fin + max_paths;
+        V.ahead = look_ahead ? reinterpret_cast<uint4*>(V.fin + max_paths) : nullptr;
+        V.sro = V.fin + 2 * max_paths;
         V.srd = V.sro + n_shadow;
         V.scon = V.srd + n_shadow;
         uint32_t* u32 = reinterpret_cast<uint32_t*>(V.scon + n_shadow);
@@ -2219,6 +2282,15 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const float ext = D.root_hi[a] - D.root_lo[a];
         R.box_lo[a] = D.root_lo[a];
         R.box_scale[a] = ext > 0.0f ? (static_cast<float>(1 << mb) - 0.001f) / ext : 0.0f;
+    }
+    // Look-ahead probes (MCG_LOOKAHEAD=0: off): the hit bits of the first
+    // cache points (up to 2 key bits) go between the slot and the Morton part.
+    R.key_pat = R.key_shift;
+    R.pat_mask = 0u;
+    if (look_ahead && R.key_shift) {
+        const uint32_t pb = std::min<uint32_t>(2u, std::min(mcgd::kAhead, D.max_cache_points));
+        R.pat_mask = (1u << pb) - 1u;
+        R.key_shift += pb;
     }
     const int key_bits = static_cast<int>(R.key_shift) + slot_bits;
     // Shadow rays over the SAH tree of the reference's leaves (exact for
@@ -2298,6 +2370,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
             ls.done();
         }
+        if (look_ahead) {
+            LaunchScope ls(ctx, "lookahead", 0.0, sm);
+            k_lookahead<<<grid, 256, 0, sm>>>(R, nullptr);
+            ls.done();
+        }
         for (int b = 0; b <= P.max_bounces; ++b) {
             // Stable radix sort of (key -> layout position): hits in
             // material order first, paths without a hit (key n_programs) last.
@@ -2355,6 +2432,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 LaunchScope ls(ctx, "trace_closest", 0.0, sm);
                 k_trace_closest_ww<<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, sm>>>(
                     R, R.shadow_count + 2, b + 1);
+                ls.done();
+            }
+            if (b < P.max_bounces && look_ahead) {
+                LaunchScope ls(ctx, "lookahead", 0.0, sm);
+                k_lookahead<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
                 ls.done();
             }
             if (fork) cuda_check(cudaStreamWaitEvent(sm, lane_join[l], 0), "wait");

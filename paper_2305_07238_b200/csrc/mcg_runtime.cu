@@ -1557,7 +1557,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         if (s != MCG_OK) fail(s, mcg_last_error());
         DeviceScene& D = ctx->scene;
         D.reset();
-        if (D.bufs.size() < 19) D.bufs.resize(19);
+        if (D.bufs.size() < 20) D.bufs.resize(20);
         auto up = [&](int k, const void* p, size_t bytes) -> const void* {
             D.bufs[k].ensure(std::max<size_t>(bytes, 16));
             if (bytes) cuda_check(cudaMemcpyAsync(D.bufs[k].p, p, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D scene");
@@ -1710,6 +1710,21 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         // one spare word past the last program: the VM fetches pc + 1 ahead
         D.bufs[7].ensure((f.n_code + 1) * sizeof(mcg_insn));
         v.code = static_cast<const mcg_insn*>(up(7, f.code, f.n_code * sizeof(mcg_insn)));
+        // The look-ahead table: each program's first kAhead cache points
+        // (CacheLookup node and uses_uv flag, in bracket order).
+        {
+            std::vector<uint2> acp(static_cast<size_t>(f.n_programs) * mcgd::kAhead, make_uint2(0u, 0u));
+            for (uint32_t i = 0; i < f.n_programs; ++i) {
+                const mcg_program& pr = f.programs[i];
+                for (uint32_t c = 0; c < pr.code_len; ++c) {
+                    const mcg_insn& in = f.code[pr.code_offset + c];
+                    if (in.op == MCG_OP_CACHE_LOOKUP && in.bracket < mcgd::kAhead) {
+                        acp[i * mcgd::kAhead + in.bracket] = make_uint2(in.arg, (in.flags & MCG_F_USES_UV) | mcgd::kAheadValid);
+                    }
+                }
+            }
+            v.ahead_cp = static_cast<const uint2*>(up(19, acp.data(), acp.size() * sizeof(uint2)));
+        }
         v.consts = static_cast<const mcg_const*>(up(8, f.consts, f.n_consts * sizeof(mcg_const)));
         v.noise = static_cast<const mcg_noise*>(up(9, f.noise, f.n_noise * sizeof(mcg_noise)));
         v.ramps = static_cast<const mcg_ramp*>(up(10, f.ramps, f.n_ramps * sizeof(mcg_ramp)));

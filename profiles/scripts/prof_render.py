@@ -15,7 +15,7 @@ cache = (sys.argv[2] != "0") if len(sys.argv) > 2 else True
 ctx = Context(0)
 scene = load_scene(bench.make_scene(tempfile.mkdtemp()))
 cfg = RenderConfig(width=bench.W, height=bench.H, spp=spp, cache_enabled=cache,
-                   n_cells=bench.N_CELLS, n_entries=bench.N_ENTRIES)
+                   n_cells=bench.N_CELLS, n_entries=bench.N_ENTRIES, mip_offset=bench.MIP_OFFSET)
 for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     r = render(scene, cfg, ctx=ctx)
 print("ok", r.stats.shading_points, r.stats.hits)

@@ -55,19 +55,20 @@ def test_bench_band_concurrent_rmse_within_reference(ctx, ref, scene_dir, lanes,
     sample per pass (what 1920x1080 resolves to), passes alternating on two
     stream lanes (MCG_LANES=2, the default) -- on the band of tiles the CPU
     baseline renders (contiguous tiles 8/16 of the 1080p frame, ~130K
-    pixels), 32 spp: 32 passes in flight two at a time."""
+    pixels), 32 spp: 32 passes in flight two at a time. Medians of 5 GPU
+    and 3 reference renders (the first-insert race makes both random)."""
     import bench
     monkeypatch.setenv("MCG_LANES", lanes)
     path = bench.make_scene(scene_dir + "/bench_band")
     s = load_scene(path)
     W, H, spp = bench.W, bench.H, 32
     band = dict(width=W, height=H, spp=spp, n_cells=NC, n_entries=NE, shard_rank=bench.CPU_BAND,
-                shard_count=bench.CPU_BANDS, shard_mode=1, samples_per_pass=1)
+                shard_count=bench.CPU_BANDS, shard_mode=1, samples_per_pass=1, mip_offset=bench.MIP_OFFSET)
     off = render(s, RenderConfig(**band), ctx=ctx)
     mask = off.frame.samples > 0
     off_img = off.frame.radiance_image()[mask]
     gpu = []
-    for _ in range(3):
+    for _ in range(5):
         r = render(s, RenderConfig(cache_enabled=True, **band), ctx=ctx)
         check_invariants(r, off)
         gpu.append(errors(r.frame.radiance_image()[mask], off_img))
