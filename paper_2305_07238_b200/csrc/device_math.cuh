@@ -226,17 +226,15 @@ __device__ __forceinline__ float fade(float t) {
     return t * t * t * (t * (t * 6.0f - 15.0f) + 10.0f);
 }
 __device__ __forceinline__ float lerp(float a, float b, float t) { return a + (b - a) * t; }
+// grad2 (noise.cpp): the 8 gradients as selects, not an 8-way switch (the
+// hash is per lane, so a switch diverges inside the FBM loop). Same values
+// bit for bit: x - y is x + (-y) in IEEE arithmetic, and +-dx / +-dy are
+// returned unrounded as the switch returns them.
 __device__ __forceinline__ float grad2(int h, float dx, float dy) {
-    switch (h & 7) {
-        case 0: return dx + dy;
-        case 1: return -dx + dy;
-        case 2: return dx - dy;
-        case 3: return -dx - dy;
-        case 4: return dx;
-        case 5: return -dx;
-        case 6: return dy;
-        default: return -dy;
-    }
+    const float xs = (h & 1) ? -dx : dx;
+    const float ys = (h & 2) ? -dy : dy;
+    const float axis = (h & 2) ? ((h & 1) ? -dy : dy) : xs;   // h = 4, 5: +-dx; 6, 7: +-dy
+    return (h & 4) ? axis : xs + ys;
 }
 
 // perlin2 (noise.cpp:53-75); perm is the 256-entry table staged in shared memory.

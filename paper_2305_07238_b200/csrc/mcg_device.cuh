@@ -932,9 +932,15 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                         // One CAS per distinct (cell, check) in the warp; the
                         // others saw the same empty slot and now find it taken
                         // by their own key (AlreadyPresent).
+                        // The group's CAS carries the value of a lane picked by
+                        // a hash of its path key, not the lowest lane: lanes sit
+                        // in Morton order, so "lowest" would always store the
+                        // value at one corner of the texel (a biased first insert).
                         const unsigned long long key = (p_cell << 32) ^ p_check;
                         const unsigned peers = __match_any_sync(m, key);
-                        const int leader = __ffs(peers) - 1;
+                        const uint32_t rk = (order_key >> 6) * 0x9E3779B1u;
+                        const uint32_t rmin = __reduce_min_sync(peers, rk);
+                        const int leader = __ffs(__ballot_sync(peers, rk == rmin) & peers) - 1;
                         int res = MCG_INSERT_ALREADY_PRESENT;
                         if (static_cast<int>(lane) == leader) {
                             int32_t at = -1;

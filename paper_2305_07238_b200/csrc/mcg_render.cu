@@ -93,6 +93,7 @@ struct RenderView {
     uint32_t key_pat;         // bits below the look-ahead hit pattern (the direction/Morton part)
     uint32_t pat_mask;        // look-ahead hit bits that enter the key (0: none)
     uint4* ahead;             // per path (at its layout position): look-ahead probe results (mcgd::kAhead)
+    uint32_t shade_perm;      // k_shade block order: block b runs sorted block (b * shade_perm) % grid (1 = in order)
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
     float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
     const uint32_t* order;    // sorted layout positions
@@ -1992,7 +1993,13 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     __shared__ uint8_t s_perm[256];
     mcgd::stage_perm(s_perm);
     __syncthreads();
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    // Blocks visit the sorted list in a scattered order (concurrent mode):
+    // the paths of one texel are contiguous there (Morton order), and the
+    // first block to store wins the texel -- in sorted order that would be
+    // the path at the texel's spatial corner every time, a biased first
+    // insert (larger cached-vs-uncached error than the reference's threads).
+    const uint32_t blk = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * R.shade_perm) % gridDim.x);
+    const uint32_t i = blk * blockDim.x + threadIdx.x;
     const uint32_t slot = i < R.n_paths ? key_slot(R, skey[i]) : R.S.n_programs;
     const bool valid = slot < R.S.n_programs;
     const unsigned live = __ballot_sync(mcgd::kFull, valid);
@@ -2074,6 +2081,16 @@ __global__ void __launch_bounds__(256) k_accumulate(RenderView R, uint32_t k) {
     }
 }
 
+// An integer near frac * n that is coprime to n (b -> b * m mod n is then a
+// permutation of [0, n)).
+uint32_t coprime_near(uint32_t n, double frac) {
+    if (n <= 2) return 1u;
+    uint32_t m = std::max<uint32_t>(1u, static_cast<uint32_t>(n * frac)) | 1u;
+    auto gcd = [](uint32_t a, uint32_t b) { while (b) { const uint32_t t = a % b; a = b; b = t; } return a; };
+    while (gcd(m, n) != 1u) m += 2u;
+    return m % n ? m % n : 1u;
+}
+
 bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
     if (p.shard_count <= 1) return true;
     if (p.shard_mode == MCG_SHARD_INTERLEAVED) return tile % p.shard_count == p.shard_rank;
@@ -2111,6 +2128,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint64_t launches0 = ctx->launches;
     const bool cache_on = P.cache_mode != MCG_CACHE_OFF;
     const bool deferred = P.cache_mode == MCG_CACHE_DETERMINISTIC;
+    const char* sc_env = std::getenv("MCG_SHADE_SCATTER");
+    const bool scatter = !(sc_env && std::string(sc_env) == "0");
     const char* la_env = std::getenv("MCG_LOOKAHEAD");
     const bool look_ahead_req = cache_on && D.max_cache_points > 0 && D.view.ahead_cp &&
                                 !(la_env && std::string(la_env) == "0");
@@ -2386,6 +2405,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             {
                 LaunchScope ls(ctx, "shade", 0.0, sm);
                 const unsigned sg = grid_for(R.n_paths, block);
+                R.shade_perm = scatter && !deferred ? coprime_near(sg, 0.6180339887) : 1u;
                 const uint32_t wh32 = static_cast<uint32_t>(wh);
                 // deterministic mode: stores are queued and applied after the
                 // shade (NEE and the bounce need none of them)
