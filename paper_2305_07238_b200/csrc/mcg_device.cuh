@@ -656,6 +656,9 @@ struct VmResult {
 // kDeferred: deterministic mode -- lookups read the epoch-start table and
 // stores are queued with an order key (applied later, lowest key first);
 // otherwise stores CAS immediately (concurrent mode).
+#ifndef MCG_VM_REPROBE
+#define MCG_VM_REPROBE 1   // concurrent mode: a look-ahead miss probes again at CacheLookup
+#endif
 template <bool kDeferred>
 // MCG_VM_PREFETCH=1 (experiment, off): fetch the next instruction word
 // while the current one executes; neutral (636.6-637.7 vs 636.4-638.3 ms per
@@ -855,22 +858,31 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                     hash_desc(desc, h, p_check);
                     const uint64_t cell = fast_mod(h, C.n_cells, C.magic);
                     p_cell = cell;
-                    if (!ahead) {
+                    // Probe now: without a look-ahead result, or (concurrent
+                    // mode) again for a look-ahead miss -- a store that landed
+                    // since then is a hit, as it would be for the reference's
+                    // lookup at this point. (Deterministic mode reads the
+                    // epoch-start table, which the look-ahead already saw.)
+                    const bool probe_now = !ahead || (MCG_VM_REPROBE && !kDeferred && !pr.hit);
+                    const unsigned pm = __ballot_sync(grp, probe_now);
+                    if (probe_now) {
                         // Lanes asking for the same (cell, check) share one probe.
                         const unsigned long long key = (cell << 32) ^ p_check;
-                        const unsigned peers = __match_any_sync(grp, key);
+                        const unsigned peers = __match_any_sync(pm, key);
                         const int leader = __ffs(peers) - 1;
 #ifdef MCG_VM_GROUP_PROBE
                         // cooperative scan by the group (measured slower in the VM:
                         // 115 vs 96 registers, and few leaders per warp after the
                         // Morton sort -- profiles/README.md)
-                        pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, grp);
+                        pr = probe_group16(C, p_cell, p_check, static_cast<int>(lane) == leader, pm);
 #else
-                        if (static_cast<int>(lane) == leader) pr = probe_cell_t<MCG_VM_FIRST_PAIRS>(C, p_cell, p_check);
+                        Probe np{0u, -1, false};
+                        if (static_cast<int>(lane) == leader) np = probe_cell_t<MCG_VM_FIRST_PAIRS>(C, p_cell, p_check);
+                        pr = np;
 #endif
-                        pr.payload = __shfl_sync(grp, pr.payload, leader);
-                        pr.where = __shfl_sync(grp, pr.where, leader);
-                        pr.hit = __shfl_sync(grp, static_cast<int>(pr.hit), leader) != 0;
+                        pr.payload = __shfl_sync(peers, pr.payload, leader);
+                        pr.where = __shfl_sync(peers, pr.where, leader);
+                        pr.hit = __shfl_sync(peers, static_cast<int>(pr.hit), leader) != 0;
                     }
                     if (C.trace) {
                         // descriptor log (SURVEY §8d trace replay): warp-aggregated append

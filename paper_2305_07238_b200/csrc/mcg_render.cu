@@ -93,6 +93,7 @@ struct RenderView {
     uint32_t key_pat;         // bits below the look-ahead hit pattern (the direction/Morton part)
     uint32_t pat_mask;        // look-ahead hit bits that enter the key (0: none)
     uint4* ahead;             // per path (at its layout position): look-ahead probe results (mcgd::kAhead)
+    uint32_t ahead_fused;     // 1: the trace kernels run the look-ahead probe (no k_lookahead launch)
     uint32_t shade_perm;      // k_shade block order: block b runs sorted block (b * shade_perm) % grid (1 = in order)
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
     float box_lo[3], box_scale[3];  // scene bounds -> 8-bit grid for the Morton code
@@ -525,6 +526,42 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
     d = mcgd::normalize((fwd + right * a) + up * bq);
 }
 
+// The look-ahead probe of the live hit at layout position q with shading
+// point `in` (k_lookahead below): its material's first kAhead cache points,
+// results to R.ahead[q]; returns the sort key with the hit bits added.
+__device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, uint32_t key,
+                                               const mcgd::ShadeIn& in) {
+    const uint32_t slot = key_slot(R, key);
+    const mcg_program prog = R.S.programs[slot];
+    const uint32_t ncp = min(prog.cache_point_count, mcgd::kAhead);
+    uint4 out = make_uint4(0xffffff00u, 0u, 0u, 0u);
+    uint32_t pay[mcgd::kAhead] = {0u, 0u, 0u};
+#pragma unroll
+    for (uint32_t c = 0; c < mcgd::kAhead; ++c) {
+        if (c >= ncp) break;
+        const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
+        mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
+        if (cp.y & MCG_F_USES_UV) {
+            desc.mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
+            desc.tx = mcgd::texel_index(in.u, desc.mip);
+            desc.ty = mcgd::texel_index(in.v, desc.mip);
+        }
+        uint64_t h;
+        uint32_t check;
+        mcgd::hash_desc(desc, h, check);
+        const mcgd::Probe pr = mcgd::probe_cell_t<1>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
+        if (pr.hit) out.x |= 1u << c;
+        pay[c] = pr.payload;
+        const uint32_t wb = pr.where < 0 ? 0xffu : static_cast<uint32_t>(pr.where);
+        out.x = (out.x & ~(0xffu << (8u + 8u * c))) | (wb << (8u + 8u * c));
+    }
+    out.y = pay[0];
+    out.z = pay[1];
+    out.w = pay[2];
+    R.ahead[q] = out;
+    return key | ((out.x & R.pat_mask) << R.key_pat);
+}
+
 // Closest hit of the path at layout position q (path id pid): the hit
 // record (primitive, t, barycentrics: 16 bytes) at q, the propagated cone
 // width into ro.w, and the sort key; on a miss the path ends: radiance +
@@ -547,7 +584,15 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     R.hrec[q] = make_float4(__uint_as_float(prim), t, b1, b2);
     const uint32_t slot_j = pid / R.n_pix;
     const uint64_t rkey = mcgd::path_key(R.seed, R.pix[pid - slot_j * R.n_pix], R.sample0 + slot_j);
-    return sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+    const uint32_t key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
+    if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
+    // the look-ahead probe right here (the shading point is shade_input's:
+    // the same surface and the footprint of the propagated cone)
+    float2 g1, g2;
+    mcgd::footprint(ro.w, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+    const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
+                           s.u, s.v, g1.x, g1.y, g2.x, g2.y};
+    return look_ahead(R, q, key, in);
 }
 
 // The shading point of a hit record (ShadingPoint, geom.hpp:49-56): the
@@ -1897,40 +1942,10 @@ __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t*
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (count ? *count : R.n_paths)) return;
     const uint32_t key = R.keys[q];
-    const uint32_t slot = key_slot(R, key);
-    if (slot >= R.S.n_programs) return;
-    const mcg_program prog = R.S.programs[slot];
-    const uint32_t ncp = min(prog.cache_point_count, mcgd::kAhead);
-    uint4 out = make_uint4(0xffffff00u, 0u, 0u, 0u);
-    if (ncp) {
-        uint32_t slot_hit;
-        const mcgd::ShadeIn in = shade_input(R.S, R.ro[q], R.rd[q], R.hrec[q], slot_hit);
-        uint32_t pay[mcgd::kAhead] = {0u, 0u, 0u};
-#pragma unroll
-        for (uint32_t c = 0; c < mcgd::kAhead; ++c) {
-            if (c >= ncp) break;
-            const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
-            mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
-            if (cp.y & MCG_F_USES_UV) {
-                desc.mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
-                desc.tx = mcgd::texel_index(in.u, desc.mip);
-                desc.ty = mcgd::texel_index(in.v, desc.mip);
-            }
-            uint64_t h;
-            uint32_t check;
-            mcgd::hash_desc(desc, h, check);
-            const mcgd::Probe pr = mcgd::probe_cell_t<1>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
-            if (pr.hit) out.x |= 1u << c;
-            pay[c] = pr.payload;
-            const uint32_t wb = pr.where < 0 ? 0xffu : static_cast<uint32_t>(pr.where);
-            out.x = (out.x & ~(0xffu << (8u + 8u * c))) | (wb << (8u + 8u * c));
-        }
-        out.y = pay[0];
-        out.z = pay[1];
-        out.w = pay[2];
-    }
-    R.ahead[q] = out;
-    R.keys[q] = key | ((out.x & R.pat_mask) << R.key_pat);
+    if (key_slot(R, key) >= R.S.n_programs) return;
+    uint32_t slot_hit;
+    const mcgd::ShadeIn in = shade_input(R.S, R.ro[q], R.rd[q], R.hrec[q], slot_hit);
+    R.keys[q] = look_ahead(R, q, key, in);
 }
 
 // Finishes vertex b at sorted position i, after the shadow rays and the
@@ -2219,6 +2234,9 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     // (a descriptor trace records lookups in the VM's order: no look-ahead
     // then; the where-hint packs into 8 bits)
     const bool look_ahead = look_ahead_req && R.C.trace == nullptr && R.C.n_entries < 255u;
+    // MCG_LOOKAHEAD=2: the probe as its own kernel after each trace (else
+    // fused into the trace kernels' hit-record epilogue)
+    R.ahead_fused = look_ahead && !(la_env && std::string(la_env) == "2") ? 1u : 0u;
     R.cache_on = cache_on ? 1 : 0;
     R.mip_offset = P.mip_offset;
     camera_setup(D.cam, W, H, R.cam);
@@ -2389,7 +2407,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
             ls.done();
         }
-        if (look_ahead) {
+        if (look_ahead && !R.ahead_fused) {
             LaunchScope ls(ctx, "lookahead", 0.0, sm);
             k_lookahead<<<grid, 256, 0, sm>>>(R, nullptr);
             ls.done();
@@ -2454,7 +2472,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                     R, R.shadow_count + 2, b + 1);
                 ls.done();
             }
-            if (b < P.max_bounces && look_ahead) {
+            if (b < P.max_bounces && look_ahead && !R.ahead_fused) {
                 LaunchScope ls(ctx, "lookahead", 0.0, sm);
                 k_lookahead<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
                 ls.done();
