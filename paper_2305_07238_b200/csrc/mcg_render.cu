@@ -1990,12 +1990,13 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 // Material evaluation of every live hit, in sorted (material, Morton)
 // order, then NEE and the bounce; the path's state moves from its old layout
 // position q = order[i] to i in the next layout.
-// (128, 4): the VM keeps its natural 110 registers. With two passes in
-// flight the (128, 5) cap (102 registers, from the one-lane tuning) costs
-// more than the extra resident block gains: same call 636-638 vs 647 ms
-// per bench render (MINB 2/3 compile to the same 110 registers).
+// (128, 5): 96 registers (a few spill slots) and five resident blocks. With
+// the look-ahead sort the subtrees run with full warps and the kernel is
+// bound by dependent-latency stalls ("wait"), so the extra resident warps pay:
+// 795.7 vs 784.7 ms per bench render (MINB 4: 115 registers; MINB 6: 80
+// registers with 156 bytes of spills, 794 ms).
 #ifndef MCG_SHADE_MINB
-#define MCG_SHADE_MINB 4
+#define MCG_SHADE_MINB 5
 #endif
 template <bool kDeferred>
 #ifndef MCG_SHADE_BLOCK
