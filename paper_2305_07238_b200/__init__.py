@@ -601,6 +601,12 @@ class RenderStats:
     paths: int = 0
     device_ms: float = 0.0       # CUDA-event time of the render on the context's stream
     shadow_occluded: int = 0     # shadow rays that found an occluder
+    bvh_nodes: int = 0           # traversal work: closest hit + shadow rays
+    prims_tested: int = 0
+    bvh_nodes_shadow: int = 0
+    prims_tested_shadow: int = 0
+    closest_rays: int = 0
+    tex_samples: int = 0
 
 
 @dataclass
@@ -634,7 +640,8 @@ def render(scene: Scene, config: RenderConfig, external_cache: Optional[Material
                         (st.hits / st.lookups) if st.lookups else 0.0, st.inserts_won,
                         st.inserts_lost_full, st.stores_attempted, st.instructions_executed,
                         [int(x) for x in hps], st.shading_points, st.shadow_rays, st.paths,
-                        st.device_ms, st.shadow_occluded)
+                        st.device_ms, st.shadow_occluded, st.bvh_nodes, st.prims_tested,
+                        st.bvh_nodes_shadow, st.prims_tested_shadow, st.closest_rays, st.tex_samples)
     return RenderResult(fb, stats)
 
 

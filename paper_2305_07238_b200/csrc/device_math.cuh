@@ -7,10 +7,33 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 #include "../../include/mcg.h"
 
 namespace mcgd {
+
+// Checked builds (-DMCG_CHECKS=1; profiles/scripts/checked.sh): device-side
+// bounds checks on every index the hot path computes -- the stand-in for
+// compute-sanitizer, which this GPU pool does not allow. A failed check
+// prints where and traps, so the launch (and the test driving it) fails.
+#ifndef MCG_CHECKS
+#define MCG_CHECKS 0
+#endif
+#if MCG_CHECKS
+#define MCG_CHECK(cond)                                                                        \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("MCG_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,    \
+                   __LINE__, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));     \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define MCG_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 constexpr int kMaxMip = 24;                       // raycone.hpp:18
 constexpr float kTwoPi = 6.28318530717958647692f; // value.hpp:126
@@ -292,6 +315,8 @@ __device__ __forceinline__ float3 bilinear(const mcg_texture& t, const float4* t
     const int y0 = wrap_index(static_cast<int>(fy), t.height, clamp);
     const int y1 = wrap_index(static_cast<int>(fy) + 1, t.height, clamp);
     const float4* px = texels + t.offset;
+    MCG_CHECK(x0 >= 0 && x0 < t.width && x1 >= 0 && x1 < t.width && y0 >= 0 && y0 < t.height && y1 >= 0 &&
+              y1 < t.height);
     const float4 c00 = __ldg(px + static_cast<size_t>(y0) * t.width + x0);
     const float4 c10 = __ldg(px + static_cast<size_t>(y0) * t.width + x1);
     const float4 c01 = __ldg(px + static_cast<size_t>(y1) * t.width + x0);

@@ -155,6 +155,7 @@ struct mcg_ctx {
     std::vector<mcg_ctx*> peers;
     std::vector<void*> nccl_comms;
     bool devices_distinct = true;
+    mcg::DevMem build_mem;    // device BVH build scratch (mcg_build.cu)
     mcg::DevMem gather_tmp;   // device-copy gather (a device listed twice)
 };
 
@@ -211,6 +212,12 @@ void sort_pairs_u64(mcg_ctx* ctx, const unsigned long long* keys_in, unsigned lo
 void sort_pairs_u32(mcg_ctx* ctx, const uint32_t* keys_in, uint32_t* keys_out,
                     const uint32_t* vals_in, uint32_t* vals_out, size_t n, int end_bit,
                     cudaStream_t stream = nullptr, DevMem* temp = nullptr);
+
+// The any-hit tree over the reference BVH's leaves (build_shadow_tree's
+// binned SAH, collapsed to `width`-wide nodes), built on the device
+// (mcg_build.cu).
+std::vector<mcg_bvh_node> build_shadow_tree_device(mcg_ctx* ctx, const std::vector<mcg_bvh_node>& leaves,
+                                                   int width, int32_t& root_a, int32_t& root_b);
 
 // Applies sorted (cell << order_bits | order) -> (check << 32 | payload)
 // records cell by cell in order (the deterministic-insert rule). Outcomes are

@@ -60,6 +60,7 @@ __device__ __forceinline__ void log_insert(const CacheView& c, uint32_t mat, uin
 // A striped table keeps cell c on stripe c % world at local cell c / world,
 // so every device sees the same logical table.
 __device__ __forceinline__ uint64_t* head_words(const CacheView& c, uint64_t cell) {
+    MCG_CHECK(cell < c.n_cells);
     if (c.world <= 1u) return c.slots + cell * c.head_n;
     return c.stripes[2 * (cell % c.world)] + (cell / c.world) * c.head_n;
 }
@@ -69,6 +70,7 @@ __device__ __forceinline__ uint64_t* tail_words(const CacheView& c, uint64_t cel
     return c.stripes[2 * (cell % c.world) + 1] + (cell / c.world) * tn;
 }
 __device__ __forceinline__ uint64_t* slot_ptr(const CacheView& c, uint64_t cell, uint32_t e) {
+    MCG_CHECK(cell < c.n_cells && e < c.n_entries);
     return e < c.head_n ? head_words(c, cell) + e : tail_words(c, cell) + (e - c.head_n);
 }
 // Result of scanning one cell as lookup() does (cache.cpp:121-136): a match,
@@ -611,7 +613,9 @@ struct Stack {
     float* z;
     int stride;
     int tid;
+    int limit;   // the program's max_stack slots (checked builds)
     __device__ __forceinline__ void put(int s, float a, float b, float c, bool scalar) const {
+        MCG_CHECK(s >= 0 && s < limit);
         x[s * stride + tid] = a;
         if (!scalar) {
             y[s * stride + tid] = b;
@@ -619,6 +623,7 @@ struct Stack {
         }
     }
     __device__ __forceinline__ float3 get(int s, bool scalar) const {
+        MCG_CHECK(s >= 0 && s < limit);
         const float a = x[s * stride + tid];
         if (scalar) return make_float3(a, a, a);
         return make_float3(a, y[s * stride + tid], z[s * stride + tid]);
@@ -696,6 +701,7 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
         const uint4 w = w_next;
         w_next = __ldg(code + pc + 1);
 #else
+        MCG_CHECK(static_cast<uint32_t>(pc) < prog.code_len);
         const uint4 w = __ldg(code + pc);
 #endif
         const uint8_t op = static_cast<uint8_t>(w.x & 0xffu);
@@ -863,7 +869,10 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                     // since then is a hit, as it would be for the reference's
                     // lookup at this point. (Deterministic mode reads the
                     // epoch-start table, which the look-ahead already saw.)
-                    const bool probe_now = !ahead || (MCG_VM_REPROBE && !kDeferred && !pr.hit);
+                    // (A look-ahead that found the cell full without the key is
+                    // final: slots are write-once, so the key can never enter
+                    // that cell -- no second probe.)
+                    const bool probe_now = !ahead || (MCG_VM_REPROBE && !kDeferred && !pr.hit && pr.where >= 0);
                     const unsigned pm = __ballot_sync(grp, probe_now);
                     if (probe_now) {
                         // Lanes asking for the same (cell, check) share one probe.

@@ -54,6 +54,22 @@ enum {
     kStatCount = 17
 };
 
+// A path's ray record (64 bytes, one DRAM access when gathered): ro.w is the
+// cone width at the ray origin (each reader propagates it over the hit
+// distance itself, raycone.cpp:15-18, with the same arithmetic); hrec is the
+// closest hit (primitive as uint bits, t, b1, b2) -- k_shade rebuilds the
+// shading point from it (surface + footprint, shade_input); ahead holds the
+// look-ahead probe results (mcgd::kAhead).
+struct __align__(64) PathRay {
+    float4 ro, rd, hrec;
+    uint4 ahead;
+};
+// A path's value record (32 bytes): throughput.rgb + nodes_found (uint bits),
+// radiance.rgb + path id (uint bits: pass slot j * n_pix + shard pixel index).
+struct __align__(32) PathVal {
+    float4 thr, L;
+};
+
 struct RenderView {
     mcgd::SceneView S;
     mcgd::CacheView C;
@@ -73,26 +89,22 @@ struct RenderView {
     // Path state at the current layout (index = position in the last sort
     // output; the primary pass starts at pid order) and the next layout,
     // written by k_shade at the sorted position.
-    float4* ro;               // origin.xyz, cone width
-    float4* rd;               // direction.xyz, cone spread
-    float4* thr;              // throughput.rgb, nodes_found (uint bits)
-    float4* L;                // radiance.rgb
-    uint32_t* pid;            // path id: pass slot j * n_pix + shard pixel index
-    float4* ro2;
-    float4* rd2;
-    float4* thr2;
-    float4* L2;
-    uint32_t* pid2;
+    // Path state in two records per layout position, so the shade's gather
+    // is two random accesses (a 64-byte and a 32-byte record) instead of one
+    // per field, while every other kernel reads and writes whole records:
+    PathRay* pa;              // ray (origin, cone width at the origin; direction, spread), closest
+                              // hit and look-ahead results -- the trace kernels' record
+    PathVal* pb;              // throughput + hits, radiance + path id -- the resolve's record
+    PathRay* pa2;             // the same at the next layout (written by k_shade)
+    PathVal* pb2;
     float4* fin;              // by path id: final radiance.rgb, nodes_found (uint bits)
-    float4* hrec;             // closest hit: primitive (uint bits), t, b1, b2 -- k_shade rebuilds
-                              // the shading record from it (surface + footprint, same arithmetic)
     uint32_t* keys;           // unsorted (material slot | n_programs = no hit)
     uint32_t* vals;           // unsorted layout positions
     const uint32_t* skey;     // sorted keys: hits first, in material order
     uint32_t key_shift;       // key = slot << key_shift | look-ahead hits << key_pat | Morton code
     uint32_t key_pat;         // bits below the look-ahead hit pattern (the direction/Morton part)
     uint32_t pat_mask;        // look-ahead hit bits that enter the key (0: none)
-    uint4* ahead;             // per path (at its layout position): look-ahead probe results (mcgd::kAhead)
+    uint32_t ahead_on;        // look-ahead probes: results in PathRay::ahead
     uint32_t ahead_fused;     // 1: the trace kernels run the look-ahead probe (no k_lookahead launch)
     uint32_t shade_perm;      // k_shade block order: block b runs sorted block (b * shade_perm) % grid (1 = in order)
     uint32_t key_dir;         // 1: a 5-bit direction class of the next bounce above the Morton code
@@ -558,7 +570,7 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
     out.y = pay[0];
     out.z = pay[1];
     out.w = pay[2];
-    R.ahead[q] = out;
+    R.pa[q].ahead = out;
     return key | ((out.x & R.pat_mask) << R.key_pat);
 }
 
@@ -581,7 +593,7 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     }
     const Surface s = surface(R.S, o, d, prim, t, b1, b2);
     ro.w = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
-    R.hrec[q] = make_float4(__uint_as_float(prim), t, b1, b2);
+    R.pa[q].hrec = make_float4(__uint_as_float(prim), t, b1, b2);
     const uint32_t slot_j = pid / R.n_pix;
     const uint64_t rkey = mcgd::path_key(R.seed, R.pix[pid - slot_j * R.n_pix], R.sample0 + slot_j);
     const uint32_t key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
@@ -676,6 +688,7 @@ __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint
             unsigned basepos = 0;
             if (static_cast<int>(lane) == ldr) basepos = atomicAdd(R.shadow_count, static_cast<unsigned>(__popc(m)));
             basepos = __shfl_sync(act, basepos, ldr);
+            MCG_CHECK(!cand || basepos + __popc(m & ((1u << lane) - 1u)) < R.n_paths * nl);
             if (cand) R.squeue[basepos + __popc(m & ((1u << lane) - 1u))] = s;
         }
     }
@@ -697,10 +710,10 @@ __device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint
         thr.x = thr.x * alb.x;
         thr.y = thr.y * alb.y;
         thr.z = thr.z * alb.z;
-        R.ro2[i] = make_float4(o.x, o.y, o.z, width);
-        R.rd2[i] = make_float4(nd.x, nd.y, nd.z, spread + R.diffuse_spread);  // widen
+        R.pa2[i].ro = make_float4(o.x, o.y, o.z, width);
+        R.pa2[i].rd = make_float4(nd.x, nd.y, nd.z, spread + R.diffuse_spread);  // widen
     }
-    R.thr2[i] = thr;
+    R.pb2[i].thr = thr;
 }
 
 // ---------------------------------------------------------------------------
@@ -1347,7 +1360,10 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             if (B[k] != 0 && !(T1[k] < E[k])) {
-                                if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
+                                if (has_n) {
+                                    MCG_CHECK(top < 64);
+                                    st[top++] = make_int2(nc, __float_as_int(ne));
+                                }
                                 nc = entry_code(A[k], B[k]);
                                 ne = E[k];
                                 has_n = true;
@@ -1363,7 +1379,10 @@ __device__ __forceinline__ bool closest_ww4s(const mcgd::SceneView& S, bool acti
                             float E, T1;
                             slab(o, inv, lo, hi, tmin, E, T1);
                             if (!(T1 < E)) {
-                                if (has_n) st[top++] = make_int2(nc, __float_as_int(ne));
+                                if (has_n) {
+                                    MCG_CHECK(top < 64);
+                                    st[top++] = make_int2(nc, __float_as_int(ne));
+                                }
                                 nc = entry_code(__float_as_int(lo.w), eb);
                                 ne = E;
                                 has_n = true;
@@ -1491,10 +1510,12 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
                                     best = E[k];
                                     has_n = true;
                                 } else if (E[k] < best) {
+                                    MCG_CHECK(top < 64);
                                     st[top++] = nc;
                                     nc = code;
                                     best = E[k];
                                 } else {
+                                    MCG_CHECK(top < 64);
                                     st[top++] = code;
                                 }
                             }
@@ -1515,11 +1536,13 @@ __device__ __forceinline__ bool any_wws(const float4* Q, int32_t root_a, int32_t
                                 best = E;
                                 has_n = true;
                             } else if (E < best) {
-                                st[top++] = nc;
+                                MCG_CHECK(top < 64);
+                                    st[top++] = nc;
                                 nc = code;
                                 best = E;
                             } else {
-                                st[top++] = code;
+                                MCG_CHECK(top < 64);
+                                    st[top++] = code;
                             }
                         }
                     }
@@ -1760,16 +1783,15 @@ __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
     if (active) {
-        float4 ro = make_float4(o.x, o.y, o.z, 0.0f);
+        const float4 ro0 = make_float4(o.x, o.y, o.z, 0.0f);
+        float4 ro = ro0;
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
         const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
         const float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         const uint32_t key = hit_record(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
-        R.ro[i] = ro;
-        R.rd[i] = rd;
-        R.thr[i] = thr;
-        R.L[i] = L;
-        R.pid[i] = i;
+        R.pa[i].ro = ro0;   // the width at the origin (the shade propagates it)
+        R.pa[i].rd = rd;
+        R.pb[i] = PathVal{thr, make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(i))};
         R.keys[i] = key;
         R.vals[i] = i;
     }
@@ -1899,8 +1921,8 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
     const bool active = q < *count;
     float4 ro{}, rd{};
     if (active) {
-        ro = R.ro[q];
-        rd = R.rd[q];
+        ro = R.pa[q].ro;
+        rd = R.pa[q].rd;
     }
     const V3 o{ro.x, ro.y, ro.z}, d = active ? V3{rd.x, rd.y, rd.z} : V3{1.0f, 1.0f, 1.0f};
     uint32_t prim = 0;
@@ -1908,12 +1930,11 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
     if (active) {
-        const uint32_t pid = R.pid[q];
+        const uint32_t pid = __float_as_uint(R.pb[q].L.w);
         uint32_t key;
         if (found) {
             key = hit_record(R, q, pid, ro, rd, make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), true, prim, t,
                              b1, b2, vtx);
-            R.ro[q] = ro;
         } else {
             // the path ends; k_resolve_lights (which runs after this kernel
             // and the shadow rays) adds throughput * env to its final radiance
@@ -1943,8 +1964,10 @@ __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t*
     if (q >= (count ? *count : R.n_paths)) return;
     const uint32_t key = R.keys[q];
     if (key_slot(R, key) >= R.S.n_programs) return;
+    const PathRay pr = R.pa[q];
+    const float4 ro = make_float4(pr.ro.x, pr.ro.y, pr.ro.z, pr.ro.w + pr.hrec.y * pr.rd.w);  // propagate
     uint32_t slot_hit;
-    const mcgd::ShadeIn in = shade_input(R.S, R.ro[q], R.rd[q], R.hrec[q], slot_hit);
+    const mcgd::ShadeIn in = shade_input(R.S, ro, pr.rd, pr.hrec, slot_hit);
     R.keys[q] = look_ahead(R, q, key, in);
 }
 
@@ -1960,7 +1983,9 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
     const bool live = slot < R.S.n_programs;
     if (live) {
         const uint32_t nl = R.S.n_plights + R.S.n_rlights;
-        float4 L = R.L[i];
+        const PathVal pv = R.pb[i];
+        float4 L = pv.L;
+        const uint32_t pid = __float_as_uint(pv.L.w);
         for (uint32_t j = 0; j < nl; ++j) {
             const uint32_t s = i * nl + j;
             const float4 c = R.scon[s];
@@ -1971,14 +1996,14 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
             }
         }
         if (b >= R.max_bounces) {
-            R.fin[R.pid[i]] = make_float4(L.x, L.y, L.z, R.thr[i].w);
+            R.fin[pid] = make_float4(L.x, L.y, L.z, pv.thr.w);
         } else if (R.keys[i] == no_hit_key(R)) {
             // the continuation ray missed (k_trace_closest_ww): env term, path ends
-            const float4 thr = R.thr[i];
-            R.fin[R.pid[i]] = make_float4(L.x + thr.x * R.S.env[0], L.y + thr.y * R.S.env[1],
+            const float4 thr = pv.thr;
+            R.fin[pid] = make_float4(L.x + thr.x * R.S.env[0], L.y + thr.y * R.S.env[1],
                                           L.z + thr.z * R.S.env[2], thr.w);
         } else {
-            R.L[i] = L;
+            R.pb[i].L = L;
         }
     } else {
         R.keys[i] = no_hit_key(R);
@@ -2026,26 +2051,29 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t q = i;   // timing experiment only: no permutation (wrong images)
 #else
     const uint32_t q = order[i];
+    MCG_CHECK(q < R.n_paths);
 #endif
     const unsigned grp = __match_any_sync(live, slot);
-    const float4 hr = R.hrec[q], ro = R.ro[q], rd = R.rd[q];
-    const uint32_t pid = R.pid[q];
+    const PathRay pr = R.pa[q];
+    const PathVal pv = R.pb[q];
+    const float4 hr = pr.hrec, rd = pr.rd;
+    const float4 ro = make_float4(pr.ro.x, pr.ro.y, pr.ro.z, pr.ro.w + hr.y * rd.w);  // propagate (raycone.cpp:15-18)
+    const uint32_t pid = __float_as_uint(pv.L.w);
+    MCG_CHECK(pid < R.n_paths);
     // the rest of the path's state is loaded now, in the same round trip as
     // the hit record, not after the VM; what the VM does not change is
     // written to the next layout right away, so little of it stays live
-    float4 thr = R.thr[q];
-    R.L2[i] = R.L[q];
-    R.pid2[i] = pid;
+    float4 thr = pv.thr;
+    R.pb2[i].L = pv.L;
     uint32_t slot_hit;
     const mcgd::ShadeIn in = shade_input(R.S, ro, rd, hr, slot_hit);
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
-                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
+                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x), max_stack};
     const uint32_t slot_j = pid / R.n_pix;
     const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
-    mcgd::Ahead ah{make_uint4(0u, 0u, 0u, 0u), R.ahead != nullptr};
-    if (ah.on) ah.w = R.ahead[q];
+    const mcgd::Ahead ah{pr.ahead, R.ahead_on != 0};
     const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                           slot, in, grp, st, s_perm, okey, R.q, cnt, ah);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
@@ -2225,7 +2253,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
     if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
-    const size_t lane_bytes = f4 * 11 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
+    const size_t lane_bytes = f4 * 13 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
     ctx->path_mem.ensure(lane_bytes);
     for (int l = 1; l < lanes; ++l) ctx->lane_path[l].ensure(lane_bytes);
     RenderView R{};
@@ -2249,18 +2277,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.diffuse_spread = P.diffuse_spread;
     R.n_pix = n_pix;
     auto layout = [&](RenderView& V, char* base) {
-        V.ro = reinterpret_cast<float4*>(base);
-        V.rd = V.ro + max_paths;
-        V.thr = V.rd + max_paths;
-        V.L = V.thr + max_paths;
-        V.ro2 = V.L + max_paths;
-        V.rd2 = V.ro2 + max_paths;
-        V.thr2 = V.rd2 + max_paths;
-        V.L2 = V.thr2 + max_paths;
-        V.hrec = V.L2 + max_paths;
-        V.fin = V.hrec + max_paths;
-        V.ahead = look_ahead ? reinterpret_cast<uint4*>(V.fin + max_paths) : nullptr;
-        V.sro = V.fin + 2 * max_paths;
+        V.pa = reinterpret_cast<PathRay*>(base);          // 4 float4 per path
+        V.pa2 = V.pa + max_paths;                          // 4
+        V.pb = reinterpret_cast<PathVal*>(V.pa2 + max_paths);   // 2
+        V.pb2 = V.pb + max_paths;                          // 2
+        V.fin = reinterpret_cast<float4*>(V.pb2 + max_paths);   // 1
+        V.ahead_on = look_ahead ? 1u : 0u;
+        V.sro = V.fin + max_paths;
         V.srd = V.sro + n_shadow;
         V.scon = V.srd + n_shadow;
         uint32_t* u32 = reinterpret_cast<uint32_t*>(V.scon + n_shadow);
@@ -2268,8 +2291,6 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         V.vals = u32 + max_paths;
         uint32_t* skey_ = u32 + 2 * max_paths;
         uint32_t* order_ = u32 + 3 * max_paths;
-        V.pid = u32 + 4 * max_paths;
-        V.pid2 = u32 + 5 * max_paths;
         V.skey = skey_;
         V.order = order_;
         V.squeue = u32 + 6 * max_paths;
@@ -2433,11 +2454,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 ls.done();
             }
             // the path state now lives at the sorted positions
-            std::swap(R.ro, R.ro2);
-            std::swap(R.rd, R.rd2);
-            std::swap(R.thr, R.thr2);
-            std::swap(R.L, R.L2);
-            std::swap(R.pid, R.pid2);
+            std::swap(R.pa, R.pa2);
+            std::swap(R.pb, R.pb2);
             if (deferred) {   // one lane: sm == ctx->stream
                 unsigned int count = 0;
                 cuda_check(cudaMemcpyAsync(&count, R.q.count, 4, cudaMemcpyDeviceToHost, sm), "D2H");

@@ -491,7 +491,7 @@ __global__ void k_execute(mcgd::SceneView S, CacheView C, int cache_on, int mip_
     const unsigned grp = __ballot_sync(mcgd::kFull, valid);
     if (!valid) return;
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
-                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x)};
+                   static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x), max_stack};
     const float* p = sp + 15 * i;
     const mcgd::ShadeIn in{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8],
                            p[9], p[10], p[11], p[12], p[13], p[14]};
@@ -1667,7 +1667,19 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         // the slab test is monotone, so ancestors never reject first) -- so
         // any hierarchy over the same leaves answers exactly as the
         // reference's tree does.
-        std::vector<mcg_bvh_node> squads = build_shadow_tree(f, mcgd::kShadowWidth, v.sroot_a, v.sroot_b);
+        // MCG_SHADOW_BUILD=host: the host builder; default: the same SAH
+        // tree built on the device (mcg_build.cu)
+        std::vector<mcg_bvh_node> squads;
+        const char* sb_env = std::getenv("MCG_SHADOW_BUILD");
+        if (sb_env && std::string(sb_env) == "host") {
+            squads = build_shadow_tree(f, mcgd::kShadowWidth, v.sroot_a, v.sroot_b);
+        } else {
+            std::vector<mcg_bvh_node> leaves;
+            const mcg_bvh_node* rn = static_cast<const mcg_bvh_node*>(f.nodes);
+            for (uint32_t i = 0; i < f.n_nodes; ++i)
+                if (rn[i].a < 0) leaves.push_back(rn[i]);
+            squads = build_shadow_tree_device(ctx, leaves, mcgd::kShadowWidth, v.sroot_a, v.sroot_b);
+        }
         D.max_stack_s = stack_need(squads, mcgd::kShadowWidth);
         if (D.max_stack_s > 63) fail(MCG_ERR_INVALID_ARGUMENT, "shadow BVH too deep for the traversal stack");
         v.squads = static_cast<const float4*>(up(16, squads.data(), squads.size() * sizeof(mcg_bvh_node)));

@@ -5,7 +5,8 @@ seconds under the tool. Run as
     compute-sanitizer --tool memcheck  python profiles/scripts/sanitize.py
     compute-sanitizer --tool racecheck python profiles/scripts/sanitize.py
 
-(profiles/scripts/sanitize.sh runs all four and keeps the logs)."""
+(compute-sanitizer is closed on this GPU pool; profiles/scripts/checked.sh runs
+this workload and the -m gpu suite on the bounds-checked build instead)."""
 import os
 import sys
 import tempfile
