@@ -570,25 +570,32 @@ def main() -> None:
     # 8 Ne per lookup / store attempt (+8 per won CAS), 48 per TexSample,
     # 40 per BVH node visited (the reference's BvhNode), 48 per triangle
     # tested -- and (b) the compulsory HBM bytes, what must cross HBM at
-    # least once: per shading point the record + path state in (104 B) and
-    # the continuation out (48 B), per shadow-ray candidate 52 B out (16 B
-    # per rejected light); per continuation ray 36 B in, 72 B out per hit,
-    # 48 B per miss; per shadow ray 37 B; plus the scene once per launch.
-    # The traversal kernels' node and triangle bytes are served by L1/L2
-    # (the bench BVH is a few hundred KB): (a) >> (b) for them.
+    # least once. The first probe of every lookup runs in the trace kernels'
+    # epilogue (look-ahead, before the sort); the shade re-probes the misses
+    # (concurrent mode, cells not seen full) and stores. Shade: per shading
+    # point the two path records in (64 + 32 B) and out (32 + 32 B), per
+    # shadow-ray candidate 52 B out (16 B per rejected light); closest hit:
+    # per ray the ray record and path id in (32 + 32 B), the hit record +
+    # look-ahead result and sort key out per hit (40 B), the key per miss;
+    # per shadow ray 37 B; plus the scene once per launch. The traversal
+    # kernels' node and triangle bytes are served by L1/L2 (the bench BVH is
+    # a few hundred KB): (a) >> (b) for them.
     nodes_closest = st_s.bvh_nodes - st_s.bvh_nodes_shadow
     prims_closest = st_s.prims_tested - st_s.prims_tested_shadow
-    probe_bytes = st_s.lookups * 8 * ne + st_s.stores_attempted * 8 * ne + st_s.inserts_won * 8
+    lookahead_bytes = st_s.lookups * 8 * ne
+    shade_probe_bytes = ((st_s.lookups - st_s.hits) * 8 * ne + st_s.stores_attempted * 8 * ne
+                         + st_s.inserts_won * 8)
     scene_once = f.n_prims * (48 + 24 + 4) + f.n_nodes * 64
     algorithmic = {
-        "shade": probe_bytes + st_s.tex_samples * 48,
-        "trace_closest": nodes_closest * 40 + prims_closest * 48,
+        "shade": shade_probe_bytes + st_s.tex_samples * 48,
+        "trace_closest": nodes_closest * 40 + prims_closest * 48 + lookahead_bytes,
         "trace_shadow": st_s.bvh_nodes_shadow * 40 + st_s.prims_tested_shadow * 48,
     }
     compulsory = {
-        "shade": probe_bytes + st_s.tex_samples * 48 + st_s.shading_points * (104 + 48)
+        "shade": shade_probe_bytes + st_s.tex_samples * 48 + st_s.shading_points * (96 + 64)
                  + st_s.shadow_rays * 52 + (n_lights * st_s.shading_points - st_s.shadow_rays) * 16,
-        "trace_closest": st_s.closest_rays * 36 + closest_hits * 72 + (st_s.closest_rays - closest_hits) * 48,
+        "trace_closest": (st_s.closest_rays * 64 + closest_hits * 40 + (st_s.closest_rays - closest_hits) * 8
+                          + lookahead_bytes),
         "trace_shadow": st_s.shadow_rays * 37,
     }
     # ncu DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum
@@ -637,7 +644,9 @@ def main() -> None:
     roof["fits_in_step"] = bool(roof["per_launch_ms"] * roof["launches_per_step"] <= ms / args.steps)
     roof["limiter"] = ("issue/latency: warp divergence in BVH traversal (L1/L2-resident tree) -- the "
                        "8(d) bytes are L1/L2-served, HBM (hbm_compulsory) is not the bound"
-                       if dname.startswith("trace") else "random HBM access (cache probes)")
+                       if dname.startswith("trace") else
+                       "random HBM accesses (the path-record gather, re-probes, textures) and dependent "
+                       "FP latency in the material VM; see roofline.issue and traffic")
     roof["peak_source"] = peak_src
     # The north-star kernel (material VM + cache probes) beside it.
     roof_shade = kernel_roofline("shade")

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MCG_ABI_VERSION 3   /* 2: mcg_render_stats.shadow_occluded; 3: write_slots, insert log, n_devices */
+#define MCG_ABI_VERSION 4   /* 2: mcg_render_stats.shadow_occluded; 3: write_slots, insert log, n_devices; 4: mcg_shadow_tree */
 
 typedef enum mcg_status {
     MCG_OK = 0,
@@ -519,6 +519,16 @@ mcg_status mcg_intersect_batch(mcg_ctx* ctx, const float* rays, size_t n, float 
                                int32_t variant, float* out);
 mcg_status mcg_occluded_batch(mcg_ctx* ctx, const float* rays, size_t n, float t_min,
                               const float* t_max, int32_t variant, uint8_t* out);
+
+/* The any-hit (shadow) hierarchy of the uploaded scene, as built (on the
+ * device by default; MCG_SHADOW_BUILD=host at upload: the host builder):
+ * *n_out 4-wide nodes of mcg_bvh_node entries (leaf: a = ~first, b = count
+ * with the reference leaf's exact box; node: a = index, b = -1; unused:
+ * b = 0) copied to out when cap >= *n_out * 4, and the root entry. No
+ * reference counterpart (the reference traces shadow rays over its own
+ * tree, scene.cpp:280-298); for tests and tools. */
+mcg_status mcg_shadow_tree(mcg_ctx* ctx, mcg_bvh_node* out, size_t cap, size_t* n_out, int32_t* root_a,
+                           int32_t* root_b);
 
 /* Per-shading-point material evaluation (execute, stackvm.cpp:248-368) on the
  * device for a batch of shading points of one material slot of the uploaded

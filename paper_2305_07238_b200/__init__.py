@@ -263,6 +263,18 @@ class Context:
         return out
 
 
+    def shadow_tree(self):
+        """The uploaded scene's any-hit hierarchy (include/mcg.h mcg_shadow_tree):
+        ((n, 4) structured array of mcg_bvh_node entries, (root_a, root_b))."""
+        n, ra, rb = C.c_size_t(), C.c_int32(), C.c_int32()
+        check(N.lib().mcg_shadow_tree(self.handle, None, 0, C.byref(n), C.byref(ra), C.byref(rb)))
+        dt = np.dtype([("lo", np.float32, 3), ("a", np.int32), ("hi", np.float32, 3), ("b", np.int32)])
+        out = np.zeros(n.value * 4, dt)
+        check(N.lib().mcg_shadow_tree(self.handle, _ptr(out), out.shape[0], C.byref(n), C.byref(ra),
+                                      C.byref(rb)))
+        return out.reshape(-1, 4), (ra.value, rb.value)
+
+
 # --------------------------------------------------------------------------
 # Material cache (cache.hpp:69-115), resident in HBM
 # --------------------------------------------------------------------------

@@ -152,6 +152,7 @@ _SIGS = [
     ("mcg_execute_batch", C.c_int, [vp, u32, vp, C.c_size_t, vp, i32, i32, vp, vp, vp]),
     ("mcg_intersect_batch", C.c_int, [vp, vp, C.c_size_t, f32, f32, i32, vp]),
     ("mcg_occluded_batch", C.c_int, [vp, vp, C.c_size_t, f32, vp, i32, vp]),
+    ("mcg_shadow_tree", C.c_int, [vp, vp, C.c_size_t, P(C.c_size_t), P(i32), P(i32)]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]
@@ -159,7 +160,7 @@ EXPORTED = [s[0] for s in _SIGS]
 _lib = None
 
 
-ABI_VERSION = 3   # include/mcg.h MCG_ABI_VERSION (the struct layouts below)
+ABI_VERSION = 4   # include/mcg.h MCG_ABI_VERSION (the struct layouts below)
 
 
 def lib():

@@ -62,6 +62,7 @@ struct DeviceScene {
     float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};   // scene bounds (BVH root)
     uint32_t max_stack4 = 1;   // worst-case LIFO stack of the 4-wide traversal
     uint32_t max_stack_s = 1;  // same for the shadow (SAH) tree
+    std::vector<mcg_bvh_node> shadow_nodes;   // host copy of the shadow tree (mcg_shadow_tree)
     mcg_flat_scene cam{};   // camera/env fields only (no pointers used)
     bool loaded = false;
     void clear() {

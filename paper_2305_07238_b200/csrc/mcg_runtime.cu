@@ -1681,6 +1681,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
             squads = build_shadow_tree_device(ctx, leaves, mcgd::kShadowWidth, v.sroot_a, v.sroot_b);
         }
         D.max_stack_s = stack_need(squads, mcgd::kShadowWidth);
+        D.shadow_nodes = squads;
         if (D.max_stack_s > 63) fail(MCG_ERR_INVALID_ARGUMENT, "shadow BVH too deep for the traversal stack");
         v.squads = static_cast<const float4*>(up(16, squads.data(), squads.size() * sizeof(mcg_bvh_node)));
         // The same 4-wide nodes transposed (mcg_device.cuh, closest_q4): eight
@@ -1754,6 +1755,19 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         D.cam.prim_geom = nullptr;  // only camera/env fields are used later
         D.loaded = true;
         sync(ctx);
+    });
+}
+
+mcg_status mcg_shadow_tree(mcg_ctx* ctx, mcg_bvh_node* out, size_t cap, size_t* n_out, int32_t* root_a,
+                           int32_t* root_b) {
+    return guarded([&] {
+        need(ctx && n_out && root_a && root_b, "null argument");
+        need(ctx->scene.loaded, "no scene uploaded");
+        const std::vector<mcg_bvh_node>& t = ctx->scene.shadow_nodes;
+        *n_out = t.size() / mcgd::kShadowWidth;
+        *root_a = ctx->scene.view.sroot_a;
+        *root_b = ctx->scene.view.sroot_b;
+        if (out && cap >= t.size()) std::memcpy(out, t.data(), t.size() * sizeof(mcg_bvh_node));
     });
 }
 

@@ -26,6 +26,7 @@ for tps in (24, 96, 300):
         t0 = time.perf_counter()
         ctx.upload(s)
         t_up = time.perf_counter() - t0
+        render(s, RenderConfig(width=1920, height=1080, spp=8), ctx=ctx)   # warm-up (allocations)
         r = render(s, RenderConfig(width=1920, height=1080, spp=8), ctx=ctx)
         row[mode] = {"upload_s": t_up, "render_ms": r.stats.device_ms,
                      "shadow_nodes": r.stats.bvh_nodes_shadow, "shadow_prims": r.stats.prims_tested_shadow}

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_function(built):
     assert not missing, f"not exported: {missing}"
     # and the Python binding covers all of them
     assert sorted(set(names) - set(N.EXPORTED)) == []
-    assert N.lib().mcg_abi_version() == N.ABI_VERSION == 3
+    assert N.lib().mcg_abi_version() == N.ABI_VERSION == 4
 
 
 def test_memory_bytes():
