@@ -569,6 +569,7 @@ struct SceneView {
     const mcg_ramp_stop* stops;
     const mcg_texture* textures;
     const float4* texels;
+    uint32_t n_code;              // instruction words of all programs (shared-memory staging)
     float env[3];
     // Per program, its first kAhead cache points in bracket order: (node_idx,
     // flags | kAheadValid) -- what the look-ahead probe needs to build their
@@ -664,7 +665,7 @@ struct VmResult {
 #ifndef MCG_VM_REPROBE
 #define MCG_VM_REPROBE 1   // concurrent mode: a look-ahead miss probes again at CacheLookup
 #endif
-template <bool kDeferred>
+template <bool kDeferred, bool kSmemCode = false>
 // MCG_VM_PREFETCH=1 (experiment, off): fetch the next instruction word
 // while the current one executes; neutral (636.6-637.7 vs 636.4-638.3 ms per
 // bench render): the 16-byte words are L1 hits and not the VM's bound.
@@ -676,9 +677,12 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                                                 const ShadeIn& sp, unsigned grp, const Stack& st,
                                                 const uint8_t* perm, uint32_t order_key,
                                                 const StoreQueue& q, VmCounters& cnt,
-                                                const Ahead& ah = Ahead{}) {
+                                                const Ahead& ah = Ahead{}, const uint4* s_code = nullptr) {
     const mcg_program prog = S.programs[slot];
-    const uint4* code = reinterpret_cast<const uint4*>(S.code + prog.code_offset);
+    // kSmemCode: every program's words staged in shared memory by the
+    // calling kernel (one 16-byte broadcast LDS per dispatch); else L1-cached
+    // global loads
+    const uint4* code = (kSmemCode ? s_code : reinterpret_cast<const uint4*>(S.code)) + prog.code_offset;
     const unsigned lane = threadIdx.x & 31u;
     bool parked = false;
     int resume = -1;
@@ -702,7 +706,7 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
         w_next = __ldg(code + pc + 1);
 #else
         MCG_CHECK(static_cast<uint32_t>(pc) < prog.code_len);
-        const uint4 w = __ldg(code + pc);
+        const uint4 w = kSmemCode ? code[pc] : __ldg(code + pc);
 #endif
         const uint8_t op = static_cast<uint8_t>(w.x & 0xffu);
         const uint8_t flags = static_cast<uint8_t>((w.x >> 8) & 0xffu);

@@ -2023,7 +2023,7 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 #ifndef MCG_SHADE_MINB
 #define MCG_SHADE_MINB 5
 #endif
-template <bool kDeferred>
+template <bool kDeferred, bool kSmemCode>
 #ifndef MCG_SHADE_BLOCK
 #define MCG_SHADE_BLOCK 128
 #endif
@@ -2033,6 +2033,13 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     extern __shared__ float smem[];
     __shared__ uint8_t s_perm[256];
     mcgd::stage_perm(s_perm);
+    // the bytecode of every program, after the operand stack (north_star:
+    // node bytecode in shared memory)
+    uint4* s_code = reinterpret_cast<uint4*>(smem + 3 * max_stack * blockDim.x);
+    if (kSmemCode) {
+        const uint4* g = reinterpret_cast<const uint4*>(R.S.code);
+        for (uint32_t k = threadIdx.x; k < R.S.n_code; k += blockDim.x) s_code[k] = __ldg(g + k);
+    }
     __syncthreads();
     // Blocks visit the sorted list in a scattered order (concurrent mode):
     // the paths of one texel are contiguous there (Morton order), and the
@@ -2074,8 +2081,9 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
     const mcgd::Ahead ah{pr.ahead, R.ahead_on != 0};
-    const mcgd::VmResult r = mcgd::run_program<kDeferred>(R.S, R.C, R.cache_on != 0, R.mip_offset,
-                                                          slot, in, grp, st, s_perm, okey, R.q, cnt, ah);
+    const mcgd::VmResult r = mcgd::run_program<kDeferred, kSmemCode>(R.S, R.C, R.cache_on != 0, R.mip_offset,
+                                                                     slot, in, grp, st, s_perm, okey, R.q, cnt, ah,
+                                                                     s_code);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
     nee_bounce(R, i, pid, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, ro.w, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
@@ -2401,8 +2409,16 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     cudaFuncSetAttribute(k_trace_closest_ww, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
     cudaFuncSetAttribute(k_shadow_ww<true>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
     cudaFuncSetAttribute(k_primary, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
-    cudaFuncSetAttribute(k_shade<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_shade<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // programs up to 32 KB of bytecode are staged in shared memory per block
+    // (MCG_CODE_SMEM=0: read from global memory through L1)
+    const char* cs_env = std::getenv("MCG_CODE_SMEM");
+    const size_t code_bytes = static_cast<size_t>(D.view.n_code) * sizeof(mcg_insn);
+    const bool code_smem = !(cs_env && std::string(cs_env) == "0") && code_bytes <= 32 * 1024;
+    const size_t smem_launch = smem + (code_smem ? code_bytes : 0);
+    cudaFuncSetAttribute(k_shade<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_shade<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_launch));
+    cudaFuncSetAttribute(k_shade<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_launch));
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cuda_check(cudaEventCreate(&ev0), "event");
     cuda_check(cudaEventCreate(&ev1), "event");
@@ -2449,8 +2465,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
                 const uint32_t wh32 = static_cast<uint32_t>(wh);
                 // deterministic mode: stores are queued and applied after the
                 // shade (NEE and the bounce need none of them)
-                if (deferred) k_shade<true><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
-                else k_shade<false><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                if (code_smem) {
+                    if (deferred) k_shade<true, true><<<sg, block, smem_launch, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                    else k_shade<false, true><<<sg, block, smem_launch, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                } else {
+                    if (deferred) k_shade<true, false><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                    else k_shade<false, false><<<sg, block, smem, sm>>>(R, R.skey, R.order, max_stack, wh32, b);
+                }
                 ls.done();
             }
             // the path state now lives at the sorted positions

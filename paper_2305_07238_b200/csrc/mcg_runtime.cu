@@ -1723,6 +1723,7 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         // one spare word past the last program: the VM fetches pc + 1 ahead
         D.bufs[7].ensure((f.n_code + 1) * sizeof(mcg_insn));
         v.code = static_cast<const mcg_insn*>(up(7, f.code, f.n_code * sizeof(mcg_insn)));
+        v.n_code = f.n_code;
         // The look-ahead table: each program's first kAhead cache points
         // (CacheLookup node and uses_uv flag, in bracket order).
         {
