@@ -1767,7 +1767,12 @@ __device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& cod
 #ifndef MCG_PRIMARY_BLOCK
 #define MCG_PRIMARY_BLOCK 128
 #endif
-__global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
+// MCG_PRIMARY_PK=1 (experiment): camera rays through the warp-packet
+// traversal (coherent rays; one shared stack per warp, closest_pk)
+#ifndef MCG_PRIMARY_PK
+#define MCG_PRIMARY_PK 0
+#endif
+__global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R, int pk_depth) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = i < R.n_paths;
@@ -1780,8 +1785,17 @@ __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     }
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
+#if MCG_PRIMARY_PK
+    int32_t* pc;
+    uint32_t* pm;
+    float* pe;
+    pk_stacks(pk_depth, true, pc, pm, pe);
+    const bool found = closest_pk(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
+                                  nvis, ntest, pc, pm, pe);
+#else
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
+#endif
     if (active) {
         const float4 ro0 = make_float4(o.x, o.y, o.z, 0.0f);
         float4 ro = ro0;
@@ -2442,7 +2456,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0, sm);
-            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
+            const int pk_depth = static_cast<int>(D.max_stack4) + 1;
+            const size_t pk_smem = MCG_PRIMARY_PK ? static_cast<size_t>(pk_depth) * 34 * 4 * (MCG_PRIMARY_BLOCK / 32) : 0;
+            if (MCG_PRIMARY_PK) cudaFuncSetAttribute(k_primary, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_smem));
+            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, pk_smem, sm>>>(R, pk_depth);
             ls.done();
         }
         if (look_ahead && !R.ahead_fused) {
