@@ -54,15 +54,20 @@ enum {
     kStatCount = 17
 };
 
-// A path's ray record (64 bytes, one DRAM access when gathered): ro.w is the
-// cone width at the ray origin (each reader propagates it over the hit
-// distance itself, raycone.cpp:15-18, with the same arithmetic); hrec is the
-// closest hit (primitive as uint bits, t, b1, b2) -- k_shade rebuilds the
-// shading point from it (surface + footprint, shade_input); ahead holds the
-// look-ahead probe results (mcgd::kAhead).
-struct __align__(64) PathRay {
-    float4 ro, rd, hrec;
-    uint4 ahead;
+// A path's ray record (128 bytes: one line, one DRAM access when gathered):
+// the ray the trace kernels read (ro.w = cone width at the origin); the
+// shading point of its closest hit, written by the trace kernel that found
+// it (surface, scene.cpp:211-247, and footprint gradients, raycone.cpp:50-65,
+// of the cone propagated over the hit distance) -- the shade reads it instead
+// of rebuilding it from the primitive; and the look-ahead probe results.
+struct __align__(128) PathRay {
+    float4 ro, rd;
+    float4 sp0;     // hit position, propagated cone width
+    float4 sp1;     // shading normal, pixel index (uint bits)
+    float4 sp2;     // u, v, g1
+    float4 sp3;     // g2, -, -
+    uint4 ahead;    // look-ahead results (mcgd::kAhead)
+    float4 pad;
 };
 // A path's value record (32 bytes): throughput.rgb + nodes_found (uint bits),
 // radiance.rgb + path id (uint bits: pass slot j * n_pix + shard pixel index).
@@ -593,42 +598,39 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     }
     const Surface s = surface(R.S, o, d, prim, t, b1, b2);
     ro.w = ro.w + t * rd.w;  // propagate (raycone.cpp:15-18)
-    R.pa[q].hrec = make_float4(__uint_as_float(prim), t, b1, b2);
     const uint32_t slot_j = pid / R.n_pix;
-    const uint64_t rkey = mcgd::path_key(R.seed, R.pix[pid - slot_j * R.n_pix], R.sample0 + slot_j);
+    const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
+    const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
     const uint32_t key = sort_key(R, s.slot, s.p.x, s.p.y, s.p.z, s.n, rkey, vtx);
-    if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
-    // the look-ahead probe right here (the shading point is shade_input's:
-    // the same surface and the footprint of the propagated cone)
+    // the shading point (ShadingPoint, geom.hpp:49-56) for the shade
     float2 g1, g2;
     mcgd::footprint(ro.w, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
+    PathRay& rec = R.pa[q];
+    rec.sp0 = make_float4(s.p.x, s.p.y, s.p.z, ro.w);
+    rec.sp1 = make_float4(s.n.x, s.n.y, s.n.z, __uint_as_float(pixel));
+    rec.sp2 = make_float4(s.u, s.v, g1.x, g1.y);
+    rec.sp3 = make_float4(g2.x, g2.y, 0.0f, 0.0f);
+    if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
+    // the look-ahead probe right here
     const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
                            s.u, s.v, g1.x, g1.y, g2.x, g2.y};
     return look_ahead(R, q, key, in);
 }
 
-// The shading point of a hit record (ShadingPoint, geom.hpp:49-56): the
-// surface (scene.cpp:211-247) and the footprint gradients of the cone of
-// width ro.w (raycone.cpp:50-65).
-__device__ __forceinline__ mcgd::ShadeIn shade_input(const mcgd::SceneView& S, const float4& ro, const float4& rd,
-                                                     const float4& hr, uint32_t& slot_out) {
-    const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
-    const Surface s = surface(S, o, d, __float_as_uint(hr.x), hr.y, hr.z, hr.w);
-    float2 g1, g2;
-    mcgd::footprint(ro.w, d, s.n, s.e1, s.e2, s.d1, s.d2, g1, g2);
-    slot_out = s.slot;
-    return mcgd::ShadeIn{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
-                         s.u, s.v, g1.x, g1.y, g2.x, g2.y};
+// The shading point the trace kernel stored in a path's ray record.
+__device__ __forceinline__ mcgd::ShadeIn shade_input(const float4& rd, const float4& sp0, const float4& sp1,
+                                                     const float4& sp2, const float4& sp3) {
+    return mcgd::ShadeIn{sp0.x, sp0.y, sp0.z, sp1.x, sp1.y, sp1.z, rd.x, rd.y, rd.z,
+                         sp2.x, sp2.y, sp2.z, sp2.w, sp3.x, sp3.y};
 }
 
 // Next-event estimation and the cosine bounce of vertex b of path pid, whose
 // state goes to sorted position i: one shadow-ray candidate per light -- its
 // contribution computed now, applied in light order by k_resolve once
 // visibility is known -- and the continuation ray.
-__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, int b, V3 pos,
-                                           V3 n, float3 bc, float4 thr, float width, float spread) {
+__device__ __forceinline__ void nee_bounce(const RenderView& R, uint32_t i, uint32_t pid, uint32_t pixel, int b,
+                                           V3 pos, V3 n, float3 bc, float4 thr, float width, float spread) {
     const uint32_t slot_j = pid / R.n_pix;
-    const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
     const uint64_t rkey = mcgd::path_key(R.seed, pixel, R.sample0 + slot_j);
     const V3 alb{fminf(fmaxf(bc.x, 0.0f), 1.0f), fminf(fmaxf(bc.y, 0.0f), 1.0f),
                  fminf(fmaxf(bc.z, 0.0f), 1.0f)};
@@ -1767,12 +1769,7 @@ __device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& cod
 #ifndef MCG_PRIMARY_BLOCK
 #define MCG_PRIMARY_BLOCK 128
 #endif
-// MCG_PRIMARY_PK=1 (experiment): camera rays through the warp-packet
-// traversal (coherent rays; one shared stack per warp, closest_pk)
-#ifndef MCG_PRIMARY_PK
-#define MCG_PRIMARY_PK 0
-#endif
-__global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R, int pk_depth) {
+__global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
     const bool active = i < R.n_paths;
@@ -1785,17 +1782,8 @@ __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R, int
     }
     uint32_t prim = 0;
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
-#if MCG_PRIMARY_PK
-    int32_t* pc;
-    uint32_t* pm;
-    float* pe;
-    pk_stacks(pk_depth, true, pc, pm, pe);
-    const bool found = closest_pk(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
-                                  nvis, ntest, pc, pm, pe);
-#else
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
-#endif
     if (active) {
         const float4 ro0 = make_float4(o.x, o.y, o.z, 0.0f);
         float4 ro = ro0;
@@ -1978,10 +1966,8 @@ __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t*
     if (q >= (count ? *count : R.n_paths)) return;
     const uint32_t key = R.keys[q];
     if (key_slot(R, key) >= R.S.n_programs) return;
-    const PathRay pr = R.pa[q];
-    const float4 ro = make_float4(pr.ro.x, pr.ro.y, pr.ro.z, pr.ro.w + pr.hrec.y * pr.rd.w);  // propagate
-    uint32_t slot_hit;
-    const mcgd::ShadeIn in = shade_input(R.S, ro, pr.rd, pr.hrec, slot_hit);
+    const PathRay& pr = R.pa[q];
+    const mcgd::ShadeIn in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
     R.keys[q] = look_ahead(R, q, key, in);
 }
 
@@ -2075,10 +2061,10 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     MCG_CHECK(q < R.n_paths);
 #endif
     const unsigned grp = __match_any_sync(live, slot);
-    const PathRay pr = R.pa[q];
+    const PathRay& pr = R.pa[q];
+    const float4 rd = pr.rd, sp0 = pr.sp0, sp1 = pr.sp1, sp2 = pr.sp2, sp3 = pr.sp3;
+    const uint4 ahw = pr.ahead;
     const PathVal pv = R.pb[q];
-    const float4 hr = pr.hrec, rd = pr.rd;
-    const float4 ro = make_float4(pr.ro.x, pr.ro.y, pr.ro.z, pr.ro.w + hr.y * rd.w);  // propagate (raycone.cpp:15-18)
     const uint32_t pid = __float_as_uint(pv.L.w);
     MCG_CHECK(pid < R.n_paths);
     // the rest of the path's state is loaded now, in the same round trip as
@@ -2086,20 +2072,19 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     // written to the next layout right away, so little of it stays live
     float4 thr = pv.thr;
     R.pb2[i].L = pv.L;
-    uint32_t slot_hit;
-    const mcgd::ShadeIn in = shade_input(R.S, ro, rd, hr, slot_hit);
+    const mcgd::ShadeIn in = shade_input(rd, sp0, sp1, sp2, sp3);
     mcgd::Stack st{smem, smem + max_stack * blockDim.x, smem + 2 * max_stack * blockDim.x,
                    static_cast<int>(blockDim.x), static_cast<int>(threadIdx.x), max_stack};
     const uint32_t slot_j = pid / R.n_pix;
-    const uint32_t pixel = R.pix[pid - slot_j * R.n_pix];
+    const uint32_t pixel = __float_as_uint(sp1.w);
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
-    const mcgd::Ahead ah{pr.ahead, R.ahead_on != 0};
+    const mcgd::Ahead ah{ahw, R.ahead_on != 0};
     const mcgd::VmResult r = mcgd::run_program<kDeferred, kSmemCode>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                                      slot, in, grp, st, s_perm, okey, R.q, cnt, ah,
                                                                      s_code);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
-    nee_bounce(R, i, pid, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, ro.w, rd.w);
+    nee_bounce(R, i, pid, pixel, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, sp0.w, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
     mcgd::warp_add(R.stats + kStatHits, cnt.hits);
     mcgd::warp_add(R.stats + kStatWon, cnt.won);
@@ -2275,7 +2260,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const uint64_t n_shadow = max_paths * std::max<uint32_t>(1, n_lights);
     const size_t f4 = max_paths * sizeof(float4);
     if (static_cast<uint32_t>(P.spp) <= k) lanes = 1;   // a single pass
-    const size_t lane_bytes = f4 * 13 + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
+    const size_t lane_bytes = f4 * (2 * sizeof(PathRay) / 16 + 2 * sizeof(PathVal) / 16 + 1) + n_shadow * (48 + 4 + 1) + max_paths * 4 * 6 + n_pix * 4ull + 1024;
     ctx->path_mem.ensure(lane_bytes);
     for (int l = 1; l < lanes; ++l) ctx->lane_path[l].ensure(lane_bytes);
     RenderView R{};
@@ -2299,11 +2284,11 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     R.diffuse_spread = P.diffuse_spread;
     R.n_pix = n_pix;
     auto layout = [&](RenderView& V, char* base) {
-        V.pa = reinterpret_cast<PathRay*>(base);          // 4 float4 per path
-        V.pa2 = V.pa + max_paths;                          // 4
-        V.pb = reinterpret_cast<PathVal*>(V.pa2 + max_paths);   // 2
-        V.pb2 = V.pb + max_paths;                          // 2
-        V.fin = reinterpret_cast<float4*>(V.pb2 + max_paths);   // 1
+        V.pa = reinterpret_cast<PathRay*>(base);          // 128 B per path
+        V.pa2 = V.pa + max_paths;
+        V.pb = reinterpret_cast<PathVal*>(V.pa2 + max_paths);   // 32 B
+        V.pb2 = V.pb + max_paths;
+        V.fin = reinterpret_cast<float4*>(V.pb2 + max_paths);   // 16 B
         V.ahead_on = look_ahead ? 1u : 0u;
         V.sro = V.fin + max_paths;
         V.srd = V.sro + n_shadow;
@@ -2456,10 +2441,7 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0, sm);
-            const int pk_depth = static_cast<int>(D.max_stack4) + 1;
-            const size_t pk_smem = MCG_PRIMARY_PK ? static_cast<size_t>(pk_depth) * 34 * 4 * (MCG_PRIMARY_BLOCK / 32) : 0;
-            if (MCG_PRIMARY_PK) cudaFuncSetAttribute(k_primary, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_smem));
-            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, pk_smem, sm>>>(R, pk_depth);
+            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
             ls.done();
         }
         if (look_ahead && !R.ahead_fused) {
