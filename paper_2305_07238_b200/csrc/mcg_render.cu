@@ -2142,6 +2142,12 @@ uint32_t coprime_near(uint32_t n, double frac) {
     return m % n ? m % n : 1u;
 }
 
+// cache counters [lookups, hits, inserts won, lost to full cells] += the
+// render's (kStat* order: lookups, hits, won, full)
+__global__ void k_add_counters(unsigned long long* ctr, const unsigned long long* stats) {
+    if (threadIdx.x < 4) ctr[threadIdx.x] += stats[threadIdx.x];
+}
+
 bool tile_mine(const mcg_render_params& p, int tile, int n_tiles) {
     if (p.shard_count <= 1) return true;
     if (p.shard_mode == MCG_SHARD_INTERLEAVED) return tile % p.shard_count == p.shard_rank;
@@ -2540,6 +2546,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->ev_lane[l], 0), "wait");
     }
     cuda_check(cudaEventRecord(ev1, ctx->stream), "event record");
+    if (cache_ctr) {
+        // Mirror the render's lookups/hits/inserts into the table's counters
+        // (MaterialCache::counters after a render, cache.cpp:146-150), on the
+        // render's stream (no host round trip, no legacy-stream sync).
+        k_add_counters<<<1, 32, 0, ctx->stream>>>(cache_ctr, R.stats);
+        ++ctx->launches;
+    }
     unsigned long long st[kStatCount];
     cuda_check(cudaMemcpyAsync(st, R.stats, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream), "D2H stats");
     if (stats && stats->hits_per_sample) {
@@ -2550,15 +2563,6 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     cudaEventElapsedTime(&dev_ms, ev0, ev1);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    if (cache_ctr) {
-        // Mirror the render's lookups/hits/inserts into the table's counters
-        // (MaterialCache::counters after a render, cache.cpp:146-150).
-        unsigned long long add[4] = {st[kStatLookups], st[kStatHits], st[kStatWon], st[kStatFull]};
-        unsigned long long cur[4];
-        cuda_check(cudaMemcpy(cur, cache_ctr, sizeof(cur), cudaMemcpyDeviceToHost), "D2H");
-        for (int q = 0; q < 4; ++q) cur[q] += add[q];
-        cuda_check(cudaMemcpy(cache_ctr, cur, sizeof(cur), cudaMemcpyHostToDevice), "H2D");
-    }
     const auto t1 = std::chrono::steady_clock::now();
     if (stats) {
         uint64_t* hps = stats->hits_per_sample;
