@@ -474,6 +474,22 @@ def main() -> None:
                          else ms_off)
                 tun[name] = {"ms_cache": on.device_ms, "ms_no_cache": t_off, "speedup": t_off / on.device_ms,
                              "hit_rate": on.hit_rate, "samples_per_s": W * H * SPP / (on.device_ms / 1e3)}
+            # BASELINE configs[3]: the Bmw-like analogue with every lookup on
+            # the finest virtual level (mip_offset 24: hit rate ~0, the table
+            # fills, then every insert finds its cell full) vs its no-cache
+            # render -- north_star: >= 90% of no-cache throughput
+            bmw = load_scene(S.build_scene(S.SceneSpec("bmw", W, H, tris_per_side=TRIS_PER_SIDE, uv_span=UV_SPAN),
+                                           os.path.join(tmp, "bmw")))
+            base = dict(width=W, height=H, spp=SPP, n_cells=N_CELLS, n_entries=N_ENTRIES, mip_offset=24)
+            api_render(bmw, RenderConfig(**base), ctx=ctx)
+            t_off = statistics.median(api_render(bmw, RenderConfig(**base), ctx=ctx).stats.device_ms
+                                      for _ in range(2))
+            ons = [api_render(bmw, RenderConfig(cache_enabled=True, **base), ctx=ctx).stats for _ in range(2)]
+            t_on = statistics.median(o.device_ms for o in ons)
+            extras["worst_case"] = {"scene": "bmw-like, unit uv, mip_offset 24 (BASELINE configs[3])",
+                                    "ms_cache": t_on, "ms_no_cache": t_off,
+                                    "throughput_vs_no_cache": t_off / t_on, "hit_rate": ons[-1].hit_rate,
+                                    "inserts_lost_full": ons[-1].inserts_lost_full, "target": 0.9}
             ctx.upload(scene)
             extras["tunings"] = tun
         if rank == 0:

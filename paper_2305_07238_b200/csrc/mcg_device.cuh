@@ -677,12 +677,14 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                                                 const ShadeIn& sp, unsigned grp, const Stack& st,
                                                 const uint8_t* perm, uint32_t order_key,
                                                 const StoreQueue& q, VmCounters& cnt,
-                                                const Ahead& ah = Ahead{}, const uint4* s_code = nullptr) {
+                                                const Ahead& ah = Ahead{}, const uint4* s_code = nullptr,
+                                                uint32_t s_code_base = 0) {
     const mcg_program prog = S.programs[slot];
-    // kSmemCode: every program's words staged in shared memory by the
-    // calling kernel (one 16-byte broadcast LDS per dispatch); else L1-cached
-    // global loads
-    const uint4* code = (kSmemCode ? s_code : reinterpret_cast<const uint4*>(S.code)) + prog.code_offset;
+    // kSmemCode: the program's words staged in shared memory by the calling
+    // kernel from word s_code_base on (one 16-byte broadcast LDS per
+    // dispatch); else L1-cached global loads
+    const uint4* code = kSmemCode ? s_code + (prog.code_offset - s_code_base)
+                                  : reinterpret_cast<const uint4*>(S.code) + prog.code_offset;
     const unsigned lane = threadIdx.x & 31u;
     bool parked = false;
     int resume = -1;

@@ -2032,15 +2032,8 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
                                                uint32_t wh, int b) {
     extern __shared__ float smem[];
     __shared__ uint8_t s_perm[256];
+    __shared__ uint32_t s_code_lo, s_code_hi;
     mcgd::stage_perm(s_perm);
-    // the bytecode of every program, after the operand stack (north_star:
-    // node bytecode in shared memory)
-    uint4* s_code = reinterpret_cast<uint4*>(smem + 3 * max_stack * blockDim.x);
-    if (kSmemCode) {
-        const uint4* g = reinterpret_cast<const uint4*>(R.S.code);
-        for (uint32_t k = threadIdx.x; k < R.S.n_code; k += blockDim.x) s_code[k] = __ldg(g + k);
-    }
-    __syncthreads();
     // Blocks visit the sorted list in a scattered order (concurrent mode):
     // the paths of one texel are contiguous there (Morton order), and the
     // first block to store wins the texel -- in sorted order that would be
@@ -2049,6 +2042,32 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t blk = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) * R.shade_perm) % gridDim.x);
     const uint32_t i = blk * blockDim.x + threadIdx.x;
     const uint32_t slot = i < R.n_paths ? key_slot(R, skey[i]) : R.S.n_programs;
+    // The bytecode of the block's programs (its sorted paths span one or a
+    // few material slots), after the operand stack (north_star: node bytecode
+    // in shared memory).
+    uint4* s_code = reinterpret_cast<uint4*>(smem + 3 * max_stack * blockDim.x);
+    if (kSmemCode) {
+        if (threadIdx.x == 0) {
+            const uint32_t n_prog = R.S.n_programs;
+            const uint32_t first = blk * blockDim.x;
+            const uint32_t last = min(first + blockDim.x, R.n_paths) - 1u;
+            const uint32_t s0 = first < R.n_paths ? key_slot(R, skey[first]) : n_prog;
+            const uint32_t s1 = min(key_slot(R, skey[last]), n_prog - 1u);
+            uint32_t lo = 0xffffffffu, hi = 0u;
+            for (uint32_t sl = s0; sl <= s1 && sl < n_prog; ++sl) {
+                const mcg_program pg = R.S.programs[sl];
+                lo = min(lo, pg.code_offset);
+                hi = max(hi, pg.code_offset + pg.code_len);
+            }
+            s_code_lo = lo > hi ? 0u : lo;
+            s_code_hi = hi;
+        }
+        __syncthreads();
+        const uint4* g = reinterpret_cast<const uint4*>(R.S.code);
+        const uint32_t lo = s_code_lo, hi = s_code_hi;
+        for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x) s_code[k - lo] = __ldg(g + k);
+    }
+    __syncthreads();
     const bool valid = slot < R.S.n_programs;
     const unsigned live = __ballot_sync(mcgd::kFull, valid);
     if (!valid) return;
@@ -2082,7 +2101,7 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const mcgd::Ahead ah{ahw, R.ahead_on != 0};
     const mcgd::VmResult r = mcgd::run_program<kDeferred, kSmemCode>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                                      slot, in, grp, st, s_perm, okey, R.q, cnt, ah,
-                                                                     s_code);
+                                                                     s_code, kSmemCode ? s_code_lo : 0u);
     thr.w = __uint_as_float(__float_as_uint(thr.w) + cnt.hits);
     nee_bounce(R, i, pid, pixel, b, V3{in.px, in.py, in.pz}, V3{in.nx, in.ny, in.nz}, r.value, thr, sp0.w, rd.w);
     mcgd::warp_add(R.stats + kStatLookups, cnt.lookups);
