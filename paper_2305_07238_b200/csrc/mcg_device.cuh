@@ -859,7 +859,11 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                     const uint32_t wb = (ah.w.x >> (8u + 8u * bi)) & 0xffu;
                     pr.where = wb == 0xffu ? -1 : static_cast<int32_t>(wb);
                 }
-                if (!ahead || C.trace || !__all_sync(grp, pr.hit)) {
+                // (No lane needs the descriptor when every lane hit, or --
+                // concurrent mode -- every lane's look-ahead found its cell
+                // full: no probe and no insert can follow.)
+                if (!ahead || C.trace ||
+                    !__all_sync(grp, pr.hit || (!kDeferred && MCG_VM_REPROBE && pr.where < 0))) {
                     Desc desc{prog.material_id, arg, 0u, 0u, 0u};
                     if (flags & MCG_F_USES_UV) {
                         desc.mip = mip_level(sp.g1x, sp.g1y, sp.g2x, sp.g2y, mip_offset);
@@ -942,7 +946,8 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 if (act) {
                     ++cnt.stores;
                     const float3 v = st.get(d - 1, ta);
-                    const uint32_t payload = encode_rgbe(v.x, v.y, v.z);
+                    // (a cell seen full takes no insert: no payload needed)
+                    const uint32_t payload = (kDeferred || p_where >= 0) ? encode_rgbe(v.x, v.y, v.z) : 0u;
                     if (kDeferred) {
                         const unsigned rank = __popc(m & ((1u << lane) - 1u));
                         const int ldr = __ffs(m) - 1;

@@ -566,7 +566,10 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
         uint64_t h;
         uint32_t check;
         mcgd::hash_desc(desc, h, check);
-        const mcgd::Probe pr = mcgd::probe_cell_t<1>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
+        // the whole cell in one round trip (head block + first tail pair): the
+        // epilogue has bandwidth to spare, and a filling table makes most
+        // scans run past the first pair
+        const mcgd::Probe pr = mcgd::probe_cell_t<5>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
         if (pr.hit) out.x |= 1u << c;
         pay[c] = pr.payload;
         const uint32_t wb = pr.where < 0 ? 0xffu : static_cast<uint32_t>(pr.where);
