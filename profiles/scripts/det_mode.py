@@ -16,7 +16,7 @@ scene = load_scene(bench.make_scene(tempfile.mkdtemp()))
 out = {}
 for det in (False, True):
     cfg = RenderConfig(width=bench.W, height=bench.H, spp=bench.SPP, cache_enabled=True, deterministic=det,
-                       n_cells=bench.N_CELLS, n_entries=bench.N_ENTRIES)
+                       n_cells=bench.N_CELLS, n_entries=bench.N_ENTRIES, mip_offset=bench.MIP_OFFSET)
     render(scene, cfg, ctx=ctx)
     a = render(scene, cfg, ctx=ctx)
     b = render(scene, cfg, ctx=ctx)
