@@ -605,10 +605,12 @@ def main() -> None:
     # least once. The first probe of every lookup runs in the trace kernels'
     # epilogue (look-ahead, before the sort); the shade re-probes the misses
     # (concurrent mode, cells not seen full) and stores. Shade: per shading
-    # point the two path records in (64 + 32 B) and out (32 + 32 B), per
+    # point the two path records in (64 + 32 B: shading point, direction,
+    # look-ahead result; throughput, radiance) and out (32 + 32 B), per
     # shadow-ray candidate 52 B out (16 B per rejected light); closest hit:
-    # per ray the ray record and path id in (32 + 32 B), the hit record +
-    # look-ahead result and sort key out per hit (40 B), the key per miss;
+    # per ray the ray and path id in (32 + 32 B), per hit the shading point
+    # (64 B), look-ahead result (16 B) and sort key/value (8 B) out, the key
+    # per miss;
     # per shadow ray 37 B; plus the scene once per launch. The traversal
     # kernels' node and triangle bytes are served by L1/L2 (the bench BVH is
     # a few hundred KB): (a) >> (b) for them.
@@ -626,7 +628,7 @@ def main() -> None:
     compulsory = {
         "shade": shade_probe_bytes + st_s.tex_samples * 48 + st_s.shading_points * (96 + 64)
                  + st_s.shadow_rays * 52 + (n_lights * st_s.shading_points - st_s.shadow_rays) * 16,
-        "trace_closest": (st_s.closest_rays * 64 + closest_hits * 40 + (st_s.closest_rays - closest_hits) * 8
+        "trace_closest": (st_s.closest_rays * 64 + closest_hits * 88 + (st_s.closest_rays - closest_hits) * 8
                           + lookahead_bytes),
         "trace_shadow": st_s.shadow_rays * 37,
     }

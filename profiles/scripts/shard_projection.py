@@ -17,7 +17,7 @@ from paper_2305_07238_b200 import Context, RenderConfig, load_scene, render  # n
 ctx = Context(0)
 scene = load_scene(bench.make_scene(tempfile.mkdtemp()))
 base = dict(width=bench.W, height=bench.H, spp=bench.SPP, cache_enabled=True, n_cells=bench.N_CELLS,
-            n_entries=bench.N_ENTRIES)
+            n_entries=bench.N_ENTRIES, mip_offset=bench.MIP_OFFSET)
 render(scene, RenderConfig(**base), ctx=ctx)
 full = render(scene, RenderConfig(**base), ctx=ctx)
 t1 = full.stats.device_ms
@@ -36,5 +36,6 @@ for n in (2, 4, 8):
                                         "efficiency": t1 / proj / n, "hit_rate": hits / max(1, looks)}
         print(f"N={n} {name:11s}: max shard {proj:.1f} ms (min {min(ts):.1f}) -> projected speed-up "
               f"{t1 / proj:.2f}x ({t1 / proj / n * 100:.0f}%), hit rate {hits / max(1, looks):.4f}", flush=True)
-with open(os.path.join(ROOT, "profiles", "shard_projection.json"), "w") as f:
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+with open(os.path.join(ROOT, "gpurun_out", "shard_projection.json"), "w") as f:
     json.dump(out, f, indent=1)
