@@ -10,7 +10,7 @@ Checked: inserts by one process are seen by the other; an ordered insert
 through the stripes leaves, cell by cell, exactly the words one table would
 (split by stripe); concurrent inserts from both processes keep the table's
 invariants (each cell a prefix of occupied slots, no check-hash twice, and
-every key inserted is found by both ranks unless its cell filled up)."""
+every key a rank won a slot for is found by both ranks)."""
 import os
 import socket
 import tempfile
@@ -65,7 +65,8 @@ def _worker(rank, port, out):
         tdist.barrier()
         d2, rgb2 = _descs(100 + rank, 12_000)
         shared, rgbs = _descs(7, 6_000)
-        st.update_batch(np.concatenate([d2, shared]), np.concatenate([rgb2, rgbs]), ordered=False)
+        outcome, _, _ = st.update_batch(np.concatenate([d2, shared]), np.concatenate([rgb2, rgbs]), ordered=False)
+        np.save(os.path.join(out, f"p2_outcome{rank}.npy"), outcome)
         ctx.synchronize()
         tdist.barrier()
         np.save(os.path.join(out, f"p2_words{rank}.npy"), st.slot_words())
@@ -105,14 +106,13 @@ def test_striped_table_across_processes(ctx, oracle):
     for row, o in zip(checks, occ):
         c = row[o]
         assert len(np.unique(c)) == len(c), "a check hash appears twice in one cell"
-    cell_full = occ.all(axis=1)
-    from paper_2305_07238_b200 import hash_cell
+    # every key a rank won a slot for is found by every rank (slots are
+    # write-once); LostRace drops a key, as the reference's single CAS does
     for k in range(WORLD):
         dk, _ = _descs(100 + k, 12_000)
         shared, _ = _descs(7, 6_000)
-        keys = np.concatenate([dk, shared])
-        cells = np.array([hash_cell(x) % NC for x in keys[:2000]])
+        won = L(f"p2_outcome{k}.npy") == 0          # MCG_INSERT_WON
+        assert won.sum() > 0.5 * won.size
         for r in range(WORLD):
-            h = L(f"p2_hit{r}_{k}.npy")[:2000]
-            # every key rank k inserted is found by every rank, unless its cell filled up
-            assert (h | cell_full[cells]).all()
+            h = L(f"p2_hit{r}_{k}.npy")
+            assert h[won].all()
