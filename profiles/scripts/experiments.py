@@ -56,7 +56,7 @@ def main():
     ap.add_argument("--quick", action="store_true", help="smaller sizes (smoke run)")
     ap.add_argument("--uv-span", type=float, default=0.0)
     ap.add_argument("--mip", type=int, default=0, help="mip_offset of the cached C2/C3/C5 renders")
-    ap.add_argument("--sections", default="C1,C3,C2,C5,A5,A6")
+    ap.add_argument("--sections", default="C1,C3,C2,C5,A5,A6,A7")
     ap.add_argument("--out", default=None, help="output JSON (default profiles/experiments_r1.json)")
     args = ap.parse_args()
     global UV_SPAN
@@ -105,7 +105,7 @@ def main():
             base = RenderConfig(width=W, height=H, spp=128 if not q else 8, n_cells=10_000_000, n_entries=10)
             render(s, base, ctx=ctx)
             t_off, _ = timed(s, base, ctx, 3)
-            on = RenderConfig(**{**base.__dict__, "cache_enabled": True})
+            on = RenderConfig(**{**base.__dict__, "cache_enabled": True, "mip_offset": args.mip})
             t_on, r = timed(s, on, ctx, 3)
             n = W * H * base.spp
             c3[kind] = {"ms_no_cache": t_off, "ms_cache": t_on, "speedup": t_off / t_on,
@@ -118,9 +118,9 @@ def main():
     # ---- C2: classroom WxHx32 sweep Nc x Ne ----
     if "C2" in sections:
         s = build("classroom", W, H, tmp)
-        rows = sweep(s, RenderConfig(width=W, height=H, spp=32 if not q else 4),
+        rows = sweep(s, RenderConfig(width=W, height=H, spp=32 if not q else 4, mip_offset=args.mip),
                      [100_000, 1_000_000, 10_000_000], [2, 4, 6, 8, 10], repeats=1, ctx=ctx)
-        write_sweep_csv(rows, os.path.join(OUT, "sweep_c2_classroom.csv"))
+        write_sweep_csv(rows, os.path.join(os.path.dirname(args.out) if args.out else OUT, "sweep_c2_classroom.csv"))
         res["C2"] = [r.__dict__ for r in rows]
         print("C2 done", flush=True)
 
@@ -129,7 +129,7 @@ def main():
         if not q:
             s5 = build("classroom", 3840, 2160, tmp)
             cfg5 = RenderConfig(width=3840, height=2160, spp=512, cache_enabled=True,
-                                n_cells=10_000_000, n_entries=10)
+                                n_cells=10_000_000, n_entries=10, mip_offset=args.mip)
             ms5, r5 = timed(s5, cfg5, ctx, 1)
             res["C5"] = {"ms": ms5, "samples_per_s": 3840 * 2160 * 512 / (ms5 / 1e3),
                          "hit_rate": r5.stats.hit_rate, "n_gpus": 1}
@@ -181,20 +181,24 @@ def main():
         print("A6", res["A6_cache_size_trend"]["hit_rate_nondecreasing_in_cells"], ent, sat, flush=True)
 
     # ---- A7: speed-up direction (median of 3) ----
-    a7 = {}
-    for kind in ("classroom", "hostile"):
-        s = build(kind, W, H, tmp)
-        base = RenderConfig(width=W, height=H, spp=128 if not q else 8, n_cells=10_000_000, n_entries=10)
-        render(s, base, ctx=ctx)
-        t_off, _ = timed(s, base, ctx, 3)
-        t_on, _ = timed(s, RenderConfig(**{**base.__dict__, "cache_enabled": True}), ctx, 3)
-        a7[kind] = {"relative_time_pct": 100 * t_on / t_off}
-    a7["criterion7"] = bool(a7["classroom"]["relative_time_pct"] <= 95 and
-                            a7["hostile"]["relative_time_pct"] <= 103)
-    res["A7_speedup_direction"] = a7
-    print("A7", a7, flush=True)
+    if "A7" in sections:
+        a7 = {}
+        for kind in ("classroom", "hostile"):
+            s = build(kind, W, H, tmp)
+            base = RenderConfig(width=W, height=H, spp=128 if not q else 8, n_cells=10_000_000, n_entries=10)
+            render(s, base, ctx=ctx)
+            t_off, _ = timed(s, base, ctx, 3)
+            t_on, _ = timed(s, RenderConfig(**{**base.__dict__, "cache_enabled": True, "mip_offset": args.mip}),
+                            ctx, 3)
+            a7[kind] = {"relative_time_pct": 100 * t_on / t_off}
+        a7["criterion7"] = bool(a7["classroom"]["relative_time_pct"] <= 95 and
+                                a7["hostile"]["relative_time_pct"] <= 103)
+        res["A7_speedup_direction"] = a7
+        print("A7", a7, flush=True)
 
-    with open(os.path.join(OUT, "experiments_r1.json" if not q else "experiments_quick.json"), "w") as f:
+    res["tuning"] = {"uv_span": args.uv_span, "mip_offset": args.mip}
+    out = args.out or os.path.join(OUT, "experiments_r1.json" if not q else "experiments_quick.json")
+    with open(out, "w") as f:
         json.dump(res, f, indent=1)
 
 
