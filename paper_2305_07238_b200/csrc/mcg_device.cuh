@@ -577,14 +577,17 @@ struct SceneView {
     const uint2* ahead_cp;
 };
 
-// Cache points per material probed ahead of the shade (k_lookahead); their
-// results travel in one uint4 per path: x = hit bits (0..2) and the first
-// empty slot each probe saw (bits 8+8c, 0xff = cell full), y/z/w = payloads.
-constexpr uint32_t kAhead = 3;
+// Cache points per material probed ahead of the shade (look_ahead, in the
+// trace kernels); their results travel in the path's ray record: a flags
+// word (bit c: cache point c hit; bit 8 + c: its cell was full without the
+// key) and one payload word per cache point.
+constexpr uint32_t kAhead = 8;
 constexpr uint32_t kAheadValid = 0x100u;
+constexpr uint32_t kAheadFull = 8u;   // flags shift of the cell-full bits
 
 struct Ahead {
-    uint4 w;
+    uint32_t flags;
+    const uint32_t* pay;   // kAhead payload words (in the path's record)
     bool on;
 };
 
@@ -854,10 +857,11 @@ __device__ __forceinline__ VmResult run_program(const SceneView& S, const CacheV
                 const bool ahead = ah.on && bi < kAhead;
                 Probe pr{0u, -1, false};
                 if (ahead) {
-                    pr.hit = ((ah.w.x >> bi) & 1u) != 0u;
-                    pr.payload = bi == 0u ? ah.w.y : (bi == 1u ? ah.w.z : ah.w.w);
-                    const uint32_t wb = (ah.w.x >> (8u + 8u * bi)) & 0xffu;
-                    pr.where = wb == 0xffu ? -1 : static_cast<int32_t>(wb);
+                    // (no slot hint: a miss in a cell with room probes again
+                    // below -- concurrent mode -- or is queued -- deterministic)
+                    pr.hit = ((ah.flags >> bi) & 1u) != 0u;
+                    if (pr.hit) pr.payload = __ldg(ah.pay + bi);
+                    pr.where = ((ah.flags >> (kAheadFull + bi)) & 1u) ? -1 : 0;
                 }
                 // (No lane needs the descriptor when every lane hit, or --
                 // concurrent mode -- every lane's look-ahead found its cell

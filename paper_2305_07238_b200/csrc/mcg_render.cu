@@ -65,9 +65,8 @@ struct __align__(128) PathRay {
     float4 sp0;     // hit position, propagated cone width
     float4 sp1;     // shading normal, pixel index (uint bits)
     float4 sp2;     // u, v, g1
-    float4 sp3;     // g2, -, -
-    uint4 ahead;    // look-ahead results (mcgd::kAhead)
-    float4 pad;
+    float4 sp3;     // g2, look-ahead flags (uint bits), -
+    uint32_t ahead[8];   // look-ahead payloads (mcgd::kAhead)
 };
 // A path's value record (32 bytes): throughput.rgb + nodes_found (uint bits),
 // radiance.rgb + path id (uint bits: pass slot j * n_pix + shard pixel index).
@@ -551,17 +550,17 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
     const uint32_t slot = key_slot(R, key);
     const mcg_program prog = R.S.programs[slot];
     const uint32_t ncp = min(prog.cache_point_count, mcgd::kAhead);
-    uint4 out = make_uint4(0xffffff00u, 0u, 0u, 0u);
-    uint32_t pay[mcgd::kAhead] = {0u, 0u, 0u};
-#pragma unroll
-    for (uint32_t c = 0; c < mcgd::kAhead; ++c) {
-        if (c >= ncp) break;
+    uint32_t flags = 0u;
+    PathRay& rec = R.pa[q];
+    const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
+    const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
+    for (uint32_t c = 0; c < ncp; ++c) {
         const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
         mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
         if (cp.y & MCG_F_USES_UV) {
-            desc.mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
-            desc.tx = mcgd::texel_index(in.u, desc.mip);
-            desc.ty = mcgd::texel_index(in.v, desc.mip);
+            desc.mip = mip;
+            desc.tx = tx;
+            desc.ty = ty;
         }
         uint64_t h;
         uint32_t check;
@@ -570,16 +569,15 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
         // epilogue has bandwidth to spare, and a filling table makes most
         // scans run past the first pair
         const mcgd::Probe pr = mcgd::probe_cell_t<5>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
-        if (pr.hit) out.x |= 1u << c;
-        pay[c] = pr.payload;
-        const uint32_t wb = pr.where < 0 ? 0xffu : static_cast<uint32_t>(pr.where);
-        out.x = (out.x & ~(0xffu << (8u + 8u * c))) | (wb << (8u + 8u * c));
+        if (pr.hit) {
+            flags |= 1u << c;
+            rec.ahead[c] = pr.payload;
+        } else if (pr.where < 0) {
+            flags |= 1u << (mcgd::kAheadFull + c);
+        }
     }
-    out.y = pay[0];
-    out.z = pay[1];
-    out.w = pay[2];
-    R.pa[q].ahead = out;
-    return key | ((out.x & R.pat_mask) << R.key_pat);
+    rec.sp3.z = __uint_as_float(flags);
+    return key | ((flags & R.pat_mask) << R.key_pat);
 }
 
 // Closest hit of the path at layout position q (path id pid): the hit
@@ -612,7 +610,7 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     rec.sp0 = make_float4(s.p.x, s.p.y, s.p.z, ro.w);
     rec.sp1 = make_float4(s.n.x, s.n.y, s.n.z, __uint_as_float(pixel));
     rec.sp2 = make_float4(s.u, s.v, g1.x, g1.y);
-    rec.sp3 = make_float4(g2.x, g2.y, 0.0f, 0.0f);
+    rec.sp3 = make_float4(g2.x, g2.y, __uint_as_float(0u), 0.0f);
     if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
     // the look-ahead probe right here
     const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
@@ -2085,7 +2083,6 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const unsigned grp = __match_any_sync(live, slot);
     const PathRay& pr = R.pa[q];
     const float4 rd = pr.rd, sp0 = pr.sp0, sp1 = pr.sp1, sp2 = pr.sp2, sp3 = pr.sp3;
-    const uint4 ahw = pr.ahead;
     const PathVal pv = R.pb[q];
     const uint32_t pid = __float_as_uint(pv.L.w);
     MCG_CHECK(pid < R.n_paths);
@@ -2101,7 +2098,7 @@ __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(Rende
     const uint32_t pixel = __float_as_uint(sp1.w);
     const uint32_t okey = (slot_j * wh + pixel) << 6;
     mcgd::VmCounters cnt;
-    const mcgd::Ahead ah{ahw, R.ahead_on != 0};
+    const mcgd::Ahead ah{__float_as_uint(sp3.z), pr.ahead, R.ahead_on != 0};
     const mcgd::VmResult r = mcgd::run_program<kDeferred, kSmemCode>(R.S, R.C, R.cache_on != 0, R.mip_offset,
                                                                      slot, in, grp, st, s_perm, okey, R.q, cnt, ah,
                                                                      s_code, kSmemCode ? s_code_lo : 0u);
