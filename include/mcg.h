@@ -184,13 +184,11 @@ mcg_status mcg_cache_counters_get(mcg_cache* cache, mcg_cache_counters* out);
 mcg_status mcg_cache_counters_reset(mcg_cache* cache);
 /* dump (cache.cpp:159-173): u64 n_cells, u64 n_entries, then every slot word, LE. */
 mcg_status mcg_cache_dump(mcg_cache* cache, const char* path);
-/* Device pointer of the slot array, for tooling. Layout: for
- * 8 < n_entries <= 16, one 128-byte record per cell (the cell's n_entries
- * words, then zero padding to 16 words: a full scan stays in one line);
- * otherwise a head array of n_cells x min(n_entries, 8) words (one 64-byte
- * DRAM block per cell), then a tail array of n_cells x (n_entries - 8) words
- * when n_entries > 16. Slot indices everywhere else in this API are the
- * logical cell * n_entries + entry. */
+/* Device pointer of the slot array, for tooling. Layout: a head array of
+ * n_cells x min(n_entries, 8) words (a cell's first slots, one 64-byte DRAM
+ * block), then a tail array of n_cells x (n_entries - 8) words when
+ * n_entries > 8. Slot indices everywhere else in this API are the logical
+ * cell * n_entries + entry. */
 uint64_t* mcg_cache_device_slots(mcg_cache* cache);
 
 /* Striped shared table (one logical Nc x Ne table over `world`

@@ -108,27 +108,11 @@ struct mcg_cache {
     uint32_t* ilog = nullptr;
     unsigned long long* ilog_count = nullptr;
     uint64_t ilog_cap = 0, ilog_alloc = 0;
-    // physical layout (mcgd::CacheView): 128-byte cell records for
-    // 8 < n_entries <= 16, else dense head and tail arrays
-    uint32_t head_stride = 0, tail_stride = 0;
-    bool interleaved = false;
-    void set_layout() {
-        head_n = head_slots(n_entries);
-        interleaved = n_entries > 8u && n_entries <= 16u;
-        head_stride = interleaved ? 16u : head_n;
-        tail_stride = interleaved ? 16u : n_entries - head_n;
-    }
-    uint64_t local_words() const { return local_cells * n_entries; }   // logical slots held here
-    uint64_t alloc_words() const { return interleaved ? local_cells * 16u : local_words(); }  // incl. padding
-    // the tail array of a stripe whose head array starts at `base`
-    uint64_t* tail_of(uint64_t* base, uint64_t cells) const {
-        if (n_entries <= head_n || !base) return nullptr;
-        return interleaved ? base + 8 : base + cells * head_n;
-    }
-    uint64_t* tail() const { return tail_of(slots, local_cells); }
+    uint64_t local_words() const { return local_cells * n_entries; }   // slots held here (head + tail)
+    uint64_t* tail() const { return n_entries > head_n ? slots + local_cells * head_n : nullptr; }
     mcgd::CacheView view() const {
         return {slots, tail(), n_cells, magic, n_entries, head_n, world, stripes, trace, trace_count, trace_cap,
-                ilog_cap ? ilog : nullptr, ilog_count, ilog_cap, head_stride, tail_stride};
+                ilog_cap ? ilog : nullptr, ilog_count, ilog_cap};
     }
 };
 

@@ -16,16 +16,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // ---------------------------------------------------------------------------
 // Table view
 // ---------------------------------------------------------------------------
-// Physical layout of a table (mcg_ctx.cuh mcg_cache::set_layout): a cell's
-// first head_n = min(Ne, 8) slots (one 64-byte DRAM block) at
-// slots + cell * head_stride, the rest at tail + cell * tail_stride. For
-// 8 < Ne <= 16 every cell is one 128-byte record (head_stride = tail_stride
-// = 16 words, tail = slots + 8): a full scan of a cell stays inside one
-// 128-byte line -- one random DRAM access, not two. Otherwise heads and
-// tails are two dense arrays.
 struct CacheView {
-    uint64_t* slots;          // head words
-    uint64_t* tail;           // tail words, or null
+    uint64_t* slots;          // head words: n_cells x head_n, cell-major
+    uint64_t* tail;           // tail words: n_cells x (n_entries - head_n), or null
     uint64_t n_cells;
     uint64_t magic;           // floor((2^64-1) / n_cells) for fast_mod
     uint32_t n_entries;
@@ -38,8 +31,6 @@ struct CacheView {
     uint32_t* ilog;           // optional log of won inserts: 7 words each (mcg_insert_record)
     unsigned long long* ilog_count;
     uint64_t ilog_cap;
-    uint32_t head_stride;     // words from one cell's head to the next's
-    uint32_t tail_stride;     // words from one cell's tail to the next's
 };
 
 // Appends a won insert (descriptor, entry within the cell, payload) to the
@@ -70,12 +61,13 @@ __device__ __forceinline__ void log_insert(const CacheView& c, uint32_t mat, uin
 // so every device sees the same logical table.
 __device__ __forceinline__ uint64_t* head_words(const CacheView& c, uint64_t cell) {
     MCG_CHECK(cell < c.n_cells);
-    if (c.world <= 1u) return c.slots + cell * c.head_stride;
-    return c.stripes[2 * (cell % c.world)] + (cell / c.world) * c.head_stride;
+    if (c.world <= 1u) return c.slots + cell * c.head_n;
+    return c.stripes[2 * (cell % c.world)] + (cell / c.world) * c.head_n;
 }
 __device__ __forceinline__ uint64_t* tail_words(const CacheView& c, uint64_t cell) {
-    if (c.world <= 1u) return c.tail + cell * c.tail_stride;
-    return c.stripes[2 * (cell % c.world) + 1] + (cell / c.world) * c.tail_stride;
+    const uint32_t tn = c.n_entries - c.head_n;
+    if (c.world <= 1u) return c.tail + cell * tn;
+    return c.stripes[2 * (cell % c.world) + 1] + (cell / c.world) * tn;
 }
 __device__ __forceinline__ uint64_t* slot_ptr(const CacheView& c, uint64_t cell, uint32_t e) {
     MCG_CHECK(cell < c.n_cells && e < c.n_entries);

@@ -959,10 +959,9 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
         c->ctx = ctx;
         c->n_cells = n_cells;
         c->n_entries = n_entries;
+        c->head_n = head_slots(n_entries);
         c->magic = mod_magic(n_cells);
         c->local_cells = n_cells;
-        c->set_layout();
-        bytes = std::max<uint64_t>(8, c->alloc_words() * 8);
         cudaError_t e = cudaMalloc(&c->slots, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -982,8 +981,7 @@ mcg_status mcg_cache_create(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_entries, 
 static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* out) {
     mcg_ctx* ctx = cache->ctx;
     const uint32_t ne = cache->n_entries, hn = cache->head_n, tn = ne - hn;
-    const uint32_t hs = cache->head_stride, ts = cache->tail_stride;
-    if (tn == 0 && hs == ne) {
+    if (tn == 0) {
         dev_download(ctx, out, cache->slots + first, n);
         sync(ctx);
         return;
@@ -991,12 +989,10 @@ static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* o
     const uint64_t c0 = first / ne, c1 = (first + n + ne - 1) / ne;
     std::vector<uint64_t> tmp((c1 - c0) * ne);
     // heads into columns [0, hn), tails into [hn, ne) of each logical cell
-    cuda_check(cudaMemcpy2DAsync(tmp.data(), ne * 8ull, cache->slots + c0 * hs, hs * 8ull, hn * 8ull, c1 - c0,
+    cuda_check(cudaMemcpy2DAsync(tmp.data(), ne * 8ull, cache->slots + c0 * hn, hn * 8ull, hn * 8ull, c1 - c0,
                                  cudaMemcpyDeviceToHost, ctx->stream), "D2H heads");
-    if (tn) {
-        cuda_check(cudaMemcpy2DAsync(tmp.data() + hn, ne * 8ull, cache->tail() + c0 * ts, ts * 8ull, tn * 8ull,
-                                     c1 - c0, cudaMemcpyDeviceToHost, ctx->stream), "D2H tails");
-    }
+    cuda_check(cudaMemcpy2DAsync(tmp.data() + hn, ne * 8ull, cache->tail() + c0 * tn, tn * 8ull, tn * 8ull,
+                                 c1 - c0, cudaMemcpyDeviceToHost, ctx->stream), "D2H tails");
     sync(ctx);
     std::memcpy(out, tmp.data() + (first - c0 * ne), n * 8);
 }
@@ -1006,8 +1002,7 @@ static void read_logical(mcg_cache* cache, uint64_t first, size_t n, uint64_t* o
 static void write_logical(mcg_cache* cache, uint64_t first, size_t n, const uint64_t* in) {
     mcg_ctx* ctx = cache->ctx;
     const uint32_t ne = cache->n_entries, hn = cache->head_n, tn = ne - hn;
-    const uint32_t hs = cache->head_stride, ts = cache->tail_stride;
-    if (tn == 0 && hs == ne) {
+    if (tn == 0) {
         cuda_check(cudaMemcpyAsync(cache->slots + first, in, n * 8ull, cudaMemcpyHostToDevice, ctx->stream), "H2D");
         sync(ctx);
         return;
@@ -1016,12 +1011,10 @@ static void write_logical(mcg_cache* cache, uint64_t first, size_t n, const uint
     std::vector<uint64_t> tmp((c1 - c0) * ne);
     if (first % ne != 0 || (first + n) % ne != 0) read_logical(cache, c0 * ne, tmp.size(), tmp.data());
     std::memcpy(tmp.data() + (first - c0 * ne), in, n * 8);
-    cuda_check(cudaMemcpy2DAsync(cache->slots + c0 * hs, hs * 8ull, tmp.data(), ne * 8ull, hn * 8ull, c1 - c0,
+    cuda_check(cudaMemcpy2DAsync(cache->slots + c0 * hn, hn * 8ull, tmp.data(), ne * 8ull, hn * 8ull, c1 - c0,
                                  cudaMemcpyHostToDevice, ctx->stream), "H2D heads");
-    if (tn) {
-        cuda_check(cudaMemcpy2DAsync(cache->tail() + c0 * ts, ts * 8ull, tmp.data() + hn, ne * 8ull, tn * 8ull,
-                                     c1 - c0, cudaMemcpyHostToDevice, ctx->stream), "H2D tails");
-    }
+    cuda_check(cudaMemcpy2DAsync(cache->tail() + c0 * tn, tn * 8ull, tmp.data() + hn, ne * 8ull, tn * 8ull,
+                                 c1 - c0, cudaMemcpyHostToDevice, ctx->stream), "H2D tails");
     sync(ctx);
 }
 
@@ -1059,9 +1052,9 @@ mcg_status mcg_cache_create_stripe(mcg_ctx* ctx, uint64_t n_cells, uint32_t n_en
         c->magic = mod_magic(n_cells);
         c->world = world;
         c->rank = rank;
+        c->head_n = head_slots(n_entries);
         c->local_cells = n_cells > rank ? (n_cells - rank + world - 1) / world : 0;
-        c->set_layout();
-        const size_t local_bytes = std::max<uint64_t>(8, c->alloc_words() * 8);
+        const size_t local_bytes = std::max<uint64_t>(8, c->local_words() * 8);
         cudaError_t e = cudaMalloc(&c->slots, local_bytes);
         if (e == cudaSuccess) e = cudaMalloc(&c->counters, 8 * sizeof(unsigned long long));
         if (e != cudaSuccess) {
@@ -1130,7 +1123,7 @@ mcg_status mcg_cache_attach_ipc(mcg_cache* cache, const void* handles, uint32_t 
             cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
             cache->ipc_opened.push_back(p);
             ptrs[2 * r] = static_cast<uint64_t*>(p);
-            ptrs[2 * r + 1] = cache->tail_of(ptrs[2 * r], cells_r);
+            ptrs[2 * r + 1] = cache->n_entries > cache->head_n ? ptrs[2 * r] + cells_r * cache->head_n : nullptr;
         }
         upload_stripes(cache, ptrs);
     });
@@ -1149,7 +1142,7 @@ mcg_status mcg_cache_stripe_info(const mcg_cache* cache, uint32_t* rank, uint32_
 mcg_status mcg_cache_clear(mcg_cache* cache) {
     return guarded([&] {
         need(cache != nullptr, "null cache");
-        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->alloc_words() * 8,
+        cuda_check(cudaMemsetAsync(cache->slots, 0, cache->local_words() * 8,
                                    cache->ctx->stream), "memset cache");
         cuda_check(cudaMemsetAsync(cache->counters, 0, 8 * sizeof(unsigned long long),
                                    cache->ctx->stream), "memset counters");
@@ -1286,7 +1279,7 @@ mcg_status mcg_cache_occupied(mcg_cache* cache, uint64_t* occupied) {
         need(cache && occupied, "null argument");
         mcg_ctx* ctx = cache->ctx;
         cuda_check(cudaMemsetAsync(cache->counters + 7, 0, 8, ctx->stream), "memset");
-        const uint64_t n = cache->alloc_words();   // head and tail words (padding words stay zero)
+        const uint64_t n = cache->local_words();   // head and tail arrays
         LaunchScope ls(ctx, "occupied", n * 8.0);
         k_occupied<<<148 * 8, 256, 0, ctx->stream>>>(cache->slots, n, cache->counters + 7);
         ls.done();
