@@ -545,16 +545,19 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // The look-ahead probe of the live hit at layout position q with shading
 // point `in` (k_lookahead below): its material's first kAhead cache points,
 // results to R.ahead[q]; returns the sort key with the hit bits added.
+// cache points probed in the trace kernels' epilogue (the sort key's hit bits)
+constexpr uint32_t kAheadInTrace = 2;
+
 __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, uint32_t key,
-                                               const mcgd::ShadeIn& in) {
+                                               const mcgd::ShadeIn& in, uint32_t c_begin = 0u,
+                                               uint32_t c_end = mcgd::kAhead, uint32_t flags = 0u) {
     const uint32_t slot = key_slot(R, key);
     const mcg_program prog = R.S.programs[slot];
-    const uint32_t ncp = min(prog.cache_point_count, mcgd::kAhead);
-    uint32_t flags = 0u;
+    const uint32_t ncp = min(min(prog.cache_point_count, mcgd::kAhead), c_end);
     PathRay& rec = R.pa[q];
     const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
     const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
-    for (uint32_t c = 0; c < ncp; ++c) {
+    for (uint32_t c = c_begin; c < ncp; ++c) {
         const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
         mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
         if (cp.y & MCG_F_USES_UV) {
@@ -612,10 +615,12 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     rec.sp2 = make_float4(s.u, s.v, g1.x, g1.y);
     rec.sp3 = make_float4(g2.x, g2.y, __uint_as_float(0u), 0.0f);
     if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
-    // the look-ahead probe right here
+    // the look-ahead probes of the first cache points right here (their hit
+    // bits enter the sort key); the rest run in k_lookahead_rest, off this
+    // issue-bound kernel's latency chain
     const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
                            s.u, s.v, g1.x, g1.y, g2.x, g2.y};
-    return look_ahead(R, q, key, in);
+    return look_ahead(R, q, key, in, 0u, kAheadInTrace);
 }
 
 // The shading point the trace kernel stored in a path's ray record.
@@ -1962,6 +1967,21 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
 // interleavings the reference's threads allow (slots are write-once, a hit
 // stays valid). Deterministic mode: the probe runs after the previous epoch's
 // ordered apply, so it reads the epoch-start table -- the same rule.
+// Look-ahead probes of cache points kAheadInTrace.. of every live hit
+// (materials with more cache points than the trace epilogue probes): a
+// light, high-occupancy kernel after the trace kernel, concurrent with the
+// shadow rays; ORs its hit / cell-full bits into the record's flags.
+__global__ void __launch_bounds__(256) k_lookahead_rest(RenderView R, const uint32_t* count) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (count ? *count : R.n_paths)) return;
+    const uint32_t key = R.keys[q];
+    const uint32_t slot = key_slot(R, key);
+    if (slot >= R.S.n_programs || R.S.programs[slot].cache_point_count <= kAheadInTrace) return;
+    const PathRay& pr = R.pa[q];
+    const mcgd::ShadeIn in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
+    look_ahead(R, q, key, in, kAheadInTrace, mcgd::kAhead, __float_as_uint(pr.sp3.z));
+}
+
 __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t* count) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (count ? *count : R.n_paths)) return;
@@ -2359,7 +2379,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     const bool morton = sort_mode != "material";
     const int slot_bits = std::max(1, bits_for(D.view.n_programs));
     const char* mb_env = std::getenv("MCG_MORTON_BITS");   // 2^b cells per axis
-    const int mb = mb_env ? std::min(8, std::max(1, std::atoi(mb_env))) : (sort_mode == "morton" ? 7 : 6);
+    int mb = mb_env ? std::min(8, std::max(1, std::atoi(mb_env))) : (sort_mode == "morton" ? 7 : 6);
+    if (!mb_env && sort_mode == "dir3") {
+        // keep the key within 24 bits (three radix passes): scenes with more
+        // materials and look-ahead bits give up Morton precision first
+        const int pb = look_ahead ? static_cast<int>(std::min<uint32_t>(2u, D.max_cache_points)) : 0;
+        while (mb > 4 && 3 * mb + 3 + pb + slot_bits > 24) --mb;
+    }
     R.key_shift = (morton && slot_bits <= 8) ? static_cast<uint32_t>(3 * mb) : 0u;
     R.key_dir = 0u;
     if (R.key_shift && sort_mode == "dir") {
@@ -2473,6 +2499,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             LaunchScope ls(ctx, "lookahead", 0.0, sm);
             k_lookahead<<<grid, 256, 0, sm>>>(R, nullptr);
             ls.done();
+        } else if (look_ahead && D.max_cache_points > kAheadInTrace) {
+            LaunchScope ls(ctx, "lookahead", 0.0, sm);
+            k_lookahead_rest<<<grid, 256, 0, sm>>>(R, nullptr);
+            ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
             // Stable radix sort of (key -> layout position): hits in
@@ -2539,6 +2569,10 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             if (b < P.max_bounces && look_ahead && !R.ahead_fused) {
                 LaunchScope ls(ctx, "lookahead", 0.0, sm);
                 k_lookahead<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
+                ls.done();
+            } else if (b < P.max_bounces && look_ahead && D.max_cache_points > kAheadInTrace) {
+                LaunchScope ls(ctx, "lookahead", 0.0, sm);
+                k_lookahead_rest<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
                 ls.done();
             }
             if (fork) cuda_check(cudaStreamWaitEvent(sm, lane_join[l], 0), "wait");
