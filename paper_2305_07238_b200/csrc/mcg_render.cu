@@ -545,9 +545,6 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // The look-ahead probe of the live hit at layout position q with shading
 // point `in` (k_lookahead below): its material's first kAhead cache points,
 // results to R.ahead[q]; returns the sort key with the hit bits added.
-// cache points probed in the trace kernels' epilogue (the sort key's hit bits)
-constexpr uint32_t kAheadInTrace = 2;
-
 __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, uint32_t key,
                                                const mcgd::ShadeIn& in, uint32_t c_begin = 0u,
                                                uint32_t c_end = mcgd::kAhead, uint32_t flags = 0u) {
@@ -615,12 +612,12 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     rec.sp2 = make_float4(s.u, s.v, g1.x, g1.y);
     rec.sp3 = make_float4(g2.x, g2.y, __uint_as_float(0u), 0.0f);
     if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
-    // the look-ahead probes of the first cache points right here (their hit
-    // bits enter the sort key); the rest run in k_lookahead_rest, off this
-    // issue-bound kernel's latency chain
+    // the look-ahead probes right here (a separate kernel for the cache
+    // points past the first two, after the trace, measured slower: monster
+    // analogue 1363 vs 1285 ms per render)
     const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
                            s.u, s.v, g1.x, g1.y, g2.x, g2.y};
-    return look_ahead(R, q, key, in, 0u, kAheadInTrace);
+    return look_ahead(R, q, key, in);
 }
 
 // The shading point the trace kernel stored in a path's ray record.
@@ -1967,21 +1964,6 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
 // interleavings the reference's threads allow (slots are write-once, a hit
 // stays valid). Deterministic mode: the probe runs after the previous epoch's
 // ordered apply, so it reads the epoch-start table -- the same rule.
-// Look-ahead probes of cache points kAheadInTrace.. of every live hit
-// (materials with more cache points than the trace epilogue probes): a
-// light, high-occupancy kernel after the trace kernel, concurrent with the
-// shadow rays; ORs its hit / cell-full bits into the record's flags.
-__global__ void __launch_bounds__(256) k_lookahead_rest(RenderView R, const uint32_t* count) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= (count ? *count : R.n_paths)) return;
-    const uint32_t key = R.keys[q];
-    const uint32_t slot = key_slot(R, key);
-    if (slot >= R.S.n_programs || R.S.programs[slot].cache_point_count <= kAheadInTrace) return;
-    const PathRay& pr = R.pa[q];
-    const mcgd::ShadeIn in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
-    look_ahead(R, q, key, in, kAheadInTrace, mcgd::kAhead, __float_as_uint(pr.sp3.z));
-}
-
 __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t* count) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (count ? *count : R.n_paths)) return;
@@ -2499,10 +2481,6 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             LaunchScope ls(ctx, "lookahead", 0.0, sm);
             k_lookahead<<<grid, 256, 0, sm>>>(R, nullptr);
             ls.done();
-        } else if (look_ahead && D.max_cache_points > kAheadInTrace) {
-            LaunchScope ls(ctx, "lookahead", 0.0, sm);
-            k_lookahead_rest<<<grid, 256, 0, sm>>>(R, nullptr);
-            ls.done();
         }
         for (int b = 0; b <= P.max_bounces; ++b) {
             // Stable radix sort of (key -> layout position): hits in
@@ -2569,10 +2547,6 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             if (b < P.max_bounces && look_ahead && !R.ahead_fused) {
                 LaunchScope ls(ctx, "lookahead", 0.0, sm);
                 k_lookahead<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
-                ls.done();
-            } else if (b < P.max_bounces && look_ahead && D.max_cache_points > kAheadInTrace) {
-                LaunchScope ls(ctx, "lookahead", 0.0, sm);
-                k_lookahead_rest<<<grid, 256, 0, sm>>>(R, R.shadow_count + 2);
                 ls.done();
             }
             if (fork) cuda_check(cudaStreamWaitEvent(sm, lane_join[l], 0), "wait");
