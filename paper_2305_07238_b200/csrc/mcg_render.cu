@@ -552,6 +552,7 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
     const mcg_program prog = R.S.programs[slot];
     const uint32_t ncp = min(min(prog.cache_point_count, mcgd::kAhead), c_end);
     PathRay& rec = R.pa[q];
+    uint32_t kbits = 0u;   // hit bits of the table's first two entries (the sort key's)
     const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
     const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
     for (uint32_t c = c_begin; c < ncp; ++c) {
@@ -569,15 +570,17 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
         // epilogue has bandwidth to spare, and a filling table makes most
         // scans run past the first pair
         const mcgd::Probe pr = mcgd::probe_cell_t<5>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
+        const uint32_t bi = (cp.y >> 16) & 0xffu;   // the bracket: flag bits and payloads are by bracket
         if (pr.hit) {
-            flags |= 1u << c;
-            rec.ahead[c] = pr.payload;
+            flags |= 1u << bi;
+            rec.ahead[bi] = pr.payload;
+            if (c < 2u) kbits |= 1u << c;
         } else if (pr.where < 0) {
-            flags |= 1u << (mcgd::kAheadFull + c);
+            flags |= 1u << (mcgd::kAheadFull + bi);
         }
     }
     rec.sp3.z = __uint_as_float(flags);
-    return key | ((flags & R.pat_mask) << R.key_pat);
+    return key | ((kbits & R.pat_mask) << R.key_pat);
 }
 
 // Closest hit of the path at layout position q (path id pid): the hit

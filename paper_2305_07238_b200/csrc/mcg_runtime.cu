@@ -1724,18 +1724,29 @@ mcg_status mcg_upload_scene(mcg_ctx* ctx, const mcg_scene* scene) {
         D.bufs[7].ensure((f.n_code + 1) * sizeof(mcg_insn));
         v.code = static_cast<const mcg_insn*>(up(7, f.code, f.n_code * sizeof(mcg_insn)));
         v.n_code = f.n_code;
-        // The look-ahead table: each program's first kAhead cache points
-        // (CacheLookup node and uses_uv flag, in bracket order).
+        // The look-ahead table: per program, its cache points with bracket
+        // < kAhead (CacheLookup node, uses_uv flag, bracket index in bits
+        // 16-23), largest subtree (skip_offset) first: the first two give
+        // the sort key's hit bits, so warps are uniform on the brackets that
+        // cost the most (MCG_AHEAD_ORDER=bracket: bracket order).
         {
+            const char* ao_env = std::getenv("MCG_AHEAD_ORDER");
+            const bool by_size = !(ao_env && std::string(ao_env) == "bracket");
             std::vector<uint2> acp(static_cast<size_t>(f.n_programs) * mcgd::kAhead, make_uint2(0u, 0u));
             for (uint32_t i = 0; i < f.n_programs; ++i) {
                 const mcg_program& pr = f.programs[i];
+                std::vector<std::pair<int32_t, uint2>> cps;   // (-subtree size, entry)
                 for (uint32_t c = 0; c < pr.code_len; ++c) {
                     const mcg_insn& in = f.code[pr.code_offset + c];
                     if (in.op == MCG_OP_CACHE_LOOKUP && in.bracket < mcgd::kAhead) {
-                        acp[i * mcgd::kAhead + in.bracket] = make_uint2(in.arg, (in.flags & MCG_F_USES_UV) | mcgd::kAheadValid);
+                        const uint2 e = make_uint2(in.arg, (in.flags & MCG_F_USES_UV) | mcgd::kAheadValid |
+                                                               (static_cast<uint32_t>(in.bracket) << 16));
+                        cps.push_back({by_size ? -in.imm.i : static_cast<int32_t>(in.bracket), e});
                     }
                 }
+                std::stable_sort(cps.begin(), cps.end(),
+                                 [](const auto& a, const auto& b) { return a.first < b.first; });
+                for (size_t k = 0; k < cps.size() && k < mcgd::kAhead; ++k) acp[i * mcgd::kAhead + k] = cps[k].second;
             }
             v.ahead_cp = static_cast<const uint2*>(up(19, acp.data(), acp.size() * sizeof(uint2)));
         }
