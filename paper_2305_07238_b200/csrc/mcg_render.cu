@@ -545,58 +545,41 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // The look-ahead probe of the live hit at layout position q with shading
 // point `in` (k_lookahead below): its material's first kAhead cache points,
 // results to R.ahead[q]; returns the sort key with the hit bits added.
-__device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, bool valid, uint32_t key,
-                                               const mcgd::ShadeIn& in) {
-    const unsigned lane = threadIdx.x & 31u;
-    const unsigned vm = __ballot_sync(mcgd::kFull, valid);
-    if (!vm) return key;
-    const uint32_t slot = valid ? key_slot(R, key) : 0u;
-    const uint32_t ncp = valid ? min(R.S.programs[slot].cache_point_count, mcgd::kAhead) : 0u;
-    const uint32_t mat = valid ? R.S.programs[slot].material_id : 0u;
-    const uint32_t maxc = __reduce_max_sync(mcgd::kFull, ncp);
-    uint32_t mip = 0u, tx = 0u, ty = 0u;
-    if (valid) {
-        mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
-        tx = mcgd::texel_index(in.u, mip);
-        ty = mcgd::texel_index(in.v, mip);
-    }
-    uint32_t flags = 0u, kbits = 0u;
-    for (uint32_t c = 0; c < maxc; ++c) {
-        const bool has = c < ncp;
-        const unsigned pm = __ballot_sync(mcgd::kFull, has);
-        if (has) {
-            const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
-            mcgd::Desc desc{mat, cp.x, 0u, 0u, 0u};
-            if (cp.y & MCG_F_USES_UV) {
-                desc.mip = mip;
-                desc.tx = tx;
-                desc.ty = ty;
-            }
-            uint64_t h;
-            uint32_t check;
-            mcgd::hash_desc(desc, h, check);
-            const uint64_t cell = mcgd::fast_mod(h, R.C.n_cells, R.C.magic);
-            // lanes asking for the same (cell, check) share one probe (one
-            // leader reads the whole cell: head block + first tail pair)
-            const unsigned peers = __match_any_sync(pm, (cell << 32) ^ check);
-            const int leader = __ffs(peers) - 1;
-            mcgd::Probe pr{0u, -1, false};
-            if (static_cast<int>(lane) == leader) pr = mcgd::probe_cell_t<5>(R.C, cell, check);
-            const bool hit = __shfl_sync(peers, static_cast<int>(pr.hit), leader) != 0;
-            const uint32_t payload = __shfl_sync(peers, pr.payload, leader);
-            const bool full = __shfl_sync(peers, pr.where, leader) < 0;
-            const uint32_t bi = (cp.y >> 16) & 0xffu;   // the bracket: flag bits and payloads are by bracket
-            if (hit) {
-                flags |= 1u << bi;
-                R.pa[q].ahead[bi] = payload;
-                if (c < 2u) kbits |= 1u << c;
-            } else if (full) {
-                flags |= 1u << (mcgd::kAheadFull + bi);
-            }
+__device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, uint32_t key,
+                                               const mcgd::ShadeIn& in, uint32_t c_begin = 0u,
+                                               uint32_t c_end = mcgd::kAhead, uint32_t flags = 0u) {
+    const uint32_t slot = key_slot(R, key);
+    const mcg_program prog = R.S.programs[slot];
+    const uint32_t ncp = min(min(prog.cache_point_count, mcgd::kAhead), c_end);
+    PathRay& rec = R.pa[q];
+    uint32_t kbits = 0u;   // hit bits of the table's first two entries (the sort key's)
+    const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
+    const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
+    for (uint32_t c = c_begin; c < ncp; ++c) {
+        const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
+        mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
+        if (cp.y & MCG_F_USES_UV) {
+            desc.mip = mip;
+            desc.tx = tx;
+            desc.ty = ty;
+        }
+        uint64_t h;
+        uint32_t check;
+        mcgd::hash_desc(desc, h, check);
+        // the whole cell in one round trip (head block + first tail pair): the
+        // epilogue has bandwidth to spare, and a filling table makes most
+        // scans run past the first pair
+        const mcgd::Probe pr = mcgd::probe_cell_t<5>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
+        const uint32_t bi = (cp.y >> 16) & 0xffu;   // the bracket: flag bits and payloads are by bracket
+        if (pr.hit) {
+            flags |= 1u << bi;
+            rec.ahead[bi] = pr.payload;
+            if (c < 2u) kbits |= 1u << c;
+        } else if (pr.where < 0) {
+            flags |= 1u << (mcgd::kAheadFull + bi);
         }
     }
-    if (!valid) return key;
-    R.pa[q].sp3.z = __uint_as_float(flags);
+    rec.sp3.z = __uint_as_float(flags);
     return key | ((kbits & R.pat_mask) << R.key_pat);
 }
 
@@ -610,7 +593,7 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
 __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, uint32_t pid, float4& ro,
                                                const float4& rd, const float4& thr, const float4& L,
                                                bool found, uint32_t prim, float t, float b1, float b2,
-                                               int vtx, mcgd::ShadeIn& in) {
+                                               int vtx) {
     const V3 o{ro.x, ro.y, ro.z}, d{rd.x, rd.y, rd.z};
     if (!found) {
         R.fin[pid] = make_float4(L.x + thr.x * R.S.env[0], L.y + thr.y * R.S.env[1],
@@ -631,10 +614,13 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     rec.sp1 = make_float4(s.n.x, s.n.y, s.n.z, __uint_as_float(pixel));
     rec.sp2 = make_float4(s.u, s.v, g1.x, g1.y);
     rec.sp3 = make_float4(g2.x, g2.y, __uint_as_float(0u), 0.0f);
-    // for the caller's look-ahead (warp-collective, after every lane's hit)
-    in = mcgd::ShadeIn{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
-                       s.u, s.v, g1.x, g1.y, g2.x, g2.y};
-    return key;
+    if (!R.ahead_fused || s.slot >= R.S.n_programs) return key;
+    // the look-ahead probes right here (a separate kernel for the cache
+    // points past the first two, after the trace, measured slower: monster
+    // analogue 1363 vs 1285 ms per render)
+    const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
+                           s.u, s.v, g1.x, g1.y, g2.x, g2.y};
+    return look_ahead(R, q, key, in);
 }
 
 // The shading point the trace kernel stored in a path's ray record.
@@ -1804,22 +1790,19 @@ __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
-    uint32_t key = 0u;
-    mcgd::ShadeIn in{};
     if (active) {
         const float4 ro0 = make_float4(o.x, o.y, o.z, 0.0f);
         float4 ro = ro0;
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
         const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
         const float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        key = hit_record(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0, in);
+        const uint32_t key = hit_record(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
         R.pa[i].ro = ro0;   // the width at the origin (the shade propagates it)
         R.pa[i].rd = rd;
         R.pb[i] = PathVal{thr, make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(i))};
+        R.keys[i] = key;
         R.vals[i] = i;
     }
-    if (R.ahead_fused) key = look_ahead(R, i, active && found && key_slot(R, key) < R.S.n_programs, key, in);
-    if (active) R.keys[i] = key;
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
 }
@@ -1954,24 +1937,20 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
     float t = 0.0f, b1 = 0.0f, b2 = 0.0f;
     const bool found = closest_ww4s(R.S, active, o, d, kTMin, __int_as_float(0x7f800000), prim, t, b1, b2,
                                     nvis, ntest);
-    uint32_t key = 0u;
-    mcgd::ShadeIn in{};
     if (active) {
         const uint32_t pid = __float_as_uint(R.pb[q].L.w);
+        uint32_t key;
         if (found) {
             key = hit_record(R, q, pid, ro, rd, make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), true, prim, t,
-                             b1, b2, vtx, in);
+                             b1, b2, vtx);
         } else {
             // the path ends; k_resolve_lights (which runs after this kernel
             // and the shadow rays) adds throughput * env to its final radiance
             key = no_hit_key(R);
         }
+        R.keys[q] = key;
         R.vals[q] = q;
     }
-    // the look-ahead probes of the hits, the warp's identical (cell, check)
-    // pairs probed once
-    if (R.ahead_fused) key = look_ahead(R, q, active && found && key_slot(R, key) < R.S.n_programs, key, in);
-    if (active) R.keys[q] = key;
     mcgd::warp_add(R.stats + kStatClosestRays, active ? 1u : 0u);
     mcgd::warp_add(R.stats + kStatNodes, nvis);
     mcgd::warp_add(R.stats + kStatPrims, ntest);
@@ -1990,16 +1969,12 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
 // ordered apply, so it reads the epoch-start table -- the same rule.
 __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t* count) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in_range = q < (count ? *count : R.n_paths);
-    const uint32_t key = in_range ? R.keys[q] : 0u;
-    const bool valid = in_range && key_slot(R, key) < R.S.n_programs;
-    mcgd::ShadeIn in{};
-    if (valid) {
-        const PathRay& pr = R.pa[q];
-        in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
-    }
-    const uint32_t k2 = look_ahead(R, q, valid, key, in);
-    if (valid) R.keys[q] = k2;
+    if (q >= (count ? *count : R.n_paths)) return;
+    const uint32_t key = R.keys[q];
+    if (key_slot(R, key) >= R.S.n_programs) return;
+    const PathRay& pr = R.pa[q];
+    const mcgd::ShadeIn in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
+    R.keys[q] = look_ahead(R, q, key, in);
 }
 
 // Finishes vertex b at sorted position i, after the shadow rays and the
