@@ -545,17 +545,22 @@ __device__ __forceinline__ void camera_ray(const RenderView& R, uint32_t pixel, 
 // The look-ahead probe of the live hit at layout position q with shading
 // point `in` (k_lookahead below): its material's first kAhead cache points,
 // results to R.ahead[q]; returns the sort key with the hit bits added.
+// kMax: the kernel's bound on the cache points probed (3 when no material of
+// the scene has more: the loop unrolls, as the one-bracket scenes want)
+template <uint32_t kMax>
 __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, uint32_t key,
-                                               const mcgd::ShadeIn& in, uint32_t c_begin = 0u,
-                                               uint32_t c_end = mcgd::kAhead, uint32_t flags = 0u) {
+                                               const mcgd::ShadeIn& in) {
+    uint32_t flags = 0u;
     const uint32_t slot = key_slot(R, key);
     const mcg_program prog = R.S.programs[slot];
-    const uint32_t ncp = min(min(prog.cache_point_count, mcgd::kAhead), c_end);
+    const uint32_t ncp = min(prog.cache_point_count, kMax);
     PathRay& rec = R.pa[q];
     uint32_t kbits = 0u;   // hit bits of the table's first two entries (the sort key's)
     const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
     const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
-    for (uint32_t c = c_begin; c < ncp; ++c) {
+#pragma unroll
+    for (uint32_t c = 0; c < kMax; ++c) {
+        if (c >= ncp) break;
         const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
         mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
         if (cp.y & MCG_F_USES_UV) {
@@ -590,6 +595,7 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
 // rebuilds the shading record (position, normal, uv, footprint gradients)
 // from the hit record with the same arithmetic (shade_input), so one 16-byte
 // gather replaces three.
+template <uint32_t kMax>
 __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, uint32_t pid, float4& ro,
                                                const float4& rd, const float4& thr, const float4& L,
                                                bool found, uint32_t prim, float t, float b1, float b2,
@@ -620,7 +626,7 @@ __device__ __forceinline__ uint32_t hit_record(const RenderView& R, uint32_t q, 
     // analogue 1363 vs 1285 ms per render)
     const mcgd::ShadeIn in{s.p.x, s.p.y, s.p.z, s.n.x, s.n.y, s.n.z, d.x, d.y, d.z,
                            s.u, s.v, g1.x, g1.y, g2.x, g2.y};
-    return look_ahead(R, q, key, in);
+    return look_ahead<kMax>(R, q, key, in);
 }
 
 // The shading point the trace kernel stored in a path's ray record.
@@ -1775,6 +1781,7 @@ __device__ __forceinline__ void pk_stacks(int depth, bool closest, int32_t*& cod
 #ifndef MCG_PRIMARY_BLOCK
 #define MCG_PRIMARY_BLOCK 128
 #endif
+template <uint32_t kMax>
 __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -1796,7 +1803,7 @@ __global__ void __launch_bounds__(MCG_PRIMARY_BLOCK) k_primary(RenderView R) {
         const float4 rd = make_float4(d.x, d.y, d.z, R.cam[11]);
         const float4 thr = make_float4(1.0f, 1.0f, 1.0f, __uint_as_float(0u));
         const float4 L = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        const uint32_t key = hit_record(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
+        const uint32_t key = hit_record<kMax>(R, i, i, ro, rd, thr, L, found, prim, t, b1, b2, 0);
         R.pa[i].ro = ro0;   // the width at the origin (the shade propagates it)
         R.pa[i].rd = rd;
         R.pb[i] = PathVal{thr, make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(i))};
@@ -1923,6 +1930,7 @@ __global__ void __launch_bounds__(MCG_SHADOW_BLOCK, MCG_SHADOW_MINB) k_shadow_ww
 #ifndef MCG_TRACE_BLOCK
 #define MCG_TRACE_BLOCK 128
 #endif
+template <uint32_t kMax>
 __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_closest_ww(RenderView R, const uint32_t* count, int vtx) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t nvis = 0, ntest = 0;
@@ -1941,7 +1949,7 @@ __global__ void __launch_bounds__(MCG_TRACE_BLOCK, MCG_TRACE_MINB) k_trace_close
         const uint32_t pid = __float_as_uint(R.pb[q].L.w);
         uint32_t key;
         if (found) {
-            key = hit_record(R, q, pid, ro, rd, make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), true, prim, t,
+            key = hit_record<kMax>(R, q, pid, ro, rd, make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), true, prim, t,
                              b1, b2, vtx);
         } else {
             // the path ends; k_resolve_lights (which runs after this kernel
@@ -1974,7 +1982,7 @@ __global__ void __launch_bounds__(256) k_lookahead(RenderView R, const uint32_t*
     if (key_slot(R, key) >= R.S.n_programs) return;
     const PathRay& pr = R.pa[q];
     const mcgd::ShadeIn in = shade_input(pr.rd, pr.sp0, pr.sp1, pr.sp2, pr.sp3);
-    R.keys[q] = look_ahead(R, q, key, in);
+    R.keys[q] = look_ahead<mcgd::kAhead>(R, q, key, in);
 }
 
 // Finishes vertex b at sorted position i, after the shadow rays and the
@@ -2441,9 +2449,14 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
     // traversal kernels use no shared memory: ask for the whole L1 (the tree
     // and triangles are ~1 MB; 12% of the node loads miss L1). Same call:
     // 646.6 / 647.1 vs 649.2 / 648.5 ms per bench render.
-    cudaFuncSetAttribute(k_trace_closest_ww, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
+    cudaFuncSetAttribute(k_trace_closest_ww<3>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
+    cudaFuncSetAttribute(k_trace_closest_ww<mcgd::kAhead>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
     cudaFuncSetAttribute(k_shadow_ww<true>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
-    cudaFuncSetAttribute(k_primary, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
+    cudaFuncSetAttribute(k_primary<3>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
+    cudaFuncSetAttribute(k_primary<mcgd::kAhead>, cudaFuncAttributePreferredSharedMemoryCarveout, MCG_TRACE_CARVEOUT);
+    // scenes whose materials have at most three cache points take the
+    // kernels with the short, unrolled look-ahead loop
+    const bool many_cps = D.max_cache_points > 3;
     // programs up to 32 KB of bytecode are staged in shared memory per block
     // (MCG_CODE_SMEM=0: read from global memory through L1)
     const char* cs_env = std::getenv("MCG_CODE_SMEM");
@@ -2477,7 +2490,8 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
         const unsigned grid = grid_for(R.n_paths, 256);
         {
             LaunchScope ls(ctx, "primary", 0.0, sm);
-            k_primary<<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
+            if (many_cps) k_primary<mcgd::kAhead><<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
+            else k_primary<3><<<grid_for(R.n_paths, MCG_PRIMARY_BLOCK), MCG_PRIMARY_BLOCK, 0, sm>>>(R);
             ls.done();
         }
         if (look_ahead && !R.ahead_fused) {
@@ -2543,8 +2557,13 @@ void render_device(mcg_ctx* ctx, const mcg_render_params& P, mcg_cache* external
             if (fork) cuda_check(cudaEventRecord(lane_join[l], sa), "event");
             if (b < P.max_bounces) {
                 LaunchScope ls(ctx, "trace_closest", 0.0, sm);
-                k_trace_closest_ww<<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, sm>>>(
-                    R, R.shadow_count + 2, b + 1);
+                if (many_cps) {
+                    k_trace_closest_ww<mcgd::kAhead><<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, sm>>>(
+                        R, R.shadow_count + 2, b + 1);
+                } else {
+                    k_trace_closest_ww<3><<<grid_for(R.n_paths, MCG_TRACE_BLOCK), MCG_TRACE_BLOCK, 0, sm>>>(
+                        R, R.shadow_count + 2, b + 1);
+                }
                 ls.done();
             }
             if (b < P.max_bounces && look_ahead && !R.ahead_fused) {
