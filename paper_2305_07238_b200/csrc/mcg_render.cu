@@ -558,7 +558,9 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
     uint32_t kbits = 0u;   // hit bits of the table's first two entries (the sort key's)
     const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
     const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
-#pragma unroll
+    // unrolled for the short bound only (an unrolled eight-step loop made the
+    // many-cache-point kernels 15% slower)
+#pragma unroll (kMax <= 3u ? kMax : 1u)
     for (uint32_t c = 0; c < kMax; ++c) {
         if (c >= ncp) break;
         const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
