@@ -558,7 +558,6 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
     uint32_t kbits = 0u;   // hit bits of the table's first two entries (the sort key's)
     const uint32_t mip = mcgd::mip_level(in.g1x, in.g1y, in.g2x, in.g2y, R.mip_offset);
     const uint32_t tx = mcgd::texel_index(in.u, mip), ty = mcgd::texel_index(in.v, mip);
-    const bool dense = 2ull * __ldcg(R.stats + kStatWon) > R.C.n_cells * R.C.n_entries;
     auto probe = [&](uint32_t c) {
         const uint2 cp = __ldg(R.S.ahead_cp + slot * mcgd::kAhead + c);
         mcgd::Desc desc{prog.material_id, cp.x, 0u, 0u, 0u};
@@ -570,13 +569,10 @@ __device__ __forceinline__ uint32_t look_ahead(const RenderView& R, uint32_t q, 
         uint64_t h;
         uint32_t check;
         mcgd::hash_desc(desc, h, check);
-        // a filling table (more than half its slots won in this render so
-        // far) makes most scans run past the first pair: then the whole cell
-        // in one round trip (head block + first tail pair); a sparse one ends
-        // on the first pair (one 16-byte read)
-        const uint64_t cell = mcgd::fast_mod(h, R.C.n_cells, R.C.magic);
-        const mcgd::Probe pr = dense ? mcgd::probe_cell_t<5>(R.C, cell, check)
-                                     : mcgd::probe_cell_t<1>(R.C, cell, check);
+        // the whole cell in one round trip (head block + first tail pair): the
+        // epilogue has bandwidth to spare, and a filling table makes most
+        // scans run past the first pair
+        const mcgd::Probe pr = mcgd::probe_cell_t<5>(R.C, mcgd::fast_mod(h, R.C.n_cells, R.C.magic), check);
         const uint32_t bi = (cp.y >> 16) & 0xffu;   // the bracket: flag bits and payloads are by bracket
         if (pr.hit) {
             flags |= 1u << bi;
