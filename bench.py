@@ -506,6 +506,14 @@ def main() -> None:
                                     "ms_cache": t_on, "ms_no_cache": t_off,
                                     "throughput_vs_no_cache": t_off / t_on, "hit_rate": ons[-1].hit_rate,
                                     "inserts_lost_full": ons[-1].inserts_lost_full, "target": 0.9}
+            # the deterministic-insert mode (north_star) on the bench workload
+            dcfg = RenderConfig(width=W, height=H, spp=SPP, n_cells=N_CELLS, n_entries=N_ENTRIES,
+                                mip_offset=MIP_OFFSET, cache_enabled=True, deterministic=True)
+            api_render(scene, dcfg, ctx=ctx)
+            dst = api_render(scene, dcfg, ctx=ctx).stats
+            extras["deterministic"] = {"ms": dst.device_ms, "samples_per_s": W * H * SPP / (dst.device_ms / 1e3),
+                                       "hit_rate": dst.hit_rate,
+                                       "note": "epoch-deferred ordered inserts, one pass lane; bit-identical runs"}
             ctx.upload(scene)
             extras["tunings"] = tun
         if rank == 0:
