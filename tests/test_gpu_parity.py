@@ -245,13 +245,14 @@ def test_render_cache_off_matches_oracle(ctx, oracle, scene_dir, kind, libm, sph
     assert res.stats.shading_points == st.shading_points
 
 
-@pytest.mark.parametrize("lookahead", ["1", "0"])
+@pytest.mark.parametrize("lookahead", ["1", "0", "2"])
 @pytest.mark.parametrize("kind,k,spheres", [("cornell", 1, 0), ("junkshop", 2, 0), ("italianflat", 3, 0),
                                             ("classroom", 2, 16), ("monster", 2, 0)])
 def test_render_deterministic_matches_oracle(ctx, oracle, scene_dir, kind, k, spheres, lookahead, monkeypatch):
     """Deterministic mode, bit-exact: with the look-ahead probes (the default:
-    the first cache points probed before the material sort, their hit bits in
-    the sort key) and without (every probe inline in the VM)."""
+    the cache points probed in the trace kernels' epilogue before the material
+    sort, their hit bits in the sort key), with them as a separate kernel
+    (MCG_LOOKAHEAD=2) and without (every probe inline in the VM)."""
     monkeypatch.setenv("MCG_LOOKAHEAD", lookahead)
     w, h, spp, nc, ne = 64, 48, 6, 4099, 4
     path = scenes.build_scene(scenes.SceneSpec(kind, w, h, tris_per_side=6, libm_ops=True, spheres=spheres),
