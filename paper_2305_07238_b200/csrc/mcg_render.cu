@@ -2040,17 +2040,19 @@ __global__ void __launch_bounds__(256) k_resolve_lights(RenderView R, int b) {
 // Material evaluation of every live hit, in sorted (material, Morton)
 // order, then NEE and the bounce; the path's state moves from its old layout
 // position q = order[i] to i in the next layout.
-// (128, 5): 96 registers (a few spill slots) and five resident blocks. With
+// (256, 3): 80 registers (a few spill slots), three resident blocks. With
 // the look-ahead sort the subtrees run with full warps and the kernel is
-// bound by dependent-latency stalls ("wait"), so the extra resident warps pay:
-// 795.7 vs 784.7 ms per bench render (MINB 4: 115 registers; MINB 6: 80
-// registers with 156 bytes of spills, 794 ms).
+// bound by dependent-latency stalls, so resident warps pay; 256-thread
+// blocks halve the blocks that stage their programs' bytecode. Measured per
+// bench render: (128, 4) 795.7 ms, (128, 5) 784.7 -> 767.8 on later builds,
+// (256, 3) 764.5, (256, 5: 48 registers, 824 bytes of spills) 764.5,
+// (128, 8 / 10) 801.1 / 788.4.
 #ifndef MCG_SHADE_MINB
-#define MCG_SHADE_MINB 5
+#define MCG_SHADE_MINB 3
 #endif
 template <bool kDeferred, bool kSmemCode>
 #ifndef MCG_SHADE_BLOCK
-#define MCG_SHADE_BLOCK 128
+#define MCG_SHADE_BLOCK 256
 #endif
 __global__ void __launch_bounds__(MCG_SHADE_BLOCK, MCG_SHADE_MINB) k_shade(RenderView R, const uint32_t* __restrict__ skey,
                                                const uint32_t* __restrict__ order, int max_stack,
